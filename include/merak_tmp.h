@@ -1,0 +1,183 @@
+/*
+ * merak_tmp.h -- C ABI of the B200-native sub-pipelined tensor-model-parallel (TMP)
+ * transformer layer (Merak, arXiv 2206.04959, Section 6.3 "Sub-pipelined TMP").
+ *
+ * Citations: "P:n" = PAPER.md line n.
+ *   P:557  a layer = attention block + FFN block
+ *   P:107  Megatron TMP: weights split along rows/columns, AllReduce after row-parallel GEMMs
+ *   P:558  two AllReduces in the forward pass, two in the backward pass
+ *   P:571  "evenly split each microbatch ... into two sub-microbatches, whose procedures are
+ *          independent ... when one sub-microbatch is communicating, the other ... calculations"
+ *   P:572  communication and computation "overlapped across transformer layers"
+ *   P:576  "asynchronous communication operations and an alternate execution schedule for
+ *          both forward and backward passes"
+ *   P:555  problem statement: hidden size, sequence length, microbatch size
+ *   P:763  TMP degree = number of GPUs
+ *
+ * What a call computes: one pre-LN GPT decoder layer (readings R1-R7),
+ *   forward   y  = x1 + gelu(LN2(x1) W1^T + b1) W2^T + b2,  x1 = x + Attn(LN1(x)) Wo^T + bo
+ *   backward  dx and += weight/bias/LN gradients for cotangent dy,
+ * executed on this rank's weight shard with the four TMP all-reduces done in-kernel over
+ * NVLink peer memory, the microbatch split into n_sub sub-microbatches pipelined across a
+ * compute stream and a communication stream.
+ *
+ * Conventions
+ *  - Every function returns merak_status (0 = OK); none aborts or throws across the ABI.
+ *    The text of the last error is available from merak_tmp_last_error().
+ *  - All device pointers are plain CUDA device pointers (16-byte aligned; 256 recommended).
+ *    Host pointers appear only in merak_tmp_init (config, callback) and the query calls.
+ *  - All work is enqueued asynchronously in the order of the caller's stream `st`
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream).  The library owns two
+ *    internal streams (compute, communication); they wait on an event recorded on `st` at
+ *    entry, and `st` waits on the library's final event before the call returns (unless
+ *    MERAK_FLAG_CHAIN defers that join, see below).
+ *  - A handle is bound to one (process, device, layer shape); it is not thread-safe.
+ *
+ * Tensor layouts (token-major, features contiguous; tokens = B*s, token t = b*s + i):
+ *  x, y, dx, dy : [B*s, h] bf16, replicated on every rank of the TMP group.
+ *  Rank r owns heads [e0_r, e0_r + H_r) with H_r = H/T + (r < H % T) (reading R8: whole
+ *  heads, uneven split allowed), h_r = H_r * d, and FFN rows [r f_r, (r+1) f_r), f_r = f/T.
+ *  merak_tmp_weights (bf16, this rank's shard, nn.Linear [out, in] layout):
+ *    ln1_g, ln1_b, ln2_g, ln2_b, b_o, b_2 : [h] replicated
+ *    w_qkv : [3 h_r, h]  rows = q rows of the rank's heads, then k rows, then v rows;
+ *            head e of the rank occupies rows e*d .. e*d+d-1 inside each of the three blocks
+ *    b_qkv : [3 h_r]
+ *    w_o   : [h, h_r]     (row-parallel: columns of the global w_o for the rank's heads)
+ *    w_1   : [f_r, h]     b_1 : [f_r]
+ *    w_2   : [h, f_r]     (row-parallel)
+ *  merak_tmp_grads: same shapes, fp32, ACCUMULATED (+=).  The caller zeroes them.
+ *  Replicated grads (LN, b_o, b_2) come out identical on every rank.
+ *  saved: caller-owned device buffer of merak_tmp_saved_bytes() bytes written by layer_fwd
+ *  and read by layer_bwd; its layout does not depend on n_sub.
+ *
+ * Numerics (reading R10-R12): bf16 operands (RNE), fp32 accumulation and
+ * statistics; each all-reduce sums bf16 partials in fp32 in fixed rank order 0..T-1, adds
+ * bias and residual in fp32 and rounds once to bf16; every reduction over tokens (bias,
+ * LN and weight gradients) runs in a fixed order that does not depend on n_sub, so the
+ * sub-pipelined (n_sub > 1) and the non-sub-pipelined (n_sub = 1) runs are bit-identical.
+ */
+#ifndef MERAK_TMP_H
+#define MERAK_TMP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct merak_tmp merak_tmp_t; /* opaque handle */
+
+typedef enum {
+  MERAK_OK = 0,
+  MERAK_EINVAL = -1,       /* NULL/misaligned pointer, non-positive size, bad enum value      */
+  MERAK_EINDIVISIBLE = -2, /* B % n_sub, h % H or f % T non-zero, or H < T                    */
+  MERAK_EUNSUPPORTED = -3, /* head dim not in {32,64,80,96,128}, T not in {1,2,4,8}, no P2P   */
+  MERAK_ECUDA = -4,        /* a CUDA runtime/driver call failed (message has the CUDA error)  */
+  MERAK_EPEER = -5,        /* IPC handle exchange / peer mapping failed                       */
+  MERAK_ENOMEM = -6,       /* device allocation failed                                        */
+  MERAK_ETIMEOUT = -7,     /* the in-kernel peer handshake watchdog fired (peer hung/absent); */
+                           /* reported by the next call, the handle is unusable afterwards    */
+  MERAK_ESTATE = -8        /* call not allowed in the current state (e.g. open chain)         */
+} merak_status;
+
+enum { MERAK_BF16 = 0, MERAK_FP32_CHECK = 1 };      /* merak_tmp_config.precision */
+enum { MERAK_COMM_PEER = 0, MERAK_COMM_NCCL = 1 };  /* merak_tmp_config.comm      */
+
+/* flags for layer_fwd / layer_bwd */
+enum {
+  MERAK_FLAG_CHAIN = 1u,   /* do not join the caller stream at the end; the next merak call
+                              on this handle (or merak_tmp_join) joins.  Lets layer k+1's first
+                              sub-batch start while layer k's last all-reduce is in flight.        */
+  MERAK_FLAG_NO_COMM = 2u  /* measurement only: every all-reduce reads the local partial alone
+                              (wrong result for T > 1); used to measure exposed communication.   */
+};
+
+typedef struct {
+  int32_t hidden;      /* h */
+  int32_t heads;       /* H                                                           */
+  int32_t seq_len;     /* s */
+  int32_t microbatch;  /* B */
+  int32_t tmp_degree;  /* T: GPUs in the TMP group */
+  int32_t tmp_rank;    /* r in [0, T)                                                 */
+  int32_t n_sub;       /* sub-microbatches n (P:571 uses 2); 1 = Megatron baseline     */
+  int32_t ffn_hidden;  /* f; 0 => 4h (reading R7)                                     */
+  float ln_eps;        /* LayerNorm epsilon; 0 => 1e-5 (reading R3)                   */
+  int32_t precision;   /* MERAK_BF16 (MERAK_FP32_CHECK: reserved, returns EUNSUPPORTED)*/
+  int32_t comm;        /* MERAK_COMM_PEER | MERAK_COMM_NCCL                           */
+  int32_t comm_ctas;   /* CTAs used by each all-reduce kernel; 0 => auto              */
+  int32_t device;      /* CUDA device ordinal this handle lives on                    */
+} merak_tmp_config;
+
+/* Collective used ONLY during init to exchange CUDA IPC handles (and the NCCL unique id):
+ * gathers `bytes_per_rank` bytes from every rank of the TMP group into `recv` in rank order
+ * (recv holds T * bytes_per_rank bytes).  Returns 0 on success.  The Python binding implements
+ * it with torch.distributed.all_gather on the caller's process group. */
+typedef int (*merak_allgather_fn)(void *ctx, const void *send, void *recv, size_t bytes_per_rank);
+
+typedef struct {
+  const void *ln1_g, *ln1_b, *w_qkv, *b_qkv, *w_o, *b_o, *ln2_g, *ln2_b, *w_1, *b_1, *w_2, *b_2;
+} merak_tmp_weights;
+
+typedef struct {
+  float *ln1_g, *ln1_b, *w_qkv, *b_qkv, *w_o, *b_o, *ln2_g, *ln2_b, *w_1, *b_1, *w_2, *b_2;
+} merak_tmp_grads;
+
+/* Create a handle.  Validates the config (EINVAL / EINDIVISIBLE / EUNSUPPORTED), allocates the
+ * peer-visible all-reduce slots, flags and the workspace on cfg->device (ENOMEM), creates the
+ * two internal streams, and for T > 1 exchanges CUDA IPC handles through `ag` and maps every
+ * peer's slots (EPEER); with comm == MERAK_COMM_NCCL it also creates an NCCL communicator.
+ * Collective over the TMP group: every rank must call it with the same shape fields.
+ * On success *out owns everything; release with merak_tmp_destroy. */
+merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, void *ag_ctx,
+                            merak_tmp_t **out);
+
+/* Change the number of sub-microbatches.  Requires B % n_sub == 0 (EINDIVISIBLE) and no
+ * open chain (ESTATE).  Takes effect for the next layer_fwd/layer_bwd; all ranks must agree. */
+merak_status merak_tmp_set_subbatches(merak_tmp_t *h, int32_t n_sub);
+
+/* Bytes of the caller-owned `saved` buffer (activations kept from fwd for bwd). */
+size_t merak_tmp_saved_bytes(const merak_tmp_t *h);
+
+/* Forward: reads x (device, [B*s, h] bf16) and the weight shard, writes
+ * y (device, [B*s, h] bf16) and `saved`.  Collective over the TMP group.  `st` = cudaStream_t. */
+merak_status merak_tmp_layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const void *x, void *y,
+                                 void *saved, uint32_t flags, void *st);
+
+/* Backward: reads x, `saved` (from the matching layer_fwd), dy; writes dx
+ * ([B*s, h] bf16) and ACCUMULATES fp32 gradients into *g.  Collective over the TMP group. */
+merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const void *x,
+                                 const void *saved, const void *dy, void *dx, const merak_tmp_grads *g,
+                                 uint32_t flags, void *st);
+
+/* Join a MERAK_FLAG_CHAIN sequence: make `st` wait for every outstanding all-reduce. */
+merak_status merak_tmp_join(merak_tmp_t *h, void *st);
+
+/* Release all resources (synchronises the internal streams first).  NULL is a no-op. */
+merak_status merak_tmp_destroy(merak_tmp_t *h);
+
+/* Text of the last error on this handle (or of the last failed init when h == NULL). */
+const char *merak_tmp_last_error(const merak_tmp_t *h);
+
+/* ---- measurement hooks (used by bench.py; cheap, off by default) -------------------------- */
+
+/* Kernel classes timed when profiling is on (cudaEvents around each launch on its stream). */
+enum {
+  MERAK_K_GEMM = 0, MERAK_K_ATTN_FWD = 1, MERAK_K_ATTN_BWD = 2, MERAK_K_LN = 3,
+  MERAK_K_ALLREDUCE = 4, MERAK_K_REDUCE = 5, MERAK_K_NUM = 6
+};
+
+/* Turn per-kernel-class event timing on/off (resets the accumulators). */
+merak_status merak_tmp_set_profiling(merak_tmp_t *h, int32_t on);
+
+/* Sum of device milliseconds, launch counts and algorithmic FLOPs per class since
+ * set_profiling(1) (synchronises the internal streams).  Arrays have MERAK_K_NUM entries. */
+merak_status merak_tmp_get_profile(merak_tmp_t *h, double *ms, int64_t *launches, double *flops);
+
+/* Total kernels this handle launched since init (all classes, profiling on or off). */
+int64_t merak_tmp_launch_count(const merak_tmp_t *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MERAK_TMP_H */

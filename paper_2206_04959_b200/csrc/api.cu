@@ -1,0 +1,755 @@
+// api.cu -- the C ABI (include/merak_tmp.h): handle, CUDA-IPC peer mapping, and the two-stream
+// sub-microbatch scheduler of the sub-pipelined TMP layer (Merak P:571-576, fig:pipedtp(b)).
+//
+// Streams: cs = computation stream, ms = communication stream ("executing the communication
+// stream and computation stream together").  For sub-batch j the compute stream runs the
+// column-parallel GEMMs, attention and the row-parallel GEMM whose epilogue writes the partial
+// into this rank's peer-visible slot; the comm stream runs the in-kernel NVLink all-reduce of j
+// while the compute stream proceeds with sub-batch j+1 ("when one sub-microbatch is
+// communicating, the other sub-microbatch will do calculations").  Backward mirrors it with the
+// weight-gradient GEMMs filling the all-reduce gaps ("alternate execution schedule").
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "../../include/merak_tmp.h"
+#include "../../include/merak_tmp_testing.h"
+#include "kernels.h"
+
+using namespace mk;
+typedef __nv_bfloat16 bf16;
+
+namespace {
+
+constexpr int MAXN = 64;  // max sub-batches
+constexpr int NSLOT = 4;  // AR#1..AR#4 partial slots
+
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+  double flops;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+struct merak_tmp {
+  merak_tmp_config cfg;
+  int h, H, s, B, T, r, n, f, d, Hr, hr, fr, e0, M;
+  float eps;
+  int dev;
+  cudaStream_t cs = nullptr, ms = nullptr;
+  // peer-visible memory: NSLOT slots of [M, h] bf16 followed by the flag array
+  char *pv = nullptr;
+  size_t slot_bytes = 0, flags_off = 0, pv_bytes = 0;
+  char *peer_pv[MAX_T] = {};
+  uint32_t epoch = 0;
+  int *err_host = nullptr, *err_dev = nullptr;
+  // workspace
+  char *ws = nullptr;
+  bf16 *dz = nullptr, *dx1 = nullptr, *dctx = nullptr, *dqkv = nullptr;
+  float *delta = nullptr, *part_col = nullptr, *part_lng = nullptr, *part_lnb = nullptr;
+  int G = 16;
+  // events
+  cudaEvent_t ev_entry = nullptr, ev_cs_end = nullptr;
+  bool have_prev = false;
+  cudaEvent_t ev_p[MAXN] = {};
+  cudaEvent_t ev_ar[NSLOT][MAXN] = {};
+  bool ev_ar_valid[NSLOT][MAXN] = {};
+  cudaEvent_t prev_out[MAXN] = {};
+  bool chain_open = false;
+  // measurement
+  bool prof = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> evpool;
+  size_t evnext = 0;
+  double prof_ms[MERAK_K_NUM] = {}, prof_flops[MERAK_K_NUM] = {};
+  int64_t prof_launch[MERAK_K_NUM] = {};
+  int64_t launches = 0;
+  std::string err;
+};
+
+static std::string g_init_err;
+
+static merak_status fail(merak_tmp_t *h, merak_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (h)
+    h->err = buf;
+  else
+    g_init_err = buf;
+  return st;
+}
+
+#define CK(h, call)                                                                                 \
+  do {                                                                                              \
+    cudaError_t _e = (call);                                                                        \
+    if (_e != cudaSuccess) return fail((h), MERAK_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(_e), __FILE__, __LINE__); \
+  } while (0)
+
+// ------------------------------------------------------------------------------ measurement
+static cudaEvent_t pool_event(merak_tmp_t *h) {
+  if (h->evnext == h->evpool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    h->evpool.push_back(e);
+  }
+  return h->evpool[h->evnext++];
+}
+
+struct Launch {
+  merak_tmp_t *h;
+  int cls;
+  cudaStream_t st;
+  double flops;
+  int nk;
+  cudaEvent_t a = nullptr;
+  Launch(merak_tmp_t *h_, int cls_, cudaStream_t st_, double flops_, int nk_ = 1)
+      : h(h_), cls(cls_), st(st_), flops(flops_), nk(nk_) {
+    if (h->prof) {
+      a = pool_event(h);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~Launch() {
+    h->launches += nk;
+    if (h->prof) {
+      cudaEvent_t b = pool_event(h);
+      cudaEventRecord(b, st);
+      h->recs.push_back({cls, a, b, flops});
+      h->prof_launch[cls] += nk;
+    }
+  }
+};
+
+// ------------------------------------------------------------------------------ shapes / layout
+struct SavedLayout {
+  size_t u, mean1, rstd1, qkv, ctx, lse, x1, mean2, rstd2, u2, z, g, total;
+};
+static SavedLayout saved_layout(const merak_tmp_t *h) {
+  SavedLayout L;
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t at = o; o += align256(bytes); return at; };
+  const size_t M = h->M;
+  L.u = take(M * h->h * 2);
+  L.mean1 = take(M * 4);
+  L.rstd1 = take(M * 4);
+  L.qkv = take(M * 3 * h->hr * 2);
+  L.ctx = take(M * h->hr * 2);
+  L.lse = take((size_t)h->B * h->Hr * h->s * 4);
+  L.x1 = take(M * h->h * 2);
+  L.mean2 = take(M * 4);
+  L.rstd2 = take(M * 4);
+  L.u2 = take(M * h->h * 2);
+  L.z = take(M * h->fr * 2);
+  L.g = take(M * h->fr * 2);
+  L.total = o;
+  return L;
+}
+
+static PeerSync make_sync(merak_tmp_t *h, bool comm) {
+  PeerSync ps;
+  memset(&ps, 0, sizeof(ps));
+  ps.T = h->T;
+  ps.rank = h->r;
+  ps.enabled = comm && h->T > 1;
+  ps.epoch = ++h->epoch;
+  ps.flags_local = reinterpret_cast<uint32_t *>(h->pv + h->flags_off);
+  for (int q = 0; q < h->T; ++q) ps.flags_peer[q] = reinterpret_cast<uint32_t *>(h->peer_pv[q] + h->flags_off);
+  ps.err_word = h->err_dev;
+  ps.timeout_ns = 20ull * 1000 * 1000 * 1000;  // 20 s
+  return ps;
+}
+
+static bf16 *slot_ptr(merak_tmp_t *h, int rank, int slot) {
+  return reinterpret_cast<bf16 *>(h->peer_pv[rank] + (size_t)slot * h->slot_bytes);
+}
+
+// ------------------------------------------------------------------------------ kernel wrappers
+static merak_status run_gemm(merak_tmp_t *h, const GemmArgs &a) {
+  Launch L(h, MERAK_K_GEMM, h->cs, 2.0 * a.M * a.N * a.K);
+  CK(h, gemm(a, h->cs));
+  return MERAK_OK;
+}
+static GemmArgs gargs(const void *A, const void *B, int M, int N, int K, int lda, int ldb, bool a_mn, bool b_mn,
+                      int epi) {
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.A = A; a.B = B; a.M = M; a.N = N; a.K = K; a.lda = lda; a.ldb = ldb; a.a_mn = a_mn; a.b_mn = b_mn; a.epi = epi;
+  return a;
+}
+static merak_status run_colsum(merak_tmp_t *h, const bf16 *X, int ld, int m, int n, float *g) {
+  Launch L(h, MERAK_K_REDUCE, h->cs, 0.0, 2);
+  CK(h, colsum_partial(X, ld, m, n, h->part_col, h->cs));
+  CK(h, chain_add(h->part_col, m / 16, n, g, h->cs));
+  return MERAK_OK;
+}
+
+#define TRY(x)                          \
+  do {                                  \
+    merak_status _s = (x);              \
+    if (_s != MERAK_OK) return _s;      \
+  } while (0)
+
+static merak_status check_async_error(merak_tmp_t *h) {
+  if (h->err_host && *(volatile int *)h->err_host)
+    return fail(h, MERAK_ETIMEOUT, "peer handshake watchdog fired in a previous all-reduce (peer absent or hung)");
+  return MERAK_OK;
+}
+
+static merak_status enter(merak_tmp_t *h, cudaStream_t st) {
+  TRY(check_async_error(h));
+  CK(h, cudaSetDevice(h->dev));
+  CK(h, cudaEventRecord(h->ev_entry, st));
+  CK(h, cudaStreamWaitEvent(h->cs, h->ev_entry, 0));
+  CK(h, cudaStreamWaitEvent(h->ms, h->ev_entry, 0));
+  // the comm stream may reuse workspace only after the previous call's compute work is done
+  if (h->have_prev) CK(h, cudaStreamWaitEvent(h->ms, h->ev_cs_end, 0));
+  return MERAK_OK;
+}
+
+static merak_status leave(merak_tmp_t *h, cudaStream_t st, uint32_t flags, int last_slot) {
+  CK(h, cudaEventRecord(h->ev_cs_end, h->cs));
+  h->have_prev = true;
+  for (int j = 0; j < h->n; ++j) h->prev_out[j] = h->ev_ar[last_slot][j];
+  if (flags & MERAK_FLAG_CHAIN) {
+    h->chain_open = true;
+  } else {
+    CK(h, cudaStreamWaitEvent(st, h->ev_cs_end, 0));
+    CK(h, cudaStreamWaitEvent(st, h->ev_ar[last_slot][h->n - 1], 0));
+    h->chain_open = false;
+  }
+  return MERAK_OK;
+}
+
+// ------------------------------------------------------------------------------ forward
+static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const bf16 *x, bf16 *y, char *saved,
+                              uint32_t flags, cudaStream_t st) {
+  const SavedLayout L = saved_layout(h);
+  const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr;
+  const bool comm = !(flags & MERAK_FLAG_NO_COMM);
+  TRY(enter(h, st));
+  auto S = [&](size_t off) { return saved + off; };
+  // ---- attention block, sub-batch j: LN1 -> QKV -> attention -> proj (partial into slot 0) -> AR#1
+  for (int j = 0; j < n; ++j) {
+    if (h->chain_open) CK(h, cudaStreamWaitEvent(h->cs, h->prev_out[j], 0));
+    const size_t r0 = (size_t)j * m;
+    const bf16 *xj = x + r0 * hh;
+    bf16 *u = (bf16 *)S(L.u) + r0 * hh;
+    float *mean1 = (float *)S(L.mean1) + r0, *rstd1 = (float *)S(L.rstd1) + r0;
+    bf16 *qkv = (bf16 *)S(L.qkv) + r0 * 3 * hr;
+    bf16 *ctx = (bf16 *)S(L.ctx) + r0 * hr;
+    float *lse = (float *)S(L.lse) + (size_t)j * b * h->Hr * h->s;
+    {
+      Launch Lk(h, MERAK_K_LN, h->cs, 0.0);
+      CK(h, ln_fwd(xj, (const bf16 *)w->ln1_g, (const bf16 *)w->ln1_b, u, mean1, rstd1, m, hh, h->eps, h->cs));
+    }
+    GemmArgs g = gargs(u, w->w_qkv, m, 3 * hr, hh, hh, hh, false, false, EPI_BIAS_BF16);
+    g.out = qkv; g.ldo = 3 * hr; g.bias = w->b_qkv;
+    TRY(run_gemm(h, g));
+    {
+      AttnArgs a;
+      memset(&a, 0, sizeof(a));
+      a.qkv = qkv; a.ctx = ctx; a.lse = lse; a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
+      Launch Lk(h, MERAK_K_ATTN_FWD, h->cs, 2.0 * b * hr * (double)h->s * (h->s + 1));
+      CK(h, attn_fwd(a, h->cs));
+    }
+    if (h->ev_ar_valid[0][j]) CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[0][j], 0));
+    g = gargs(ctx, w->w_o, m, hh, hr, hr, hr, false, false, EPI_STORE_BF16);
+    g.out = slot_ptr(h, h->r, 0) + r0 * hh; g.ldo = hh;
+    TRY(run_gemm(h, g));
+    CK(h, cudaEventRecord(h->ev_p[j], h->cs));
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
+    {
+      ArFwdArgs a;
+      memset(&a, 0, sizeof(a));
+      a.T = comm ? h->T : 1;
+      for (int q = 0; q < a.T; ++q) a.partial[q] = slot_ptr(h, comm ? q : h->r, 0) + r0 * hh;
+      a.m = m; a.h = hh; a.resid = xj; a.bias = (const bf16 *)w->b_o; a.out = (bf16 *)S(L.x1) + r0 * hh;
+      a.do_ln = true; a.gamma = (const bf16 *)w->ln2_g; a.beta = (const bf16 *)w->ln2_b;
+      a.ln_out = (bf16 *)S(L.u2) + r0 * hh; a.mean = (float *)S(L.mean2) + r0; a.rstd = (float *)S(L.rstd2) + r0;
+      a.eps = h->eps; a.ctas = h->cfg.comm_ctas;
+      PeerSync ps = make_sync(h, comm);
+      Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+      CK(h, ar_fwd(a, ps, h->ms));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[0][j], h->ms));
+    h->ev_ar_valid[0][j] = true;
+  }
+  // ---- FFN block, sub-batch j: fc1 (+bias+GeLU) -> fc2 (partial into slot 1) -> AR#2
+  for (int j = 0; j < n; ++j) {
+    const size_t r0 = (size_t)j * m;
+    CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[0][j], 0));
+    bf16 *u2 = (bf16 *)S(L.u2) + r0 * hh;
+    bf16 *z = (bf16 *)S(L.z) + r0 * fr, *gg = (bf16 *)S(L.g) + r0 * fr;
+    GemmArgs g = gargs(u2, w->w_1, m, fr, hh, hh, hh, false, false, EPI_BIAS_GELU);
+    g.out = z; g.ldo = fr; g.out2 = gg; g.ldo2 = fr; g.bias = w->b_1;
+    TRY(run_gemm(h, g));
+    if (h->ev_ar_valid[1][j]) CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[1][j], 0));
+    g = gargs(gg, w->w_2, m, hh, fr, fr, fr, false, false, EPI_STORE_BF16);
+    g.out = slot_ptr(h, h->r, 1) + r0 * hh; g.ldo = hh;
+    TRY(run_gemm(h, g));
+    CK(h, cudaEventRecord(h->ev_p[j], h->cs));
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
+    {
+      ArFwdArgs a;
+      memset(&a, 0, sizeof(a));
+      a.T = comm ? h->T : 1;
+      for (int q = 0; q < a.T; ++q) a.partial[q] = slot_ptr(h, comm ? q : h->r, 1) + r0 * hh;
+      a.m = m; a.h = hh; a.resid = (const bf16 *)S(L.x1) + r0 * hh; a.bias = (const bf16 *)w->b_2;
+      a.out = y + r0 * hh; a.do_ln = false; a.ctas = h->cfg.comm_ctas;
+      PeerSync ps = make_sync(h, comm);
+      Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+      CK(h, ar_fwd(a, ps, h->ms));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[1][j], h->ms));
+    h->ev_ar_valid[1][j] = true;
+  }
+  return leave(h, st, flags, 1);
+}
+
+// ------------------------------------------------------------------------------ backward
+static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const bf16 *x, const char *saved_c,
+                              const bf16 *dy, bf16 *dx, const merak_tmp_grads *gr, uint32_t flags, cudaStream_t st) {
+  char *saved = const_cast<char *>(saved_c);
+  const SavedLayout L = saved_layout(h);
+  const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr;
+  const bool comm = !(flags & MERAK_FLAG_NO_COMM);
+  TRY(enter(h, st));
+  auto S = [&](size_t off) { return saved + off; };
+  // ---- FFN block: fc2 dgrad (x GeLU') -> fc1 dgrad (partial, slot 2) -> AR#3 ; wgrads fill the gap
+  for (int j = 0; j < n; ++j) {
+    if (h->chain_open) CK(h, cudaStreamWaitEvent(h->cs, h->prev_out[j], 0));
+    const size_t r0 = (size_t)j * m;
+    const bf16 *dyj = dy + r0 * hh;
+    bf16 *dz = h->dz + r0 * fr;
+    GemmArgs g = gargs(dyj, w->w_2, m, fr, hh, hh, fr, false, true, EPI_GELU_BWD);
+    g.out = dz; g.ldo = fr; g.aux = (const bf16 *)S(L.z) + r0 * fr; g.ld_aux = fr;
+    TRY(run_gemm(h, g));
+    if (h->ev_ar_valid[2][j]) CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[2][j], 0));
+    g = gargs(dz, w->w_1, m, hh, fr, fr, hh, false, true, EPI_STORE_BF16);
+    g.out = slot_ptr(h, h->r, 2) + r0 * hh; g.ldo = hh;
+    TRY(run_gemm(h, g));
+    CK(h, cudaEventRecord(h->ev_p[j], h->cs));
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
+    {
+      ArBwdArgs a;
+      memset(&a, 0, sizeof(a));
+      a.T = comm ? h->T : 1;
+      for (int q = 0; q < a.T; ++q) a.partial[q] = slot_ptr(h, comm ? q : h->r, 2) + r0 * hh;
+      a.m = m; a.h = hh; a.x_ln = (const bf16 *)S(L.x1) + r0 * hh;
+      a.mean = (const float *)S(L.mean2) + r0; a.rstd = (const float *)S(L.rstd2) + r0;
+      a.gamma = (const bf16 *)w->ln2_g; a.dres = dyj; a.dx = h->dx1 + r0 * hh;
+      a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
+      PeerSync ps = make_sync(h, comm);
+      {
+        Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+        CK(h, ar_bwd(a, ps, h->ms));
+      }
+      Launch Lk(h, MERAK_K_REDUCE, h->ms, 0.0, 2);
+      CK(h, chain_add(h->part_lng, m / h->G, hh, gr->ln2_g, h->ms));
+      CK(h, chain_add(h->part_lnb, m / h->G, hh, gr->ln2_b, h->ms));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[2][j], h->ms));
+    h->ev_ar_valid[2][j] = true;
+    // weight / bias gradients of the FFN block for sub-batch j (overlap AR#3(j))
+    g = gargs(dyj, S(L.g) + r0 * fr * 2, hh, fr, m, hh, fr, true, true, EPI_ACC_F32);
+    g.out32 = gr->w_2; g.ld32 = fr;
+    TRY(run_gemm(h, g));
+    g = gargs(dz, S(L.u2) + r0 * hh * 2, fr, hh, m, fr, hh, true, true, EPI_ACC_F32);
+    g.out32 = gr->w_1; g.ld32 = hh;
+    TRY(run_gemm(h, g));
+    TRY(run_colsum(h, dz, fr, m, fr, gr->b_1));
+    TRY(run_colsum(h, dyj, hh, m, hh, gr->b_2));
+  }
+  // ---- attention block: proj dgrad -> attention bwd -> QKV dgrad (partial, slot 3) -> AR#4
+  for (int j = 0; j < n; ++j) {
+    const size_t r0 = (size_t)j * m;
+    CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[2][j], 0));
+    const bf16 *dx1 = h->dx1 + r0 * hh;
+    bf16 *dctx = h->dctx + r0 * hr, *dqkv = h->dqkv + r0 * 3 * hr;
+    const bf16 *qkv = (const bf16 *)S(L.qkv) + r0 * 3 * hr, *ctx = (const bf16 *)S(L.ctx) + r0 * hr;
+    GemmArgs g = gargs(dx1, w->w_o, m, hr, hh, hh, hr, false, true, EPI_STORE_BF16);
+    g.out = dctx; g.ldo = hr;
+    TRY(run_gemm(h, g));
+    {
+      AttnArgs a;
+      memset(&a, 0, sizeof(a));
+      a.qkv = qkv; a.ctx = (void *)ctx; a.lse = (float *)S(L.lse) + (size_t)j * b * h->Hr * h->s;
+      a.dctx = dctx; a.dqkv = dqkv; a.delta = h->delta; a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
+      Launch Lk(h, MERAK_K_ATTN_BWD, h->cs, 4.0 * b * hr * (double)h->s * (h->s + 1), 2);
+      CK(h, attn_bwd(a, h->cs));
+    }
+    if (h->ev_ar_valid[3][j]) CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[3][j], 0));
+    g = gargs(dqkv, w->w_qkv, m, hh, 3 * hr, 3 * hr, hh, false, true, EPI_STORE_BF16);
+    g.out = slot_ptr(h, h->r, 3) + r0 * hh; g.ldo = hh;
+    TRY(run_gemm(h, g));
+    CK(h, cudaEventRecord(h->ev_p[j], h->cs));
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
+    {
+      ArBwdArgs a;
+      memset(&a, 0, sizeof(a));
+      a.T = comm ? h->T : 1;
+      for (int q = 0; q < a.T; ++q) a.partial[q] = slot_ptr(h, comm ? q : h->r, 3) + r0 * hh;
+      a.m = m; a.h = hh; a.x_ln = x + r0 * hh;
+      a.mean = (const float *)S(L.mean1) + r0; a.rstd = (const float *)S(L.rstd1) + r0;
+      a.gamma = (const bf16 *)w->ln1_g; a.dres = dx1; a.dx = dx + r0 * hh;
+      a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
+      PeerSync ps = make_sync(h, comm);
+      {
+        Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+        CK(h, ar_bwd(a, ps, h->ms));
+      }
+      Launch Lk(h, MERAK_K_REDUCE, h->ms, 0.0, 2);
+      CK(h, chain_add(h->part_lng, m / h->G, hh, gr->ln1_g, h->ms));
+      CK(h, chain_add(h->part_lnb, m / h->G, hh, gr->ln1_b, h->ms));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[3][j], h->ms));
+    h->ev_ar_valid[3][j] = true;
+    // weight / bias gradients of the attention block for sub-batch j (overlap AR#4(j))
+    g = gargs(dx1, ctx, hh, hr, m, hh, hr, true, true, EPI_ACC_F32);
+    g.out32 = gr->w_o; g.ld32 = hr;
+    TRY(run_gemm(h, g));
+    TRY(run_colsum(h, dx1, hh, m, hh, gr->b_o));
+    g = gargs(dqkv, S(L.u) + r0 * hh * 2, 3 * hr, hh, m, 3 * hr, hh, true, true, EPI_ACC_F32);
+    g.out32 = gr->w_qkv; g.ld32 = hh;
+    TRY(run_gemm(h, g));
+    TRY(run_colsum(h, dqkv, 3 * hr, m, 3 * hr, gr->b_qkv));
+  }
+  return leave(h, st, flags, 3);
+}
+
+// ------------------------------------------------------------------------------ init / destroy
+static merak_status validate(const merak_tmp_config *c) {
+  if (!c) return fail(nullptr, MERAK_EINVAL, "config is NULL");
+  if (c->hidden <= 0 || c->heads <= 0 || c->seq_len <= 0 || c->microbatch <= 0 || c->tmp_degree <= 0 ||
+      c->n_sub <= 0 || c->ffn_hidden < 0)
+    return fail(nullptr, MERAK_EINVAL, "non-positive size in config");
+  if (c->tmp_rank < 0 || c->tmp_rank >= c->tmp_degree) return fail(nullptr, MERAK_EINVAL, "tmp_rank out of range");
+  if (c->precision != MERAK_BF16 && c->precision != MERAK_FP32_CHECK)
+    return fail(nullptr, MERAK_EINVAL, "bad precision");
+  if (c->comm != MERAK_COMM_PEER && c->comm != MERAK_COMM_NCCL) return fail(nullptr, MERAK_EINVAL, "bad comm");
+  const int T = c->tmp_degree, f = c->ffn_hidden ? c->ffn_hidden : 4 * c->hidden;
+  if (c->hidden % c->heads) return fail(nullptr, MERAK_EINDIVISIBLE, "hidden %% heads != 0");
+  if (c->heads < T) return fail(nullptr, MERAK_EINDIVISIBLE, "heads < tmp_degree");
+  if (f % T) return fail(nullptr, MERAK_EINDIVISIBLE, "ffn %% tmp_degree != 0");
+  if (c->microbatch % c->n_sub) return fail(nullptr, MERAK_EINDIVISIBLE, "microbatch %% n_sub != 0");
+  if (c->n_sub > MAXN) return fail(nullptr, MERAK_EUNSUPPORTED, "n_sub > %d", MAXN);
+  const int d = c->hidden / c->heads;
+  if (d != 32 && d != 64 && d != 80 && d != 96 && d != 128)
+    return fail(nullptr, MERAK_EUNSUPPORTED, "head dim %d not in {32,64,80,96,128}", d);
+  if (T != 1 && T != 2 && T != 4 && T != 8) return fail(nullptr, MERAK_EUNSUPPORTED, "tmp_degree not in {1,2,4,8}");
+  if (((c->microbatch / c->n_sub) * c->seq_len) % 16)
+    return fail(nullptr, MERAK_EUNSUPPORTED, "tokens per sub-batch must be a multiple of 16");
+  if (c->hidden % 8 || (f / T) % 8) return fail(nullptr, MERAK_EUNSUPPORTED, "h and f/T must be multiples of 8");
+  if (c->precision == MERAK_FP32_CHECK) return fail(nullptr, MERAK_EUNSUPPORTED, "fp32 check mode not built yet");
+  if (c->comm == MERAK_COMM_NCCL) return fail(nullptr, MERAK_EUNSUPPORTED, "NCCL baseline not built yet");
+  return MERAK_OK;
+}
+
+static void release(merak_tmp_t *h) {
+  if (!h) return;
+  cudaSetDevice(h->dev);
+  if (h->cs) cudaStreamSynchronize(h->cs);
+  if (h->ms) cudaStreamSynchronize(h->ms);
+  for (int q = 0; q < MAX_T; ++q)
+    if (h->peer_pv[q] && h->peer_pv[q] != h->pv) cudaIpcCloseMemHandle(h->peer_pv[q]);
+  if (h->pv) cudaFree(h->pv);
+  if (h->ws) cudaFree(h->ws);
+  if (h->err_host) cudaFreeHost(h->err_host);
+  for (auto e : h->evpool) cudaEventDestroy(e);
+  if (h->ev_entry) cudaEventDestroy(h->ev_entry);
+  if (h->ev_cs_end) cudaEventDestroy(h->ev_cs_end);
+  for (int j = 0; j < MAXN; ++j) {
+    if (h->ev_p[j]) cudaEventDestroy(h->ev_p[j]);
+    for (int k = 0; k < NSLOT; ++k)
+      if (h->ev_ar[k][j]) cudaEventDestroy(h->ev_ar[k][j]);
+  }
+  if (h->cs) cudaStreamDestroy(h->cs);
+  if (h->ms) cudaStreamDestroy(h->ms);
+  delete h;
+}
+
+extern "C" {
+
+merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, void *ag_ctx, merak_tmp_t **out) {
+  if (!out) return fail(nullptr, MERAK_EINVAL, "out is NULL");
+  *out = nullptr;
+  TRY(validate(cfg));
+  if (cfg->tmp_degree > 1 && !ag) return fail(nullptr, MERAK_EINVAL, "tmp_degree > 1 needs an allgather callback");
+  merak_tmp_t *h = new merak_tmp();
+  h->cfg = *cfg;
+  h->h = cfg->hidden; h->H = cfg->heads; h->s = cfg->seq_len; h->B = cfg->microbatch;
+  h->T = cfg->tmp_degree; h->r = cfg->tmp_rank; h->n = cfg->n_sub;
+  h->f = cfg->ffn_hidden ? cfg->ffn_hidden : 4 * cfg->hidden;
+  h->d = h->h / h->H;
+  h->Hr = h->H / h->T + (h->r < h->H % h->T ? 1 : 0);  // reading R8
+  h->e0 = 0;
+  for (int q = 0; q < h->r; ++q) h->e0 += h->H / h->T + (q < h->H % h->T ? 1 : 0);
+  h->hr = h->Hr * h->d;
+  h->fr = h->f / h->T;
+  h->M = h->B * h->s;
+  h->eps = cfg->ln_eps > 0 ? cfg->ln_eps : 1e-5f;
+  h->dev = cfg->device;
+  h->G = ar_bwd_group_rows(h->h);
+  auto bail = [&](merak_status st) {
+    g_init_err = h->err;
+    release(h);
+    return st;
+  };
+#define CKI(call)                                                                                          \
+  do {                                                                                                     \
+    cudaError_t _e = (call);                                                                               \
+    if (_e != cudaSuccess) {                                                                               \
+      fail(h, _e == cudaErrorMemoryAllocation ? MERAK_ENOMEM : MERAK_ECUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+      return bail(_e == cudaErrorMemoryAllocation ? MERAK_ENOMEM : MERAK_ECUDA);                          \
+    }                                                                                                      \
+  } while (0)
+  CKI(cudaSetDevice(h->dev));
+  int prio_lo = 0, prio_hi = 0;
+  CKI(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CKI(cudaStreamCreateWithPriority(&h->cs, cudaStreamNonBlocking, prio_lo));
+  CKI(cudaStreamCreateWithPriority(&h->ms, cudaStreamNonBlocking, prio_hi));  // comm first when both ready
+  CKI(cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming));
+  CKI(cudaEventCreateWithFlags(&h->ev_cs_end, cudaEventDisableTiming));
+  for (int j = 0; j < MAXN; ++j) {
+    CKI(cudaEventCreateWithFlags(&h->ev_p[j], cudaEventDisableTiming));
+    for (int k = 0; k < NSLOT; ++k) CKI(cudaEventCreateWithFlags(&h->ev_ar[k][j], cudaEventDisableTiming));
+  }
+  // peer-visible slots + flags
+  h->slot_bytes = align256((size_t)h->M * h->h * 2);
+  h->flags_off = NSLOT * h->slot_bytes;
+  h->pv_bytes = h->flags_off + align256(2 * MAX_AR_CTAS * MAX_T * sizeof(uint32_t));
+  CKI(cudaMalloc(&h->pv, h->pv_bytes));
+  CKI(cudaMemset(h->pv + h->flags_off, 0, h->pv_bytes - h->flags_off));
+  CKI(cudaHostAlloc(&h->err_host, sizeof(int), cudaHostAllocMapped));
+  *h->err_host = 0;
+  CKI(cudaHostGetDevicePointer((void **)&h->err_dev, h->err_host, 0));
+  // workspace
+  {
+    const size_t M = h->M;
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t at = o; o += align256(bytes); return at; };
+    const size_t o_dz = take(M * h->fr * 2), o_dx1 = take(M * h->h * 2), o_dctx = take(M * h->hr * 2);
+    const size_t o_dqkv = take(M * 3 * h->hr * 2), o_delta = take((size_t)h->B * h->Hr * h->s * 4);
+    const int ncol = std::max(std::max(3 * h->hr, h->fr), h->h);
+    const size_t o_pc = take((M / 16) * (size_t)ncol * 4);
+    const size_t o_pg = take((M / h->G) * (size_t)h->h * 4), o_pb = take((M / h->G) * (size_t)h->h * 4);
+    CKI(cudaMalloc(&h->ws, o));
+    h->dz = (bf16 *)(h->ws + o_dz); h->dx1 = (bf16 *)(h->ws + o_dx1); h->dctx = (bf16 *)(h->ws + o_dctx);
+    h->dqkv = (bf16 *)(h->ws + o_dqkv); h->delta = (float *)(h->ws + o_delta);
+    h->part_col = (float *)(h->ws + o_pc); h->part_lng = (float *)(h->ws + o_pg); h->part_lnb = (float *)(h->ws + o_pb);
+  }
+  CKI(cudaDeviceSynchronize());
+  for (int q = 0; q < MAX_T; ++q) h->peer_pv[q] = nullptr;
+  h->peer_pv[h->r] = h->pv;
+  if (h->T > 1) {
+    cudaIpcMemHandle_t mine;
+    CKI(cudaIpcGetMemHandle(&mine, h->pv));
+    std::vector<cudaIpcMemHandle_t> all(h->T);
+    if (ag(ag_ctx, &mine, all.data(), sizeof(mine)) != 0) {
+      fail(h, MERAK_EPEER, "allgather of IPC handles failed");
+      return bail(MERAK_EPEER);
+    }
+    for (int q = 0; q < h->T; ++q) {
+      if (q == h->r) continue;
+      void *p = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&p, all[q], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        fail(h, MERAK_EPEER, "cudaIpcOpenMemHandle(rank %d): %s", q, cudaGetErrorString(e));
+        return bail(MERAK_EPEER);
+      }
+      h->peer_pv[q] = (char *)p;
+    }
+    // second exchange: every rank has mapped every peer and zeroed its flags before any kernel runs
+    int dummy = h->r, gathered[MAX_T];
+    if (ag(ag_ctx, &dummy, gathered, sizeof(int)) != 0) {
+      fail(h, MERAK_EPEER, "allgather barrier failed");
+      return bail(MERAK_EPEER);
+    }
+  }
+#undef CKI
+  *out = h;
+  return MERAK_OK;
+}
+
+merak_status merak_tmp_set_subbatches(merak_tmp_t *h, int32_t n_sub) {
+  if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
+  if (h->chain_open) return fail(h, MERAK_ESTATE, "set_subbatches while a MERAK_FLAG_CHAIN sequence is open");
+  if (n_sub <= 0 || n_sub > MAXN) return fail(h, MERAK_EINVAL, "n_sub out of range");
+  if (h->B % n_sub) return fail(h, MERAK_EINDIVISIBLE, "microbatch %% n_sub != 0");
+  if (((h->B / n_sub) * h->s) % 16) return fail(h, MERAK_EUNSUPPORTED, "tokens per sub-batch must be a multiple of 16");
+  // all outstanding work of the old split must finish before slot/event indices are reinterpreted
+  CK(h, cudaStreamSynchronize(h->cs));
+  CK(h, cudaStreamSynchronize(h->ms));
+  memset(h->ev_ar_valid, 0, sizeof(h->ev_ar_valid));
+  h->n = n_sub;
+  h->cfg.n_sub = n_sub;
+  return MERAK_OK;
+}
+
+size_t merak_tmp_saved_bytes(const merak_tmp_t *h) { return h ? saved_layout(h).total : 0; }
+
+static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+merak_status merak_tmp_layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const void *x, void *y, void *saved,
+                                 uint32_t flags, void *st) {
+  if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
+  if (!w || !x || !y || !saved) return fail(h, MERAK_EINVAL, "NULL argument");
+  const void *ps[] = {w->ln1_g, w->ln1_b, w->w_qkv, w->b_qkv, w->w_o, w->b_o, w->ln2_g, w->ln2_b, w->w_1, w->b_1, w->w_2, w->b_2, x, y, saved};
+  for (const void *p : ps)
+    if (!p || !aligned16(p)) return fail(h, MERAK_EINVAL, "NULL or non-16B-aligned pointer");
+  return layer_fwd(h, w, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st);
+}
+
+merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const void *x, const void *saved,
+                                 const void *dy, void *dx, const merak_tmp_grads *g, uint32_t flags, void *st) {
+  if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
+  if (!w || !x || !saved || !dy || !dx || !g) return fail(h, MERAK_EINVAL, "NULL argument");
+  const void *ps[] = {w->ln1_g, w->ln1_b, w->w_qkv, w->b_qkv, w->w_o, w->b_o, w->ln2_g, w->ln2_b, w->w_1, w->b_1,
+                      w->w_2, w->b_2, x, saved, dy, dx, g->ln1_g, g->ln1_b, g->w_qkv, g->b_qkv, g->w_o, g->b_o,
+                      g->ln2_g, g->ln2_b, g->w_1, g->b_1, g->w_2, g->b_2};
+  for (const void *p : ps)
+    if (!p || !aligned16(p)) return fail(h, MERAK_EINVAL, "NULL or non-16B-aligned pointer");
+  return layer_bwd(h, w, (const bf16 *)x, (const char *)saved, (const bf16 *)dy, (bf16 *)dx, g, flags,
+                   (cudaStream_t)st);
+}
+
+merak_status merak_tmp_join(merak_tmp_t *h, void *st) {
+  if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
+  if (!h->have_prev) return MERAK_OK;
+  CK(h, cudaStreamWaitEvent((cudaStream_t)st, h->ev_cs_end, 0));
+  for (int j = 0; j < h->n; ++j) CK(h, cudaStreamWaitEvent((cudaStream_t)st, h->prev_out[j], 0));
+  h->chain_open = false;
+  return MERAK_OK;
+}
+
+merak_status merak_tmp_destroy(merak_tmp_t *h) {
+  release(h);
+  return MERAK_OK;
+}
+
+const char *merak_tmp_last_error(const merak_tmp_t *h) { return h ? h->err.c_str() : g_init_err.c_str(); }
+
+merak_status merak_tmp_set_profiling(merak_tmp_t *h, int32_t on) {
+  if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
+  CK(h, cudaStreamSynchronize(h->cs));
+  CK(h, cudaStreamSynchronize(h->ms));
+  h->prof = on != 0;
+  h->recs.clear();
+  h->evnext = 0;
+  for (int k = 0; k < MERAK_K_NUM; ++k) {
+    h->prof_ms[k] = 0;
+    h->prof_flops[k] = 0;
+    h->prof_launch[k] = 0;
+  }
+  return MERAK_OK;
+}
+
+merak_status merak_tmp_get_profile(merak_tmp_t *h, double *ms, int64_t *launches, double *flops) {
+  if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
+  CK(h, cudaStreamSynchronize(h->cs));
+  CK(h, cudaStreamSynchronize(h->ms));
+  for (auto &r : h->recs) {
+    float t = 0;
+    CK(h, cudaEventElapsedTime(&t, r.a, r.b));
+    h->prof_ms[r.cls] += t;
+    h->prof_flops[r.cls] += r.flops;
+  }
+  h->recs.clear();
+  h->evnext = 0;
+  for (int k = 0; k < MERAK_K_NUM; ++k) {
+    if (ms) ms[k] = h->prof_ms[k];
+    if (launches) launches[k] = h->prof_launch[k];
+    if (flops) flops[k] = h->prof_flops[k];
+  }
+  return MERAK_OK;
+}
+
+int64_t merak_tmp_launch_count(const merak_tmp_t *h) { return h ? h->launches : 0; }
+
+// ------------------------------------------------------------------------------ testing entry points
+int merak_test_gemm(const void *A, const void *B, int M, int N, int K, int lda, int ldb, int a_mn, int b_mn, int epi,
+                    void *out, int ldo, void *out2, int ldo2, const void *bias, const void *aux, int ld_aux,
+                    float *out32, int ld32, int max_ctas, void *stream) {
+  GemmArgs a = gargs(A, B, M, N, K, lda, ldb, a_mn != 0, b_mn != 0, epi);
+  a.out = out; a.ldo = ldo; a.out2 = out2; a.ldo2 = ldo2; a.bias = bias; a.aux = aux; a.ld_aux = ld_aux;
+  a.out32 = out32; a.ld32 = ld32; a.max_ctas = max_ctas;
+  return (int)gemm(a, (cudaStream_t)stream);
+}
+
+int merak_test_attn_fwd(const void *qkv, void *ctx, float *lse, int b, int s, int heads, int d, void *stream) {
+  AttnArgs a;
+  memset(&a, 0, sizeof(a));
+  a.qkv = qkv; a.ctx = ctx; a.lse = lse; a.b = b; a.s = s; a.heads = heads; a.d = d;
+  return (int)attn_fwd(a, (cudaStream_t)stream);
+}
+
+int merak_test_attn_bwd(const void *qkv, const void *ctx, const float *lse, const void *dctx, void *dqkv, float *delta,
+                        int b, int s, int heads, int d, void *stream) {
+  AttnArgs a;
+  memset(&a, 0, sizeof(a));
+  a.qkv = qkv; a.ctx = (void *)ctx; a.lse = (float *)lse; a.dctx = dctx; a.dqkv = dqkv; a.delta = delta;
+  a.b = b; a.s = s; a.heads = heads; a.d = d;
+  return (int)attn_bwd(a, (cudaStream_t)stream);
+}
+
+int merak_test_ln_fwd(const void *x, const void *gamma, const void *beta, void *u, float *mean, float *rstd, int m,
+                      int h, float eps, void *stream) {
+  return (int)ln_fwd((const bf16 *)x, (const bf16 *)gamma, (const bf16 *)beta, (bf16 *)u, mean, rstd, m, h, eps,
+                     (cudaStream_t)stream);
+}
+
+int merak_test_ar_fwd(const void *const *partials, int T, int m, int h, const void *resid, const void *bias, void *out,
+                      int do_ln, const void *gamma, const void *beta, void *ln_out, float *mean, float *rstd, float eps,
+                      int ctas, void *stream) {
+  if (T < 1 || T > MAX_T) return (int)cudaErrorInvalidValue;
+  ArFwdArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int q = 0; q < T; ++q) a.partial[q] = (const bf16 *)partials[q];
+  a.T = T; a.m = m; a.h = h; a.resid = (const bf16 *)resid; a.bias = (const bf16 *)bias; a.out = (bf16 *)out;
+  a.do_ln = do_ln != 0; a.gamma = (const bf16 *)gamma; a.beta = (const bf16 *)beta; a.ln_out = (bf16 *)ln_out;
+  a.mean = mean; a.rstd = rstd; a.eps = eps; a.ctas = ctas;
+  PeerSync ps;
+  memset(&ps, 0, sizeof(ps));
+  ps.enabled = false;
+  return (int)ar_fwd(a, ps, (cudaStream_t)stream);
+}
+
+int merak_test_ar_bwd(const void *const *partials, int T, int m, int h, const void *x_ln, const float *mean,
+                      const float *rstd, const void *gamma, const void *dres, void *dx, float *dgamma, float *dbeta,
+                      float *ws, int ctas, void *stream) {
+  if (T < 1 || T > MAX_T) return (int)cudaErrorInvalidValue;
+  ArBwdArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int q = 0; q < T; ++q) a.partial[q] = (const bf16 *)partials[q];
+  a.T = T; a.m = m; a.h = h; a.x_ln = (const bf16 *)x_ln; a.mean = mean; a.rstd = rstd; a.gamma = (const bf16 *)gamma;
+  a.dres = (const bf16 *)dres; a.dx = (bf16 *)dx; a.G = ar_bwd_group_rows(h);
+  if (m % a.G) return (int)cudaErrorInvalidValue;
+  a.part_dg = ws; a.part_db = ws + (size_t)(m / a.G) * h; a.ctas = ctas;
+  PeerSync ps;
+  memset(&ps, 0, sizeof(ps));
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = ar_bwd(a, ps, st);
+  if (e == cudaSuccess) e = chain_add(a.part_dg, m / a.G, h, dgamma, st);
+  if (e == cudaSuccess) e = chain_add(a.part_db, m / a.G, h, dbeta, st);
+  return (int)e;
+}
+
+int merak_test_colsum(const void *X, int ld, int m, int n, float *g, float *ws, void *stream) {
+  cudaError_t e = colsum_partial((const bf16 *)X, ld, m, n, ws, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = chain_add(ws, m / 16, n, g, (cudaStream_t)stream);
+  return (int)e;
+}
+
+}  // extern "C"

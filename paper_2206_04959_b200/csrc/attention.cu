@@ -1,0 +1,527 @@
+// attention.cu -- fused causal attention core (SURVEY §8(a) F3 forward, B6 backward).
+//
+// Per (sample, local head e): S = Q_e K_e^T / sqrt(d), causal mask (diagonal kept, masked
+// probability exactly 0: DESIGN.md reading R4), P = softmax(S), ctx = P V_e.  One CTA owns a
+// 64-row query tile (4 warps x 16 rows) and streams 64-key K/V tiles through a cp.async double
+// buffer with an online softmax (base-2, fp32 statistics); the score/probability tiles never
+// touch HBM.  The forward stores lse2 = log2(sum exp2(S*scale*log2e)) per row for the backward.
+//
+// Backward is deterministic (bit-identity rule ii): no atomics.  Kernel 1 (per query tile)
+// computes delta = rowsum(dO * O) and dQ; kernel 2 (per key tile) recomputes P^T and produces
+// dK, dV.  P and dS are rounded to bf16 as MMA operands; every accumulation is fp32.
+//
+// Round-1 implementation uses mma.sync m16n8k16 (HMMA); attention is 2.7-5.1 % of the layer's
+// FLOPs at the BASELINE configs.  A tcgen05/TMEM version is the next step.
+#include <math.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace mk {
+
+constexpr int ABQ = 64;  // query rows per CTA / keys per tile
+
+template <int D>
+struct AttnSmem {
+  static constexpr int LDS = D + 8;  // +16 B pad: conflict-free ldmatrix for every d
+  static constexpr int TILE = ABQ * LDS;
+};
+
+// cp.async a [64 x D] tile of rows row0.. of the packed qkv/ctx matrix (row stride ld, column col)
+template <int D>
+MK_DEV void load_tile(__nv_bfloat16 *dst, const __nv_bfloat16 *base, int ld, int col, int row0, int s) {
+  constexpr int LDS = AttnSmem<D>::LDS;
+  constexpr int CH = D / 8;
+  for (int idx = threadIdx.x; idx < ABQ * CH; idx += blockDim.x) {
+    const int r = idx / CH, c = idx % CH;
+    const bool valid = (row0 + r) < s;
+    const __nv_bfloat16 *src = base + (size_t)(valid ? row0 + r : 0) * ld + col + c * 8;
+    cp_async16(smem_u32(dst + r * LDS + c * 8), src, valid);
+  }
+}
+
+// A fragments (16 rows x 16 cols) of a row-major smem tile
+MK_DEV void lds_a(uint32_t (&a)[4], const __nv_bfloat16 *tile, int lds, int row0, int col0) {
+  const int lane = lane_id(), mi = lane >> 3, lr = lane & 7;
+  const __nv_bfloat16 *p = tile + (row0 + (mi & 1) * 8 + lr) * lds + col0 + (mi >> 1) * 8;
+  ldsm_x4(smem_u32(p), a[0], a[1], a[2], a[3]);
+}
+// B fragments for two n8 tiles where B^T is stored row-major [n][k] (e.g. K for Q K^T):
+// r0,r1 = (n-tile n0, k lo/hi), r2,r3 = (n-tile n0+8, k lo/hi)
+MK_DEV void lds_bt(uint32_t (&r)[4], const __nv_bfloat16 *tile, int lds, int n0, int k0) {
+  const int lane = lane_id(), mi = lane >> 3, lr = lane & 7;
+  const __nv_bfloat16 *p = tile + (n0 + (mi >> 1) * 8 + lr) * lds + k0 + (mi & 1) * 8;
+  ldsm_x4(smem_u32(p), r[0], r[1], r[2], r[3]);
+}
+// B fragments for two n8 tiles where B is stored row-major [k][n] (e.g. V for P V):
+// r0,r1 = (n-tile n0, k lo/hi), r2,r3 = (n-tile n0+8, k lo/hi)
+MK_DEV void lds_b(uint32_t (&r)[4], const __nv_bfloat16 *tile, int lds, int k0, int n0) {
+  const int lane = lane_id(), mi = lane >> 3, lr = lane & 7;
+  const __nv_bfloat16 *p = tile + (k0 + (mi & 1) * 8 + lr) * lds + n0 + (mi >> 1) * 8;
+  ldsm_x4_t(smem_u32(p), r[0], r[1], r[2], r[3]);
+}
+
+// ------------------------------------------------------------------------------------------ forward
+template <int D>
+__global__ void __launch_bounds__(128) attn_fwd_kernel(AttnArgs a) {
+  constexpr int LDS = AttnSmem<D>::LDS, TILE = AttnSmem<D>::TILE;
+  constexpr int KC = D / 16, NT = D / 8;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  __nv_bfloat16 *sQ = reinterpret_cast<__nv_bfloat16 *>(smraw);
+  __nv_bfloat16 *sK = sQ + TILE;      // [2][TILE]
+  __nv_bfloat16 *sV = sK + 2 * TILE;  // [2][TILE]
+
+  const int s = a.s, H = a.heads;
+  const int nqt = (s + ABQ - 1) / ABQ;
+  const int qt = nqt - 1 - blockIdx.x;  // heaviest tiles first
+  const int head = blockIdx.y, bi = blockIdx.z;
+  const int hr = H * D, ld = 3 * hr;
+  const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(a.qkv) + (size_t)bi * s * ld;
+  const int cq = head * D, ck = hr + head * D, cv = 2 * hr + head * D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const float sl2 = 1.4426950408889634f / sqrtf((float)D);
+
+  load_tile<D>(sQ, base, ld, cq, qt * ABQ, s);
+  load_tile<D>(sK, base, ld, ck, 0, s);
+  load_tile<D>(sV, base, ld, cv, 0, s);
+  cp_async_commit();
+
+  uint32_t qf[KC][4];
+  float o[NT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const int qi0 = qt * ABQ + warp * 16 + g, qi1 = qi0 + 8;
+
+  for (int t = 0; t <= qt; ++t) {
+    if (t < qt) {
+      load_tile<D>(sK + ((t + 1) & 1) * TILE, base, ld, ck, (t + 1) * ABQ, s);
+      load_tile<D>(sV + ((t + 1) & 1) * TILE, base, ld, cv, (t + 1) * ABQ, s);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (t == 0) {
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) lds_a(qf[kc], sQ, LDS, warp * 16, kc * 16);
+    }
+    const __nv_bfloat16 *tK = sK + (t & 1) * TILE, *tV = sV + (t & 1) * TILE;
+    float sc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
+#pragma unroll
+    for (int np = 0; np < 4; ++np) {
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) {
+        uint32_t r[4];
+        lds_bt(r, tK, LDS, np * 16, kc * 16);
+        mma16816(sc[2 * np], qf[kc], r[0], r[1]);
+        mma16816(sc[2 * np + 1], qf[kc], r[2], r[3]);
+      }
+    }
+    // causal mask (diagonal tile) and sequence tail
+    if (t == qt || (t + 1) * ABQ > s) {
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int kj = t * ABQ + nt * 8 + 2 * tq + e;
+          if (kj > qi0 || kj >= s) sc[nt][e] = -INFINITY;
+          if (kj > qi1 || kj >= s) sc[nt][2 + e] = -INFINITY;
+        }
+      }
+    }
+    float mx0 = m0, mx1 = m1;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      mx0 = fmaxf(mx0, fmaxf(sc[nt][0], sc[nt][1]));
+      mx1 = fmaxf(mx1, fmaxf(sc[nt][2], sc[nt][3]));
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+    const float c0 = fast_exp2((m0 - mx0) * sl2), c1 = fast_exp2((m1 - mx1) * sl2);
+    m0 = mx0;
+    m1 = mx1;
+    const float ms0 = mx0 * sl2, ms1 = mx1 * sl2;
+    float rs0 = 0.f, rs1 = 0.f;
+    uint32_t pa[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float p0 = fast_exp2(fmaf(sc[nt][0], sl2, -ms0)), p1 = fast_exp2(fmaf(sc[nt][1], sl2, -ms0));
+      const float p2 = fast_exp2(fmaf(sc[nt][2], sl2, -ms1)), p3 = fast_exp2(fmaf(sc[nt][3], sl2, -ms1));
+      rs0 += p0 + p1;
+      rs1 += p2 + p3;
+      pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
+      pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
+    }
+    l0 = l0 * c0 + rs0;
+    l1 = l1 * c1 + rs1;
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+      o[i][0] *= c0; o[i][1] *= c0; o[i][2] *= c1; o[i][3] *= c1;
+    }
+#pragma unroll
+    for (int dp = 0; dp < NT / 2; ++dp) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        uint32_t r[4];
+        lds_b(r, tV, LDS, kk * 16, dp * 16);
+        mma16816(o[2 * dp], pa[kk], r[0], r[1]);
+        mma16816(o[2 * dp + 1], pa[kk], r[2], r[3]);
+      }
+    }
+    __syncthreads();
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float i0 = 1.f / l0, i1 = 1.f / l1;
+  __nv_bfloat16 *ctx = reinterpret_cast<__nv_bfloat16 *>(a.ctx) + (size_t)bi * s * hr + head * D;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int c = nt * 8 + 2 * tq;
+    if (qi0 < s) *reinterpret_cast<uint32_t *>(ctx + (size_t)qi0 * hr + c) = pack_bf16(o[nt][0] * i0, o[nt][1] * i0);
+    if (qi1 < s) *reinterpret_cast<uint32_t *>(ctx + (size_t)qi1 * hr + c) = pack_bf16(o[nt][2] * i1, o[nt][3] * i1);
+  }
+  if (tq == 0) {
+    float *lse = a.lse + ((size_t)bi * H + head) * s;
+    if (qi0 < s) lse[qi0] = m0 * sl2 + log2f(l0);
+    if (qi1 < s) lse[qi1] = m1 * sl2 + log2f(l1);
+  }
+}
+
+// ------------------------------------------------------------------------------- backward: dQ (+delta)
+template <int D>
+__global__ void __launch_bounds__(128) attn_bwd_dq_kernel(AttnArgs a) {
+  constexpr int LDS = AttnSmem<D>::LDS, TILE = AttnSmem<D>::TILE;
+  constexpr int KC = D / 16, NT = D / 8;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  __nv_bfloat16 *sQ = reinterpret_cast<__nv_bfloat16 *>(smraw);
+  __nv_bfloat16 *sdO = sQ + TILE;
+  __nv_bfloat16 *sK = sdO + TILE;     // [2][TILE]
+  __nv_bfloat16 *sV = sK + 2 * TILE;  // [2][TILE]
+  float *sLse = reinterpret_cast<float *>(sV + 2 * TILE);
+  float *sDel = sLse + ABQ;
+
+  const int s = a.s, H = a.heads;
+  const int nqt = (s + ABQ - 1) / ABQ;
+  const int qt = nqt - 1 - blockIdx.x;
+  const int head = blockIdx.y, bi = blockIdx.z;
+  const int hr = H * D, ld = 3 * hr;
+  const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(a.qkv) + (size_t)bi * s * ld;
+  const __nv_bfloat16 *dO = reinterpret_cast<const __nv_bfloat16 *>(a.dctx) + (size_t)bi * s * hr;
+  const __nv_bfloat16 *O = reinterpret_cast<const __nv_bfloat16 *>(a.ctx) + (size_t)bi * s * hr;
+  const int cq = head * D, ck = hr + head * D, cv = 2 * hr + head * D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const float scale = 1.f / sqrtf((float)D), sl2 = 1.4426950408889634f * scale;
+
+  load_tile<D>(sQ, base, ld, cq, qt * ABQ, s);
+  load_tile<D>(sdO, dO, hr, head * D, qt * ABQ, s);
+  load_tile<D>(sK, base, ld, ck, 0, s);
+  load_tile<D>(sV, base, ld, cv, 0, s);
+  cp_async_commit();
+  // delta = rowsum(dO * O) for the 64 rows (warp w: rows w*16..w*16+15), lse
+  const size_t srow = ((size_t)bi * H + head) * s;
+  for (int rr = 0; rr < 16; ++rr) {
+    const int r = warp * 16 + rr, qi = qt * ABQ + r;
+    float acc = 0.f;
+    if (qi < s) {
+      for (int c = lane; c < D; c += 32)
+        acc += __bfloat162float(dO[(size_t)qi * hr + head * D + c]) * __bfloat162float(O[(size_t)qi * hr + head * D + c]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0) {
+      sDel[r] = acc;
+      sLse[r] = qi < s ? a.lse[srow + qi] : INFINITY;
+      if (qi < s) a.delta[srow + qi] = acc;
+    }
+  }
+  const int r0 = warp * 16 + g, r1 = r0 + 8;
+  const int qi0 = qt * ABQ + r0, qi1 = qt * ABQ + r1;
+
+  uint32_t qf[KC][4], df[KC][4];
+  float dq[NT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
+  float lse0 = 0.f, lse1 = 0.f, del0 = 0.f, del1 = 0.f;
+
+  for (int t = 0; t <= qt; ++t) {
+    if (t < qt) {
+      load_tile<D>(sK + ((t + 1) & 1) * TILE, base, ld, ck, (t + 1) * ABQ, s);
+      load_tile<D>(sV + ((t + 1) & 1) * TILE, base, ld, cv, (t + 1) * ABQ, s);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    if (t == 0) {
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) {
+        lds_a(qf[kc], sQ, LDS, warp * 16, kc * 16);
+        lds_a(df[kc], sdO, LDS, warp * 16, kc * 16);
+      }
+      lse0 = sLse[r0]; lse1 = sLse[r1]; del0 = sDel[r0]; del1 = sDel[r1];
+    }
+    const __nv_bfloat16 *tK = sK + (t & 1) * TILE, *tV = sV + (t & 1) * TILE;
+    float sc[8][4], dp[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
+      dp[i][0] = dp[i][1] = dp[i][2] = dp[i][3] = 0.f;
+    }
+#pragma unroll
+    for (int np = 0; np < 4; ++np) {
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) {
+        uint32_t r[4];
+        lds_bt(r, tK, LDS, np * 16, kc * 16);
+        mma16816(sc[2 * np], qf[kc], r[0], r[1]);
+        mma16816(sc[2 * np + 1], qf[kc], r[2], r[3]);
+        lds_bt(r, tV, LDS, np * 16, kc * 16);
+        mma16816(dp[2 * np], df[kc], r[0], r[1]);
+        mma16816(dp[2 * np + 1], df[kc], r[2], r[3]);
+      }
+    }
+    const bool need_mask = (t == qt) || ((t + 1) * ABQ > s);
+    uint32_t da[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      float p[4];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int kj = t * ABQ + nt * 8 + 2 * tq + e;
+        p[e] = fast_exp2(fmaf(sc[nt][e], sl2, -lse0));
+        p[2 + e] = fast_exp2(fmaf(sc[nt][2 + e], sl2, -lse1));
+        if (need_mask) {
+          if (kj > qi0 || kj >= s) p[e] = 0.f;
+          if (kj > qi1 || kj >= s) p[2 + e] = 0.f;
+        }
+      }
+      const float d0 = p[0] * (dp[nt][0] - del0), d1 = p[1] * (dp[nt][1] - del0);
+      const float d2 = p[2] * (dp[nt][2] - del1), d3 = p[3] * (dp[nt][3] - del1);
+      da[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(d0, d1);
+      da[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(d2, d3);
+    }
+#pragma unroll
+    for (int dn = 0; dn < NT / 2; ++dn) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        uint32_t r[4];
+        lds_b(r, tK, LDS, kk * 16, dn * 16);
+        mma16816(dq[2 * dn], da[kk], r[0], r[1]);
+        mma16816(dq[2 * dn + 1], da[kk], r[2], r[3]);
+      }
+    }
+    __syncthreads();
+  }
+  __nv_bfloat16 *dqkv = reinterpret_cast<__nv_bfloat16 *>(a.dqkv) + (size_t)bi * s * ld + cq;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int c = nt * 8 + 2 * tq;
+    if (qi0 < s) *reinterpret_cast<uint32_t *>(dqkv + (size_t)qi0 * ld + c) = pack_bf16(dq[nt][0] * scale, dq[nt][1] * scale);
+    if (qi1 < s) *reinterpret_cast<uint32_t *>(dqkv + (size_t)qi1 * ld + c) = pack_bf16(dq[nt][2] * scale, dq[nt][3] * scale);
+  }
+}
+
+// ------------------------------------------------------------------------------- backward: dK, dV
+template <int D>
+__global__ void __launch_bounds__(128) attn_bwd_dkdv_kernel(AttnArgs a) {
+  constexpr int LDS = AttnSmem<D>::LDS, TILE = AttnSmem<D>::TILE;
+  constexpr int KC = D / 16, NT = D / 8;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  __nv_bfloat16 *sK = reinterpret_cast<__nv_bfloat16 *>(smraw);
+  __nv_bfloat16 *sV = sK + TILE;
+  __nv_bfloat16 *sQ = sV + TILE;      // [2][TILE]
+  __nv_bfloat16 *sdO = sQ + 2 * TILE; // [2][TILE]
+  float *sLse = reinterpret_cast<float *>(sdO + 2 * TILE);  // [2][64]
+  float *sDel = sLse + 2 * ABQ;                              // [2][64]
+
+  const int s = a.s, H = a.heads;
+  const int nqt = (s + ABQ - 1) / ABQ;
+  const int kt = blockIdx.x;  // kt = 0 has the most query tiles: scheduled first
+  const int head = blockIdx.y, bi = blockIdx.z;
+  const int hr = H * D, ld = 3 * hr;
+  const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(a.qkv) + (size_t)bi * s * ld;
+  const __nv_bfloat16 *dO = reinterpret_cast<const __nv_bfloat16 *>(a.dctx) + (size_t)bi * s * hr;
+  const int cq = head * D, ck = hr + head * D, cv = 2 * hr + head * D;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+  const float scale = 1.f / sqrtf((float)D), sl2 = 1.4426950408889634f * scale;
+  const size_t srow = ((size_t)bi * H + head) * s;
+
+  auto load_q = [&](int qt, int buf) {
+    load_tile<D>(sQ + buf * TILE, base, ld, cq, qt * ABQ, s);
+    load_tile<D>(sdO + buf * TILE, dO, hr, head * D, qt * ABQ, s);
+    for (int r = threadIdx.x; r < ABQ; r += blockDim.x) {
+      const int qi = qt * ABQ + r;
+      sLse[buf * ABQ + r] = qi < s ? a.lse[srow + qi] : INFINITY;
+      sDel[buf * ABQ + r] = qi < s ? a.delta[srow + qi] : 0.f;
+    }
+  };
+  load_tile<D>(sK, base, ld, ck, kt * ABQ, s);
+  load_tile<D>(sV, base, ld, cv, kt * ABQ, s);
+  load_q(kt, 0);
+  cp_async_commit();
+
+  float dk[NT][4], dv[NT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    dk[i][0] = dk[i][1] = dk[i][2] = dk[i][3] = 0.f;
+    dv[i][0] = dv[i][1] = dv[i][2] = dv[i][3] = 0.f;
+  }
+  const int kj0 = kt * ABQ + warp * 16 + g, kj1 = kj0 + 8;
+
+  for (int qt = kt; qt < nqt; ++qt) {
+    const int buf = (qt - kt) & 1;
+    if (qt + 1 < nqt) {
+      load_q(qt + 1, buf ^ 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const __nv_bfloat16 *tQ = sQ + buf * TILE, *tdO = sdO + buf * TILE;
+    const float *tL = sLse + buf * ABQ, *tD = sDel + buf * ABQ;
+    // S^T = K Q^T and dP^T = V dO^T for this warp's 16 keys x 64 queries
+    float st[8][4], dpt[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      st[i][0] = st[i][1] = st[i][2] = st[i][3] = 0.f;
+      dpt[i][0] = dpt[i][1] = dpt[i][2] = dpt[i][3] = 0.f;
+    }
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) {
+      uint32_t kf[4], vf[4];
+      lds_a(kf, sK, LDS, warp * 16, kc * 16);
+      lds_a(vf, sV, LDS, warp * 16, kc * 16);
+#pragma unroll
+      for (int np = 0; np < 4; ++np) {
+        uint32_t r[4];
+        lds_bt(r, tQ, LDS, np * 16, kc * 16);
+        mma16816(st[2 * np], kf, r[0], r[1]);
+        mma16816(st[2 * np + 1], kf, r[2], r[3]);
+        lds_bt(r, tdO, LDS, np * 16, kc * 16);
+        mma16816(dpt[2 * np], vf, r[0], r[1]);
+        mma16816(dpt[2 * np + 1], vf, r[2], r[3]);
+      }
+    }
+    uint32_t pa[4][4], da[4][4];
+    const bool diag = (qt == kt);
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      float p[4], d[4];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int qc = nt * 8 + 2 * tq + e;
+        const int qi = qt * ABQ + qc;
+        const float L = tL[qc], Dl = tD[qc];
+        p[e] = fast_exp2(fmaf(st[nt][e], sl2, -L));
+        p[2 + e] = fast_exp2(fmaf(st[nt][2 + e], sl2, -L));
+        if (diag) {
+          if (kj0 > qi) p[e] = 0.f;
+          if (kj1 > qi) p[2 + e] = 0.f;
+        }
+        d[e] = p[e] * (dpt[nt][e] - Dl);
+        d[2 + e] = p[2 + e] * (dpt[nt][2 + e] - Dl);
+      }
+      pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p[0], p[1]);
+      pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p[2], p[3]);
+      da[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(d[0], d[1]);
+      da[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(d[2], d[3]);
+    }
+    // dV += P^T dO ; dK += dS^T Q
+#pragma unroll
+    for (int dn = 0; dn < NT / 2; ++dn) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        uint32_t r[4];
+        lds_b(r, tdO, LDS, kk * 16, dn * 16);
+        mma16816(dv[2 * dn], pa[kk], r[0], r[1]);
+        mma16816(dv[2 * dn + 1], pa[kk], r[2], r[3]);
+        lds_b(r, tQ, LDS, kk * 16, dn * 16);
+        mma16816(dk[2 * dn], da[kk], r[0], r[1]);
+        mma16816(dk[2 * dn + 1], da[kk], r[2], r[3]);
+      }
+    }
+    __syncthreads();
+  }
+  __nv_bfloat16 *dqkv = reinterpret_cast<__nv_bfloat16 *>(a.dqkv) + (size_t)bi * s * ld;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int c = nt * 8 + 2 * tq;
+    if (kj0 < s) {
+      *reinterpret_cast<uint32_t *>(dqkv + (size_t)kj0 * ld + ck + c) = pack_bf16(dk[nt][0] * scale, dk[nt][1] * scale);
+      *reinterpret_cast<uint32_t *>(dqkv + (size_t)kj0 * ld + cv + c) = pack_bf16(dv[nt][0], dv[nt][1]);
+    }
+    if (kj1 < s) {
+      *reinterpret_cast<uint32_t *>(dqkv + (size_t)kj1 * ld + ck + c) = pack_bf16(dk[nt][2] * scale, dk[nt][3] * scale);
+      *reinterpret_cast<uint32_t *>(dqkv + (size_t)kj1 * ld + cv + c) = pack_bf16(dv[nt][2], dv[nt][3]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------ host
+template <int D>
+static cudaError_t fwd_d(const AttnArgs &a, cudaStream_t st) {
+  constexpr int smem = 5 * AttnSmem<D>::TILE * 2;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((a.s + ABQ - 1) / ABQ, a.heads, a.b);
+  attn_fwd_kernel<D><<<grid, 128, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t bwd_d(const AttnArgs &a, cudaStream_t st) {
+  constexpr int smem_q = 6 * AttnSmem<D>::TILE * 2 + 2 * ABQ * 4;
+  constexpr int smem_k = 6 * AttnSmem<D>::TILE * 2 + 4 * ABQ * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(attn_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_k);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((a.s + ABQ - 1) / ABQ, a.heads, a.b);
+  attn_bwd_dq_kernel<D><<<grid, 128, smem_q, st>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  attn_bwd_dkdv_kernel<D><<<grid, 128, smem_k, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st) {
+  switch (a.d) {
+    case 32: return fwd_d<32>(a, st);
+    case 64: return fwd_d<64>(a, st);
+    case 80: return fwd_d<80>(a, st);
+    case 96: return fwd_d<96>(a, st);
+    case 128: return fwd_d<128>(a, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st) {
+  switch (a.d) {
+    case 32: return bwd_d<32>(a, st);
+    case 64: return bwd_d<64>(a, st);
+    case 80: return bwd_d<80>(a, st);
+    case 96: return bwd_d<96>(a, st);
+    case 128: return bwd_d<128>(a, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+}  // namespace mk

@@ -1,0 +1,397 @@
+// gemm.cu -- persistent warp-specialised tcgen05 GEMM for sm_100a with fused epilogues.
+//
+// Every dense contraction of the sub-pipelined TMP layer runs here (SURVEY §8(a) F2, F4, F6, F7,
+// B1, B2, B3, B5, B7): forward (both operands K-major), dgrad (weight operand MN-major) and
+// wgrad (both operands MN-major, fp32 accumulator preloaded into TMEM so the per-element
+// accumulation chain over tokens is the same whatever the sub-batch split -- bit-identity rule v).
+//
+// CTA = 256 threads, one CTA per SM (smem-bound), grid = min(tiles, SMs), static tile schedule.
+//   warp 0 : TMA producer (one lane)      -> smem ring of STAGES {A 128x64, B BNx64} bf16 tiles
+//   warp 1 : MMA issuer (one lane)        -> tcgen05.mma 128xBNx16 into a TMEM accumulator
+//   warp 2 : TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
+//   warps 4-7 : epilogue (tcgen05.ld 32x32b -> registers -> fused op -> global)
+// Smem tiles use the 128-byte swizzle; the UMMA descriptors describe the same canonical layouts:
+//   K-major : rows of 64 K-elements (128 B), 8-row groups 1024 B apart (SBO)
+//   MN-major: K-rows of 64 MN-elements (128 B), 8-K-row groups 1024 B apart (SBO),
+//             64-wide MN chunks BLOCK_K*128 = 8 KB apart (LBO)
+#include <cuda.h>
+#include <stdio.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace mk {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+struct EpiParams {
+  int M, N, K;
+  int epi;
+  __nv_bfloat16 *out;
+  int ldo;
+  __nv_bfloat16 *out2;
+  int ldo2;
+  const __nv_bfloat16 *bias;
+  const __nv_bfloat16 *aux;
+  int ld_aux;
+  float *out32;
+  int ld32;
+};
+
+template <int EPI>
+MK_DEV void epi_store_chunk(const EpiParams &p, int gm, int gn0, const uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  const bool full = (gn0 + 32 <= p.N);
+  if constexpr (EPI == EPI_ACC_F32) {
+    float *dst = p.out32 + (size_t)gm * p.ld32 + gn0;
+    if (full && (p.ld32 % 4 == 0)) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+      for (int i = 0; i < 32; ++i)
+        if (gn0 + i < p.N) dst[i] = v[i];
+    }
+    return;
+  } else {
+    if constexpr (EPI == EPI_BIAS_BF16 || EPI == EPI_BIAS_GELU) {
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 bv = *reinterpret_cast<const uint4 *>(p.bias + gn0 + i);
+          float2 b0 = unpack_bf16(bv.x), b1 = unpack_bf16(bv.y), b2 = unpack_bf16(bv.z), b3 = unpack_bf16(bv.w);
+          v[i + 0] += b0.x; v[i + 1] += b0.y; v[i + 2] += b1.x; v[i + 3] += b1.y;
+          v[i + 4] += b2.x; v[i + 5] += b2.y; v[i + 6] += b3.x; v[i + 7] += b3.y;
+        }
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (gn0 + i < p.N) v[i] += __bfloat162float(p.bias[gn0 + i]);
+      }
+    }
+    if constexpr (EPI == EPI_GELU_BWD) {
+      const __nv_bfloat16 *z = p.aux + (size_t)gm * p.ld_aux + gn0;
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 zv = *reinterpret_cast<const uint4 *>(z + i);
+          float2 z0 = unpack_bf16(zv.x), z1 = unpack_bf16(zv.y), z2 = unpack_bf16(zv.z), z3 = unpack_bf16(zv.w);
+          v[i + 0] *= gelu_grad_f(z0.x); v[i + 1] *= gelu_grad_f(z0.y);
+          v[i + 2] *= gelu_grad_f(z1.x); v[i + 3] *= gelu_grad_f(z1.y);
+          v[i + 4] *= gelu_grad_f(z2.x); v[i + 5] *= gelu_grad_f(z2.y);
+          v[i + 6] *= gelu_grad_f(z3.x); v[i + 7] *= gelu_grad_f(z3.y);
+        }
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (gn0 + i < p.N) v[i] *= gelu_grad_f(__bfloat162float(z[i]));
+      }
+    }
+    __nv_bfloat16 *dst = p.out + (size_t)gm * p.ldo + gn0;
+    if (full) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 8) {
+        uint4 o;
+        o.x = pack_bf16(v[i + 0], v[i + 1]); o.y = pack_bf16(v[i + 2], v[i + 3]);
+        o.z = pack_bf16(v[i + 4], v[i + 5]); o.w = pack_bf16(v[i + 6], v[i + 7]);
+        *reinterpret_cast<uint4 *>(dst + i) = o;
+      }
+    } else {
+      for (int i = 0; i < 32; ++i)
+        if (gn0 + i < p.N) dst[i] = __float2bfloat16_rn(v[i]);
+    }
+    if constexpr (EPI == EPI_BIAS_GELU) {
+      __nv_bfloat16 *dst2 = p.out2 + (size_t)gm * p.ldo2 + gn0;
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 o;
+          o.x = pack_bf16(gelu_f(v[i + 0]), gelu_f(v[i + 1])); o.y = pack_bf16(gelu_f(v[i + 2]), gelu_f(v[i + 3]));
+          o.z = pack_bf16(gelu_f(v[i + 4]), gelu_f(v[i + 5])); o.w = pack_bf16(gelu_f(v[i + 6]), gelu_f(v[i + 7]));
+          *reinterpret_cast<uint4 *>(dst2 + i) = o;
+        }
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (gn0 + i < p.N) dst2[i] = __float2bfloat16_rn(gelu_f(v[i]));
+      }
+    }
+  }
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(256, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams p) {
+  using C = GemmCfg<BN>;
+  constexpr int S = C::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *smA = smem;
+  uint8_t *smB = smem + S * C::A_BYTES;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S * C::STAGE_BYTES);
+  uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tfree = bars + 2 * S + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+  const int tiles_m = (p.M + BM - 1) / BM;
+  const int tiles_n = (p.N + BN - 1) / BN;
+  const int ntiles = tiles_m * tiles_n;
+  const int nk = (p.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tfree[i], 4);
+    }
+    fence_mbar_init();
+    fence_proxy_async();
+  }
+  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % S;
+        const uint32_t ph = (it / S) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        if (lane == 0) {
+          mbar_expect_tx(&full[s], C::STAGE_BYTES);
+          uint8_t *a = smA + s * C::A_BYTES;
+          uint8_t *b = smB + s * C::B_BYTES;
+          if constexpr (!A_MN) {
+            tma_load_2d(a, &tmA, &full[s], kb * BK, tm * BM);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 8192, &tmA, &full[s], tm * BM + c * 64, kb * BK);
+          }
+          if constexpr (!B_MN) {
+            tma_load_2d(b, &tmB, &full[s], kb * BK, tn * BN);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b + c * 8192, &tmB, &full[s], tn * BN + c * 64, kb * BK);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+    constexpr uint32_t a_lbo = A_MN ? 8192u : 16u, a_sbo = 1024u, a_kstep = A_MN ? 2048u : 32u;
+    constexpr uint32_t b_lbo = B_MN ? 8192u : 16u, b_sbo = 1024u, b_kstep = B_MN ? 2048u : 32u;
+    int it = 0, lt = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      const int buf = lt & 1;
+      mbar_wait(&tfree[buf], (lt >> 1) & 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + buf * BN;
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % S;
+        mbar_wait(&full[s], (it / S) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(smA + s * C::A_BYTES);
+          const uint32_t b0 = smem_u32(smB + s * C::B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = sdesc_sw128(a0 + kk * a_kstep, a_lbo, a_sbo);
+            const uint64_t bd = sdesc_sw128(b0 + kk * b_kstep, b_lbo, b_sbo);
+            const uint32_t acc = (EPI == EPI_ACC_F32 || kb > 0 || kk > 0) ? 1u : 0u;
+            tc_mma_f16(d_tmem, ad, bd, idesc, acc);
+          }
+          tc_commit(&empty[s]);
+          if (kb == nk - 1) tc_commit(&tfull[buf]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const uint32_t row_base = tmem_base + ((uint32_t)(q * 32) << 16);
+    auto preload = [&](int tile, int buf) {
+      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      const int gm = tm * BM + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int gn0 = tn * BN + c * 32;
+        uint32_t r[32];
+        const float *src = p.out32 + (size_t)gm * p.ld32 + gn0;
+        if (gm < p.M && gn0 + 32 <= p.N && (p.ld32 % 4 == 0)) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            float4 f = *reinterpret_cast<const float4 *>(src + i);
+            r[i] = __float_as_uint(f.x); r[i + 1] = __float_as_uint(f.y);
+            r[i + 2] = __float_as_uint(f.z); r[i + 3] = __float_as_uint(f.w);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = (gm < p.M && gn0 + i < p.N) ? __float_as_uint(src[i]) : 0u;
+        }
+        tmem_st32(row_base + buf * BN + c * 32, r);
+      }
+      tmem_st_wait();
+    };
+    // initial release of both accumulator buffers (after preloading C for ACC mode)
+#pragma unroll 1
+    for (int bb = 0; bb < 2; ++bb) {
+      const int tile = blockIdx.x + bb * gridDim.x;
+      if (EPI == EPI_ACC_F32 && tile < ntiles) preload(tile, bb);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tfree[bb]);
+    }
+    int lt = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      const int buf = lt & 1;
+      mbar_wait(&tfull[buf], (lt >> 1) & 1);
+      tc_fence_after();
+      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      const int gm = tm * BM + q * 32 + lane;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int gn0 = tn * BN + c * 32;
+        if (gn0 >= p.N) break;  // warp-uniform
+        uint32_t r[32];
+        tmem_ld32(row_base + buf * BN + c * 32, r);
+        tmem_ld_wait();
+        if (gm < p.M) epi_store_chunk<EPI>(p, gm, gn0, r);
+      }
+      tc_fence_before();
+      const int next = tile + 2 * gridDim.x;
+      if (EPI == EPI_ACC_F32 && next < ntiles) {
+        preload(next, buf);
+        tc_fence_before();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tfree[buf]);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor [rows, cols] (cols contiguous, row stride ld elements), box {64 cols, box_rows}.
+static bool make_map(CUtensorMap *m, const void *ptr, int rows, int cols, int ld, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64u, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int gemm_num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int BN, bool A_MN, bool B_MN, int EPI>
+static cudaError_t launch(const GemmArgs &a, const CUtensorMap &ma, const CUtensorMap &mb, const EpiParams &p,
+                          cudaStream_t st) {
+  using C = GemmCfg<BN>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int ntiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
+  int grid = a.max_ctas > 0 ? a.max_ctas : gemm_num_sms();
+  if (grid > ntiles) grid = ntiles;
+  kern<<<grid, 256, C::SMEM, st>>>(ma, mb, p);
+  return cudaGetLastError();
+}
+
+template <int BN>
+static cudaError_t dispatch(const GemmArgs &a, const CUtensorMap &ma, const CUtensorMap &mb, const EpiParams &p,
+                           cudaStream_t st) {
+  if (!a.a_mn && !a.b_mn) {
+    switch (a.epi) {
+      case EPI_STORE_BF16: return launch<BN, false, false, EPI_STORE_BF16>(a, ma, mb, p, st);
+      case EPI_BIAS_BF16: return launch<BN, false, false, EPI_BIAS_BF16>(a, ma, mb, p, st);
+      case EPI_BIAS_GELU: return launch<BN, false, false, EPI_BIAS_GELU>(a, ma, mb, p, st);
+    }
+  } else if (!a.a_mn && a.b_mn) {
+    switch (a.epi) {
+      case EPI_STORE_BF16: return launch<BN, false, true, EPI_STORE_BF16>(a, ma, mb, p, st);
+      case EPI_GELU_BWD: return launch<BN, false, true, EPI_GELU_BWD>(a, ma, mb, p, st);
+    }
+  } else if (a.a_mn && a.b_mn) {
+    if (a.epi == EPI_ACC_F32) return launch<BN, true, true, EPI_ACC_F32>(a, ma, mb, p, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
+  if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaErrorInvalidValue;
+  const int BN = (a.N > 128) ? 256 : 128;
+  CUtensorMap ma, mb;
+  // A: K-major stored [M, K]; MN-major stored [K, M]
+  bool ok = a.a_mn ? make_map(&ma, a.A, a.K, a.M, a.lda, BK) : make_map(&ma, a.A, a.M, a.K, a.lda, BM);
+  ok = ok && (a.b_mn ? make_map(&mb, a.B, a.K, a.N, a.ldb, BK) : make_map(&mb, a.B, a.N, a.K, a.ldb, BN));
+  if (!ok) return cudaErrorInvalidValue;
+  EpiParams p;
+  p.M = a.M; p.N = a.N; p.K = a.K; p.epi = a.epi;
+  p.out = (__nv_bfloat16 *)a.out; p.ldo = a.ldo;
+  p.out2 = (__nv_bfloat16 *)a.out2; p.ldo2 = a.ldo2;
+  p.bias = (const __nv_bfloat16 *)a.bias;
+  p.aux = (const __nv_bfloat16 *)a.aux; p.ld_aux = a.ld_aux;
+  p.out32 = a.out32; p.ld32 = a.ld32;
+  return BN == 256 ? dispatch<256>(a, ma, mb, p, st) : dispatch<128>(a, ma, mb, p, st);
+}
+
+}  // namespace mk

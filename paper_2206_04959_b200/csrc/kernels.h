@@ -1,0 +1,122 @@
+// kernels.h -- host-side launch interface of the sm_100a kernels (internal, not part of the ABI).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace mk {
+
+// ---------------------------------------------------------------- GEMM (gemm.cu)
+// C[M,N] = A[M,K] * B[N,K]^T on tcgen05 (bf16 in, fp32 accumulate in TMEM).
+// Operand storage:
+//   a_mn = false: A stored [M rows, K cols] (K contiguous), row stride lda elements
+//   a_mn = true : A stored [K rows, M cols] (M contiguous), row stride lda   (A = stored^T)
+//   b_mn = false: B stored [N rows, K cols] (K contiguous), row stride ldb
+//   b_mn = true : B stored [K rows, N cols] (N contiguous), row stride ldb   (B = stored^T)
+// Reduction order per output element is fixed: K walked in 64-wide blocks in increasing order,
+// 16-wide MMA steps inside; it never depends on M (bit-identity across sub-batch counts).
+enum Epi : int {
+  EPI_STORE_BF16 = 0,  // out = bf16(acc)
+  EPI_BIAS_BF16 = 1,   // out = bf16(acc + bias[n])
+  EPI_BIAS_GELU = 2,   // z = acc + bias[n]; out = bf16(z); out2 = bf16(gelu(z))
+  EPI_GELU_BWD = 3,    // out = bf16(acc * gelu'(aux[m,n]))   (aux = saved z, bf16)
+  EPI_ACC_F32 = 4      // out32[m,n] (fp32) is loaded into TMEM first; out32 = acc after the K loop
+};
+
+struct GemmArgs {
+  const void *A;
+  const void *B;
+  int M, N, K;
+  int lda, ldb;
+  bool a_mn, b_mn;
+  int epi;
+  void *out;         // bf16 [M, ldo]
+  int ldo;
+  void *out2;        // bf16 [M, ldo2] (EPI_BIAS_GELU)
+  int ldo2;
+  const void *bias;  // bf16 [N]
+  const void *aux;   // bf16 [M, ld_aux] (EPI_GELU_BWD)
+  int ld_aux;
+  float *out32;      // fp32 [M, ld32] (EPI_ACC_F32)
+  int ld32;
+  int max_ctas;      // persistent grid cap (0 = all SMs)
+};
+cudaError_t gemm(const GemmArgs &a, cudaStream_t st);
+int gemm_num_sms();
+
+// ---------------------------------------------------------------- attention (attention.cu)
+// Causal flash attention over packed qkv [tokens, 3*hr] (q | k | v column blocks, head e at
+// columns e*d..e*d+d-1 of each block), b samples of s tokens, H_r local heads of dim d.
+struct AttnArgs {
+  const void *qkv;   // bf16 [b*s, 3*hr]
+  void *ctx;         // bf16 [b*s, hr]          (fwd out / bwd in as O)
+  float *lse;        // [b, H_r, s] base-2 log-sum-exp of scaled scores (fwd out / bwd in)
+  const void *dctx;  // bf16 [b*s, hr]          (bwd in)
+  void *dqkv;        // bf16 [b*s, 3*hr]        (bwd out)
+  float *delta;      // [b, H_r, s] rowsum(dO*O) workspace (bwd)
+  int b, s, heads, d;
+};
+cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st);
+cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st);  // 2 launches: dQ (+delta), then dK/dV
+
+// ---------------------------------------------------------------- LN / all-reduce / reductions (ln_ar.cu)
+constexpr int MAX_T = 8;
+constexpr int MAX_AR_CTAS = 256;
+
+// Peer handshake for one all-reduce launch.  flags_local: this rank's flag array; flags_peer[r]:
+// rank r's flag array mapped into this process (flags_peer[rank] == flags_local).  Layout per rank:
+// ready[MAX_AR_CTAS][MAX_T] then done[MAX_AR_CTAS][MAX_T] (uint32 epochs).
+struct PeerSync {
+  int T, rank;
+  bool enabled;               // false: fake peers on one device / T == 1 (no handshake)
+  uint32_t epoch;
+  uint32_t *flags_local;
+  uint32_t *flags_peer[MAX_T];
+  int *err_word;              // device word set to 1 on watchdog timeout
+  uint64_t timeout_ns;
+};
+
+struct ArFwdArgs {
+  const __nv_bfloat16 *partial[MAX_T];  // rank-ordered partial sums, rows [0, m) of this sub-batch
+  int T;                                // number of partials summed (1 with NO_COMM)
+  int m, h;
+  const __nv_bfloat16 *resid;           // [m, h]
+  const __nv_bfloat16 *bias;            // [h]
+  __nv_bfloat16 *out;                   // [m, h]   x1 (AR#1) or y (AR#2)
+  // LayerNorm of the stored (bf16) out, AR#1 only (u2 = LN2(x1))
+  bool do_ln;
+  const __nv_bfloat16 *gamma, *beta;
+  __nv_bfloat16 *ln_out;
+  float *mean, *rstd;
+  float eps;
+  int ctas;
+};
+cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st);
+
+struct ArBwdArgs {
+  const __nv_bfloat16 *partial[MAX_T];
+  int T;
+  int m, h;
+  const __nv_bfloat16 *x_ln;    // LN input (x1 for LN2, x for LN1)      [m, h]
+  const float *mean, *rstd;     // saved LN stats                         [m]
+  const __nv_bfloat16 *gamma;   // [h]
+  const __nv_bfloat16 *dres;    // residual-path gradient (dy or dx1)     [m, h]
+  __nv_bfloat16 *dx;            // out: dres + LN^T(sum partials)          [m, h]
+  float *part_dg, *part_db;     // out: per-group column partials [m/G, h]
+  int G;                        // rows per group (16 if h <= 3072 else 8)
+  int ctas;
+};
+cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st);
+int ar_bwd_group_rows(int h);
+
+// LayerNorm forward of x (bf16 [m,h]) -> u (bf16), mean/rstd (fp32)
+cudaError_t ln_fwd(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bfloat16 *b, __nv_bfloat16 *u,
+                   float *mean, float *rstd, int m, int h, float eps, cudaStream_t st);
+
+// Fixed-order column sums: part[grp][c] = sum_{i<16} X[16 grp + i][c]   (bf16 X, row stride ld)
+cudaError_t colsum_partial(const __nv_bfloat16 *X, int ld, int m, int n, float *part, cudaStream_t st);
+// g[c] += part[0][c]; g[c] += part[1][c]; ... (sequential over groups: bit-identical across splits)
+cudaError_t chain_add(const float *part, int groups, int n, float *g, cudaStream_t st);
+
+}  // namespace mk

@@ -1,0 +1,359 @@
+// ln_ar.cu -- LayerNorm, the four TMP all-reduces fused with their replicated epilogues, and the
+// fixed-order token reductions for bias / LayerNorm gradients.
+//
+// All-reduce (P:107 Megatron TMP; P:558 two in FP, two in BP).
+// Each rank's row-parallel GEMM writes its bf16 partial [m, h] into its own peer-visible slot
+// (CUDA-IPC exported).  The all-reduce kernel on every rank reads the T partials of its rows
+// straight from the peers' HBM over NVLink (one-shot), sums them in fp32 in rank order 0..T-1
+// (reading R10), and applies the replicated work in the same pass:
+//   AR#1: x1 = x + sum_r P1_r + b_o ; u2 = LN2(bf16(x1))          (forward, attention block)
+//   AR#2: y  = x1 + sum_r P2_r + b_2                               (forward, FFN block)
+//   AR#3: dx1 = dy  + LN2^T(sum_r dU2_r), dgamma2/dbeta2 partials  (backward, FFN block)
+//   AR#4: dx  = dx1 + LN1^T(sum_r dU1_r), dgamma1/dbeta1 partials  (backward, attention block)
+// Every rank computes every row, so replicated outputs are bit-identical across ranks.
+//
+// Peer handshake (per CTA index c, epoch e = per-handle launch counter, identical on all ranks):
+//   start: write ready[c][my_rank] = e into every peer's flag array (st.release.sys), then wait
+//          until ready[c][r] >= e for all peers r (ld.acquire.sys).  The peer's partial was
+//          completed by its GEMM before its all-reduce kernel started (stream order).
+//   end:   after the CTA's reads, write done[c][my_rank] = e to every peer and wait for all
+//          done[c][r] >= e.  When every CTA of a rank has exited, all peers have finished reading
+//          that rank's slot, so the next GEMM may overwrite it (the caller orders that by event).
+// A watchdog (globaltimer) bounds every wait; on expiry the kernel sets *err_word and skips work.
+#include <math.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace mk {
+
+MK_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+MK_DEV void load8(const __nv_bfloat16 *p, float (&v)[8]) {
+  uint4 u = *reinterpret_cast<const uint4 *>(p);
+  float2 a = unpack_bf16(u.x), b = unpack_bf16(u.y), c = unpack_bf16(u.z), d = unpack_bf16(u.w);
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y; v[6] = d.x; v[7] = d.y;
+}
+MK_DEV void add8(const __nv_bfloat16 *p, float (&v)[8]) {
+  float t[8];
+  load8(p, t);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] += t[i];
+}
+MK_DEV void store8(__nv_bfloat16 *p, const float (&v)[8]) {
+  uint4 u;
+  u.x = pack_bf16(v[0], v[1]); u.y = pack_bf16(v[2], v[3]); u.z = pack_bf16(v[4], v[5]); u.w = pack_bf16(v[6], v[7]);
+  *reinterpret_cast<uint4 *>(p) = u;
+}
+
+// Thread 0 only.  kind 0 = ready, 1 = done.  Returns false if the watchdog fired.
+MK_DEV bool handshake(const PeerSync &ps, int kind, int cta) {
+  if (!ps.enabled) return true;
+  const size_t base = (size_t)kind * MAX_AR_CTAS * MAX_T + (size_t)cta * MAX_T;
+#pragma unroll
+  for (int r = 0; r < MAX_T; ++r)
+    if (r < ps.T && r != ps.rank) st_release_sys(ps.flags_peer[r] + base + ps.rank, ps.epoch);
+  const uint64_t t0 = globaltimer();
+  for (int r = 0; r < ps.T; ++r) {
+    if (r == ps.rank) continue;
+    while ((int)(ld_acquire_sys(ps.flags_local + base + r) - ps.epoch) < 0) {
+      if (globaltimer() - t0 > ps.timeout_ns) {
+        atomicExch(ps.err_word, 1);
+        return false;
+      }
+    }
+  }
+  return true;
+}
+
+// ------------------------------------------------------------------------------ forward all-reduce
+__global__ void __launch_bounds__(256) ar_fwd_kernel(ArFwdArgs a, PeerSync ps) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) ok = handshake(ps, 0, blockIdx.x);
+  __syncthreads();
+  if (ok) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
+    const int h = a.h, nc = h >> 3;
+    for (int row = blockIdx.x * nw + warp; row < a.m; row += gridDim.x * nw) {
+      const size_t ro = (size_t)row * h;
+      float sum = 0.f;
+      for (int c = lane; c < nc; c += 32) {
+        float v[8];
+        load8(a.partial[0] + ro + c * 8, v);
+#pragma unroll
+        for (int r = 1; r < MAX_T; ++r)
+          if (r < a.T) add8(a.partial[r] + ro + c * 8, v);  // rank order (R10)
+        add8(a.bias + c * 8, v);
+        add8(a.resid + ro + c * 8, v);
+        store8(a.out + ro + c * 8, v);
+        if (a.do_ln) {
+          float q[8];
+          load8(a.out + ro + c * 8, q);  // LN2 reads the stored bf16 x1 (reading R12)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) sum += q[i];
+        }
+      }
+      if (!a.do_ln) continue;
+      const float mean = warp_sum(sum) / h;
+      float var = 0.f;
+      for (int c = lane; c < nc; c += 32) {
+        float q[8];
+        load8(a.out + ro + c * 8, q);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) var += (q[i] - mean) * (q[i] - mean);
+      }
+      const float rstd = rsqrtf(warp_sum(var) / h + a.eps);
+      for (int c = lane; c < nc; c += 32) {
+        float q[8], gm[8], bt[8];
+        load8(a.out + ro + c * 8, q);
+        load8(a.gamma + c * 8, gm);
+        load8(a.beta + c * 8, bt);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) q[i] = (q[i] - mean) * rstd * gm[i] + bt[i];
+        store8(a.ln_out + ro + c * 8, q);
+      }
+      if (lane == 0) {
+        a.mean[row] = mean;
+        a.rstd[row] = rstd;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && ok) handshake(ps, 1, blockIdx.x);
+}
+
+// ------------------------------------------------------------------------------ backward all-reduce
+template <int G>
+__global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
+  extern __shared__ __align__(16) float du_s[];  // [G][h] fp32 sum of the partials
+  __shared__ float s_mean[G], s_rstd[G];
+  __shared__ int ok;
+  if (threadIdx.x == 0) ok = handshake(ps, 0, blockIdx.x);
+  __syncthreads();
+  if (ok) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int h = a.h, nc = h >> 3;
+    const float inv_h = 1.f / h;
+    const int ngroups = a.m / G;
+    for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+      // phase 1: warp per row -- all-reduce, LN backward, residual
+      for (int ri = warp; ri < G; ri += 8) {
+        const int row = grp * G + ri;
+        const size_t ro = (size_t)row * h;
+        const float mean = a.mean[row], rstd = a.rstd[row];
+        float acc1 = 0.f, acc2 = 0.f;
+        for (int c = lane; c < nc; c += 32) {
+          float du[8], x[8], gm[8];
+          load8(a.partial[0] + ro + c * 8, du);
+#pragma unroll
+          for (int r = 1; r < MAX_T; ++r)
+            if (r < a.T) add8(a.partial[r] + ro + c * 8, du);
+          float4 *ds = reinterpret_cast<float4 *>(du_s + ri * h + c * 8);
+          ds[0] = make_float4(du[0], du[1], du[2], du[3]);
+          ds[1] = make_float4(du[4], du[5], du[6], du[7]);
+          load8(a.x_ln + ro + c * 8, x);
+          load8(a.gamma + c * 8, gm);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float xh = (x[i] - mean) * rstd, dxh = du[i] * gm[i];
+            acc1 += dxh;
+            acc2 += dxh * xh;
+          }
+        }
+        const float m1 = warp_sum(acc1) * inv_h, m2 = warp_sum(acc2) * inv_h;
+        for (int c = lane; c < nc; c += 32) {
+          float x[8], gm[8], dr[8], o[8];
+          const float4 *ds = reinterpret_cast<const float4 *>(du_s + ri * h + c * 8);
+          const float4 d0 = ds[0], d1 = ds[1];
+          const float du[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+          load8(a.x_ln + ro + c * 8, x);
+          load8(a.gamma + c * 8, gm);
+          load8(a.dres + ro + c * 8, dr);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float xh = (x[i] - mean) * rstd, dxh = du[i] * gm[i];
+            o[i] = dr[i] + rstd * (dxh - m1 - xh * m2);
+          }
+          store8(a.dx + ro + c * 8, o);
+        }
+        if (lane == 0) {
+          s_mean[ri] = mean;
+          s_rstd[ri] = rstd;
+        }
+      }
+      __syncthreads();
+      // phase 2: fixed-order column partials over the G rows (dbeta = sum du, dgamma = sum du*xhat)
+      for (int cc = threadIdx.x; cc < nc; cc += blockDim.x) {
+        float sg[8], sb[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sg[i] = sb[i] = 0.f;
+        for (int i = 0; i < G; ++i) {
+          const size_t ro = (size_t)(grp * G + i) * h;
+          float x[8];
+          load8(a.x_ln + ro + cc * 8, x);
+          const float4 *ds = reinterpret_cast<const float4 *>(du_s + i * h + cc * 8);
+          const float4 d0 = ds[0], d1 = ds[1];
+          const float du[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            sb[k] += du[k];
+            sg[k] += du[k] * ((x[k] - s_mean[i]) * s_rstd[i]);
+          }
+        }
+        float4 *pg = reinterpret_cast<float4 *>(a.part_dg + (size_t)grp * h + cc * 8);
+        float4 *pb = reinterpret_cast<float4 *>(a.part_db + (size_t)grp * h + cc * 8);
+        pg[0] = make_float4(sg[0], sg[1], sg[2], sg[3]);
+        pg[1] = make_float4(sg[4], sg[5], sg[6], sg[7]);
+        pb[0] = make_float4(sb[0], sb[1], sb[2], sb[3]);
+        pb[1] = make_float4(sb[4], sb[5], sb[6], sb[7]);
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && ok) handshake(ps, 1, blockIdx.x);
+}
+
+// ------------------------------------------------------------------------------ LayerNorm forward
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16 *x, const __nv_bfloat16 *gamma,
+                                                     const __nv_bfloat16 *beta, __nv_bfloat16 *u, float *mean_out,
+                                                     float *rstd_out, int m, int h, float eps) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int row = blockIdx.x * nw + warp;
+  if (row >= m) return;
+  const int nc = h >> 3;
+  const size_t ro = (size_t)row * h;
+  float sum = 0.f;
+  for (int c = lane; c < nc; c += 32) {
+    float q[8];
+    load8(x + ro + c * 8, q);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sum += q[i];
+  }
+  const float mean = warp_sum(sum) / h;
+  float var = 0.f;
+  for (int c = lane; c < nc; c += 32) {
+    float q[8];
+    load8(x + ro + c * 8, q);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) var += (q[i] - mean) * (q[i] - mean);
+  }
+  const float rstd = rsqrtf(warp_sum(var) / h + eps);
+  for (int c = lane; c < nc; c += 32) {
+    float q[8], gm[8], bt[8];
+    load8(x + ro + c * 8, q);
+    load8(gamma + c * 8, gm);
+    load8(beta + c * 8, bt);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) q[i] = (q[i] - mean) * rstd * gm[i] + bt[i];
+    store8(u + ro + c * 8, q);
+  }
+  if (lane == 0) {
+    mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+// ------------------------------------------------------------------------------ token reductions
+// part[grp][c] = X[16 grp][c] + X[16 grp + 1][c] + ... + X[16 grp + 15][c]   (sequential, fp32)
+__global__ void colsum_partial_kernel(const __nv_bfloat16 *X, int ld, int m, int n, float *part) {
+  const int cc = blockIdx.x * blockDim.x + threadIdx.x;
+  const int grp = blockIdx.y;
+  if (cc * 8 >= n) return;
+  float s[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s[k] = 0.f;
+  for (int i = 0; i < 16; ++i) {
+    float v[8];
+    load8(X + (size_t)(grp * 16 + i) * ld + cc * 8, v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s[k] += v[k];
+  }
+  float4 *p = reinterpret_cast<float4 *>(part + (size_t)grp * n + cc * 8);
+  p[0] = make_float4(s[0], s[1], s[2], s[3]);
+  p[1] = make_float4(s[4], s[5], s[6], s[7]);
+}
+
+// g[c] = (((g[c] + part[0][c]) + part[1][c]) + ...)  -- the same chain whatever the sub-batch split
+__global__ void chain_add_kernel(const float *part, int groups, int n, float *g) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  float acc = g[c];
+  int i = 0;
+  for (; i + 8 <= groups; i += 8) {
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = part[(size_t)(i + k) * n + c];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc += v[k];
+  }
+  for (; i < groups; ++i) acc += part[(size_t)i * n + c];
+  g[c] = acc;
+}
+
+// ------------------------------------------------------------------------------ host
+static int clamp_ctas(int want, int work) {
+  if (want <= 0) want = 64;
+  if (want > MAX_AR_CTAS) want = MAX_AR_CTAS;
+  if (want > work) want = work;
+  return want < 1 ? 1 : want;
+}
+
+cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
+  // handshake CTA count must be identical on all ranks: it depends only on (m, ctas)
+  const int grid = clamp_ctas(a.ctas, (a.m + 7) / 8);
+  ar_fwd_kernel<<<grid, 256, 0, st>>>(a, ps);
+  return cudaGetLastError();
+}
+
+int ar_bwd_group_rows(int h) { return h <= 3072 ? 16 : 8; }
+
+cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
+  const int grid = clamp_ctas(a.ctas, a.m / a.G);
+  const size_t smem = (size_t)a.G * a.h * sizeof(float);
+  if (a.G == 16) {
+    static size_t attr16 = 0;
+    if (smem > attr16) {
+      cudaError_t e = cudaFuncSetAttribute(ar_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr16 = smem;
+    }
+    ar_bwd_kernel<16><<<grid, 256, smem, st>>>(a, ps);
+  } else if (a.G == 8) {
+    static size_t attr8 = 0;
+    if (smem > attr8) {
+      cudaError_t e = cudaFuncSetAttribute(ar_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      attr8 = smem;
+    }
+    ar_bwd_kernel<8><<<grid, 256, smem, st>>>(a, ps);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t ln_fwd(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bfloat16 *b, __nv_bfloat16 *u,
+                   float *mean, float *rstd, int m, int h, float eps, cudaStream_t st) {
+  ln_fwd_kernel<<<(m + 7) / 8, 256, 0, st>>>(x, g, b, u, mean, rstd, m, h, eps);
+  return cudaGetLastError();
+}
+
+cudaError_t colsum_partial(const __nv_bfloat16 *X, int ld, int m, int n, float *part, cudaStream_t st) {
+  if (m % 16 || n % 8) return cudaErrorInvalidValue;
+  dim3 grid((n / 8 + 127) / 128, m / 16);
+  colsum_partial_kernel<<<grid, 128, 0, st>>>(X, ld, m, n, part);
+  return cudaGetLastError();
+}
+
+cudaError_t chain_add(const float *part, int groups, int n, float *g, cudaStream_t st) {
+  chain_add_kernel<<<(n + 127) / 128, 128, 0, st>>>(part, groups, n, g);
+  return cudaGetLastError();
+}
+
+}  // namespace mk

@@ -1,0 +1,58 @@
+"""Helpers for layer-level GPU parity tests: run the C-ABI layer on seeded inputs and compare with
+the fp64 oracle.  Test infrastructure only."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from paper_2206_04959_b200 import PARAM_NAMES, TmpLayer, shard_weights, zero_grads_like
+
+TOL_BF16 = 2e-2  # north_star: relative Frobenius error <= 2e-2 for bf16 with fp32 accumulation
+
+
+def rel_err(gpu, ref) -> float:
+    g = np.asarray(gpu, dtype=np.float64)
+    r = np.asarray(ref, dtype=np.float64)
+    return float(np.linalg.norm(g - r) / max(np.linalg.norm(r), 1e-300))
+
+
+def run_gpu_layer(cfg, params, x, dy, T=1, rank=0, n_sub=None, group=None, reps=1, flags=0, device=None):
+    """Forward + backward through merak_tmp_layer_fwd/bwd.  Returns dict of torch tensors on device:
+    y, dx and the rank's fp32 gradient shards."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    n = cfg.n_sub if n_sub is None else n_sub
+    layer = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, tmp_degree=T, tmp_rank=rank, n_sub=n,
+                     device=dev.index, group=group)
+    w = shard_weights(params, cfg.heads, T, rank, dev)
+    M, h = cfg.tokens, cfg.hidden
+    X = torch.as_tensor(np.asarray(x).reshape(M, h)).to(dev, torch.bfloat16)
+    DY = torch.as_tensor(np.asarray(dy).reshape(M, h)).to(dev, torch.bfloat16)
+    Y = torch.empty_like(X)
+    DX = torch.empty_like(X)
+    saved = layer.new_saved()
+    out = None
+    for _ in range(reps):
+        grads = zero_grads_like(w)
+        layer.forward(w, X, Y, saved, flags=flags)
+        layer.backward(w, X, saved, DY, DX, grads, flags=flags)
+        torch.cuda.synchronize()
+        out = {"y": Y.clone(), "dx": DX.clone(), **{k: grads[k].clone() for k in PARAM_NAMES}}
+    layer.close()
+    return out
+
+
+def oracle_rank_slices(grads_global, cfg, T, rank):
+    """Slice the oracle's global fp64 gradients to rank `rank`'s shard using the oracle's own partition."""
+    from oracle import shard_params
+    return shard_params(grads_global, cfg.heads, T, rank)
+
+
+def compare_to_oracle(out, y_ref, dx_ref, grads_ref_rank, cfg, tol=TOL_BF16):
+    """Relative Frobenius error per tensor; b_qkv compared as one packed tensor (its k-slice is 0)."""
+    M, h = cfg.tokens, cfg.hidden
+    errs = {"y": rel_err(out["y"].float().cpu().numpy(), np.asarray(y_ref).reshape(M, h)),
+            "dx": rel_err(out["dx"].float().cpu().numpy(), np.asarray(dx_ref).reshape(M, h))}
+    for k in PARAM_NAMES:
+        errs[k] = rel_err(out[k].cpu().numpy(), grads_ref_rank[k])
+    bad = {k: v for k, v in errs.items() if not (v <= tol)}
+    return errs, bad
