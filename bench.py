@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark of the sub-pipelined TMP transformer layer (Merak §6.3) on B200.
+
+python bench.py --gpus N --steps K --warmup W            (N > 1: launched by torchrun, one rank per GPU)
+python bench.py --impl reference ...                      (the fp64 CPU oracle as the reference arm)
+
+One step = one layer forward + backward (every SURVEY §8(a) row: LN1, QKV, attention, proj, AR#1 +
+LN2, fc1 + GeLU, fc2, AR#2, and the backward mirror with AR#3/AR#4 and all weight gradients) over
+one microbatch of the BASELINE.json configs[1] workload (GPT-1.5B-shaped layer: h=1600, H=25,
+s=1024, B=8) with the TMP degree T = N (rank r holds shard r; strong scaling: the layer is fixed).
+Inputs are synthetic (synth/), resident in HBM; L2 is flushed (256 MiB write) between timed steps,
+outside the timed events.  value = whole-job algorithmic TFLOP/s of the layer ((72Bsh^2 +
+6Bhs(s+1)) FLOPs per step / device time, max over ranks).  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TMP layer fwd+bwd TFLOP/s/GPU at TMP=1/2/4/8; exposed all-reduce ms/layer"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="merak", choices=["merak", "reference"])
+    ap.add_argument("--config", default="gpt1.5b")
+    ap.add_argument("--n-sub", type=int, default=None)
+    ap.add_argument("--comm-ctas", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the n=1 / no-comm / e2e passes")
+    return ap.parse_args()
+
+
+def layer_flops(cfg):
+    B, s, h = cfg.microbatch, cfg.seq_len, cfg.hidden
+    f = cfg.ffn
+    return 6.0 * B * s * (4 * h * h + 2 * f * h) + 6.0 * B * h * s * (s + 1)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), "measured"
+    return 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.p:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        rows = [r.split(", ") for r in (self.out or "").strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in rows]
+        reasons = set()
+        for r in rows:
+            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": sorted(reasons),
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+
+
+def cpu_oracle_sample(cfg, target_s=12.0):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload: b samples of the same
+    layer shape (fwd+bwd), growing b until ~target_s of CPU work.  Returns the cpu_baseline dict."""
+    import numpy as np  # noqa: F401
+
+    from oracle import layer_flops as oflops, layer_fwd_bwd
+    from synth import make_all
+    b = 1
+    while True:
+        sub = cfg.with_(microbatch=b)
+        params, x, dy = make_all(sub)
+        t0 = time.perf_counter()
+        layer_fwd_bwd(params, x, dy, sub.heads)
+        dt = time.perf_counter() - t0
+        if dt >= target_s / 2 or b >= cfg.microbatch:
+            break
+        b = min(cfg.microbatch, b * 2)
+    fl = oflops(b, sub.seq_len, sub.hidden, sub.heads)
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [{"api": i.get("internal_api"), "threads": i.get("num_threads")} for i in threadpool_info()]
+        threads = max([i["threads"] or 1 for i in blas] or [1])
+    except Exception:
+        blas, threads = [], os.cpu_count()
+    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+            "sample": f"{b} of {cfg.microbatch} samples of the {cfg.name} layer fwd+bwd in fp64 (numpy), "
+                      f"{dt:.2f} s, {fl / 1e9:.1f} GFLOP", "seconds": dt, "blas": blas,
+            "host_cores_visible": len(os.sched_getaffinity(0))}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU oracle as it stands, each step a bounded sample (1 sample of the
+    workload's layer).  Rank 0 only; other ranks exit without work."""
+    if rank != 0:
+        return
+    from oracle import layer_flops as oflops, layer_fwd_bwd
+    from synth import make_all
+    sub = cfg.with_(microbatch=1)
+    params, x, dy = make_all(sub)
+    for _ in range(args.warmup):
+        layer_fwd_bwd(params, x, dy, sub.heads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        layer_fwd_bwd(params, x, dy, sub.heads)
+    dt = (time.perf_counter() - t0) / args.steps
+    fl = oflops(1, sub.seq_len, sub.hidden, sub.heads)
+    v = fl / dt / 1e12
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads") or 1 for i in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name} layer fwd+bwd, bounded sample: 1 of {cfg.microbatch} samples "
+                                   f"per step (h={cfg.hidden}, H={cfg.heads}, s={cfg.seq_len})"},
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+                             "sample": f"1 of {cfg.microbatch} samples per step"},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    from synth import CONFIGS
+    cfg = CONFIGS[args.config]
+    T = world
+    n_sub = args.n_sub or cfg.n_sub
+    cfg = cfg.with_(tmp_degree=T, n_sub=n_sub)
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2206_04959_b200 import FLAG_NO_COMM, TmpLayer, shard_weights, zero_grads_like
+    from synth import make_all
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    params, x, dy = make_all(cfg)
+    w = shard_weights(params, cfg.heads, T, rank, dev)
+    M, h = cfg.tokens, cfg.hidden
+    X = torch.as_tensor(x.reshape(M, h)).to(dev, torch.bfloat16)
+    DY = torch.as_tensor(dy.reshape(M, h)).to(dev, torch.bfloat16)
+    Y, DX = torch.empty_like(X), torch.empty_like(X)
+    grads = zero_grads_like(w)
+    layer = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, tmp_degree=T, tmp_rank=rank, n_sub=n_sub,
+                     comm_ctas=args.comm_ctas, device=local, group=group)
+    saved = layer.new_saved()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def step(flags=0):
+        layer.forward(w, X, Y, saved, flags=flags)
+        layer.backward(w, X, saved, DY, DX, grads, flags=flags)
+
+    def timed(nsteps, flags=0, prof=False):
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(nsteps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(nsteps)]
+        if prof:
+            layer.set_profiling(True)
+        l0 = layer.launch_count()
+        barrier()
+        for i in range(nsteps):
+            flush.zero_()
+            starts[i].record(stream)
+            step(flags)
+            ends[i].record(stream)
+        barrier()
+        launches = layer.launch_count() - l0
+        ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+        prof_d = layer.get_profile() if prof else None
+        if prof:
+            layer.set_profiling(False)
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item() / nsteps, launches, prof_d
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    with ClockSampler(local) as clk:
+        ms_step, launches, prof = timed(args.steps, prof=True)
+    clocks = clk.summary()
+    fl = layer_flops(cfg)
+    value = fl / (ms_step * 1e-3) / 1e12
+
+    extras = {}
+    if not args.no_extras:
+        # exposed communication: same kernels with every all-reduce reading only the local partial
+        if T > 1:
+            ms_nc, _, _ = timed(max(3, args.steps // 2), flags=FLAG_NO_COMM)
+            extras["exposed_allreduce_ms_per_layer"] = ms_step - ms_nc
+            extras["no_comm_ms_per_step"] = ms_nc
+        else:
+            extras["exposed_allreduce_ms_per_layer"] = 0.0
+        # n = 1 (Megatron-style, no sub-pipelining) with the same kernels: fig:ablation_pipetp analog
+        if n_sub != 1:
+            layer.set_subbatches(1)
+            for _ in range(2):
+                step()
+            ms_n1, _, _ = timed(max(3, args.steps // 2))
+            layer.set_subbatches(n_sub)
+            extras["n1_ms_per_step"] = ms_n1
+            extras["subpipelining_speedup_vs_n1"] = ms_n1 / ms_step
+        # e2e through the public API with host buffers: H2D x, dy (pinned) -> fwd -> bwd -> D2H y, dx
+        hx = X.cpu().pin_memory()
+        hdy = DY.cpu().pin_memory()
+        hy = torch.empty_like(hx).pin_memory()
+        hdx = torch.empty_like(hx).pin_memory()
+        Xe, DYe = torch.empty_like(X), torch.empty_like(DY)
+        ne = max(3, args.steps // 2)
+        barrier()
+        s_ev = [torch.cuda.Event(enable_timing=True) for _ in range(ne)]
+        e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(ne)]
+        for i in range(ne):
+            flush.zero_()
+            s_ev[i].record(stream)
+            Xe.copy_(hx, non_blocking=True)
+            DYe.copy_(hdy, non_blocking=True)
+            layer.forward(w, Xe, Y, saved)
+            layer.backward(w, Xe, saved, DYe, DX, grads)
+            hy.copy_(Y, non_blocking=True)
+            hdx.copy_(DX, non_blocking=True)
+            e_ev[i].record(stream)
+        barrier()
+        te = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(s_ev, e_ev)) / ne], dtype=torch.float64,
+                          device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        extras["e2e"] = {"value": fl / (te.item() * 1e-3) / 1e12, "unit": "TFLOP/s",
+                         "h2d_bytes_per_step": 2 * X.numel() * 2, "d2h_bytes_per_step": 2 * X.numel() * 2,
+                         "ms_per_step": te.item()}
+
+    # roofline of the dominant kernel class (the tcgen05 GEMM), from live CUDA events on its stream
+    peak_burst, peak_sust, peak_src = measured_peaks()
+    g = prof["gemm"]
+    gemm_tflops = g["flops"] / (g["ms"] * 1e-3) / 1e12 if g["ms"] > 0 else 0.0
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tr_path):
+        traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
+    share = {k: v["ms"] for k, v in prof.items()}
+    roofline = {"bound": "tensor", "achieved": gemm_tflops, "peak": peak_burst, "unit": "TFLOP/s",
+                "frac": gemm_tflops / peak_burst, "traffic": traffic,
+                "kernel": "tcgen05 bf16 GEMM (all 12 layer GEMMs; FLOPs 2MNK per launch / event-timed duration)",
+                "peak_source": f"{peak_src} bf16_tflops (burst); sustained {peak_sust}",
+                "gemm_launches": g["launches"], "gemm_ms_per_step": g["ms"] / args.steps,
+                "class_ms_per_step": {k: v / args.steps for k, v in share.items()},
+                "layer_frac_of_peak": value / world / peak_burst}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, synth/)",
+                "config": {"workload": f"{cfg.name} layer fwd+bwd: h={cfg.hidden}, H={cfg.heads}, s={cfg.seq_len}, "
+                                       f"B={cfg.microbatch}, TMP={T}, n_sub={n_sub}",
+                           "tmp_degree": T, "n_sub": n_sub, "flops_per_step": fl,
+                           "l2": "flushed between steps (256 MiB write, outside the timed events)"},
+                "value_per_gpu": value / world, "tokens_per_s": cfg.tokens / (ms_step * 1e-3),
+                "roofline": roofline, "gpu_launches": launches, "clocks": clocks}
+        line.update({k: v for k, v in extras.items() if k != "e2e"})
+        if "e2e" in extras:
+            line["e2e"] = extras["e2e"]
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_oracle_sample(cfg)
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,74 @@
+"""Multi-rank worker (launched by torchrun from tests/test_gpu_multi.py): the TMP layer on T = WORLD_SIZE
+GPUs through the C ABI, each rank holding its shard; checks vs the fp64 oracle's slices, cross-rank
+bit equality of the replicated outputs, and bit-identity of n = 1 vs n = 2 at T > 1.
+Exit code 0 = all checks passed."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from gpu_layer_util import compare_to_oracle, oracle_rank_slices, run_gpu_layer  # noqa: E402
+from oracle import layer_fwd_bwd  # noqa: E402
+from synth import CONFIGS  # noqa: E402
+from synth import make_all  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    backend = os.environ.get("MERAK_TEST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group("gloo")
+    group = dist.group.WORLD
+    T = world
+    tiny = CONFIGS["tiny"]
+    cases = {
+        "tiny": tiny.with_(tmp_degree=T),
+        "h320_H5_uneven": tiny.with_(hidden=320, heads=5, seq_len=64, microbatch=4, tmp_degree=T),
+        "h256_H8_s128_n4": tiny.with_(hidden=256, heads=8, seq_len=128, microbatch=4, n_sub=4, tmp_degree=T),
+    }
+    if os.environ.get("MERAK_TEST_FULL", "0") == "1":
+        cases["gpt1.5b"] = CONFIGS["gpt1.5b"].with_(tmp_degree=T)
+    failures = []
+    for name, cfg in cases.items():
+        if cfg.heads < T or cfg.ffn % T:
+            continue
+        params, x, dy = make_all(cfg, seed=2000 + cfg.hidden)
+        out = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group)
+        y, dx, g = layer_fwd_bwd(params, x, dy, cfg.heads)
+        errs, bad = compare_to_oracle(out, y, dx, oracle_rank_slices(g, cfg, T, rank), cfg)
+        print(f"[rank {rank}] {name} T={T}", {k: f"{v:.2e}" for k, v in errs.items()}, flush=True)
+        if bad:
+            failures.append((name, bad))
+        # replicated outputs must be bit-identical on every rank
+        for k in ("y", "dx", "ln1_g", "ln1_b", "ln2_g", "ln2_b", "b_o", "b_2"):
+            t = out[k].contiguous()
+            gathered = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(gathered, t)
+            if not all(torch.equal(gathered[0], q) for q in gathered):
+                failures.append((name, f"{k} differs across ranks"))
+        # sub-pipelined vs non-sub-pipelined bit-identity at T > 1
+        out1 = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group, n_sub=1)
+        for k in out:
+            if not torch.equal(out[k], out1[k]):
+                failures.append((name, f"{k}: n={cfg.n_sub} vs n=1 not bit-identical"))
+    dist.barrier()
+    if failures:
+        print(f"[rank {rank}] FAIL {failures}", flush=True)
+    ok = torch.tensor([0 if failures else 1], device="cuda")
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    dist.destroy_process_group()
+    sys.exit(0 if ok.item() == 1 else 1)
+
+
+if __name__ == "__main__":
+    main()
