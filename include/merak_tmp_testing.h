@@ -36,13 +36,15 @@ int merak_test_ar_fwd(const void *const *partials, int T, int m, int h, const vo
                       int ctas, void *stream);
 
 /* Backward all-reduce epilogue (fake peers): dx = dres + LN^T(sum_r partial[r]); dgamma/dbeta
- * (fp32 [h]) += fixed-order token sums. ws: fp32 workspace of 2*(m/G)*h floats, G = 16 if h<=3072 else 8. */
-int merak_test_ar_bwd(const void *const *partials, int T, int m, int h, const void *x_ln, const float *mean,
+ * (fp32 [h]) += per-sample fixed-order token sums (s = rows per sample, m % s == 0, s % 16 == 0).
+ * ws: fp32 workspace of 2*(m/G)*h floats, G = 16 if h<=3072 else 8. */
+int merak_test_ar_bwd(const void *const *partials, int T, int m, int s, int h, const void *x_ln, const float *mean,
                       const float *rstd, const void *gamma, const void *dres, void *dx, float *dgamma, float *dbeta,
                       float *ws, int ctas, void *stream);
 
-/* g[c] += sum_i X[i, c] over m rows (m % 16 == 0) in the fixed order; ws: fp32 [(m/16) * n]. */
-int merak_test_colsum(const void *X, int ld, int m, int n, float *g, float *ws, void *stream);
+/* g[c] += sum_i X[i, c] over m rows = m/s samples of s rows, per-sample fixed order then a chain over
+ * samples; ws: fp32 [(m/s) * n]. */
+int merak_test_colsum(const void *X, int ld, int m, int s, int n, float *g, float *ws, void *stream);
 
 #ifdef __cplusplus
 }

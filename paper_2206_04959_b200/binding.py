@@ -85,9 +85,9 @@ def lib():
         L.merak_test_ln_fwd.argtypes = [P, P, P, P, P, P, ctypes.c_int, ctypes.c_int, ctypes.c_float, P]
         L.merak_test_ar_fwd.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P,
                                         ctypes.c_int, P, P, P, P, P, ctypes.c_float, ctypes.c_int, P]
-        L.merak_test_ar_bwd.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P, P, P,
-                                        P, P, P, ctypes.c_int, P]
-        L.merak_test_colsum.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P]
+        L.merak_test_ar_bwd.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P,
+                                        P, P, P, P, P, P, P, P, ctypes.c_int, P]
+        L.merak_test_colsum.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P]
         _lib = L
     return _lib
 

@@ -10,7 +10,10 @@
 // weight-gradient GEMMs filling the all-reduce gaps ("alternate execution schedule").
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -37,6 +40,32 @@ struct ProfRec {
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// NCCL baseline (MERAK_COMM_NCCL): resolved at run time from the libnccl.so.2 the process already
+// uses (torch's), or from $MERAK_NCCL_LIB.  Only types come from nccl.h.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char *(*GetErrorString)(ncclResult_t) = nullptr;
+  bool load() {
+    if (AllReduce) return true;
+    void *lib = nullptr;
+    const char *env = getenv("MERAK_NCCL_LIB");
+    if (env) lib = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!lib) return false;
+    GetUniqueId = (decltype(GetUniqueId))dlsym(lib, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(lib, "ncclCommInitRank");
+    AllReduce = (decltype(AllReduce))dlsym(lib, "ncclAllReduce");
+    CommDestroy = (decltype(CommDestroy))dlsym(lib, "ncclCommDestroy");
+    GetErrorString = (decltype(GetErrorString))dlsym(lib, "ncclGetErrorString");
+    return GetUniqueId && CommInitRank && AllReduce && CommDestroy && GetErrorString;
+  }
+};
+NcclApi g_nccl;
 
 }  // namespace
 
@@ -74,6 +103,7 @@ struct merak_tmp {
   int64_t prof_launch[MERAK_K_NUM] = {};
   int64_t launches = 0;
   std::string err;
+  ncclComm_t nccl = nullptr;
 };
 
 static std::string g_init_err;
@@ -162,7 +192,7 @@ static PeerSync make_sync(merak_tmp_t *h, bool comm) {
   memset(&ps, 0, sizeof(ps));
   ps.T = h->T;
   ps.rank = h->r;
-  ps.enabled = comm && h->T > 1;
+  ps.enabled = comm && h->T > 1 && !h->nccl;
   ps.epoch = ++h->epoch;
   ps.flags_local = reinterpret_cast<uint32_t *>(h->pv + h->flags_off);
   for (int q = 0; q < h->T; ++q) ps.flags_peer[q] = reinterpret_cast<uint32_t *>(h->peer_pv[q] + h->flags_off);
@@ -190,8 +220,8 @@ static GemmArgs gargs(const void *A, const void *B, int M, int N, int K, int lda
 }
 static merak_status run_colsum(merak_tmp_t *h, const bf16 *X, int ld, int m, int n, float *g) {
   Launch L(h, MERAK_K_REDUCE, h->cs, 0.0, 2);
-  CK(h, colsum_partial(X, ld, m, n, h->part_col, h->cs));
-  CK(h, chain_add(h->part_col, m / 16, n, g, h->cs));
+  CK(h, colsum_sample(X, ld, h->s, m / h->s, n, h->part_col, h->cs));
+  CK(h, sample_reduce(h->part_col, 1, m / h->s, n, g, h->cs));
   return MERAK_OK;
 }
 
@@ -200,6 +230,25 @@ static merak_status run_colsum(merak_tmp_t *h, const bf16 *X, int ld, int m, int
     merak_status _s = (x);              \
     if (_s != MERAK_OK) return _s;      \
   } while (0)
+
+// NCCL baseline: in-place sum of this rank's slot rows on the comm stream; the fused epilogue
+// kernel then runs with the single (already reduced) local partial.
+static merak_status nccl_allreduce(merak_tmp_t *h, bf16 *rows, size_t count) {
+  Launch L(h, MERAK_K_ALLREDUCE, h->ms, 0.0, 0);
+  ncclResult_t r = g_nccl.AllReduce(rows, rows, count, ncclBfloat16, ncclSum, h->nccl, h->ms);
+  if (r != ncclSuccess) return fail(h, MERAK_ECUDA, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
+  return MERAK_OK;
+}
+
+// Partials the all-reduce epilogue kernel sums for slot `slot`, rows starting at r0.
+static int ar_partials(merak_tmp_t *h, bool comm, int slot, size_t r0, const bf16 **out) {
+  if (!comm || h->T == 1 || h->nccl) {
+    out[0] = slot_ptr(h, h->r, slot) + r0 * h->h;
+    return 1;
+  }
+  for (int q = 0; q < h->T; ++q) out[q] = slot_ptr(h, q, slot) + r0 * h->h;
+  return h->T;
+}
 
 static merak_status check_async_error(merak_tmp_t *h) {
   if (h->err_host && *(volatile int *)h->err_host)
@@ -273,8 +322,8 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     {
       ArFwdArgs a;
       memset(&a, 0, sizeof(a));
-      a.T = comm ? h->T : 1;
-      for (int q = 0; q < a.T; ++q) a.partial[q] = slot_ptr(h, comm ? q : h->r, 0) + r0 * hh;
+      if (comm && h->nccl) TRY(nccl_allreduce(h, slot_ptr(h, h->r, 0) + r0 * hh, (size_t)m * hh));
+      a.T = ar_partials(h, comm, 0, r0, a.partial);
       a.m = m; a.h = hh; a.resid = xj; a.bias = (const bf16 *)w->b_o; a.out = (bf16 *)S(L.x1) + r0 * hh;
       a.do_ln = true; a.gamma = (const bf16 *)w->ln2_g; a.beta = (const bf16 *)w->ln2_b;
       a.ln_out = (bf16 *)S(L.u2) + r0 * hh; a.mean = (float *)S(L.mean2) + r0; a.rstd = (float *)S(L.rstd2) + r0;
@@ -304,8 +353,8 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     {
       ArFwdArgs a;
       memset(&a, 0, sizeof(a));
-      a.T = comm ? h->T : 1;
-      for (int q = 0; q < a.T; ++q) a.partial[q] = slot_ptr(h, comm ? q : h->r, 1) + r0 * hh;
+      if (comm && h->nccl) TRY(nccl_allreduce(h, slot_ptr(h, h->r, 1) + r0 * hh, (size_t)m * hh));
+      a.T = ar_partials(h, comm, 1, r0, a.partial);
       a.m = m; a.h = hh; a.resid = (const bf16 *)S(L.x1) + r0 * hh; a.bias = (const bf16 *)w->b_2;
       a.out = y + r0 * hh; a.do_ln = false; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
@@ -345,8 +394,8 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     {
       ArBwdArgs a;
       memset(&a, 0, sizeof(a));
-      a.T = comm ? h->T : 1;
-      for (int q = 0; q < a.T; ++q) a.partial[q] = slot_ptr(h, comm ? q : h->r, 2) + r0 * hh;
+      if (comm && h->nccl) TRY(nccl_allreduce(h, slot_ptr(h, h->r, 2) + r0 * hh, (size_t)m * hh));
+      a.T = ar_partials(h, comm, 2, r0, a.partial);
       a.m = m; a.h = hh; a.x_ln = (const bf16 *)S(L.x1) + r0 * hh;
       a.mean = (const float *)S(L.mean2) + r0; a.rstd = (const float *)S(L.rstd2) + r0;
       a.gamma = (const bf16 *)w->ln2_g; a.dres = dyj; a.dx = h->dx1 + r0 * hh;
@@ -357,8 +406,8 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
         CK(h, ar_bwd(a, ps, h->ms));
       }
       Launch Lk(h, MERAK_K_REDUCE, h->ms, 0.0, 2);
-      CK(h, chain_add(h->part_lng, m / h->G, hh, gr->ln2_g, h->ms));
-      CK(h, chain_add(h->part_lnb, m / h->G, hh, gr->ln2_b, h->ms));
+      CK(h, sample_reduce(h->part_lng, h->s / h->G, m / h->s, hh, gr->ln2_g, h->ms));
+      CK(h, sample_reduce(h->part_lnb, h->s / h->G, m / h->s, hh, gr->ln2_b, h->ms));
     }
     CK(h, cudaEventRecord(h->ev_ar[2][j], h->ms));
     h->ev_ar_valid[2][j] = true;
@@ -399,8 +448,8 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     {
       ArBwdArgs a;
       memset(&a, 0, sizeof(a));
-      a.T = comm ? h->T : 1;
-      for (int q = 0; q < a.T; ++q) a.partial[q] = slot_ptr(h, comm ? q : h->r, 3) + r0 * hh;
+      if (comm && h->nccl) TRY(nccl_allreduce(h, slot_ptr(h, h->r, 3) + r0 * hh, (size_t)m * hh));
+      a.T = ar_partials(h, comm, 3, r0, a.partial);
       a.m = m; a.h = hh; a.x_ln = x + r0 * hh;
       a.mean = (const float *)S(L.mean1) + r0; a.rstd = (const float *)S(L.rstd1) + r0;
       a.gamma = (const bf16 *)w->ln1_g; a.dres = dx1; a.dx = dx + r0 * hh;
@@ -411,8 +460,8 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
         CK(h, ar_bwd(a, ps, h->ms));
       }
       Launch Lk(h, MERAK_K_REDUCE, h->ms, 0.0, 2);
-      CK(h, chain_add(h->part_lng, m / h->G, hh, gr->ln1_g, h->ms));
-      CK(h, chain_add(h->part_lnb, m / h->G, hh, gr->ln1_b, h->ms));
+      CK(h, sample_reduce(h->part_lng, h->s / h->G, m / h->s, hh, gr->ln1_g, h->ms));
+      CK(h, sample_reduce(h->part_lnb, h->s / h->G, m / h->s, hh, gr->ln1_b, h->ms));
     }
     CK(h, cudaEventRecord(h->ev_ar[3][j], h->ms));
     h->ev_ar_valid[3][j] = true;
@@ -449,11 +498,10 @@ static merak_status validate(const merak_tmp_config *c) {
   if (d != 32 && d != 64 && d != 80 && d != 96 && d != 128)
     return fail(nullptr, MERAK_EUNSUPPORTED, "head dim %d not in {32,64,80,96,128}", d);
   if (T != 1 && T != 2 && T != 4 && T != 8) return fail(nullptr, MERAK_EUNSUPPORTED, "tmp_degree not in {1,2,4,8}");
-  if (((c->microbatch / c->n_sub) * c->seq_len) % 16)
-    return fail(nullptr, MERAK_EUNSUPPORTED, "tokens per sub-batch must be a multiple of 16");
+  if (c->seq_len % 16) return fail(nullptr, MERAK_EUNSUPPORTED, "seq_len must be a multiple of 16");
+  if (c->microbatch > 256) return fail(nullptr, MERAK_EUNSUPPORTED, "microbatch > 256");
   if (c->hidden % 8 || (f / T) % 8) return fail(nullptr, MERAK_EUNSUPPORTED, "h and f/T must be multiples of 8");
   if (c->precision == MERAK_FP32_CHECK) return fail(nullptr, MERAK_EUNSUPPORTED, "fp32 check mode not built yet");
-  if (c->comm == MERAK_COMM_NCCL) return fail(nullptr, MERAK_EUNSUPPORTED, "NCCL baseline not built yet");
   return MERAK_OK;
 }
 
@@ -464,6 +512,7 @@ static void release(merak_tmp_t *h) {
   if (h->ms) cudaStreamSynchronize(h->ms);
   for (int q = 0; q < MAX_T; ++q)
     if (h->peer_pv[q] && h->peer_pv[q] != h->pv) cudaIpcCloseMemHandle(h->peer_pv[q]);
+  if (h->nccl) g_nccl.CommDestroy(h->nccl);
   if (h->pv) cudaFree(h->pv);
   if (h->ws) cudaFree(h->ws);
   if (h->err_host) cudaFreeHost(h->err_host);
@@ -543,7 +592,7 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
     const size_t o_dz = take(M * h->fr * 2), o_dx1 = take(M * h->h * 2), o_dctx = take(M * h->hr * 2);
     const size_t o_dqkv = take(M * 3 * h->hr * 2), o_delta = take((size_t)h->B * h->Hr * h->s * 4);
     const int ncol = std::max(std::max(3 * h->hr, h->fr), h->h);
-    const size_t o_pc = take((M / 16) * (size_t)ncol * 4);
+    const size_t o_pc = take((size_t)h->B * ncol * 4);
     const size_t o_pg = take((M / h->G) * (size_t)h->h * 4), o_pb = take((M / h->G) * (size_t)h->h * 4);
     CKI(cudaMalloc(&h->ws, o));
     h->dz = (bf16 *)(h->ws + o_dz); h->dx1 = (bf16 *)(h->ws + o_dx1); h->dctx = (bf16 *)(h->ws + o_dctx);
@@ -578,6 +627,28 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
       return bail(MERAK_EPEER);
     }
   }
+  if (cfg->comm == MERAK_COMM_NCCL && h->T > 1) {
+    if (!g_nccl.load()) {
+      fail(h, MERAK_EUNSUPPORTED, "libnccl.so.2 not found (set MERAK_NCCL_LIB)");
+      return bail(MERAK_EUNSUPPORTED);
+    }
+    ncclUniqueId id;
+    memset(&id, 0, sizeof(id));
+    if (h->r == 0 && g_nccl.GetUniqueId(&id) != ncclSuccess) {
+      fail(h, MERAK_EPEER, "ncclGetUniqueId failed");
+      return bail(MERAK_EPEER);
+    }
+    std::vector<ncclUniqueId> ids(h->T);
+    if (ag(ag_ctx, &id, ids.data(), sizeof(id)) != 0) {
+      fail(h, MERAK_EPEER, "allgather of the NCCL unique id failed");
+      return bail(MERAK_EPEER);
+    }
+    ncclResult_t nr = g_nccl.CommInitRank(&h->nccl, h->T, ids[0], h->r);
+    if (nr != ncclSuccess) {
+      fail(h, MERAK_EPEER, "ncclCommInitRank: %s", g_nccl.GetErrorString(nr));
+      return bail(MERAK_EPEER);
+    }
+  }
 #undef CKI
   *out = h;
   return MERAK_OK;
@@ -588,7 +659,6 @@ merak_status merak_tmp_set_subbatches(merak_tmp_t *h, int32_t n_sub) {
   if (h->chain_open) return fail(h, MERAK_ESTATE, "set_subbatches while a MERAK_FLAG_CHAIN sequence is open");
   if (n_sub <= 0 || n_sub > MAXN) return fail(h, MERAK_EINVAL, "n_sub out of range");
   if (h->B % n_sub) return fail(h, MERAK_EINDIVISIBLE, "microbatch %% n_sub != 0");
-  if (((h->B / n_sub) * h->s) % 16) return fail(h, MERAK_EUNSUPPORTED, "tokens per sub-batch must be a multiple of 16");
   // all outstanding work of the old split must finish before slot/event indices are reinterpreted
   CK(h, cudaStreamSynchronize(h->cs));
   CK(h, cudaStreamSynchronize(h->ms));
@@ -726,7 +796,7 @@ int merak_test_ar_fwd(const void *const *partials, int T, int m, int h, const vo
   return (int)ar_fwd(a, ps, (cudaStream_t)stream);
 }
 
-int merak_test_ar_bwd(const void *const *partials, int T, int m, int h, const void *x_ln, const float *mean,
+int merak_test_ar_bwd(const void *const *partials, int T, int m, int s, int h, const void *x_ln, const float *mean,
                       const float *rstd, const void *gamma, const void *dres, void *dx, float *dgamma, float *dbeta,
                       float *ws, int ctas, void *stream) {
   if (T < 1 || T > MAX_T) return (int)cudaErrorInvalidValue;
@@ -735,20 +805,21 @@ int merak_test_ar_bwd(const void *const *partials, int T, int m, int h, const vo
   for (int q = 0; q < T; ++q) a.partial[q] = (const bf16 *)partials[q];
   a.T = T; a.m = m; a.h = h; a.x_ln = (const bf16 *)x_ln; a.mean = mean; a.rstd = rstd; a.gamma = (const bf16 *)gamma;
   a.dres = (const bf16 *)dres; a.dx = (bf16 *)dx; a.G = ar_bwd_group_rows(h);
-  if (m % a.G) return (int)cudaErrorInvalidValue;
+  if (m % s || s % a.G) return (int)cudaErrorInvalidValue;
   a.part_dg = ws; a.part_db = ws + (size_t)(m / a.G) * h; a.ctas = ctas;
   PeerSync ps;
   memset(&ps, 0, sizeof(ps));
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = ar_bwd(a, ps, st);
-  if (e == cudaSuccess) e = chain_add(a.part_dg, m / a.G, h, dgamma, st);
-  if (e == cudaSuccess) e = chain_add(a.part_db, m / a.G, h, dbeta, st);
+  if (e == cudaSuccess) e = sample_reduce(a.part_dg, s / a.G, m / s, h, dgamma, st);
+  if (e == cudaSuccess) e = sample_reduce(a.part_db, s / a.G, m / s, h, dbeta, st);
   return (int)e;
 }
 
-int merak_test_colsum(const void *X, int ld, int m, int n, float *g, float *ws, void *stream) {
-  cudaError_t e = colsum_partial((const bf16 *)X, ld, m, n, ws, (cudaStream_t)stream);
-  if (e == cudaSuccess) e = chain_add(ws, m / 16, n, g, (cudaStream_t)stream);
+int merak_test_colsum(const void *X, int ld, int m, int s, int n, float *g, float *ws, void *stream) {
+  if (m % s) return (int)cudaErrorInvalidValue;
+  cudaError_t e = colsum_sample((const bf16 *)X, ld, s, m / s, n, ws, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = sample_reduce(ws, 1, m / s, n, g, (cudaStream_t)stream);
   return (int)e;
 }
 

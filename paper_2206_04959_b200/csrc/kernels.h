@@ -62,7 +62,7 @@ cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st);  // 2 launches: dQ (+d
 
 // ---------------------------------------------------------------- LN / all-reduce / reductions (ln_ar.cu)
 constexpr int MAX_T = 8;
-constexpr int MAX_AR_CTAS = 256;
+constexpr int MAX_AR_CTAS = 1024;
 
 // Peer handshake for one all-reduce launch.  flags_local: this rank's flag array; flags_peer[r]:
 // rank r's flag array mapped into this process (flags_peer[rank] == flags_local).  Layout per rank:
@@ -114,9 +114,10 @@ int ar_bwd_group_rows(int h);
 cudaError_t ln_fwd(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bfloat16 *b, __nv_bfloat16 *u,
                    float *mean, float *rstd, int m, int h, float eps, cudaStream_t st);
 
-// Fixed-order column sums: part[grp][c] = sum_{i<16} X[16 grp + i][c]   (bf16 X, row stride ld)
-cudaError_t colsum_partial(const __nv_bfloat16 *X, int ld, int m, int n, float *part, cudaStream_t st);
-// g[c] += part[0][c]; g[c] += part[1][c]; ... (sequential over groups: bit-identical across splits)
-cudaError_t chain_add(const float *part, int groups, int n, float *g, cudaStream_t st);
+// Token reductions with a per-sample fixed structure (bit-identical across sub-batch splits):
+// Q[i][c] = fixed-order sum of the s rows of sample i of X (bf16, row stride ld), i < b
+cudaError_t colsum_sample(const __nv_bfloat16 *X, int ld, int s, int b, int n, float *Q, cudaStream_t st);
+// g[c] += sum over samples i (in order) of the fixed-order sum of part[i*gps .. i*gps+gps-1][c]
+cudaError_t sample_reduce(const float *part, int gps, int b, int n, float *g, cudaStream_t st);
 
 }  // namespace mk

@@ -260,45 +260,81 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16 *x, con
 }
 
 // ------------------------------------------------------------------------------ token reductions
-// part[grp][c] = X[16 grp][c] + X[16 grp + 1][c] + ... + X[16 grp + 15][c]   (sequential, fp32)
-__global__ void colsum_partial_kernel(const __nv_bfloat16 *X, int ld, int m, int n, float *part) {
-  const int cc = blockIdx.x * blockDim.x + threadIdx.x;
-  const int grp = blockIdx.y;
-  if (cc * 8 >= n) return;
-  float s[8];
+// Reductions over tokens (bias and LayerNorm gradients) use a structure fixed per SAMPLE, so the
+// result is the same whatever the sub-batch split (sub-batches are whole samples, reading R9):
+//   per-sample sum in a fixed order, then a chain over samples in order that continues across
+//   sub-batch launches through the fp32 gradient itself (bit-identity rule vi).
+
+// Q[i][c] = sum of X over the s rows of sample i: thread (tx, ty) owns 8 columns and rows
+// ty, ty+8, ty+16, ... (sequential), then the 8 row-slices are added in order ty = 0..7.
+__global__ void __launch_bounds__(256) colsum_sample_kernel(const __nv_bfloat16 *X, int ld, int s, int n, float *Q) {
+  __shared__ float red[8][256];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int cc = blockIdx.x * 32 + tx;
+  const int i = blockIdx.y;
+  float acc[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) s[k] = 0.f;
-  for (int i = 0; i < 16; ++i) {
-    float v[8];
-    load8(X + (size_t)(grp * 16 + i) * ld + cc * 8, v);
+  for (int k = 0; k < 8; ++k) acc[k] = 0.f;
+  if (cc * 8 < n) {
+    const __nv_bfloat16 *base = X + (size_t)i * s * ld + cc * 8;
+#pragma unroll 4
+    for (int r = ty; r < s; r += 8) {
+      float v[8];
+      load8(base + (size_t)r * ld, v);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s[k] += v[k];
+      for (int k = 0; k < 8; ++k) acc[k] += v[k];
+    }
   }
-  float4 *p = reinterpret_cast<float4 *>(part + (size_t)grp * n + cc * 8);
-  p[0] = make_float4(s[0], s[1], s[2], s[3]);
-  p[1] = make_float4(s[4], s[5], s[6], s[7]);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) red[ty][tx * 8 + k] = acc[k];
+  __syncthreads();
+  if (ty == 0 && cc * 8 < n) {
+    float t[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t[k] = red[0][tx * 8 + k];
+    for (int y = 1; y < 8; ++y)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t[k] += red[y][tx * 8 + k];
+    float4 *q = reinterpret_cast<float4 *>(Q + (size_t)i * n + cc * 8);
+    q[0] = make_float4(t[0], t[1], t[2], t[3]);
+    q[1] = make_float4(t[4], t[5], t[6], t[7]);
+  }
 }
 
-// g[c] = (((g[c] + part[0][c]) + part[1][c]) + ...)  -- the same chain whatever the sub-batch split
-__global__ void chain_add_kernel(const float *part, int groups, int n, float *g) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
-  float acc = g[c];
-  int i = 0;
-  for (; i + 8 <= groups; i += 8) {
-    float v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = part[(size_t)(i + k) * n + c];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc += v[k];
+// g[c] += sum_i ( part[i*gps][c] + part[i*gps+1][c] + ... + part[i*gps+gps-1][c] ),  i = 0..b-1 in order
+__global__ void __launch_bounds__(256) sample_reduce_kernel(const float *part, int gps, int b, int n, float *g) {
+  extern __shared__ float q[];  // [b][32]
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int c = blockIdx.x * 32 + tx;
+  for (int i = ty; i < b; i += 8) {
+    float acc = 0.f;
+    if (c < n) {
+      const float *p = part + (size_t)i * gps * n + c;
+#pragma unroll 8
+      for (int k = 0; k < gps; ++k) acc += p[(size_t)k * n];
+    }
+    q[i * 32 + tx] = acc;
   }
-  for (; i < groups; ++i) acc += part[(size_t)i * n + c];
-  g[c] = acc;
+  __syncthreads();
+  if (ty == 0 && c < n) {
+    float a = g[c];
+    for (int i = 0; i < b; ++i) a += q[i * 32 + tx];
+    g[c] = a;
+  }
 }
 
 // ------------------------------------------------------------------------------ host
-static int clamp_ctas(int want, int work) {
-  if (want <= 0) want = 64;
+// CTAs that can be resident at once (the handshake needs every CTA index to make progress; the
+// grid also has to be identical on all ranks, so it depends only on the shape and the device).
+static int resident_ctas(const void *kern, int threads, size_t smem) {
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  return per_sm * sms;
+}
+static int clamp_ctas(int want, int work, int resident) {
+  if (want <= 0 || want > resident) want = resident;
   if (want > MAX_AR_CTAS) want = MAX_AR_CTAS;
   if (want > work) want = work;
   return want < 1 ? 1 : want;
@@ -306,7 +342,9 @@ static int clamp_ctas(int want, int work) {
 
 cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
   // handshake CTA count must be identical on all ranks: it depends only on (m, ctas)
-  const int grid = clamp_ctas(a.ctas, (a.m + 7) / 8);
+  static int resident = 0;
+  if (!resident) resident = resident_ctas((const void *)ar_fwd_kernel, 256, 0);
+  const int grid = clamp_ctas(a.ctas, (a.m + 7) / 8, resident);
   ar_fwd_kernel<<<grid, 256, 0, st>>>(a, ps);
   return cudaGetLastError();
 }
@@ -314,7 +352,6 @@ cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
 int ar_bwd_group_rows(int h) { return h <= 3072 ? 16 : 8; }
 
 cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
-  const int grid = clamp_ctas(a.ctas, a.m / a.G);
   const size_t smem = (size_t)a.G * a.h * sizeof(float);
   if (a.G == 16) {
     static size_t attr16 = 0;
@@ -323,6 +360,7 @@ cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
       if (e != cudaSuccess) return e;
       attr16 = smem;
     }
+    const int grid = clamp_ctas(a.ctas, a.m / a.G, resident_ctas((const void *)ar_bwd_kernel<16>, 256, smem));
     ar_bwd_kernel<16><<<grid, 256, smem, st>>>(a, ps);
   } else if (a.G == 8) {
     static size_t attr8 = 0;
@@ -331,6 +369,7 @@ cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
       if (e != cudaSuccess) return e;
       attr8 = smem;
     }
+    const int grid = clamp_ctas(a.ctas, a.m / a.G, resident_ctas((const void *)ar_bwd_kernel<8>, 256, smem));
     ar_bwd_kernel<8><<<grid, 256, smem, st>>>(a, ps);
   } else {
     return cudaErrorInvalidValue;
@@ -344,15 +383,17 @@ cudaError_t ln_fwd(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bf
   return cudaGetLastError();
 }
 
-cudaError_t colsum_partial(const __nv_bfloat16 *X, int ld, int m, int n, float *part, cudaStream_t st) {
-  if (m % 16 || n % 8) return cudaErrorInvalidValue;
-  dim3 grid((n / 8 + 127) / 128, m / 16);
-  colsum_partial_kernel<<<grid, 128, 0, st>>>(X, ld, m, n, part);
+cudaError_t colsum_sample(const __nv_bfloat16 *X, int ld, int s, int b, int n, float *Q, cudaStream_t st) {
+  if (n % 8) return cudaErrorInvalidValue;
+  dim3 grid((n / 8 + 31) / 32, b);
+  colsum_sample_kernel<<<grid, dim3(32, 8), 0, st>>>(X, ld, s, n, Q);
   return cudaGetLastError();
 }
 
-cudaError_t chain_add(const float *part, int groups, int n, float *g, cudaStream_t st) {
-  chain_add_kernel<<<(n + 127) / 128, 128, 0, st>>>(part, groups, n, g);
+cudaError_t sample_reduce(const float *part, int gps, int b, int n, float *g, cudaStream_t st) {
+  const size_t smem = (size_t)b * 32 * sizeof(float);
+  if (smem > 48 * 1024) return cudaErrorInvalidValue;
+  sample_reduce_kernel<<<(n + 31) / 32, dim3(32, 8), smem, st>>>(part, gps, b, n, g);
   return cudaGetLastError();
 }
 

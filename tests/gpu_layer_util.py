@@ -16,13 +16,13 @@ def rel_err(gpu, ref) -> float:
     return float(np.linalg.norm(g - r) / max(np.linalg.norm(r), 1e-300))
 
 
-def run_gpu_layer(cfg, params, x, dy, T=1, rank=0, n_sub=None, group=None, reps=1, flags=0, device=None):
+def run_gpu_layer(cfg, params, x, dy, T=1, rank=0, n_sub=None, group=None, reps=1, flags=0, device=None, comm=0):
     """Forward + backward through merak_tmp_layer_fwd/bwd.  Returns dict of torch tensors on device:
     y, dx and the rank's fp32 gradient shards."""
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     n = cfg.n_sub if n_sub is None else n_sub
     layer = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, tmp_degree=T, tmp_rank=rank, n_sub=n,
-                     device=dev.index, group=group)
+                     device=dev.index, group=group, comm=comm)
     w = shard_weights(params, cfg.heads, T, rank, dev)
     M, h = cfg.tokens, cfg.hidden
     X = torch.as_tensor(np.asarray(x).reshape(M, h)).to(dev, torch.bfloat16)

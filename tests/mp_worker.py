@@ -61,6 +61,12 @@ def main():
         for k in out:
             if not torch.equal(out[k], out1[k]):
                 failures.append((name, f"{k}: n={cfg.n_sub} vs n=1 not bit-identical"))
+        # NCCL baseline (MERAK_COMM_NCCL): same kernels, ncclAllReduce instead of the peer kernel
+        outn = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group, comm=1)
+        errs, bad = compare_to_oracle(outn, y, dx, oracle_rank_slices(g, cfg, T, rank), cfg)
+        print(f"[rank {rank}] {name} T={T} nccl", {k: f"{v:.2e}" for k, v in errs.items()}, flush=True)
+        if bad:
+            failures.append((name + "/nccl", bad))
     dist.barrier()
     if failures:
         print(f"[rank {rank}] FAIL {failures}", flush=True)

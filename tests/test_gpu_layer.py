@@ -19,7 +19,7 @@ TINY = CONFIGS["tiny"]
 CASES = {
     "tiny": TINY.with_(tmp_degree=1),
     "h256_d64_s128": TINY.with_(hidden=256, heads=4, seq_len=128, microbatch=4, tmp_degree=1),
-    "h320_d64_s200_ragged": TINY.with_(hidden=320, heads=5, seq_len=200, microbatch=4, tmp_degree=1),
+    "h320_d64_s208_ragged": TINY.with_(hidden=320, heads=5, seq_len=208, microbatch=2, tmp_degree=1),
     "h320_d80_s64": TINY.with_(hidden=320, heads=4, seq_len=64, microbatch=2, tmp_degree=1),
     "h384_d96_s96_n4": TINY.with_(hidden=384, heads=4, seq_len=96, microbatch=4, tmp_degree=1, n_sub=4),
     "h256_d32_s48_n1": TINY.with_(hidden=256, heads=8, seq_len=48, microbatch=2, tmp_degree=1, n_sub=1),
