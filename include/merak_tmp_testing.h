@@ -14,10 +14,11 @@ extern "C" {
 
 /* C[M,N] = A * B^T via the tcgen05 GEMM.  a_mn: A stored [K, M] (else [M, K]); b_mn: B stored
  * [K, N] (else [N, K]).  epi: 0 store bf16, 1 +bias, 2 +bias & GeLU (out=z, out2=gelu(z)),
- * 3 * gelu'(aux), 4 fp32 accumulate into out32 (preloaded). */
+ * 3 * gelu'(aux), 4 fp32 accumulate into out32 (preloaded); with db32 != NULL the last of the N columns
+ * (the ones column of B) accumulates into db32[M] instead (bias gradient). */
 int merak_test_gemm(const void *A, const void *B, int M, int N, int K, int lda, int ldb, int a_mn, int b_mn, int epi,
                     void *out, int ldo, void *out2, int ldo2, const void *bias, const void *aux, int ld_aux,
-                    float *out32, int ld32, int max_ctas, void *stream);
+                    float *out32, int ld32, float *db32, int max_ctas, void *stream);
 
 /* Causal attention forward over packed qkv [b*s, 3*heads*d] -> ctx [b*s, heads*d], lse [b,heads,s] fp32. */
 int merak_test_attn_fwd(const void *qkv, void *ctx, float *lse, int b, int s, int heads, int d, void *stream);
@@ -37,7 +38,7 @@ int merak_test_ar_fwd(const void *const *partials, int T, int m, int h, const vo
 
 /* Backward all-reduce epilogue (fake peers): dx = dres + LN^T(sum_r partial[r]); dgamma/dbeta
  * (fp32 [h]) += per-sample fixed-order token sums (s = rows per sample, m % s == 0, s % 16 == 0).
- * ws: fp32 workspace of 2*(m/G)*h floats, G = 16 if h<=3072 else 8. */
+ * ws: fp32 workspace of 2*(m/8)*h floats (LN-gradient partials per 8-row group). */
 int merak_test_ar_bwd(const void *const *partials, int T, int m, int s, int h, const void *x_ln, const float *mean,
                       const float *rstd, const void *gamma, const void *dres, void *dx, float *dgamma, float *dbeta,
                       float *ws, int ctas, void *stream);

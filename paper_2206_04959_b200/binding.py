@@ -79,7 +79,8 @@ def lib():
                    "merak_tmp_join", "merak_tmp_destroy", "merak_tmp_set_profiling", "merak_tmp_get_profile"):
             getattr(L, fn).restype = ctypes.c_int
         L.merak_test_gemm.argtypes = [P, P] + [ctypes.c_int] * 8 + [P, ctypes.c_int, P, ctypes.c_int, P, P,
-                                                                      ctypes.c_int, P, ctypes.c_int, ctypes.c_int, P]
+                                                                      ctypes.c_int, P, ctypes.c_int, P, ctypes.c_int,
+                                                                      P]
         L.merak_test_attn_fwd.argtypes = [P, P, P] + [ctypes.c_int] * 4 + [P]
         L.merak_test_attn_bwd.argtypes = [P, P, P, P, P, P] + [ctypes.c_int] * 4 + [P]
         L.merak_test_ln_fwd.argtypes = [P, P, P, P, P, P, ctypes.c_int, ctypes.c_int, ctypes.c_float, P]

@@ -163,26 +163,33 @@ struct Launch {
 };
 
 // ------------------------------------------------------------------------------ shapes / layout
+// The four activations that are the B operand of a wgrad GEMM (u, ctx, u2, g) carry an 8-wide pad
+// [1, 0, ..., 0] after their K columns (row stride K + 8): the wgrad GEMM then has one extra output
+// column that is the bias gradient dY^T 1, on the same MMA accumulation chain (bit-identity rule v).
 struct SavedLayout {
   size_t u, mean1, rstd1, qkv, ctx, lse, x1, mean2, rstd2, u2, z, g, total;
+  int ld_u, ld_ctx, ld_u2, ld_g;
 };
 static SavedLayout saved_layout(const merak_tmp_t *h) {
   SavedLayout L;
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t at = o; o += align256(bytes); return at; };
   const size_t M = h->M;
-  L.u = take(M * h->h * 2);
+  L.ld_u = L.ld_u2 = h->h + 8;
+  L.ld_ctx = h->hr + 8;
+  L.ld_g = h->fr + 8;
+  L.u = take(M * L.ld_u * 2);
   L.mean1 = take(M * 4);
   L.rstd1 = take(M * 4);
   L.qkv = take(M * 3 * h->hr * 2);
-  L.ctx = take(M * h->hr * 2);
+  L.ctx = take(M * L.ld_ctx * 2);
   L.lse = take((size_t)h->B * h->Hr * h->s * 4);
   L.x1 = take(M * h->h * 2);
   L.mean2 = take(M * 4);
   L.rstd2 = take(M * 4);
-  L.u2 = take(M * h->h * 2);
+  L.u2 = take(M * L.ld_u2 * 2);
   L.z = take(M * h->fr * 2);
-  L.g = take(M * h->fr * 2);
+  L.g = take(M * L.ld_g * 2);
   L.total = o;
   return L;
 }
@@ -218,13 +225,6 @@ static GemmArgs gargs(const void *A, const void *B, int M, int N, int K, int lda
   a.A = A; a.B = B; a.M = M; a.N = N; a.K = K; a.lda = lda; a.ldb = ldb; a.a_mn = a_mn; a.b_mn = b_mn; a.epi = epi;
   return a;
 }
-static merak_status run_colsum(merak_tmp_t *h, const bf16 *X, int ld, int m, int n, float *g) {
-  Launch L(h, MERAK_K_REDUCE, h->cs, 0.0, 2);
-  CK(h, colsum_sample(X, ld, h->s, m / h->s, n, h->part_col, h->cs));
-  CK(h, sample_reduce(h->part_col, 1, m / h->s, n, g, h->cs));
-  return MERAK_OK;
-}
-
 #define TRY(x)                          \
   do {                                  \
     merak_status _s = (x);              \
@@ -294,27 +294,35 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     if (h->chain_open) CK(h, cudaStreamWaitEvent(h->cs, h->prev_out[j], 0));
     const size_t r0 = (size_t)j * m;
     const bf16 *xj = x + r0 * hh;
-    bf16 *u = (bf16 *)S(L.u) + r0 * hh;
+    bf16 *u = (bf16 *)S(L.u) + r0 * L.ld_u;
     float *mean1 = (float *)S(L.mean1) + r0, *rstd1 = (float *)S(L.rstd1) + r0;
     bf16 *qkv = (bf16 *)S(L.qkv) + r0 * 3 * hr;
-    bf16 *ctx = (bf16 *)S(L.ctx) + r0 * hr;
+    bf16 *ctx = (bf16 *)S(L.ctx) + r0 * L.ld_ctx;
     float *lse = (float *)S(L.lse) + (size_t)j * b * h->Hr * h->s;
     {
+      // LN1, which also writes the ones-column pads of u, ctx, u2, g for these rows
+      OnesPad pad;
+      pad.n = 4;
+      pad.ptr[0] = u; pad.ld[0] = L.ld_u; pad.col[0] = hh;
+      pad.ptr[1] = ctx; pad.ld[1] = L.ld_ctx; pad.col[1] = hr;
+      pad.ptr[2] = (bf16 *)S(L.u2) + r0 * L.ld_u2; pad.ld[2] = L.ld_u2; pad.col[2] = hh;
+      pad.ptr[3] = (bf16 *)S(L.g) + r0 * L.ld_g; pad.ld[3] = L.ld_g; pad.col[3] = fr;
       Launch Lk(h, MERAK_K_LN, h->cs, 0.0);
-      CK(h, ln_fwd(xj, (const bf16 *)w->ln1_g, (const bf16 *)w->ln1_b, u, mean1, rstd1, m, hh, h->eps, h->cs));
+      CK(h, ln_fwd(xj, (const bf16 *)w->ln1_g, (const bf16 *)w->ln1_b, u, L.ld_u, mean1, rstd1, m, hh, h->eps, pad,
+                   h->cs));
     }
-    GemmArgs g = gargs(u, w->w_qkv, m, 3 * hr, hh, hh, hh, false, false, EPI_BIAS_BF16);
+    GemmArgs g = gargs(u, w->w_qkv, m, 3 * hr, hh, L.ld_u, hh, false, false, EPI_BIAS_BF16);
     g.out = qkv; g.ldo = 3 * hr; g.bias = w->b_qkv;
     TRY(run_gemm(h, g));
     {
       AttnArgs a;
       memset(&a, 0, sizeof(a));
-      a.qkv = qkv; a.ctx = ctx; a.lse = lse; a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
+      a.qkv = qkv; a.ctx = ctx; a.ld_ctx = L.ld_ctx; a.lse = lse; a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
       Launch Lk(h, MERAK_K_ATTN_FWD, h->cs, 2.0 * b * hr * (double)h->s * (h->s + 1));
       CK(h, attn_fwd(a, h->cs));
     }
     if (h->ev_ar_valid[0][j]) CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[0][j], 0));
-    g = gargs(ctx, w->w_o, m, hh, hr, hr, hr, false, false, EPI_STORE_BF16);
+    g = gargs(ctx, w->w_o, m, hh, hr, L.ld_ctx, hr, false, false, EPI_STORE_BF16);
     g.out = slot_ptr(h, h->r, 0) + r0 * hh; g.ldo = hh;
     TRY(run_gemm(h, g));
     CK(h, cudaEventRecord(h->ev_p[j], h->cs));
@@ -326,7 +334,8 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.T = ar_partials(h, comm, 0, r0, a.partial);
       a.m = m; a.h = hh; a.resid = xj; a.bias = (const bf16 *)w->b_o; a.out = (bf16 *)S(L.x1) + r0 * hh;
       a.do_ln = true; a.gamma = (const bf16 *)w->ln2_g; a.beta = (const bf16 *)w->ln2_b;
-      a.ln_out = (bf16 *)S(L.u2) + r0 * hh; a.mean = (float *)S(L.mean2) + r0; a.rstd = (float *)S(L.rstd2) + r0;
+      a.ln_out = (bf16 *)S(L.u2) + r0 * L.ld_u2; a.ld_ln = L.ld_u2;
+      a.mean = (float *)S(L.mean2) + r0; a.rstd = (float *)S(L.rstd2) + r0;
       a.eps = h->eps; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
@@ -339,13 +348,13 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
   for (int j = 0; j < n; ++j) {
     const size_t r0 = (size_t)j * m;
     CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[0][j], 0));
-    bf16 *u2 = (bf16 *)S(L.u2) + r0 * hh;
-    bf16 *z = (bf16 *)S(L.z) + r0 * fr, *gg = (bf16 *)S(L.g) + r0 * fr;
-    GemmArgs g = gargs(u2, w->w_1, m, fr, hh, hh, hh, false, false, EPI_BIAS_GELU);
-    g.out = z; g.ldo = fr; g.out2 = gg; g.ldo2 = fr; g.bias = w->b_1;
+    bf16 *u2 = (bf16 *)S(L.u2) + r0 * L.ld_u2;
+    bf16 *z = (bf16 *)S(L.z) + r0 * fr, *gg = (bf16 *)S(L.g) + r0 * L.ld_g;
+    GemmArgs g = gargs(u2, w->w_1, m, fr, hh, L.ld_u2, hh, false, false, EPI_BIAS_GELU);
+    g.out = z; g.ldo = fr; g.out2 = gg; g.ldo2 = L.ld_g; g.bias = w->b_1;
     TRY(run_gemm(h, g));
     if (h->ev_ar_valid[1][j]) CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[1][j], 0));
-    g = gargs(gg, w->w_2, m, hh, fr, fr, fr, false, false, EPI_STORE_BF16);
+    g = gargs(gg, w->w_2, m, hh, fr, L.ld_g, fr, false, false, EPI_STORE_BF16);
     g.out = slot_ptr(h, h->r, 1) + r0 * hh; g.ldo = hh;
     TRY(run_gemm(h, g));
     CK(h, cudaEventRecord(h->ev_p[j], h->cs));
@@ -365,6 +374,15 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     h->ev_ar_valid[1][j] = true;
   }
   return leave(h, st, flags, 1);
+}
+
+// wgrad: dW[M', N'] += A_s^T B_s over the sub-batch tokens, with the ones column of B_s giving the
+// bias gradient db[M'] in the same accumulation chain.
+static merak_status run_wgrad(merak_tmp_t *h, const bf16 *A, int lda, int Mo, const void *B, int ldb, int No, int m,
+                              float *dW, float *db) {
+  GemmArgs g = gargs(A, B, Mo, No + 1, m, lda, ldb, true, true, EPI_ACC_F32);
+  g.out32 = dW; g.ld32 = No; g.db32 = db;
+  return run_gemm(h, g);
 }
 
 // ------------------------------------------------------------------------------ backward
@@ -411,15 +429,9 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     }
     CK(h, cudaEventRecord(h->ev_ar[2][j], h->ms));
     h->ev_ar_valid[2][j] = true;
-    // weight / bias gradients of the FFN block for sub-batch j (overlap AR#3(j))
-    g = gargs(dyj, S(L.g) + r0 * fr * 2, hh, fr, m, hh, fr, true, true, EPI_ACC_F32);
-    g.out32 = gr->w_2; g.ld32 = fr;
-    TRY(run_gemm(h, g));
-    g = gargs(dz, S(L.u2) + r0 * hh * 2, fr, hh, m, fr, hh, true, true, EPI_ACC_F32);
-    g.out32 = gr->w_1; g.ld32 = hh;
-    TRY(run_gemm(h, g));
-    TRY(run_colsum(h, dz, fr, m, fr, gr->b_1));
-    TRY(run_colsum(h, dyj, hh, m, hh, gr->b_2));
+    // weight + bias gradients of the FFN block for sub-batch j (overlap AR#3(j))
+    TRY(run_wgrad(h, dyj, hh, hh, (const bf16 *)S(L.g) + r0 * L.ld_g, L.ld_g, fr, m, gr->w_2, gr->b_2));
+    TRY(run_wgrad(h, dz, fr, fr, (const bf16 *)S(L.u2) + r0 * L.ld_u2, L.ld_u2, hh, m, gr->w_1, gr->b_1));
   }
   // ---- attention block: proj dgrad -> attention bwd -> QKV dgrad (partial, slot 3) -> AR#4
   for (int j = 0; j < n; ++j) {
@@ -427,14 +439,14 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[2][j], 0));
     const bf16 *dx1 = h->dx1 + r0 * hh;
     bf16 *dctx = h->dctx + r0 * hr, *dqkv = h->dqkv + r0 * 3 * hr;
-    const bf16 *qkv = (const bf16 *)S(L.qkv) + r0 * 3 * hr, *ctx = (const bf16 *)S(L.ctx) + r0 * hr;
+    const bf16 *qkv = (const bf16 *)S(L.qkv) + r0 * 3 * hr, *ctx = (const bf16 *)S(L.ctx) + r0 * L.ld_ctx;
     GemmArgs g = gargs(dx1, w->w_o, m, hr, hh, hh, hr, false, true, EPI_STORE_BF16);
     g.out = dctx; g.ldo = hr;
     TRY(run_gemm(h, g));
     {
       AttnArgs a;
       memset(&a, 0, sizeof(a));
-      a.qkv = qkv; a.ctx = (void *)ctx; a.lse = (float *)S(L.lse) + (size_t)j * b * h->Hr * h->s;
+      a.qkv = qkv; a.ctx = (void *)ctx; a.ld_ctx = L.ld_ctx; a.lse = (float *)S(L.lse) + (size_t)j * b * h->Hr * h->s;
       a.dctx = dctx; a.dqkv = dqkv; a.delta = h->delta; a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
       Launch Lk(h, MERAK_K_ATTN_BWD, h->cs, 4.0 * b * hr * (double)h->s * (h->s + 1), 2);
       CK(h, attn_bwd(a, h->cs));
@@ -465,15 +477,9 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     }
     CK(h, cudaEventRecord(h->ev_ar[3][j], h->ms));
     h->ev_ar_valid[3][j] = true;
-    // weight / bias gradients of the attention block for sub-batch j (overlap AR#4(j))
-    g = gargs(dx1, ctx, hh, hr, m, hh, hr, true, true, EPI_ACC_F32);
-    g.out32 = gr->w_o; g.ld32 = hr;
-    TRY(run_gemm(h, g));
-    TRY(run_colsum(h, dx1, hh, m, hh, gr->b_o));
-    g = gargs(dqkv, S(L.u) + r0 * hh * 2, 3 * hr, hh, m, 3 * hr, hh, true, true, EPI_ACC_F32);
-    g.out32 = gr->w_qkv; g.ld32 = hh;
-    TRY(run_gemm(h, g));
-    TRY(run_colsum(h, dqkv, 3 * hr, m, 3 * hr, gr->b_qkv));
+    // weight + bias gradients of the attention block for sub-batch j (overlap AR#4(j))
+    TRY(run_wgrad(h, dx1, hh, hh, ctx, L.ld_ctx, hr, m, gr->w_o, gr->b_o));
+    TRY(run_wgrad(h, dqkv, 3 * hr, 3 * hr, (const bf16 *)S(L.u) + r0 * L.ld_u, L.ld_u, hh, m, gr->w_qkv, gr->b_qkv));
   }
   return leave(h, st, flags, 3);
 }
@@ -499,7 +505,7 @@ static merak_status validate(const merak_tmp_config *c) {
     return fail(nullptr, MERAK_EUNSUPPORTED, "head dim %d not in {32,64,80,96,128}", d);
   if (T != 1 && T != 2 && T != 4 && T != 8) return fail(nullptr, MERAK_EUNSUPPORTED, "tmp_degree not in {1,2,4,8}");
   if (c->seq_len % 16) return fail(nullptr, MERAK_EUNSUPPORTED, "seq_len must be a multiple of 16");
-  if (c->microbatch > 256) return fail(nullptr, MERAK_EUNSUPPORTED, "microbatch > 256");
+  if (c->microbatch > 48) return fail(nullptr, MERAK_EUNSUPPORTED, "microbatch > 48");
   if (c->hidden % 8 || (f / T) % 8) return fail(nullptr, MERAK_EUNSUPPORTED, "h and f/T must be multiples of 8");
   if (c->precision == MERAK_FP32_CHECK) return fail(nullptr, MERAK_EUNSUPPORTED, "fp32 check mode not built yet");
   return MERAK_OK;
@@ -751,17 +757,17 @@ int64_t merak_tmp_launch_count(const merak_tmp_t *h) { return h ? h->launches : 
 // ------------------------------------------------------------------------------ testing entry points
 int merak_test_gemm(const void *A, const void *B, int M, int N, int K, int lda, int ldb, int a_mn, int b_mn, int epi,
                     void *out, int ldo, void *out2, int ldo2, const void *bias, const void *aux, int ld_aux,
-                    float *out32, int ld32, int max_ctas, void *stream) {
+                    float *out32, int ld32, float *db32, int max_ctas, void *stream) {
   GemmArgs a = gargs(A, B, M, N, K, lda, ldb, a_mn != 0, b_mn != 0, epi);
   a.out = out; a.ldo = ldo; a.out2 = out2; a.ldo2 = ldo2; a.bias = bias; a.aux = aux; a.ld_aux = ld_aux;
-  a.out32 = out32; a.ld32 = ld32; a.max_ctas = max_ctas;
+  a.out32 = out32; a.ld32 = ld32; a.db32 = db32; a.max_ctas = max_ctas;
   return (int)gemm(a, (cudaStream_t)stream);
 }
 
 int merak_test_attn_fwd(const void *qkv, void *ctx, float *lse, int b, int s, int heads, int d, void *stream) {
   AttnArgs a;
   memset(&a, 0, sizeof(a));
-  a.qkv = qkv; a.ctx = ctx; a.lse = lse; a.b = b; a.s = s; a.heads = heads; a.d = d;
+  a.qkv = qkv; a.ctx = ctx; a.lse = lse; a.b = b; a.s = s; a.heads = heads; a.d = d; a.ld_ctx = heads * d;
   return (int)attn_fwd(a, (cudaStream_t)stream);
 }
 
@@ -770,13 +776,15 @@ int merak_test_attn_bwd(const void *qkv, const void *ctx, const float *lse, cons
   AttnArgs a;
   memset(&a, 0, sizeof(a));
   a.qkv = qkv; a.ctx = (void *)ctx; a.lse = (float *)lse; a.dctx = dctx; a.dqkv = dqkv; a.delta = delta;
-  a.b = b; a.s = s; a.heads = heads; a.d = d;
+  a.b = b; a.s = s; a.heads = heads; a.d = d; a.ld_ctx = heads * d;
   return (int)attn_bwd(a, (cudaStream_t)stream);
 }
 
 int merak_test_ln_fwd(const void *x, const void *gamma, const void *beta, void *u, float *mean, float *rstd, int m,
                       int h, float eps, void *stream) {
-  return (int)ln_fwd((const bf16 *)x, (const bf16 *)gamma, (const bf16 *)beta, (bf16 *)u, mean, rstd, m, h, eps,
+  OnesPad pad;
+  memset(&pad, 0, sizeof(pad));
+  return (int)ln_fwd((const bf16 *)x, (const bf16 *)gamma, (const bf16 *)beta, (bf16 *)u, h, mean, rstd, m, h, eps, pad,
                      (cudaStream_t)stream);
 }
 
@@ -789,6 +797,7 @@ int merak_test_ar_fwd(const void *const *partials, int T, int m, int h, const vo
   for (int q = 0; q < T; ++q) a.partial[q] = (const bf16 *)partials[q];
   a.T = T; a.m = m; a.h = h; a.resid = (const bf16 *)resid; a.bias = (const bf16 *)bias; a.out = (bf16 *)out;
   a.do_ln = do_ln != 0; a.gamma = (const bf16 *)gamma; a.beta = (const bf16 *)beta; a.ln_out = (bf16 *)ln_out;
+  a.ld_ln = h;
   a.mean = mean; a.rstd = rstd; a.eps = eps; a.ctas = ctas;
   PeerSync ps;
   memset(&ps, 0, sizeof(ps));

@@ -181,12 +181,13 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnArgs a) {
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
   const float i0 = 1.f / l0, i1 = 1.f / l1;
-  __nv_bfloat16 *ctx = reinterpret_cast<__nv_bfloat16 *>(a.ctx) + (size_t)bi * s * hr + head * D;
+  const int lc = a.ld_ctx;
+  __nv_bfloat16 *ctx = reinterpret_cast<__nv_bfloat16 *>(a.ctx) + (size_t)bi * s * lc + head * D;
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     const int c = nt * 8 + 2 * tq;
-    if (qi0 < s) *reinterpret_cast<uint32_t *>(ctx + (size_t)qi0 * hr + c) = pack_bf16(o[nt][0] * i0, o[nt][1] * i0);
-    if (qi1 < s) *reinterpret_cast<uint32_t *>(ctx + (size_t)qi1 * hr + c) = pack_bf16(o[nt][2] * i1, o[nt][3] * i1);
+    if (qi0 < s) *reinterpret_cast<uint32_t *>(ctx + (size_t)qi0 * lc + c) = pack_bf16(o[nt][0] * i0, o[nt][1] * i0);
+    if (qi1 < s) *reinterpret_cast<uint32_t *>(ctx + (size_t)qi1 * lc + c) = pack_bf16(o[nt][2] * i1, o[nt][3] * i1);
   }
   if (tq == 0) {
     float *lse = a.lse + ((size_t)bi * H + head) * s;
@@ -215,7 +216,7 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(AttnArgs a) {
   const int hr = H * D, ld = 3 * hr;
   const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(a.qkv) + (size_t)bi * s * ld;
   const __nv_bfloat16 *dO = reinterpret_cast<const __nv_bfloat16 *>(a.dctx) + (size_t)bi * s * hr;
-  const __nv_bfloat16 *O = reinterpret_cast<const __nv_bfloat16 *>(a.ctx) + (size_t)bi * s * hr;
+  const __nv_bfloat16 *O = reinterpret_cast<const __nv_bfloat16 *>(a.ctx) + (size_t)bi * s * a.ld_ctx;
   const int cq = head * D, ck = hr + head * D, cv = 2 * hr + head * D;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
   const float scale = 1.f / sqrtf((float)D), sl2 = 1.4426950408889634f * scale;
@@ -232,7 +233,8 @@ __global__ void __launch_bounds__(128) attn_bwd_dq_kernel(AttnArgs a) {
     float acc = 0.f;
     if (qi < s) {
       for (int c = lane; c < D; c += 32)
-        acc += __bfloat162float(dO[(size_t)qi * hr + head * D + c]) * __bfloat162float(O[(size_t)qi * hr + head * D + c]);
+        acc += __bfloat162float(dO[(size_t)qi * hr + head * D + c]) *
+               __bfloat162float(O[(size_t)qi * a.ld_ctx + head * D + c]);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);

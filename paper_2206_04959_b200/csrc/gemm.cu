@@ -47,6 +47,8 @@ struct EpiParams {
   int ld_aux;
   float *out32;
   int ld32;
+  float *db32;  // EPI_ACC_F32: column n_main (the ones column of B) accumulates into db32[m]
+  int n_main;
 };
 
 template <int EPI>
@@ -57,12 +59,14 @@ MK_DEV void epi_store_chunk(const EpiParams &p, int gm, int gn0, const uint32_t 
   const bool full = (gn0 + 32 <= p.N);
   if constexpr (EPI == EPI_ACC_F32) {
     float *dst = p.out32 + (size_t)gm * p.ld32 + gn0;
-    if (full && (p.ld32 % 4 == 0)) {
+    if (gn0 + 32 <= p.n_main && (p.ld32 % 4 == 0)) {
 #pragma unroll
       for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     } else {
-      for (int i = 0; i < 32; ++i)
-        if (gn0 + i < p.N) dst[i] = v[i];
+      for (int i = 0; i < 32; ++i) {
+        if (gn0 + i < p.n_main) dst[i] = v[i];
+        else if (gn0 + i == p.n_main && p.db32) p.db32[gm] = v[i];
+      }
     }
     return;
   } else {
@@ -240,7 +244,7 @@ __global__ void __launch_bounds__(256, 1)
         const int gn0 = tn * BN + c * 32;
         uint32_t r[32];
         const float *src = p.out32 + (size_t)gm * p.ld32 + gn0;
-        if (gm < p.M && gn0 + 32 <= p.N && (p.ld32 % 4 == 0)) {
+        if (gm < p.M && gn0 + 32 <= p.n_main && (p.ld32 % 4 == 0)) {
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
             float4 f = *reinterpret_cast<const float4 *>(src + i);
@@ -249,7 +253,14 @@ __global__ void __launch_bounds__(256, 1)
           }
         } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = (gm < p.M && gn0 + i < p.N) ? __float_as_uint(src[i]) : 0u;
+          for (int i = 0; i < 32; ++i) {
+            float val = 0.f;
+            if (gm < p.M) {
+              if (gn0 + i < p.n_main) val = src[i];
+              else if (gn0 + i == p.n_main && p.db32) val = p.db32[gm];
+            }
+            r[i] = __float_as_uint(val);
+          }
         }
         tmem_st32(row_base + buf * BN + c * 32, r);
       }
@@ -391,6 +402,8 @@ cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   p.bias = (const __nv_bfloat16 *)a.bias;
   p.aux = (const __nv_bfloat16 *)a.aux; p.ld_aux = a.ld_aux;
   p.out32 = a.out32; p.ld32 = a.ld32;
+  p.db32 = a.db32;
+  p.n_main = a.db32 ? a.N - 1 : a.N;
   return BN == 256 ? dispatch<256>(a, ma, mb, p, st) : dispatch<128>(a, ma, mb, p, st);
 }
 

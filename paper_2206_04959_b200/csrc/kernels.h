@@ -40,6 +40,8 @@ struct GemmArgs {
   int ld_aux;
   float *out32;      // fp32 [M, ld32] (EPI_ACC_F32)
   int ld32;
+  float *db32;       // EPI_ACC_F32 with a ones column: N includes it as the last column, whose
+                     // accumulator goes to db32[M] (bias gradient = A^T 1) instead of out32
   int max_ctas;      // persistent grid cap (0 = all SMs)
 };
 cudaError_t gemm(const GemmArgs &a, cudaStream_t st);
@@ -56,6 +58,7 @@ struct AttnArgs {
   void *dqkv;        // bf16 [b*s, 3*hr]        (bwd out)
   float *delta;      // [b, H_r, s] rowsum(dO*O) workspace (bwd)
   int b, s, heads, d;
+  int ld_ctx;        // row stride of ctx (elements; >= heads*d)
 };
 cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st);
 cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st);  // 2 launches: dQ (+delta), then dK/dV
@@ -88,6 +91,7 @@ struct ArFwdArgs {
   bool do_ln;
   const __nv_bfloat16 *gamma, *beta;
   __nv_bfloat16 *ln_out;
+  int ld_ln;                            // row stride of ln_out
   float *mean, *rstd;
   float eps;
   int ctas;
@@ -104,15 +108,23 @@ struct ArBwdArgs {
   const __nv_bfloat16 *dres;    // residual-path gradient (dy or dx1)     [m, h]
   __nv_bfloat16 *dx;            // out: dres + LN^T(sum partials)          [m, h]
   float *part_dg, *part_db;     // out: per-group column partials [m/G, h]
-  int G;                        // rows per group (16 if h <= 3072 else 8)
+  int G;                        // rows per group (8; divides s)
   int ctas;
 };
 cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st);
 int ar_bwd_group_rows(int h);
 
-// LayerNorm forward of x (bf16 [m,h]) -> u (bf16), mean/rstd (fp32)
+// LayerNorm forward of x (bf16 [m,h]) -> u (bf16, row stride ld_u), mean/rstd (fp32).
+// Optionally writes the 8-wide pad [1, 0, ..., 0] at column pad_col[k] of rows of pad_ptr[k] (row
+// stride pad_ld[k]) for k < npad: the "ones column" of saved activations that turns each wgrad
+// GEMM into dW | db (bias gradient = dY^T 1).
+struct OnesPad {
+  __nv_bfloat16 *ptr[4];
+  int ld[4], col[4];
+  int n;
+};
 cudaError_t ln_fwd(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bfloat16 *b, __nv_bfloat16 *u,
-                   float *mean, float *rstd, int m, int h, float eps, cudaStream_t st);
+                   int ld_u, float *mean, float *rstd, int m, int h, float eps, const OnesPad &pad, cudaStream_t st);
 
 // Token reductions with a per-sample fixed structure (bit-identical across sub-batch splits):
 // Q[i][c] = fixed-order sum of the s rows of sample i of X (bf16, row stride ld), i < b

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) ar_fwd_kernel(ArFwdArgs a, PeerSync ps) {
         load8(a.beta + c * 8, bt);
 #pragma unroll
         for (int i = 0; i < 8; ++i) q[i] = (q[i] - mean) * rstd * gm[i] + bt[i];
-        store8(a.ln_out + ro + c * 8, q);
+        store8(a.ln_out + (size_t)row * a.ld_ln + c * 8, q);
       }
       if (lane == 0) {
         a.mean[row] = mean;
@@ -221,8 +221,9 @@ __global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
 
 // ------------------------------------------------------------------------------ LayerNorm forward
 __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16 *x, const __nv_bfloat16 *gamma,
-                                                     const __nv_bfloat16 *beta, __nv_bfloat16 *u, float *mean_out,
-                                                     float *rstd_out, int m, int h, float eps) {
+                                                     const __nv_bfloat16 *beta, __nv_bfloat16 *u, int ld_u,
+                                                     float *mean_out, float *rstd_out, int m, int h, float eps,
+                                                     OnesPad pad) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int row = blockIdx.x * nw + warp;
   if (row >= m) return;
@@ -251,7 +252,15 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16 *x, con
     load8(beta + c * 8, bt);
 #pragma unroll
     for (int i = 0; i < 8; ++i) q[i] = (q[i] - mean) * rstd * gm[i] + bt[i];
-    store8(u + ro + c * 8, q);
+    store8(u + (size_t)row * ld_u + c * 8, q);
+  }
+  if (lane < pad.n) {
+    uint4 one;
+    one.x = pack_bf16(1.f, 0.f);
+    one.y = one.z = one.w = 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k == lane) *reinterpret_cast<uint4 *>(pad.ptr[k] + (size_t)row * pad.ld[k] + pad.col[k]) = one;
   }
   if (lane == 0) {
     mean_out[row] = mean;
@@ -301,24 +310,31 @@ __global__ void __launch_bounds__(256) colsum_sample_kernel(const __nv_bfloat16 
   }
 }
 
-// g[c] += sum_i ( part[i*gps][c] + part[i*gps+1][c] + ... + part[i*gps+gps-1][c] ),  i = 0..b-1 in order
+// g[c] += sum_i Q_i[c], i = 0..b-1 in order, where Q_i[c] = sum over the gps partial rows of sample i
+// in a fixed tree: thread ty adds rows k = ty, ty+8, ... (sequential), then the 8 thread sums are
+// added in order ty = 0..7.  The structure depends only on the sample, never on the sub-batch split.
 __global__ void __launch_bounds__(256) sample_reduce_kernel(const float *part, int gps, int b, int n, float *g) {
-  extern __shared__ float q[];  // [b][32]
+  extern __shared__ float q[];  // [b][8][32]
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int c = blockIdx.x * 32 + tx;
-  for (int i = ty; i < b; i += 8) {
+  for (int i = 0; i < b; ++i) {
     float acc = 0.f;
     if (c < n) {
       const float *p = part + (size_t)i * gps * n + c;
-#pragma unroll 8
-      for (int k = 0; k < gps; ++k) acc += p[(size_t)k * n];
+#pragma unroll 4
+      for (int k = ty; k < gps; k += 8) acc += p[(size_t)k * n];
     }
-    q[i * 32 + tx] = acc;
+    q[(i * 8 + ty) * 32 + tx] = acc;
   }
   __syncthreads();
   if (ty == 0 && c < n) {
     float a = g[c];
-    for (int i = 0; i < b; ++i) a += q[i * 32 + tx];
+    for (int i = 0; i < b; ++i) {
+      float t = q[(i * 8) * 32 + tx];
+#pragma unroll
+      for (int y = 1; y < 8; ++y) t += q[(i * 8 + y) * 32 + tx];
+      a += t;
+    }
     g[c] = a;
   }
 }
@@ -349,7 +365,7 @@ cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-int ar_bwd_group_rows(int h) { return h <= 3072 ? 16 : 8; }
+int ar_bwd_group_rows(int h) { return 8; }
 
 cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
   const size_t smem = (size_t)a.G * a.h * sizeof(float);
@@ -378,8 +394,8 @@ cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
 }
 
 cudaError_t ln_fwd(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bfloat16 *b, __nv_bfloat16 *u,
-                   float *mean, float *rstd, int m, int h, float eps, cudaStream_t st) {
-  ln_fwd_kernel<<<(m + 7) / 8, 256, 0, st>>>(x, g, b, u, mean, rstd, m, h, eps);
+                   int ld_u, float *mean, float *rstd, int m, int h, float eps, const OnesPad &pad, cudaStream_t st) {
+  ln_fwd_kernel<<<(m + 7) / 8, 256, 0, st>>>(x, g, b, u, ld_u, mean, rstd, m, h, eps, pad);
   return cudaGetLastError();
 }
 
@@ -391,7 +407,7 @@ cudaError_t colsum_sample(const __nv_bfloat16 *X, int ld, int s, int b, int n, f
 }
 
 cudaError_t sample_reduce(const float *part, int gps, int b, int n, float *g, cudaStream_t st) {
-  const size_t smem = (size_t)b * 32 * sizeof(float);
+  const size_t smem = (size_t)b * 8 * 32 * sizeof(float);
   if (smem > 48 * 1024) return cudaErrorInvalidValue;
   sample_reduce_kernel<<<(n + 31) / 32, dim3(32, 8), smem, st>>>(part, gps, b, n, g);
   return cudaGetLastError();

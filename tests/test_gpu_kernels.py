@@ -35,12 +35,13 @@ def gelu_grad_ref(z):
     return 0.5 * (1 + t) + 0.5 * z * (1 - t * t) * c * (1 + 3 * 0.044715 * z * z)
 
 
-def run_gemm(A, B, M, N, K, a_mn, b_mn, epi, bias=None, aux=None, out32=None, max_ctas=0):
+def run_gemm(A, B, M, N, K, a_mn, b_mn, epi, bias=None, aux=None, out32=None, max_ctas=0, db32=None, ldb=None):
     dev = A.device
     out = torch.zeros(M, N, dtype=torch.bfloat16, device=dev)
     out2 = torch.zeros(M, N, dtype=torch.bfloat16, device=dev)
-    err = lib().merak_test_gemm(P(A), P(B), M, N, K, A.shape[1], B.shape[1], int(a_mn), int(b_mn), epi, P(out), N,
-                                P(out2), N, P(bias), P(aux), N, P(out32), N, max_ctas, S())
+    ld32 = N - 1 if db32 is not None else N
+    err = lib().merak_test_gemm(P(A), P(B), M, N, K, A.shape[1], ldb or B.shape[1], int(a_mn), int(b_mn), epi,
+                                P(out), N, P(out2), N, P(bias), P(aux), N, P(out32), ld32, P(db32), max_ctas, S())
     assert err == 0, err
     torch.cuda.synchronize()
     return out, out2
@@ -98,6 +99,29 @@ def test_gemm_wgrad_accumulate_and_split_bit_identity(M, N, K):
         run_gemm(As[:k1], Bs[:k1], M, N, k1, True, True, 4, out32=C2)
         run_gemm(As[k1:], Bs[k1:], M, N, K - k1, True, True, 4, out32=C2)
         assert torch.equal(C, C2)
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 64, 32), (1600, 1600, 4096), (1600, 6400, 256), (96, 136, 48)])
+def test_gemm_wgrad_ones_column_bias_grad(M, N, K):
+    """wgrad with the ones column: B_s [K, N+8] whose column N is 1 (the saved-activation pad) gives
+    dW += A_s^T B_s[:, :N] and db += A_s^T 1 = column sums of A_s, split bit-identically."""
+    g = torch.Generator(device="cuda").manual_seed(K * 3 + N)
+    As = torch.randn(K, M, device="cuda", generator=g).bfloat16()
+    Bp = torch.zeros(K, N + 8, device="cuda").bfloat16()
+    Bp[:, :N] = torch.randn(K, N, device="cuda", generator=g).bfloat16()
+    Bp[:, N] = 1.0
+    C0 = torch.randn(M, N, device="cuda", generator=g)
+    d0 = torch.randn(M, device="cuda", generator=g)
+    C, d = C0.clone(), d0.clone()
+    run_gemm(As, Bp, M, N + 1, K, True, True, 4, out32=C, db32=d, ldb=N + 8)
+    assert rel(C, C0.double() + As.double().T @ Bp[:, :N].double()) < 1e-5
+    assert rel(d, d0.double() + As.double().sum(0)) < 1e-5
+    if K % 32 == 0:
+        C2, d2 = C0.clone(), d0.clone()
+        k1 = K // 2
+        run_gemm(As[:k1], Bp[:k1], M, N + 1, k1, True, True, 4, out32=C2, db32=d2, ldb=N + 8)
+        run_gemm(As[k1:], Bp[k1:], M, N + 1, K - k1, True, True, 4, out32=C2, db32=d2, ldb=N + 8)
+        assert torch.equal(C, C2) and torch.equal(d, d2)
 
 
 def test_gemm_reduction_order_independent_of_m():
@@ -203,7 +227,7 @@ def test_allreduce_bwd_fake_peers(T, m, h):
     dg = torch.randn(h, device="cuda", generator=g)
     db = torch.randn(h, device="cuda", generator=g)
     dg0, db0 = dg.clone(), db.clone()
-    G = 16 if h <= 3072 else 8
+    G = 8
     ws = torch.zeros(2 * (m // G) * h, device="cuda")
     arr = _ptr_array(parts)
     s = 32 if m % 32 == 0 else m  # rows per sample

@@ -1,0 +1,61 @@
+"""Summarise ncu outputs for profiles/: per-kernel launch table from a --metrics gpu__time_duration.sum
+CSV, and key metrics per kernel from a --set full report (via `ncu -i ... --page raw --csv`)."""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+
+def launches(path, steps=5):
+    rows = list(csv.reader(open(path)))
+    hdr, data = None, []
+    for r in rows:
+        if "Kernel Name" in r:
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            data.append(dict(zip(hdr, r)))
+    agg = collections.defaultdict(list)
+    for d in data:
+        if d.get("Metric Name") == "gpu__time_duration.sum":
+            agg[d["Kernel Name"].split("(")[0][:70]].append(float(d["Metric Value"].replace(",", "")) / 1e3)
+    tot = sum(sum(v) for v in agg.values())
+    out = ["| kernel | launches | total us | avg us | share |", "|---|---|---|---|---|"]
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        out.append(f"| `{k}` | {len(v)} | {sum(v):.1f} | {sum(v) / len(v):.1f} | {100 * sum(v) / tot:.1f}% |")
+    out.append(f"| total | {sum(len(v) for v in agg.values())} | {tot:.1f} | | |")
+    return "\n".join(out)
+
+
+METRICS = ["gpu__time_duration.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_tensor.avg.pct_of_peak_sustained_active",
+           "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+           "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+           "launch__registers_per_thread", "launch__grid_size", "sm__cycles_elapsed.avg.per_second",
+           "lts__t_bytes.sum", "l1tex__throughput.avg.pct_of_peak_sustained_active"]
+
+
+def full(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr = rows[0]
+    out = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        item = {"kernel": d.get("Kernel Name", "")[:80], "grid": d.get("Grid Size"), "block": d.get("Block Size")}
+        for m in METRICS:
+            for k in d:
+                if k.startswith(m):
+                    item[m] = d[k]
+                    break
+        out.append(item)
+    return out
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        print(launches(sys.argv[2]))
+    else:
+        for it in full(sys.argv[2]):
+            print(it)
