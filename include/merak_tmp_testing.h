@@ -38,13 +38,13 @@ int merak_test_ar_fwd(const void *const *partials, int T, int m, int h, const vo
 
 /* Backward all-reduce epilogue (fake peers): dx = dres + LN^T(sum_r partial[r]); dgamma/dbeta
  * (fp32 [h]) += per-sample fixed-order token sums (s = rows per sample, m % s == 0, s % 16 == 0).
- * ws: fp32 workspace of 2*(m/8)*h floats (LN-gradient partials per 8-row group). */
+ * ws: fp32 workspace of 2*(m/8)*h + 2*(m/s)*h floats. */
 int merak_test_ar_bwd(const void *const *partials, int T, int m, int s, int h, const void *x_ln, const float *mean,
                       const float *rstd, const void *gamma, const void *dres, void *dx, float *dgamma, float *dbeta,
                       float *ws, int ctas, void *stream);
 
 /* g[c] += sum_i X[i, c] over m rows = m/s samples of s rows, per-sample fixed order then a chain over
- * samples; ws: fp32 [(m/s) * n]. */
+ * samples; ws: fp32 [2 * (m/s) * n]. */
 int merak_test_colsum(const void *X, int ld, int m, int s, int n, float *g, float *ws, void *stream);
 
 #ifdef __cplusplus

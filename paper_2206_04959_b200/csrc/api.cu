@@ -163,9 +163,11 @@ struct Launch {
 };
 
 // ------------------------------------------------------------------------------ shapes / layout
-// The four activations that are the B operand of a wgrad GEMM (u, ctx, u2, g) carry an 8-wide pad
-// [1, 0, ..., 0] after their K columns (row stride K + 8): the wgrad GEMM then has one extra output
-// column that is the bias gradient dY^T 1, on the same MMA accumulation chain (bit-identity rule v).
+// The four activations that are the B operand of a wgrad GEMM (u, ctx, u2, g) carry a pad whose
+// first element is 1 after their K columns: the wgrad GEMM then has one extra output column, the
+// bias gradient dY^T 1, on the same MMA accumulation chain (bit-identity rule v).  The row stride
+// is rounded up to 128 B (64 bf16) past K so every TMA row stays 128-B aligned.
+static int padded_ld(int K) { return ((K + 1 + 63) / 64) * 64; }
 struct SavedLayout {
   size_t u, mean1, rstd1, qkv, ctx, lse, x1, mean2, rstd2, u2, z, g, total;
   int ld_u, ld_ctx, ld_u2, ld_g;
@@ -175,9 +177,9 @@ static SavedLayout saved_layout(const merak_tmp_t *h) {
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t at = o; o += align256(bytes); return at; };
   const size_t M = h->M;
-  L.ld_u = L.ld_u2 = h->h + 8;
-  L.ld_ctx = h->hr + 8;
-  L.ld_g = h->fr + 8;
+  L.ld_u = L.ld_u2 = padded_ld(h->h);
+  L.ld_ctx = padded_ld(h->hr);
+  L.ld_g = padded_ld(h->fr);
   L.u = take(M * L.ld_u * 2);
   L.mean1 = take(M * 4);
   L.rstd1 = take(M * 4);
@@ -424,8 +426,8 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
         CK(h, ar_bwd(a, ps, h->ms));
       }
       Launch Lk(h, MERAK_K_REDUCE, h->ms, 0.0, 2);
-      CK(h, sample_reduce(h->part_lng, h->s / h->G, m / h->s, hh, gr->ln2_g, h->ms));
-      CK(h, sample_reduce(h->part_lnb, h->s / h->G, m / h->s, hh, gr->ln2_b, h->ms));
+      CK(h, sample_reduce2(h->part_lng, h->part_lnb, h->s / h->G, m / h->s, hh, h->part_col,
+                           h->part_col + (size_t)h->B * hh, gr->ln2_g, gr->ln2_b, h->ms));
     }
     CK(h, cudaEventRecord(h->ev_ar[2][j], h->ms));
     h->ev_ar_valid[2][j] = true;
@@ -472,8 +474,8 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
         CK(h, ar_bwd(a, ps, h->ms));
       }
       Launch Lk(h, MERAK_K_REDUCE, h->ms, 0.0, 2);
-      CK(h, sample_reduce(h->part_lng, h->s / h->G, m / h->s, hh, gr->ln1_g, h->ms));
-      CK(h, sample_reduce(h->part_lnb, h->s / h->G, m / h->s, hh, gr->ln1_b, h->ms));
+      CK(h, sample_reduce2(h->part_lng, h->part_lnb, h->s / h->G, m / h->s, hh, h->part_col,
+                           h->part_col + (size_t)h->B * hh, gr->ln1_g, gr->ln1_b, h->ms));
     }
     CK(h, cudaEventRecord(h->ev_ar[3][j], h->ms));
     h->ev_ar_valid[3][j] = true;
@@ -598,7 +600,7 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
     const size_t o_dz = take(M * h->fr * 2), o_dx1 = take(M * h->h * 2), o_dctx = take(M * h->hr * 2);
     const size_t o_dqkv = take(M * 3 * h->hr * 2), o_delta = take((size_t)h->B * h->Hr * h->s * 4);
     const int ncol = std::max(std::max(3 * h->hr, h->fr), h->h);
-    const size_t o_pc = take((size_t)h->B * ncol * 4);
+    const size_t o_pc = take(2 * (size_t)h->B * ncol * 4);
     const size_t o_pg = take((M / h->G) * (size_t)h->h * 4), o_pb = take((M / h->G) * (size_t)h->h * 4);
     CKI(cudaMalloc(&h->ws, o));
     h->dz = (bf16 *)(h->ws + o_dz); h->dx1 = (bf16 *)(h->ws + o_dx1); h->dctx = (bf16 *)(h->ws + o_dctx);
@@ -820,15 +822,17 @@ int merak_test_ar_bwd(const void *const *partials, int T, int m, int s, int h, c
   memset(&ps, 0, sizeof(ps));
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = ar_bwd(a, ps, st);
-  if (e == cudaSuccess) e = sample_reduce(a.part_dg, s / a.G, m / s, h, dgamma, st);
-  if (e == cudaSuccess) e = sample_reduce(a.part_db, s / a.G, m / s, h, dbeta, st);
+  float *q = ws + 2 * (size_t)(m / a.G) * h;
+  if (e == cudaSuccess)
+    e = sample_reduce2(a.part_dg, a.part_db, s / a.G, m / s, h, q, q + (size_t)(m / s) * h, dgamma, dbeta, st);
   return (int)e;
 }
 
 int merak_test_colsum(const void *X, int ld, int m, int s, int n, float *g, float *ws, void *stream) {
   if (m % s) return (int)cudaErrorInvalidValue;
   cudaError_t e = colsum_sample((const bf16 *)X, ld, s, m / s, n, ws, (cudaStream_t)stream);
-  if (e == cudaSuccess) e = sample_reduce(ws, 1, m / s, n, g, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = sample_reduce2(ws, nullptr, 1, m / s, n, ws + (size_t)(m / s) * n, nullptr, g, nullptr,
+                                           (cudaStream_t)stream);
   return (int)e;
 }
 

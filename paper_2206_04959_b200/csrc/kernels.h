@@ -129,7 +129,9 @@ cudaError_t ln_fwd(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bf
 // Token reductions with a per-sample fixed structure (bit-identical across sub-batch splits):
 // Q[i][c] = fixed-order sum of the s rows of sample i of X (bf16, row stride ld), i < b
 cudaError_t colsum_sample(const __nv_bfloat16 *X, int ld, int s, int b, int n, float *Q, cudaStream_t st);
-// g[c] += sum over samples i (in order) of the fixed-order sum of part[i*gps .. i*gps+gps-1][c]
-cudaError_t sample_reduce(const float *part, int gps, int b, int n, float *g, cudaStream_t st);
+// g_t[c] += sum over samples i (in order) of the fixed-tree sum of p_t[i*gps .. i*gps+gps-1][c],
+// for t = 0 and (if p1) t = 1; q0/q1: fp32 workspace [b * n] each.  Two launches.
+cudaError_t sample_reduce2(const float *p0, const float *p1, int gps, int b, int n, float *q0, float *q1, float *g0,
+                           float *g1, cudaStream_t st);
 
 }  // namespace mk

@@ -310,32 +310,50 @@ __global__ void __launch_bounds__(256) colsum_sample_kernel(const __nv_bfloat16 
   }
 }
 
-// g[c] += sum_i Q_i[c], i = 0..b-1 in order, where Q_i[c] = sum over the gps partial rows of sample i
-// in a fixed tree: thread ty adds rows k = ty, ty+8, ... (sequential), then the 8 thread sums are
-// added in order ty = 0..7.  The structure depends only on the sample, never on the sub-batch split.
-__global__ void __launch_bounds__(256) sample_reduce_kernel(const float *part, int gps, int b, int n, float *g) {
-  extern __shared__ float q[];  // [b][8][32]
+// Q_t[i][c] (t < 2 arrays) = fixed-tree sum over the gps partial rows of sample i: thread ty adds
+// rows k = ty, ty+8, ... (sequential), then the 8 thread sums are added in order ty = 0..7.
+// The structure depends only on the sample, never on the sub-batch split.
+__global__ void __launch_bounds__(256) sample_sum_kernel(const float *p0, const float *p1, int gps, int n, float *q0,
+                                                         float *q1) {
+  __shared__ float red[2][8][32];
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int c = blockIdx.x * 32 + tx;
-  for (int i = 0; i < b; ++i) {
-    float acc = 0.f;
-    if (c < n) {
-      const float *p = part + (size_t)i * gps * n + c;
+  const int c = blockIdx.x * 32 + tx, i = blockIdx.y;
+  float a0 = 0.f, a1 = 0.f;
+  if (c < n) {
+    const size_t base = (size_t)i * gps * n + c;
 #pragma unroll 4
-      for (int k = ty; k < gps; k += 8) acc += p[(size_t)k * n];
+    for (int k = ty; k < gps; k += 8) {
+      a0 += p0[base + (size_t)k * n];
+      if (p1) a1 += p1[base + (size_t)k * n];
     }
-    q[(i * 8 + ty) * 32 + tx] = acc;
   }
+  red[0][ty][tx] = a0;
+  red[1][ty][tx] = a1;
   __syncthreads();
   if (ty == 0 && c < n) {
-    float a = g[c];
-    for (int i = 0; i < b; ++i) {
-      float t = q[(i * 8) * 32 + tx];
+    float t0 = red[0][0][tx], t1 = red[1][0][tx];
 #pragma unroll
-      for (int y = 1; y < 8; ++y) t += q[(i * 8 + y) * 32 + tx];
-      a += t;
+    for (int y = 1; y < 8; ++y) {
+      t0 += red[0][y][tx];
+      t1 += red[1][y][tx];
     }
-    g[c] = a;
+    q0[(size_t)i * n + c] = t0;
+    if (p1) q1[(size_t)i * n + c] = t1;
+  }
+}
+
+// g_t[c] = ((g_t[c] + Q_t[0][c]) + Q_t[1][c]) + ...   (chain over samples in order; it continues
+// across sub-batch launches through the fp32 gradient itself)
+__global__ void sample_chain_kernel(const float *q0, const float *q1, int b, int n, float *g0, float *g1) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  float a = g0[c];
+  for (int i = 0; i < b; ++i) a += q0[(size_t)i * n + c];
+  g0[c] = a;
+  if (q1) {
+    float e = g1[c];
+    for (int i = 0; i < b; ++i) e += q1[(size_t)i * n + c];
+    g1[c] = e;
   }
 }
 
@@ -406,10 +424,13 @@ cudaError_t colsum_sample(const __nv_bfloat16 *X, int ld, int s, int b, int n, f
   return cudaGetLastError();
 }
 
-cudaError_t sample_reduce(const float *part, int gps, int b, int n, float *g, cudaStream_t st) {
-  const size_t smem = (size_t)b * 8 * 32 * sizeof(float);
-  if (smem > 48 * 1024) return cudaErrorInvalidValue;
-  sample_reduce_kernel<<<(n + 31) / 32, dim3(32, 8), smem, st>>>(part, gps, b, n, g);
+cudaError_t sample_reduce2(const float *p0, const float *p1, int gps, int b, int n, float *q0, float *q1, float *g0,
+                           float *g1, cudaStream_t st) {
+  dim3 grid((n + 31) / 32, b);
+  sample_sum_kernel<<<grid, dim3(32, 8), 0, st>>>(p0, p1, gps, n, q0, q1);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  sample_chain_kernel<<<(n + 127) / 128, 128, 0, st>>>(q0, p1 ? q1 : nullptr, b, n, g0, g1);
   return cudaGetLastError();
 }
 

@@ -228,7 +228,7 @@ def test_allreduce_bwd_fake_peers(T, m, h):
     db = torch.randn(h, device="cuda", generator=g)
     dg0, db0 = dg.clone(), db.clone()
     G = 8
-    ws = torch.zeros(2 * (m // G) * h, device="cuda")
+    ws = torch.zeros(2 * (m // G) * h + 2 * m * h, device="cuda")
     arr = _ptr_array(parts)
     s = 32 if m % 32 == 0 else m  # rows per sample
     assert lib().merak_test_ar_bwd(arr, T, m, s, h, P(x), P(mean), P(rstd), P(ga), P(dres), P(dx), P(dg), P(db),
@@ -251,7 +251,7 @@ def test_colsum_fixed_order_bit_identity():
     g1 = torch.randn(320, device="cuda", generator=g)
     g2 = g1.clone()
     ref = g1.double() + X.double().sum(0)
-    ws = torch.zeros(512 // 64 * 320, device="cuda")
+    ws = torch.zeros(2 * 512 // 64 * 320, device="cuda")
     assert lib().merak_test_colsum(P(X), 320, 512, 64, 320, P(g1), P(ws), S()) == 0
     for j in range(4):  # the same 8 samples of 64 rows in four sub-batches
         assert lib().merak_test_colsum(P(X[j * 128:]), 320, 128, 64, 320, P(g2), P(ws), S()) == 0
