@@ -16,21 +16,27 @@
 //             64-wide MN chunks BLOCK_K*128 = 8 KB apart (LBO)
 #include <cuda.h>
 #include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "kernels.h"
 #include "ptx.cuh"
 
 namespace mk {
 
-constexpr int BM = 128;
+constexpr int BM = 128;  // rows of A per CTA (TMEM lanes)
 constexpr int BK = 64;
 
-template <int BN>
+// CG = CTAs per MMA (cta_group): CG = 2 pairs two SMs on a 256 x BN tile (each CTA stages its
+// 128 rows of A and BN/2 rows of B; the leader issues tcgen05.mma.cta_group::2).
+template <int CG, int BN>
 struct GemmCfg {
-  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int BNC = BN / CG;  // B rows staged per CTA
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = BNC * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (CG == 2 ? 160 : 192) * 1024 / STAGE_BYTES > 6 ? 6
+                                                                               : (CG == 2 ? 160 : 192) * 1024 / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
@@ -132,11 +138,12 @@ MK_DEV void epi_store_chunk(const EpiParams &p, int gm, int gn0, const uint32_t 
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int CG, int BN, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(256, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams p) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<CG, BN>;
   constexpr int S = C::STAGES;
+  constexpr int BMT = BM * CG;  // tile rows
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *smA = smem;
@@ -147,7 +154,9 @@ __global__ void __launch_bounds__(256, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int tiles_m = (p.M + BM - 1) / BM;
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+  const int cl = blockIdx.x / CG, ncl = gridDim.x / CG;
+  const int tiles_m = (p.M + BMT - 1) / BMT;
   const int tiles_n = (p.N + BN - 1) / BN;
   const int ntiles = tiles_m * tiles_n;
   const int nk = (p.K + BK - 1) / BK;
@@ -161,53 +170,69 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tfree[i], 4);
+      mbar_init(&tfree[i], 4 * CG);
     }
     fence_mbar_init();
     fence_proxy_async();
   }
-  if (warp == 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == 2) {
+    if constexpr (CG == 2)
+      tmem_alloc2<C::TMEM_COLS>(tmem_slot);
+    else
+      tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ---------------- TMA producer
+    // ---------------- TMA producer (both CTAs of a pair load their own halves)
     int it = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int tile = cl; tile < ntiles; tile += ncl) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
+      const int row0 = tm * BMT + rank * BM;
+      const int n0 = tn * BN + rank * C::BNC;
       for (int kb = 0; kb < nk; ++kb, ++it) {
         const int s = it % S;
         const uint32_t ph = (it / S) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         if (lane == 0) {
-          mbar_expect_tx(&full[s], C::STAGE_BYTES);
+          if (rank == 0) mbar_expect_tx(&full[s], C::STAGE_BYTES * CG);
           uint8_t *a = smA + s * C::A_BYTES;
           uint8_t *b = smB + s * C::B_BYTES;
+          auto load = [&](void *dst, const CUtensorMap *m, int c0, int c1) {
+            if constexpr (CG == 2)
+              tma_load_2d_cg2(dst, m, &full[s], c0, c1);
+            else
+              tma_load_2d(dst, m, &full[s], c0, c1);
+          };
           if constexpr (!A_MN) {
-            tma_load_2d(a, &tmA, &full[s], kb * BK, tm * BM);
+            load(a, &tmA, kb * BK, row0);
           } else {
 #pragma unroll
-            for (int c = 0; c < BM / 64; ++c) tma_load_2d(a + c * 8192, &tmA, &full[s], tm * BM + c * 64, kb * BK);
+            for (int c = 0; c < BM / 64; ++c) load(a + c * 8192, &tmA, row0 + c * 64, kb * BK);
           }
           if constexpr (!B_MN) {
-            tma_load_2d(b, &tmB, &full[s], kb * BK, tn * BN);
+            load(b, &tmB, kb * BK, n0);
           } else {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c) tma_load_2d(b + c * 8192, &tmB, &full[s], tn * BN + c * 64, kb * BK);
+            for (int c = 0; c < C::BNC / 64; ++c) load(b + c * 8192, &tmB, n0 + c * 64, kb * BK);
           }
         }
         __syncwarp();
       }
     }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer
-    constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
+  } else if (warp == 1 && rank == 0) {
+    // ---------------- MMA issuer (leader CTA)
+    constexpr uint32_t idesc = idesc_bf16(BMT, BN, A_MN, B_MN);
     constexpr uint32_t a_lbo = A_MN ? 8192u : 16u, a_sbo = 1024u, a_kstep = A_MN ? 2048u : 32u;
     constexpr uint32_t b_lbo = B_MN ? 8192u : 16u, b_sbo = 1024u, b_kstep = B_MN ? 2048u : 32u;
     int it = 0, lt = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+    for (int tile = cl; tile < ntiles; tile += ncl, ++lt) {
       const int buf = lt & 1;
       mbar_wait(&tfree[buf], (lt >> 1) & 1);
       tc_fence_after();
@@ -224,21 +249,41 @@ __global__ void __launch_bounds__(256, 1)
             const uint64_t ad = sdesc_sw128(a0 + kk * a_kstep, a_lbo, a_sbo);
             const uint64_t bd = sdesc_sw128(b0 + kk * b_kstep, b_lbo, b_sbo);
             const uint32_t acc = (EPI == EPI_ACC_F32 || kb > 0 || kk > 0) ? 1u : 0u;
-            tc_mma_f16(d_tmem, ad, bd, idesc, acc);
+            if constexpr (CG == 2)
+              tc_mma_f16_cg2(d_tmem, ad, bd, idesc, acc);
+            else
+              tc_mma_f16(d_tmem, ad, bd, idesc, acc);
           }
-          tc_commit(&empty[s]);
-          if (kb == nk - 1) tc_commit(&tfull[buf]);
+          if constexpr (CG == 2) {
+            tc_commit_cg2_mc(&empty[s], 0x3);
+            if (kb == nk - 1) tc_commit_cg2_mc(&tfull[buf], 0x3);
+          } else {
+            tc_commit(&empty[s]);
+            if (kb == nk - 1) tc_commit(&tfull[buf]);
+          }
         }
         __syncwarp();
       }
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue
+    // ---------------- epilogue (each CTA drains its own 128 TMEM lanes = its 128 rows of the tile)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const uint32_t row_base = tmem_base + ((uint32_t)(q * 32) << 16);
+    const uint32_t tfree_leader[2] = {CG == 2 ? mapa_shared(&tfree[0], 0) : 0u,
+                                      CG == 2 ? mapa_shared(&tfree[1], 0) : 0u};
+    auto release = [&](int buf) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          mbar_arrive_cluster(tfree_leader[buf]);
+        else
+          mbar_arrive(&tfree[buf]);
+      }
+    };
     auto preload = [&](int tile, int buf) {
       const int tm = tile % tiles_m, tn = tile / tiles_m;
-      const int gm = tm * BM + q * 32 + lane;
+      const int gm = tm * BMT + rank * BM + q * 32 + lane;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         const int gn0 = tn * BN + c * 32;
@@ -269,19 +314,17 @@ __global__ void __launch_bounds__(256, 1)
     // initial release of both accumulator buffers (after preloading C for ACC mode)
 #pragma unroll 1
     for (int bb = 0; bb < 2; ++bb) {
-      const int tile = blockIdx.x + bb * gridDim.x;
+      const int tile = cl + bb * ncl;
       if (EPI == EPI_ACC_F32 && tile < ntiles) preload(tile, bb);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tfree[bb]);
+      release(bb);
     }
     int lt = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+    for (int tile = cl; tile < ntiles; tile += ncl, ++lt) {
       const int buf = lt & 1;
       mbar_wait(&tfull[buf], (lt >> 1) & 1);
       tc_fence_after();
       const int tm = tile % tiles_m, tn = tile / tiles_m;
-      const int gm = tm * BM + q * 32 + lane;
+      const int gm = tm * BMT + rank * BM + q * 32 + lane;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         const int gn0 = tn * BN + c * 32;
@@ -291,20 +334,25 @@ __global__ void __launch_bounds__(256, 1)
         tmem_ld_wait();
         if (gm < p.M) epi_store_chunk<EPI>(p, gm, gn0, r);
       }
-      tc_fence_before();
-      const int next = tile + 2 * gridDim.x;
+      const int next = tile + 2 * ncl;
       if (EPI == EPI_ACC_F32 && next < ntiles) {
-        preload(next, buf);
         tc_fence_before();
+        preload(next, buf);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tfree[buf]);
+      release(buf);
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  if constexpr (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<C::TMEM_COLS>(tmem_base);
+    if constexpr (CG == 2)
+      tmem_dealloc2<C::TMEM_COLS>(tmem_base);
+    else
+      tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
 }
 
@@ -349,51 +397,74 @@ int gemm_num_sms() {
   return n;
 }
 
-template <int BN, bool A_MN, bool B_MN, int EPI>
+template <int CG, int BN, bool A_MN, bool B_MN, int EPI>
 static cudaError_t launch(const GemmArgs &a, const CUtensorMap &ma, const CUtensorMap &mb, const EpiParams &p,
                           cudaStream_t st) {
-  using C = GemmCfg<BN>;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, EPI>;
+  using C = GemmCfg<CG, BN>;
+  auto kern = gemm_kernel<CG, BN, A_MN, B_MN, EPI>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int ntiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
-  int grid = a.max_ctas > 0 ? a.max_ctas : gemm_num_sms();
-  if (grid > ntiles) grid = ntiles;
-  kern<<<grid, 256, C::SMEM, st>>>(ma, mb, p);
-  return cudaGetLastError();
+  const int ntiles = ((a.M + BM * CG - 1) / (BM * CG)) * ((a.N + BN - 1) / BN);
+  int clusters = (a.max_ctas > 0 ? a.max_ctas : gemm_num_sms()) / CG;
+  if (clusters > ntiles) clusters = ntiles;
+  if (clusters < 1) clusters = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(clusters * CG);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = CG;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ma, mb, p);
 }
 
-template <int BN>
+template <int CG, int BN>
 static cudaError_t dispatch(const GemmArgs &a, const CUtensorMap &ma, const CUtensorMap &mb, const EpiParams &p,
                            cudaStream_t st) {
   if (!a.a_mn && !a.b_mn) {
     switch (a.epi) {
-      case EPI_STORE_BF16: return launch<BN, false, false, EPI_STORE_BF16>(a, ma, mb, p, st);
-      case EPI_BIAS_BF16: return launch<BN, false, false, EPI_BIAS_BF16>(a, ma, mb, p, st);
-      case EPI_BIAS_GELU: return launch<BN, false, false, EPI_BIAS_GELU>(a, ma, mb, p, st);
+      case EPI_STORE_BF16: return launch<CG, BN, false, false, EPI_STORE_BF16>(a, ma, mb, p, st);
+      case EPI_BIAS_BF16: return launch<CG, BN, false, false, EPI_BIAS_BF16>(a, ma, mb, p, st);
+      case EPI_BIAS_GELU: return launch<CG, BN, false, false, EPI_BIAS_GELU>(a, ma, mb, p, st);
     }
   } else if (!a.a_mn && a.b_mn) {
     switch (a.epi) {
-      case EPI_STORE_BF16: return launch<BN, false, true, EPI_STORE_BF16>(a, ma, mb, p, st);
-      case EPI_GELU_BWD: return launch<BN, false, true, EPI_GELU_BWD>(a, ma, mb, p, st);
+      case EPI_STORE_BF16: return launch<CG, BN, false, true, EPI_STORE_BF16>(a, ma, mb, p, st);
+      case EPI_GELU_BWD: return launch<CG, BN, false, true, EPI_GELU_BWD>(a, ma, mb, p, st);
     }
   } else if (a.a_mn && a.b_mn) {
-    if (a.epi == EPI_ACC_F32) return launch<BN, true, true, EPI_ACC_F32>(a, ma, mb, p, st);
+    if (a.epi == EPI_ACC_F32) return launch<CG, BN, true, true, EPI_ACC_F32>(a, ma, mb, p, st);
   }
   return cudaErrorNotSupported;
 }
 
+static int gemm_cg() {
+  static int cg = 0;
+  if (!cg) {
+    const char *e = getenv("MERAK_GEMM_CG");
+    cg = (e && atoi(e) == 1) ? 1 : 2;
+  }
+  return cg;
+}
+
 cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaErrorInvalidValue;
+  const int cg = gemm_cg();
   const int BN = (a.N > 128) ? 256 : 128;
+  const int bnc = BN / cg;  // B rows staged per CTA
   CUtensorMap ma, mb;
   // A: K-major stored [M, K]; MN-major stored [K, M]
   bool ok = a.a_mn ? make_map(&ma, a.A, a.K, a.M, a.lda, BK) : make_map(&ma, a.A, a.M, a.K, a.lda, BM);
-  ok = ok && (a.b_mn ? make_map(&mb, a.B, a.K, a.N, a.ldb, BK) : make_map(&mb, a.B, a.N, a.K, a.ldb, BN));
+  ok = ok && (a.b_mn ? make_map(&mb, a.B, a.K, a.N, a.ldb, BK) : make_map(&mb, a.B, a.N, a.K, a.ldb, bnc));
   if (!ok) return cudaErrorInvalidValue;
   EpiParams p;
   p.M = a.M; p.N = a.N; p.K = a.K; p.epi = a.epi;
@@ -404,7 +475,8 @@ cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   p.out32 = a.out32; p.ld32 = a.ld32;
   p.db32 = a.db32;
   p.n_main = a.db32 ? a.N - 1 : a.N;
-  return BN == 256 ? dispatch<256>(a, ma, mb, p, st) : dispatch<128>(a, ma, mb, p, st);
+  if (cg == 2) return BN == 256 ? dispatch<2, 256>(a, ma, mb, p, st) : dispatch<2, 128>(a, ma, mb, p, st);
+  return BN == 256 ? dispatch<1, 256>(a, ma, mb, p, st) : dispatch<1, 128>(a, ma, mb, p, st);
 }
 
 }  // namespace mk
