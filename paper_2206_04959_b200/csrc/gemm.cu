@@ -37,7 +37,7 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (CG == 2 ? 160 : 192) * 1024 / STAGE_BYTES > 6 ? 6
                                                                                : (CG == 2 ? 160 : 192) * 1024 / STAGE_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;  // power of two >= 2 accumulators
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
@@ -447,6 +447,40 @@ static cudaError_t dispatch(const GemmArgs &a, const CUtensorMap &ma, const CUte
   return cudaErrorNotSupported;
 }
 
+// Forward-GEMM tile widths other than 128/256 (B K-major only: MN-major B needs 64-wide chunks).
+template <int BN>
+static cudaError_t dispatch_kk(const GemmArgs &a, const CUtensorMap &ma, const CUtensorMap &mb, const EpiParams &p,
+                              cudaStream_t st) {
+  switch (a.epi) {
+    case EPI_STORE_BF16: return launch<2, BN, false, false, EPI_STORE_BF16>(a, ma, mb, p, st);
+    case EPI_BIAS_BF16: return launch<2, BN, false, false, EPI_BIAS_BF16>(a, ma, mb, p, st);
+    case EPI_BIAS_GELU: return launch<2, BN, false, false, EPI_BIAS_GELU>(a, ma, mb, p, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+// Tile width minimising the persistent schedule's makespan: ceil(tiles / clusters) waves of a
+// tile costing ~ (BN + 32) (fixed per-tile overhead).  Never depends on M's split into sub-batches
+// in a way that changes reduction order (tiling in N never does).
+static int pick_bn(const GemmArgs &a, int cg) {
+  if (a.N <= 128) return 128;
+  if (cg != 2 || a.b_mn || a.a_mn) return 256;
+  const int clusters = (a.max_ctas > 0 ? a.max_ctas : gemm_num_sms()) / 2;
+  const int tm = (a.M + 255) / 256;
+  int best = 256;
+  double best_cost = 1e30;
+  const int cands[] = {256, 224, 192, 160, 128};
+  for (int bn : cands) {
+    const long tiles = (long)tm * ((a.N + bn - 1) / bn);
+    const double cost = (double)((tiles + clusters - 1) / clusters) * (bn + 32);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  return best;
+}
+
 static int gemm_cg() {
   static int cg = 0;
   if (!cg) {
@@ -459,7 +493,7 @@ static int gemm_cg() {
 cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaErrorInvalidValue;
   const int cg = gemm_cg();
-  const int BN = (a.N > 128) ? 256 : 128;
+  const int BN = pick_bn(a, cg);
   const int bnc = BN / cg;  // B rows staged per CTA
   CUtensorMap ma, mb;
   // A: K-major stored [M, K]; MN-major stored [K, M]
@@ -475,7 +509,15 @@ cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   p.out32 = a.out32; p.ld32 = a.ld32;
   p.db32 = a.db32;
   p.n_main = a.db32 ? a.N - 1 : a.N;
-  if (cg == 2) return BN == 256 ? dispatch<2, 256>(a, ma, mb, p, st) : dispatch<2, 128>(a, ma, mb, p, st);
+  if (cg == 2) {
+    switch (BN) {
+      case 256: return dispatch<2, 256>(a, ma, mb, p, st);
+      case 224: return dispatch_kk<224>(a, ma, mb, p, st);
+      case 192: return dispatch_kk<192>(a, ma, mb, p, st);
+      case 160: return dispatch_kk<160>(a, ma, mb, p, st);
+      default: return dispatch<2, 128>(a, ma, mb, p, st);
+    }
+  }
   return BN == 256 ? dispatch<1, 256>(a, ma, mb, p, st) : dispatch<1, 128>(a, ma, mb, p, st);
 }
 
