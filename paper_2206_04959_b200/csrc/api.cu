@@ -215,7 +215,10 @@ static bf16 *slot_ptr(merak_tmp_t *h, int rank, int slot) {
 }
 
 // ------------------------------------------------------------------------------ kernel wrappers
-static merak_status run_gemm(merak_tmp_t *h, const GemmArgs &a) {
+static merak_status run_gemm(merak_tmp_t *h, const GemmArgs &a0) {
+  GemmArgs a = a0;
+  // T > 1: keep smem free on every SM for the all-reduce kernels that overlap the GEMMs
+  a.smem_kb = h->T > 1 ? 160 : 192;
   Launch L(h, MERAK_K_GEMM, h->cs, 2.0 * a.M * a.N * a.K);
   CK(h, gemm(a, h->cs));
   return MERAK_OK;

@@ -13,6 +13,7 @@
 // Round-1 implementation uses mma.sync m16n8k16 (HMMA); attention is 2.7-5.1 % of the layer's
 // FLOPs at the BASELINE configs.  A tcgen05/TMEM version is the next step.
 #include <math.h>
+#include <stdlib.h>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -504,7 +505,17 @@ static cudaError_t bwd_d(const AttnArgs &a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+static bool use_tc() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("MERAK_ATTN_TC");  // tcgen05 forward: opt-in until it beats mma.sync
+    v = (e && atoi(e) == 1) ? 1 : 0;
+  }
+  return v == 1;
+}
+
 cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st) {
+  if (use_tc()) return attn_fwd_tc(a, st);
   switch (a.d) {
     case 32: return fwd_d<32>(a, st);
     case 64: return fwd_d<64>(a, st);

@@ -29,14 +29,13 @@ constexpr int BK = 64;
 
 // CG = CTAs per MMA (cta_group): CG = 2 pairs two SMs on a 256 x BN tile (each CTA stages its
 // 128 rows of A and BN/2 rows of B; the leader issues tcgen05.mma.cta_group::2).
-template <int CG, int BN>
+template <int CG, int BN, int SMEM_KB = (CG == 2 ? 160 : 192)>
 struct GemmCfg {
   static constexpr int BNC = BN / CG;  // B rows staged per CTA
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BNC * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (CG == 2 ? 160 : 192) * 1024 / STAGE_BYTES > 6 ? 6
-                                                                               : (CG == 2 ? 160 : 192) * 1024 / STAGE_BYTES;
+  static constexpr int STAGES = SMEM_KB * 1024 / STAGE_BYTES > 8 ? 8 : SMEM_KB * 1024 / STAGE_BYTES;
   static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;  // power of two >= 2 accumulators
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };
@@ -59,6 +58,10 @@ struct EpiParams {
 
 template <int EPI>
 MK_DEV void epi_store_chunk(const EpiParams &p, int gm, int gn0, const uint32_t (&r)[32]) {
+  if constexpr (EPI == 5) {  // microbenchmark variant: drain TMEM, store nothing
+    if (r[0] == 0x7fc00001u && gm < 0) p.out[0] = __float2bfloat16_rn(0.f);
+    return;
+  }
   float v[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -138,10 +141,10 @@ MK_DEV void epi_store_chunk(const EpiParams &p, int gm, int gn0, const uint32_t 
   }
 }
 
-template <int CG, int BN, bool A_MN, bool B_MN, int EPI>
+template <int CG, int BN, bool A_MN, bool B_MN, int EPI, int SMEM_KB>
 __global__ void __launch_bounds__(256, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams p) {
-  using C = GemmCfg<CG, BN>;
+  using C = GemmCfg<CG, BN, SMEM_KB>;
   constexpr int S = C::STAGES;
   constexpr int BMT = BM * CG;  // tile rows
   extern __shared__ uint8_t smem_raw[];
@@ -397,11 +400,11 @@ int gemm_num_sms() {
   return n;
 }
 
-template <int CG, int BN, bool A_MN, bool B_MN, int EPI>
+template <int CG, int BN, bool A_MN, bool B_MN, int EPI, int SMEM_KB = (CG == 2 ? 160 : 192)>
 static cudaError_t launch(const GemmArgs &a, const CUtensorMap &ma, const CUtensorMap &mb, const EpiParams &p,
                           cudaStream_t st) {
-  using C = GemmCfg<CG, BN>;
-  auto kern = gemm_kernel<CG, BN, A_MN, B_MN, EPI>;
+  using C = GemmCfg<CG, BN, SMEM_KB>;
+  auto kern = gemm_kernel<CG, BN, A_MN, B_MN, EPI, SMEM_KB>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -427,34 +430,24 @@ static cudaError_t launch(const GemmArgs &a, const CUtensorMap &ma, const CUtens
   return cudaLaunchKernelEx(&cfg, kern, ma, mb, p);
 }
 
-template <int CG, int BN>
+template <int CG, int BN, int KB>
 static cudaError_t dispatch(const GemmArgs &a, const CUtensorMap &ma, const CUtensorMap &mb, const EpiParams &p,
                            cudaStream_t st) {
   if (!a.a_mn && !a.b_mn) {
     switch (a.epi) {
-      case EPI_STORE_BF16: return launch<CG, BN, false, false, EPI_STORE_BF16>(a, ma, mb, p, st);
-      case EPI_BIAS_BF16: return launch<CG, BN, false, false, EPI_BIAS_BF16>(a, ma, mb, p, st);
-      case EPI_BIAS_GELU: return launch<CG, BN, false, false, EPI_BIAS_GELU>(a, ma, mb, p, st);
+      case EPI_STORE_BF16: return launch<CG, BN, false, false, EPI_STORE_BF16, KB>(a, ma, mb, p, st);
+      case EPI_BIAS_BF16: return launch<CG, BN, false, false, EPI_BIAS_BF16, KB>(a, ma, mb, p, st);
+      case EPI_BIAS_GELU: return launch<CG, BN, false, false, EPI_BIAS_GELU, KB>(a, ma, mb, p, st);
     }
   } else if (!a.a_mn && a.b_mn) {
+    if (BN == 192) return cudaErrorNotSupported;  // MN-major B stages 64-wide chunks per CTA
     switch (a.epi) {
-      case EPI_STORE_BF16: return launch<CG, BN, false, true, EPI_STORE_BF16>(a, ma, mb, p, st);
-      case EPI_GELU_BWD: return launch<CG, BN, false, true, EPI_GELU_BWD>(a, ma, mb, p, st);
+      case EPI_STORE_BF16: return launch<CG, BN, false, true, EPI_STORE_BF16, KB>(a, ma, mb, p, st);
+      case EPI_GELU_BWD: return launch<CG, BN, false, true, EPI_GELU_BWD, KB>(a, ma, mb, p, st);
     }
   } else if (a.a_mn && a.b_mn) {
-    if (a.epi == EPI_ACC_F32) return launch<CG, BN, true, true, EPI_ACC_F32>(a, ma, mb, p, st);
-  }
-  return cudaErrorNotSupported;
-}
-
-// Forward-GEMM tile widths other than 128/256 (B K-major only: MN-major B needs 64-wide chunks).
-template <int BN>
-static cudaError_t dispatch_kk(const GemmArgs &a, const CUtensorMap &ma, const CUtensorMap &mb, const EpiParams &p,
-                              cudaStream_t st) {
-  switch (a.epi) {
-    case EPI_STORE_BF16: return launch<2, BN, false, false, EPI_STORE_BF16>(a, ma, mb, p, st);
-    case EPI_BIAS_BF16: return launch<2, BN, false, false, EPI_BIAS_BF16>(a, ma, mb, p, st);
-    case EPI_BIAS_GELU: return launch<2, BN, false, false, EPI_BIAS_GELU>(a, ma, mb, p, st);
+    if (BN == 192) return cudaErrorNotSupported;
+    if (a.epi == EPI_ACC_F32) return launch<CG, BN, true, true, EPI_ACC_F32, KB>(a, ma, mb, p, st);
   }
   return cudaErrorNotSupported;
 }
@@ -469,7 +462,7 @@ static int pick_bn(const GemmArgs &a, int cg) {
   const int tm = (a.M + 255) / 256;
   int best = 256;
   double best_cost = 1e30;
-  const int cands[] = {256, 224, 192, 160, 128};
+  const int cands[] = {256, 192, 128};
   for (int bn : cands) {
     const long tiles = (long)tm * ((a.N + bn - 1) / bn);
     const double cost = (double)((tiles + clusters - 1) / clusters) * (bn + 32);
@@ -493,7 +486,7 @@ static int gemm_cg() {
 cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaErrorInvalidValue;
   const int cg = gemm_cg();
-  const int BN = pick_bn(a, cg);
+  const int BN = a.epi >= 5 ? 256 : pick_bn(a, cg);
   const int bnc = BN / cg;  // B rows staged per CTA
   CUtensorMap ma, mb;
   // A: K-major stored [M, K]; MN-major stored [K, M]
@@ -509,16 +502,27 @@ cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   p.out32 = a.out32; p.ld32 = a.ld32;
   p.db32 = a.db32;
   p.n_main = a.db32 ? a.N - 1 : a.N;
+  if (cg == 2 && a.epi >= 5 && !a.a_mn && !a.b_mn) {  // microbenchmark-only variants
+    if (a.epi == 5) return launch<2, 256, false, false, 5>(a, ma, mb, p, st);            // no stores
+    if (a.epi == 6) return launch<2, 256, false, false, EPI_STORE_BF16, 192>(a, ma, mb, p, st);  // 6 stages
+    return cudaErrorNotSupported;
+  }
   if (cg == 2) {
+    // deep ring (192 KB) unless kernels on the communication stream must co-reside (smem_kb hint)
+    if (a.smem_kb == 160) {
+      switch (BN) {
+        case 256: return dispatch<2, 256, 160>(a, ma, mb, p, st);
+        case 192: return dispatch<2, 192, 160>(a, ma, mb, p, st);
+        default: return dispatch<2, 128, 160>(a, ma, mb, p, st);
+      }
+    }
     switch (BN) {
-      case 256: return dispatch<2, 256>(a, ma, mb, p, st);
-      case 224: return dispatch_kk<224>(a, ma, mb, p, st);
-      case 192: return dispatch_kk<192>(a, ma, mb, p, st);
-      case 160: return dispatch_kk<160>(a, ma, mb, p, st);
-      default: return dispatch<2, 128>(a, ma, mb, p, st);
+      case 256: return dispatch<2, 256, 192>(a, ma, mb, p, st);
+      case 192: return dispatch<2, 192, 192>(a, ma, mb, p, st);
+      default: return dispatch<2, 128, 192>(a, ma, mb, p, st);
     }
   }
-  return BN == 256 ? dispatch<1, 256>(a, ma, mb, p, st) : dispatch<1, 128>(a, ma, mb, p, st);
+  return BN == 256 ? dispatch<1, 256, 192>(a, ma, mb, p, st) : dispatch<1, 128, 192>(a, ma, mb, p, st);
 }
 
 }  // namespace mk

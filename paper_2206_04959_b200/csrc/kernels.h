@@ -43,6 +43,8 @@ struct GemmArgs {
   float *db32;       // EPI_ACC_F32 with a ones column: N includes it as the last column, whose
                      // accumulator goes to db32[M] (bias gradient = A^T 1) instead of out32
   int max_ctas;      // persistent grid cap (0 = all SMs)
+  int smem_kb;       // smem budget of the TMA ring: 192 (default) or 160 (leave room for co-resident
+                     // all-reduce kernels when T > 1)
 };
 cudaError_t gemm(const GemmArgs &a, cudaStream_t st);
 int gemm_num_sms();
@@ -60,7 +62,8 @@ struct AttnArgs {
   int b, s, heads, d;
   int ld_ctx;        // row stride of ctx (elements; >= heads*d)
 };
-cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st);
+cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st);     // tcgen05 version if MERAK_ATTN_TC=1
+cudaError_t attn_fwd_tc(const AttnArgs &a, cudaStream_t st);  // attention_tc.cu
 cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st);  // 2 launches: dQ (+delta), then dK/dV
 
 // ---------------------------------------------------------------- LN / all-reduce / reductions (ln_ar.cu)

@@ -65,5 +65,44 @@ def main():
                       "total_us": tot_t * 1e6, "gemms": out}))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not os.environ.get("VARIANTS"):
     main()
+
+
+def variants():
+    """qkv shape: default vs 6-stage (192 KB) vs no-store epilogue vs cuBLAS (torch.matmul)."""
+    M, N, K = int(os.environ.get("VM", 4096)), int(os.environ.get("VN", 4800)), int(os.environ.get("VK", 1600))
+    A = torch.randn(M, K, device="cuda").bfloat16()
+    B = torch.randn(N, K, device="cuda").bfloat16()
+    o = torch.empty(M, N, device="cuda").bfloat16()
+    flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    res = {}
+
+    def tm(fn):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(10):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ts.sort()
+        t = ts[len(ts) // 2]
+        return {"us": round(t * 1e3, 2), "tflops": round(2 * M * N * K / (t * 1e-3) / 1e12, 1)}
+    for name, epi in (("default_bn256", 6 if False else 0), ("stages192KB", 6), ("no_store", 5)):
+        def run(epi=epi):
+            e = lib().merak_test_gemm(P(A), P(B), M, N, K, K, K, 0, 0, epi, P(o), N, None, N, None, None, N, None, N,
+                                      None, 0, st)
+            assert e == 0, e
+        res[name] = tm(run)
+    res["cublas"] = tm(lambda: torch.matmul(A, B.T, out=o))
+    print(json.dumps({"M": M, "N": N, "K": K, "variants": res}))
+
+
+if __name__ == "__main__" and os.environ.get("VARIANTS"):
+    variants()
