@@ -4,13 +4,15 @@
 python bench.py --gpus N --steps K --warmup W            (N > 1: launched by torchrun, one rank per GPU)
 python bench.py --impl reference ...                      (the fp64 CPU oracle as the reference arm)
 
-One step = one layer forward + backward (every SURVEY §8(a) row: LN1, QKV, attention, proj, AR#1 +
-LN2, fc1 + GeLU, fc2, AR#2, and the backward mirror with AR#3/AR#4 and all weight gradients) over
-one microbatch of the BASELINE.json configs[1] workload (GPT-1.5B-shaped layer: h=1600, H=25,
-s=1024, B=8) with the TMP degree T = N (rank r holds shard r; strong scaling: the layer is fixed).
+One step = forward + backward of a stack of K (default 4) chained layers with distinct weights (every
+SURVEY §8(a) row: LN1, QKV, attention, proj, AR#1 + LN2, fc1 + GeLU, fc2, AR#2, and the backward
+mirror with AR#3/AR#4 and all weight gradients), so the all-reduce of one layer overlaps the next
+layer's first sub-batch, over one microbatch of the BASELINE.json configs[1] workload
+(GPT-1.5B-shaped layer: h=1600, H=25, s=1024, B=8) with the TMP degree T = N (rank r holds shard r;
+strong scaling: the model is fixed).
 Inputs are synthetic (synth/), resident in HBM; L2 is flushed (256 MiB write) between timed steps,
 outside the timed events.  value = whole-job algorithmic TFLOP/s of the layer ((72Bsh^2 +
-6Bhs(s+1)) FLOPs per step / device time, max over ranks).  Rank 0 prints ONE JSON line.
+6Bhs(s+1)) x K FLOPs per step / device time, max over ranks).  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -32,6 +34,7 @@ def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--layers", type=int, default=4, help="K chained layers per step (distinct weights)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="merak", choices=["merak", "reference"])
     ap.add_argument("--config", default="gpt1.5b")
@@ -70,7 +73,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
@@ -180,8 +183,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2206_04959_b200 import FLAG_NO_COMM, TmpLayer, shard_weights, zero_grads_like
-    from synth import make_all
+    from paper_2206_04959_b200 import FLAG_CHAIN, FLAG_NO_COMM, TmpLayer, shard_weights, zero_grads_like
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -189,16 +191,19 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
-    params, x, dy = make_all(cfg)
-    w = shard_weights(params, cfg.heads, T, rank, dev)
+    K = args.layers
+    from synth import make_activations, make_params
+    x, dy = make_activations(cfg)
+    ws = [shard_weights(make_params(cfg, layer=k), cfg.heads, T, rank, dev) for k in range(K)]
     M, h = cfg.tokens, cfg.hidden
     X = torch.as_tensor(x.reshape(M, h)).to(dev, torch.bfloat16)
     DY = torch.as_tensor(dy.reshape(M, h)).to(dev, torch.bfloat16)
-    Y, DX = torch.empty_like(X), torch.empty_like(X)
-    grads = zero_grads_like(w)
+    Ys = [torch.empty_like(X) for _ in range(K)]      # Ys[k] = output of layer k = input of layer k+1
+    DXs = [torch.empty_like(X) for _ in range(K)]     # DXs[k] = dL/d(input of layer k)
+    grads = [zero_grads_like(w) for w in ws]
     layer = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, tmp_degree=T, tmp_rank=rank, n_sub=n_sub,
                      comm_ctas=args.comm_ctas, device=local, group=group)
-    saved = layer.new_saved()
+    saved = [layer.new_saved() for _ in range(K)]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -207,9 +212,17 @@ def main():
         if world > 1:
             dist.barrier()
 
-    def step(flags=0):
-        layer.forward(w, X, Y, saved, flags=flags)
-        layer.backward(w, X, saved, DY, DX, grads, flags=flags)
+    def step(flags=0, x_in=None, dy_in=None):
+        """K chained layers forward, then backward in reverse (overlap across layers): every
+        call but the last passes MERAK_FLAG_CHAIN so layer k+1's sub-batch 0 starts while layer k's
+        last all-reduce is in flight; the last backward joins the caller stream."""
+        x_in = X if x_in is None else x_in
+        dy_in = DY if dy_in is None else dy_in
+        for k in range(K):
+            layer.forward(ws[k], x_in if k == 0 else Ys[k - 1], Ys[k], saved[k], flags=flags | FLAG_CHAIN)
+        for k in reversed(range(K)):
+            layer.backward(ws[k], x_in if k == 0 else Ys[k - 1], saved[k], dy_in if k == K - 1 else DXs[k + 1],
+                           DXs[k], grads[k], flags=flags | (FLAG_CHAIN if k > 0 else 0))
 
     def timed(nsteps, flags=0, prof=False):
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(nsteps)]
@@ -240,7 +253,7 @@ def main():
     with ClockSampler(local) as clk:
         ms_step, launches, prof = timed(args.steps, prof=True)
     clocks = clk.summary()
-    fl = layer_flops(cfg)
+    fl = K * layer_flops(cfg)
     value = fl / (ms_step * 1e-3) / 1e12
 
     extras = {}
@@ -248,7 +261,7 @@ def main():
         # exposed communication: same kernels with every all-reduce reading only the local partial
         if T > 1:
             ms_nc, _, _ = timed(max(3, args.steps // 2), flags=FLAG_NO_COMM)
-            extras["exposed_allreduce_ms_per_layer"] = ms_step - ms_nc
+            extras["exposed_allreduce_ms_per_layer"] = (ms_step - ms_nc) / K
             extras["no_comm_ms_per_step"] = ms_nc
         else:
             extras["exposed_allreduce_ms_per_layer"] = 0.0
@@ -261,7 +274,7 @@ def main():
             layer.set_subbatches(n_sub)
             extras["n1_ms_per_step"] = ms_n1
             extras["subpipelining_speedup_vs_n1"] = ms_n1 / ms_step
-        # e2e through the public API with host buffers: H2D x, dy (pinned) -> fwd -> bwd -> D2H y, dx
+        # e2e through the public API with host buffers: H2D x, dy (pinned) -> K fwd -> K bwd -> D2H y, dx
         hx = X.cpu().pin_memory()
         hdy = DY.cpu().pin_memory()
         hy = torch.empty_like(hx).pin_memory()
@@ -276,10 +289,9 @@ def main():
             s_ev[i].record(stream)
             Xe.copy_(hx, non_blocking=True)
             DYe.copy_(hdy, non_blocking=True)
-            layer.forward(w, Xe, Y, saved)
-            layer.backward(w, Xe, saved, DYe, DX, grads)
-            hy.copy_(Y, non_blocking=True)
-            hdx.copy_(DX, non_blocking=True)
+            step(0, Xe, DYe)
+            hy.copy_(Ys[K - 1], non_blocking=True)
+            hdx.copy_(DXs[0], non_blocking=True)
             e_ev[i].record(stream)
         barrier()
         te = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(s_ev, e_ev)) / ne], dtype=torch.float64,
@@ -303,19 +315,20 @@ def main():
                 "frac": gemm_tflops / peak_burst, "traffic": traffic,
                 "kernel": "tcgen05 bf16 GEMM (all 12 layer GEMMs; FLOPs 2MNK per launch / event-timed duration)",
                 "peak_source": f"{peak_src} bf16_tflops (burst); sustained {peak_sust}",
-                "gemm_launches": g["launches"], "gemm_ms_per_step": g["ms"] / args.steps,
-                "class_ms_per_step": {k: v / args.steps for k, v in share.items()},
+                "gemm_launches": g["launches"], "gemm_ms_per_layer": g["ms"] / args.steps / K,
+                "class_ms_per_layer": {k: v / args.steps / K for k, v in share.items()},
                 "layer_frac_of_peak": value / world / peak_burst}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, synth/)",
-                "config": {"workload": f"{cfg.name} layer fwd+bwd: h={cfg.hidden}, H={cfg.heads}, s={cfg.seq_len}, "
-                                       f"B={cfg.microbatch}, TMP={T}, n_sub={n_sub}",
-                           "tmp_degree": T, "n_sub": n_sub, "flops_per_step": fl,
+                "config": {"workload": f"{cfg.name} layer fwd+bwd x {K} chained layers: h={cfg.hidden}, "
+                                       f"H={cfg.heads}, s={cfg.seq_len}, B={cfg.microbatch}, TMP={T}, n_sub={n_sub}",
+                           "layers": K, "tmp_degree": T, "n_sub": n_sub, "flops_per_step": fl,
+                           "ms_per_layer": ms_step / K,
                            "l2": "flushed between steps (256 MiB write, outside the timed events)"},
-                "value_per_gpu": value / world, "tokens_per_s": cfg.tokens / (ms_step * 1e-3),
+                "value_per_gpu": value / world, "tokens_per_s": K * cfg.tokens / (ms_step * 1e-3),
                 "roofline": roofline, "gpu_launches": launches, "clocks": clocks}
         line.update({k: v for k, v in extras.items() if k != "e2e"})
         if "e2e" in extras:

@@ -434,10 +434,11 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     }
     CK(h, cudaEventRecord(h->ev_ar[2][j], h->ms));
     h->ev_ar_valid[2][j] = true;
-    // weight + bias gradients of the FFN block for sub-batch j (overlap AR#3(j))
-    TRY(run_wgrad(h, dyj, hh, hh, (const bf16 *)S(L.g) + r0 * L.ld_g, L.ld_g, fr, m, gr->w_2, gr->b_2));
-    TRY(run_wgrad(h, dz, fr, fr, (const bf16 *)S(L.u2) + r0 * L.ld_u2, L.ld_u2, hh, m, gr->w_1, gr->b_1));
   }
+  // weight + bias gradients of the FFN block over ALL tokens (overlapping AR#3 of the last
+  // sub-batch): one accumulation chain over tokens 0..B*s-1 -- the same MMA sequence as n = 1.
+  TRY(run_wgrad(h, dy, hh, hh, (const bf16 *)S(L.g), L.ld_g, fr, h->M, gr->w_2, gr->b_2));
+  TRY(run_wgrad(h, h->dz, fr, fr, (const bf16 *)S(L.u2), L.ld_u2, hh, h->M, gr->w_1, gr->b_1));
   // ---- attention block: proj dgrad -> attention bwd -> QKV dgrad (partial, slot 3) -> AR#4
   for (int j = 0; j < n; ++j) {
     const size_t r0 = (size_t)j * m;
@@ -482,10 +483,10 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     }
     CK(h, cudaEventRecord(h->ev_ar[3][j], h->ms));
     h->ev_ar_valid[3][j] = true;
-    // weight + bias gradients of the attention block for sub-batch j (overlap AR#4(j))
-    TRY(run_wgrad(h, dx1, hh, hh, ctx, L.ld_ctx, hr, m, gr->w_o, gr->b_o));
-    TRY(run_wgrad(h, dqkv, 3 * hr, 3 * hr, (const bf16 *)S(L.u) + r0 * L.ld_u, L.ld_u, hh, m, gr->w_qkv, gr->b_qkv));
   }
+  // weight + bias gradients of the attention block over all tokens (overlapping the last AR#4)
+  TRY(run_wgrad(h, h->dx1, hh, hh, (const bf16 *)S(L.ctx), L.ld_ctx, hr, h->M, gr->w_o, gr->b_o));
+  TRY(run_wgrad(h, h->dqkv, 3 * hr, 3 * hr, (const bf16 *)S(L.u), L.ld_u, hh, h->M, gr->w_qkv, gr->b_qkv));
   return leave(h, st, flags, 3);
 }
 
