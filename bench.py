@@ -247,12 +247,18 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item() / nsteps, launches, prof_d
 
+    def stage(msg):
+        if os.environ.get("MERAK_BENCH_TRACE"):
+            print(f"[rank {rank}] {msg}", file=sys.stderr, flush=True)
+
     for _ in range(args.warmup):
         step()
     barrier()
+    stage("warmup done")
     with ClockSampler(local) as clk:
         ms_step, launches, prof = timed(args.steps, prof=True)
     clocks = clk.summary()
+    stage("timed done")
     fl = K * layer_flops(cfg)
     value = fl / (ms_step * 1e-3) / 1e12
 
@@ -263,6 +269,7 @@ def main():
             ms_nc, _, _ = timed(max(3, args.steps // 2), flags=FLAG_NO_COMM)
             extras["exposed_allreduce_ms_per_layer"] = (ms_step - ms_nc) / K
             extras["no_comm_ms_per_step"] = ms_nc
+            stage("no-comm done")
         else:
             extras["exposed_allreduce_ms_per_layer"] = 0.0
         # n = 1 (Megatron-style, no sub-pipelining) with the same kernels: fig:ablation_pipetp analog
@@ -274,6 +281,7 @@ def main():
             layer.set_subbatches(n_sub)
             extras["n1_ms_per_step"] = ms_n1
             extras["subpipelining_speedup_vs_n1"] = ms_n1 / ms_step
+            stage("n=1 done")
         # e2e through the public API with host buffers: H2D x, dy (pinned) -> K fwd -> K bwd -> D2H y, dx
         hx = X.cpu().pin_memory()
         hdy = DY.cpu().pin_memory()
@@ -298,6 +306,7 @@ def main():
                           device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        stage("e2e done")
         extras["e2e"] = {"value": fl / (te.item() * 1e-3) / 1e12, "unit": "TFLOP/s",
                          "h2d_bytes_per_step": 2 * X.numel() * 2, "d2h_bytes_per_step": 2 * X.numel() * 2,
                          "ms_per_step": te.item()}

@@ -104,6 +104,7 @@ struct merak_tmp {
   int64_t launches = 0;
   std::string err;
   ncclComm_t nccl = nullptr;
+  uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // watchdog (env MERAK_AR_TIMEOUT_MS)
 };
 
 static std::string g_init_err;
@@ -206,7 +207,7 @@ static PeerSync make_sync(merak_tmp_t *h, bool comm) {
   ps.flags_local = reinterpret_cast<uint32_t *>(h->pv + h->flags_off);
   for (int q = 0; q < h->T; ++q) ps.flags_peer[q] = reinterpret_cast<uint32_t *>(h->peer_pv[q] + h->flags_off);
   ps.err_word = h->err_dev;
-  ps.timeout_ns = 20ull * 1000 * 1000 * 1000;  // 20 s
+  ps.timeout_ns = h->timeout_ns;
   return ps;
 }
 
@@ -255,9 +256,20 @@ static int ar_partials(merak_tmp_t *h, bool comm, int slot, size_t r0, const bf1
   return h->T;
 }
 
+// 1-warp cross-rank barrier on the communication stream before an all-reduce (see ln_ar.cu)
+static merak_status sync_peers(merak_tmp_t *h, const PeerSync &ps) {
+  if (!ps.enabled) return MERAK_OK;
+  Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+  CK(h, peer_ready(ps, h->ms));
+  return MERAK_OK;
+}
+
 static merak_status check_async_error(merak_tmp_t *h) {
   if (h->err_host && *(volatile int *)h->err_host)
-    return fail(h, MERAK_ETIMEOUT, "peer handshake watchdog fired in a previous all-reduce (peer absent or hung)");
+    return fail(h, MERAK_ETIMEOUT,
+                "peer handshake watchdog fired in a previous all-reduce (peer absent or hung): epoch %d cta %d "
+                "kind %d peer %d last flag %d",
+                h->err_host[1], h->err_host[2], h->err_host[3] / 16, h->err_host[3] % 16, h->err_host[4]);
   return MERAK_OK;
 }
 
@@ -343,6 +355,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.mean = (float *)S(L.mean2) + r0; a.rstd = (float *)S(L.rstd2) + r0;
       a.eps = h->eps; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
+      TRY(sync_peers(h, ps));
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
       CK(h, ar_fwd(a, ps, h->ms));
     }
@@ -372,6 +385,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.m = m; a.h = hh; a.resid = (const bf16 *)S(L.x1) + r0 * hh; a.bias = (const bf16 *)w->b_2;
       a.out = y + r0 * hh; a.do_ln = false; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
+      TRY(sync_peers(h, ps));
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
       CK(h, ar_fwd(a, ps, h->ms));
     }
@@ -424,6 +438,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.gamma = (const bf16 *)w->ln2_g; a.dres = dyj; a.dx = h->dx1 + r0 * hh;
       a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
+      TRY(sync_peers(h, ps));
       {
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         CK(h, ar_bwd(a, ps, h->ms));
@@ -473,6 +488,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.gamma = (const bf16 *)w->ln1_g; a.dres = dx1; a.dx = dx + r0 * hh;
       a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
+      TRY(sync_peers(h, ps));
       {
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         CK(h, ar_bwd(a, ps, h->ms));
@@ -563,6 +579,7 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   h->eps = cfg->ln_eps > 0 ? cfg->ln_eps : 1e-5f;
   h->dev = cfg->device;
   h->G = ar_bwd_group_rows(h->h);
+  if (const char *t = getenv("MERAK_AR_TIMEOUT_MS")) h->timeout_ns = (uint64_t)atoll(t) * 1000000ull;
   auto bail = [&](merak_status st) {
     g_init_err = h->err;
     release(h);
@@ -593,8 +610,8 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   h->pv_bytes = h->flags_off + align256(2 * MAX_AR_CTAS * MAX_T * sizeof(uint32_t));
   CKI(cudaMalloc(&h->pv, h->pv_bytes));
   CKI(cudaMemset(h->pv + h->flags_off, 0, h->pv_bytes - h->flags_off));
-  CKI(cudaHostAlloc(&h->err_host, sizeof(int), cudaHostAllocMapped));
-  *h->err_host = 0;
+  CKI(cudaHostAlloc(&h->err_host, 8 * sizeof(int), cudaHostAllocMapped));
+  memset(h->err_host, 0, 8 * sizeof(int));
   CKI(cudaHostGetDevicePointer((void **)&h->err_dev, h->err_host, 0));
   // workspace
   {
@@ -717,6 +734,13 @@ merak_status merak_tmp_join(merak_tmp_t *h, void *st) {
 }
 
 merak_status merak_tmp_destroy(merak_tmp_t *h) {
+  if (h && h->T > 1 && !h->nccl && h->ms) {
+    // final barrier: no rank frees its slots while a peer's last all-reduce may still read them
+    cudaSetDevice(h->dev);
+    PeerSync ps = make_sync(h, true);
+    peer_ready(ps, h->ms);
+    cudaStreamSynchronize(h->ms);
+  }
   release(h);
   return MERAK_OK;
 }

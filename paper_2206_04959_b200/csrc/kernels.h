@@ -70,9 +70,9 @@ cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st);  // 2 launches: dQ (+d
 constexpr int MAX_T = 8;
 constexpr int MAX_AR_CTAS = 1024;
 
-// Peer handshake for one all-reduce launch.  flags_local: this rank's flag array; flags_peer[r]:
+// Peer synchronisation for one all-reduce.  flags_local: this rank's flag array; flags_peer[r]:
 // rank r's flag array mapped into this process (flags_peer[rank] == flags_local).  Layout per rank:
-// ready[MAX_AR_CTAS][MAX_T] then done[MAX_AR_CTAS][MAX_T] (uint32 epochs).
+// ready[MAX_T] (uint32 epochs, written by the peers).
 struct PeerSync {
   int T, rank;
   bool enabled;               // false: fake peers on one device / T == 1 (no handshake)
@@ -100,6 +100,8 @@ struct ArFwdArgs {
   int ctas;
 };
 cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st);
+// 1-warp kernel: publish ps.epoch to every peer and wait for theirs (no-op unless ps.enabled)
+cudaError_t peer_ready(const PeerSync &ps, cudaStream_t st);
 
 struct ArBwdArgs {
   const __nv_bfloat16 *partial[MAX_T];

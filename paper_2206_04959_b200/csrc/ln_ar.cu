@@ -12,14 +12,15 @@
 //   AR#4: dx  = dx1 + LN1^T(sum_r dU1_r), dgamma1/dbeta1 partials  (backward, attention block)
 // Every rank computes every row, so replicated outputs are bit-identical across ranks.
 //
-// Peer handshake (per CTA index c, epoch e = per-handle launch counter, identical on all ranks):
-//   start: write ready[c][my_rank] = e into every peer's flag array (st.release.sys), then wait
-//          until ready[c][r] >= e for all peers r (ld.acquire.sys).  The peer's partial was
-//          completed by its GEMM before its all-reduce kernel started (stream order).
-//   end:   after the CTA's reads, write done[c][my_rank] = e to every peer and wait for all
-//          done[c][r] >= e.  When every CTA of a rank has exited, all peers have finished reading
-//          that rank's slot, so the next GEMM may overwrite it (the caller orders that by event).
-// A watchdog (globaltimer) bounds every wait; on expiry the kernel sets *err_word and skips work.
+// Cross-rank synchronisation is NOT done inside these data kernels (a large grid of CTAs spinning
+// on peers can deadlock against persistent GEMM clusters competing for the same SMs).  Instead a
+// 1-warp `peer_ready` kernel runs on the communication stream right before each all-reduce: it
+// publishes this rank's epoch e (st.release.sys into every peer's flag array) and waits until every
+// peer published e (ld.acquire.sys).  A rank publishes e only after (stream order) its GEMM wrote
+// partial e AND its all-reduce e-1 finished reading the peers' slots, so `ready(e)` from all peers
+// means: every partial of e is complete, and nobody still reads a slot the next GEMMs overwrite.
+// A watchdog (globaltimer) bounds the wait; on expiry it sets *err_word (reported by the next API
+// call) and later waits fail fast.
 #include <math.h>
 
 #include "kernels.h"
@@ -50,32 +51,41 @@ MK_DEV void store8(__nv_bfloat16 *p, const float (&v)[8]) {
   *reinterpret_cast<uint4 *>(p) = u;
 }
 
-// Thread 0 only.  kind 0 = ready, 1 = done.  Returns false if the watchdog fired.
-MK_DEV bool handshake(const PeerSync &ps, int kind, int cta) {
-  if (!ps.enabled) return true;
-  const size_t base = (size_t)kind * MAX_AR_CTAS * MAX_T + (size_t)cta * MAX_T;
-#pragma unroll
-  for (int r = 0; r < MAX_T; ++r)
-    if (r < ps.T && r != ps.rank) st_release_sys(ps.flags_peer[r] + base + ps.rank, ps.epoch);
-  const uint64_t t0 = globaltimer();
-  for (int r = 0; r < ps.T; ++r) {
-    if (r == ps.rank) continue;
-    while ((int)(ld_acquire_sys(ps.flags_local + base + r) - ps.epoch) < 0) {
-      if (globaltimer() - t0 > ps.timeout_ns) {
-        atomicExch(ps.err_word, 1);
-        return false;
+// One warp: lane r < T publishes epoch e to peer r, then waits for the peers' epoch e.
+// err_word[0] = 1 on timeout; err_word[1..4] = epoch, 0, peer, last flag value seen.
+__global__ void peer_ready_kernel(PeerSync ps) {
+  const int r = threadIdx.x;
+  volatile int *err = ps.err_word;
+  if (*err) return;
+  __threadfence_system();
+  if (r < ps.T && r != ps.rank) st_release_sys(ps.flags_peer[r] + ps.rank, ps.epoch);
+  if (r < ps.T && r != ps.rank) {
+    const uint64_t t0 = globaltimer();
+    uint32_t v;
+    while ((int)((v = ld_acquire_sys(ps.flags_local + r)) - ps.epoch) < 0) {
+      if (*err || globaltimer() - t0 > ps.timeout_ns) {
+        if (atomicExch(ps.err_word, 1) == 0) {
+          err[1] = (int)ps.epoch;
+          err[2] = 0;
+          err[3] = r;
+          err[4] = (int)v;
+        }
+        return;
       }
     }
   }
-  return true;
+  __syncwarp();
+}
+
+cudaError_t peer_ready(const PeerSync &ps, cudaStream_t st) {
+  if (!ps.enabled) return cudaSuccess;
+  peer_ready_kernel<<<1, 32, 0, st>>>(ps);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------------------ forward all-reduce
 __global__ void __launch_bounds__(256) ar_fwd_kernel(ArFwdArgs a, PeerSync ps) {
-  __shared__ int ok;
-  if (threadIdx.x == 0) ok = handshake(ps, 0, blockIdx.x);
-  __syncthreads();
-  if (ok) {
+  {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nw = blockDim.x >> 5;
     const int h = a.h, nc = h >> 3;
@@ -123,8 +133,6 @@ __global__ void __launch_bounds__(256) ar_fwd_kernel(ArFwdArgs a, PeerSync ps) {
       }
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0 && ok) handshake(ps, 1, blockIdx.x);
 }
 
 // ------------------------------------------------------------------------------ backward all-reduce
@@ -132,10 +140,7 @@ template <int G>
 __global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
   extern __shared__ __align__(16) float du_s[];  // [G][h] fp32 sum of the partials
   __shared__ float s_mean[G], s_rstd[G];
-  __shared__ int ok;
-  if (threadIdx.x == 0) ok = handshake(ps, 0, blockIdx.x);
-  __syncthreads();
-  if (ok) {
+  {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int h = a.h, nc = h >> 3;
     const float inv_h = 1.f / h;
@@ -215,8 +220,6 @@ __global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
       __syncthreads();
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0 && ok) handshake(ps, 1, blockIdx.x);
 }
 
 // ------------------------------------------------------------------------------ LayerNorm forward
@@ -358,8 +361,7 @@ __global__ void sample_chain_kernel(const float *q0, const float *q1, int b, int
 }
 
 // ------------------------------------------------------------------------------ host
-// CTAs that can be resident at once (the handshake needs every CTA index to make progress; the
-// grid also has to be identical on all ranks, so it depends only on the shape and the device).
+// CTAs that can be resident at once (grid sizing only; no cross-CTA waiting happens in the kernels).
 static int resident_ctas(const void *kern, int threads, size_t smem) {
   int per_sm = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);
