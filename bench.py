@@ -251,6 +251,10 @@ def main():
         if os.environ.get("MERAK_BENCH_TRACE"):
             print(f"[rank {rank}] {msg}", file=sys.stderr, flush=True)
 
+    if os.environ.get("MERAK_BENCH_TRACE"):
+        import faulthandler
+        faulthandler.dump_traceback_later(int(os.environ.get("MERAK_BENCH_TRACE_S", "90")), exit=False)
+
     for _ in range(args.warmup):
         step()
     barrier()
@@ -301,6 +305,7 @@ def main():
             hy.copy_(Ys[K - 1], non_blocking=True)
             hdx.copy_(DXs[0], non_blocking=True)
             e_ev[i].record(stream)
+            stage(f"e2e iter {i} issued")
         barrier()
         te = torch.tensor([sum(a.elapsed_time(b) for a, b in zip(s_ev, e_ev)) / ne], dtype=torch.float64,
                           device=dev)

@@ -73,6 +73,9 @@ def lib():
         L.merak_tmp_set_profiling.argtypes = [P, I32]
         L.merak_tmp_get_profile.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
                                             ctypes.POINTER(ctypes.c_double)]
+        L.merak_tmp_get_timeline.argtypes = [P, I32, ctypes.POINTER(I32), ctypes.POINTER(I32), ctypes.POINTER(I32),
+                                             ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float)]
+        L.merak_tmp_get_timeline.restype = ctypes.c_int
         L.merak_tmp_launch_count.argtypes = [P]
         L.merak_tmp_launch_count.restype = ctypes.c_int64
         for fn in ("merak_tmp_init", "merak_tmp_set_subbatches", "merak_tmp_layer_fwd", "merak_tmp_layer_bwd",
@@ -235,6 +238,14 @@ class TmpLayer:
         ms, la, fl = (ctypes.c_double * n)(), (ctypes.c_int64 * n)(), (ctypes.c_double * n)()
         self._check(lib().merak_tmp_get_profile(self.h, ms, la, fl))
         return {k: {"ms": ms[i], "launches": la[i], "flops": fl[i]} for i, k in enumerate(KERNEL_CLASSES)}
+
+    def get_timeline(self, cap=100000) -> list:
+        """[(class, stream, t0_ms, t1_ms)] of every launch since set_profiling(True); call before get_profile."""
+        n = ctypes.c_int32()
+        cls, st = (ctypes.c_int32 * cap)(), (ctypes.c_int32 * cap)()
+        t0, t1 = (ctypes.c_float * cap)(), (ctypes.c_float * cap)()
+        self._check(lib().merak_tmp_get_timeline(self.h, cap, ctypes.byref(n), cls, st, t0, t1))
+        return [(KERNEL_CLASSES[cls[i]], "comm" if st[i] else "comp", t0[i], t1[i]) for i in range(n.value)]
 
     def launch_count(self) -> int:
         return lib().merak_tmp_launch_count(self.h)

@@ -37,6 +37,7 @@ struct ProfRec {
   int cls;
   cudaEvent_t a, b;
   double flops;
+  int sid;  // 0 = compute stream, 1 = communication stream
 };
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -157,7 +158,7 @@ struct Launch {
     if (h->prof) {
       cudaEvent_t b = pool_event(h);
       cudaEventRecord(b, st);
-      h->recs.push_back({cls, a, b, flops});
+      h->recs.push_back({cls, a, b, flops, st == h->ms ? 1 : 0});
       h->prof_launch[cls] += nk;
     }
   }
@@ -779,6 +780,30 @@ merak_status merak_tmp_get_profile(merak_tmp_t *h, double *ms, int64_t *launches
     if (launches) launches[k] = h->prof_launch[k];
     if (flops) flops[k] = h->prof_flops[k];
   }
+  return MERAK_OK;
+}
+
+merak_status merak_tmp_get_timeline(merak_tmp_t *h, int32_t cap, int32_t *count, int32_t *cls, int32_t *stream,
+                                    float *t0, float *t1) {
+  if (!h || !count) return fail(h, MERAK_EINVAL, "NULL argument");
+  CK(h, cudaStreamSynchronize(h->cs));
+  CK(h, cudaStreamSynchronize(h->ms));
+  int32_t n = 0;
+  if (!h->recs.empty()) {
+    cudaEvent_t origin = h->recs.front().a;
+    for (auto &r : h->recs) {
+      if (n >= cap) break;
+      float a = 0, b = 0;
+      CK(h, cudaEventElapsedTime(&a, origin, r.a));
+      CK(h, cudaEventElapsedTime(&b, origin, r.b));
+      if (cls) cls[n] = r.cls;
+      if (stream) stream[n] = r.sid;
+      if (t0) t0[n] = a;
+      if (t1) t1[n] = b;
+      ++n;
+    }
+  }
+  *count = n;
   return MERAK_OK;
 }
 

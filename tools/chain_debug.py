@@ -33,17 +33,35 @@ def main():
     def say(m):
         print(f"[rank {rank}] {time.time():.2f} {m}", flush=True)
 
-    def step(xi, dyi, chain=True):
+    def step(xi, dyi, chain=True, extra=0):
         for k in range(K):
-            layer.forward(ws[k], xi if k == 0 else Ys[k - 1], Ys[k], saved[k], flags=FLAG_CHAIN if chain else 0)
+            layer.forward(ws[k], xi if k == 0 else Ys[k - 1], Ys[k], saved[k],
+                          flags=(FLAG_CHAIN if chain else 0) | extra)
         for k in reversed(range(K)):
             layer.backward(ws[k], xi if k == 0 else Ys[k - 1], saved[k], dyi if k == K - 1 else DXs[k + 1], DXs[k],
-                           grads[k], flags=FLAG_CHAIN if (chain and k > 0) else 0)
+                           grads[k], flags=(FLAG_CHAIN if (chain and k > 0) else 0) | extra)
 
     for i in range(3):
         step(X, DY)
         torch.cuda.synchronize()
         say(f"plain step {i} ok")
+    for i in range(2):
+        step(X, DY, extra=2)
+        torch.cuda.synchronize()
+        say(f"no-comm step {i} ok")
+    step(X, DY)
+    torch.cuda.synchronize()
+    say("plain after no-comm ok")
+    layer.set_subbatches(1)
+    for i in range(2):
+        step(X, DY)
+        torch.cuda.synchronize()
+        say(f"n=1 step {i} ok")
+    layer.set_subbatches(cfg.n_sub)
+    for i in range(2):
+        step(X, DY)
+        torch.cuda.synchronize()
+        say(f"back to n={cfg.n_sub} step {i} ok")
     hx, hdy = X.cpu().pin_memory(), DY.cpu().pin_memory()
     hy, hdx = torch.empty_like(hx).pin_memory(), torch.empty_like(hx).pin_memory()
     Xe, DYe = torch.empty_like(X), torch.empty_like(DY)
