@@ -37,7 +37,8 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = SMEM_KB * 1024 / STAGE_BYTES > 8 ? 8 : SMEM_KB * 1024 / STAGE_BYTES;
   static constexpr int TMEM_COLS = (2 * BN <= 256) ? 256 : 512;  // power of two >= 2 accumulators
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  // ring + barriers (1 KB) + epilogue staging (4 warps x 2 boxes x 4 KB) + alignment slack
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 4 * 8192 + 1024;
 };
 
 struct EpiParams {
@@ -143,7 +144,8 @@ MK_DEV void epi_store_chunk(const EpiParams &p, int gm, int gn0, const uint32_t 
 
 template <int CG, int BN, bool A_MN, bool B_MN, int EPI, int SMEM_KB>
 __global__ void __launch_bounds__(256, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams p) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmO2, EpiParams p) {
   using C = GemmCfg<CG, BN, SMEM_KB>;
   constexpr int S = C::STAGES;
   constexpr int BMT = BM * CG;  // tile rows
@@ -322,20 +324,101 @@ __global__ void __launch_bounds__(256, 1)
       release(bb);
     }
     int lt = 0;
+    // bf16 outputs leave through TMA stores: per warp, 32 rows x 64 columns staged in a 128-B-swizzled
+    // 4 KB smem box (two boxes, alternating), so global writes are whole coalesced lines.
+    uint8_t *stg = smem + S * C::STAGE_BYTES + 1024 + q * 8192;
+    int sbuf = 0;
+    auto stage_store = [&](const CUtensorMap *map, const uint32_t (&w)[32], int gn0, int grow0) {
+      if (lane == 0) tma_store_wait_read<1>();  // the box written two stores ago has been read
+      __syncwarp();
+      uint8_t *box = stg + sbuf * 4096 + lane * 128;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<uint4 *>(box + ((j ^ (lane & 7)) << 4)) =
+            make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+      fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(map, stg + sbuf * 4096, gn0, grow0);
+        tma_store_commit();
+      }
+      sbuf ^= 1;
+    };
     for (int tile = cl; tile < ntiles; tile += ncl, ++lt) {
       const int buf = lt & 1;
       mbar_wait(&tfull[buf], (lt >> 1) & 1);
       tc_fence_after();
       const int tm = tile % tiles_m, tn = tile / tiles_m;
       const int gm = tm * BMT + rank * BM + q * 32 + lane;
+      if constexpr (EPI == EPI_ACC_F32 || EPI == 5) {
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        const int gn0 = tn * BN + c * 32;
-        if (gn0 >= p.N) break;  // warp-uniform
-        uint32_t r[32];
-        tmem_ld32(row_base + buf * BN + c * 32, r);
-        tmem_ld_wait();
-        if (gm < p.M) epi_store_chunk<EPI>(p, gm, gn0, r);
+        for (int c = 0; c < BN / 32; ++c) {
+          const int gn0 = tn * BN + c * 32;
+          if (gn0 >= p.N) break;  // warp-uniform
+          uint32_t r[32];
+          tmem_ld32(row_base + buf * BN + c * 32, r);
+          tmem_ld_wait();
+          if (gm < p.M) epi_store_chunk<EPI>(p, gm, gn0, r);
+        }
+      } else {
+        const int grow0 = tm * BMT + rank * BM + q * 32;
+#pragma unroll 1
+        for (int c = 0; c < BN / 64; ++c) {
+          const int gn0 = tn * BN + c * 64;
+          if (gn0 >= p.N) break;  // warp-uniform
+          uint32_t r[64];
+          tmem_ld32(row_base + buf * BN + c * 64, *reinterpret_cast<uint32_t(*)[32]>(r));
+          tmem_ld32(row_base + buf * BN + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+          tmem_ld_wait();
+          float v[64];
+#pragma unroll
+          for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+          const bool fulln = gn0 + 64 <= p.N;
+          if constexpr (EPI == EPI_BIAS_BF16 || EPI == EPI_BIAS_GELU) {
+            if (fulln) {
+#pragma unroll
+              for (int i = 0; i < 64; i += 8) {
+                uint4 bv = *reinterpret_cast<const uint4 *>(p.bias + gn0 + i);
+                float2 b0 = unpack_bf16(bv.x), b1 = unpack_bf16(bv.y), b2 = unpack_bf16(bv.z), b3 = unpack_bf16(bv.w);
+                v[i + 0] += b0.x; v[i + 1] += b0.y; v[i + 2] += b1.x; v[i + 3] += b1.y;
+                v[i + 4] += b2.x; v[i + 5] += b2.y; v[i + 6] += b3.x; v[i + 7] += b3.y;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 64; ++i)
+                if (gn0 + i < p.N) v[i] += __bfloat162float(p.bias[gn0 + i]);
+            }
+          }
+          if constexpr (EPI == EPI_GELU_BWD) {
+            if (gm < p.M) {
+              const __nv_bfloat16 *z = p.aux + (size_t)gm * p.ld_aux + gn0;
+              if (fulln) {
+#pragma unroll
+                for (int i = 0; i < 64; i += 8) {
+                  uint4 zv = *reinterpret_cast<const uint4 *>(z + i);
+                  float2 z0 = unpack_bf16(zv.x), z1 = unpack_bf16(zv.y), z2 = unpack_bf16(zv.z), z3 = unpack_bf16(zv.w);
+                  v[i + 0] *= gelu_grad_f(z0.x); v[i + 1] *= gelu_grad_f(z0.y);
+                  v[i + 2] *= gelu_grad_f(z1.x); v[i + 3] *= gelu_grad_f(z1.y);
+                  v[i + 4] *= gelu_grad_f(z2.x); v[i + 5] *= gelu_grad_f(z2.y);
+                  v[i + 6] *= gelu_grad_f(z3.x); v[i + 7] *= gelu_grad_f(z3.y);
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 64; ++i)
+                  if (gn0 + i < p.N) v[i] *= gelu_grad_f(__bfloat162float(z[i]));
+              }
+            }
+          }
+          uint32_t w[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) w[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+          stage_store(&tmO, w, gn0, grow0);
+          if constexpr (EPI == EPI_BIAS_GELU) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) w[i] = pack_bf16(gelu_f(v[2 * i]), gelu_f(v[2 * i + 1]));
+            stage_store(&tmO2, w, gn0, grow0);
+          }
+        }
       }
       const int next = tile + 2 * ncl;
       if (EPI == EPI_ACC_F32 && next < ntiles) {
@@ -344,6 +427,8 @@ __global__ void __launch_bounds__(256, 1)
       }
       release(buf);
     }
+    if (lane == 0) tma_store_wait<0>();
+    __syncwarp();
   }
   tc_fence_before();
   if constexpr (CG == 2)
@@ -390,6 +475,10 @@ static bool make_map(CUtensorMap *m, const void *ptr, int rows, int cols, int ld
   return r == CUDA_SUCCESS;
 }
 
+struct Maps {
+  CUtensorMap a, b, o, o2;  // operands; bf16 outputs (TMA-store boxes of 64 cols x 32 rows)
+};
+
 int gemm_num_sms() {
   static int n = 0;
   if (!n) {
@@ -401,7 +490,7 @@ int gemm_num_sms() {
 }
 
 template <int CG, int BN, bool A_MN, bool B_MN, int EPI, int SMEM_KB = (CG == 2 ? 160 : 192)>
-static cudaError_t launch(const GemmArgs &a, const CUtensorMap &ma, const CUtensorMap &mb, const EpiParams &p,
+static cudaError_t launch(const GemmArgs &a, const Maps &mp, const EpiParams &p,
                           cudaStream_t st) {
   using C = GemmCfg<CG, BN, SMEM_KB>;
   auto kern = gemm_kernel<CG, BN, A_MN, B_MN, EPI, SMEM_KB>;
@@ -427,27 +516,27 @@ static cudaError_t launch(const GemmArgs &a, const CUtensorMap &ma, const CUtens
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ma, mb, p);
+  return cudaLaunchKernelEx(&cfg, kern, mp.a, mp.b, mp.o, mp.o2, p);
 }
 
 template <int CG, int BN, int KB>
-static cudaError_t dispatch(const GemmArgs &a, const CUtensorMap &ma, const CUtensorMap &mb, const EpiParams &p,
+static cudaError_t dispatch(const GemmArgs &a, const Maps &mp, const EpiParams &p,
                            cudaStream_t st) {
   if (!a.a_mn && !a.b_mn) {
     switch (a.epi) {
-      case EPI_STORE_BF16: return launch<CG, BN, false, false, EPI_STORE_BF16, KB>(a, ma, mb, p, st);
-      case EPI_BIAS_BF16: return launch<CG, BN, false, false, EPI_BIAS_BF16, KB>(a, ma, mb, p, st);
-      case EPI_BIAS_GELU: return launch<CG, BN, false, false, EPI_BIAS_GELU, KB>(a, ma, mb, p, st);
+      case EPI_STORE_BF16: return launch<CG, BN, false, false, EPI_STORE_BF16, KB>(a, mp, p, st);
+      case EPI_BIAS_BF16: return launch<CG, BN, false, false, EPI_BIAS_BF16, KB>(a, mp, p, st);
+      case EPI_BIAS_GELU: return launch<CG, BN, false, false, EPI_BIAS_GELU, KB>(a, mp, p, st);
     }
   } else if (!a.a_mn && a.b_mn) {
     if (BN == 192) return cudaErrorNotSupported;  // MN-major B stages 64-wide chunks per CTA
     switch (a.epi) {
-      case EPI_STORE_BF16: return launch<CG, BN, false, true, EPI_STORE_BF16, KB>(a, ma, mb, p, st);
-      case EPI_GELU_BWD: return launch<CG, BN, false, true, EPI_GELU_BWD, KB>(a, ma, mb, p, st);
+      case EPI_STORE_BF16: return launch<CG, BN, false, true, EPI_STORE_BF16, KB>(a, mp, p, st);
+      case EPI_GELU_BWD: return launch<CG, BN, false, true, EPI_GELU_BWD, KB>(a, mp, p, st);
     }
   } else if (a.a_mn && a.b_mn) {
     if (BN == 192) return cudaErrorNotSupported;
-    if (a.epi == EPI_ACC_F32) return launch<CG, BN, true, true, EPI_ACC_F32, KB>(a, ma, mb, p, st);
+    if (a.epi == EPI_ACC_F32) return launch<CG, BN, true, true, EPI_ACC_F32, KB>(a, mp, p, st);
   }
   return cudaErrorNotSupported;
 }
@@ -488,10 +577,16 @@ cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   const int cg = gemm_cg();
   const int BN = a.epi >= 5 ? 256 : pick_bn(a, cg);
   const int bnc = BN / cg;  // B rows staged per CTA
-  CUtensorMap ma, mb;
+  Maps mp;
   // A: K-major stored [M, K]; MN-major stored [K, M]
-  bool ok = a.a_mn ? make_map(&ma, a.A, a.K, a.M, a.lda, BK) : make_map(&ma, a.A, a.M, a.K, a.lda, BM);
-  ok = ok && (a.b_mn ? make_map(&mb, a.B, a.K, a.N, a.ldb, BK) : make_map(&mb, a.B, a.N, a.K, a.ldb, bnc));
+  bool ok = a.a_mn ? make_map(&mp.a, a.A, a.K, a.M, a.lda, BK) : make_map(&mp.a, a.A, a.M, a.K, a.lda, BM);
+  ok = ok && (a.b_mn ? make_map(&mp.b, a.B, a.K, a.N, a.ldb, BK) : make_map(&mp.b, a.B, a.N, a.K, a.ldb, bnc));
+  // bf16 outputs [M, N] (row stride ldo / ldo2) stored by TMA in boxes of 64 cols x 32 rows
+  const bool bf16_out = a.epi != EPI_ACC_F32 && a.epi != 5;
+  ok = ok && (bf16_out ? make_map(&mp.o, a.out, a.M, a.N, a.ldo, 32) : true);
+  ok = ok && (a.epi == EPI_BIAS_GELU ? make_map(&mp.o2, a.out2, a.M, a.N, a.ldo2, 32) : true);
+  if (!bf16_out) mp.o = mp.a;
+  if (a.epi != EPI_BIAS_GELU) mp.o2 = mp.o;
   if (!ok) return cudaErrorInvalidValue;
   EpiParams p;
   p.M = a.M; p.N = a.N; p.K = a.K; p.epi = a.epi;
@@ -503,26 +598,26 @@ cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   p.db32 = a.db32;
   p.n_main = a.db32 ? a.N - 1 : a.N;
   if (cg == 2 && a.epi >= 5 && !a.a_mn && !a.b_mn) {  // microbenchmark-only variants
-    if (a.epi == 5) return launch<2, 256, false, false, 5>(a, ma, mb, p, st);            // no stores
-    if (a.epi == 6) return launch<2, 256, false, false, EPI_STORE_BF16, 192>(a, ma, mb, p, st);  // 6 stages
+    if (a.epi == 5) return launch<2, 256, false, false, 5>(a, mp, p, st);            // no stores
+    if (a.epi == 6) return launch<2, 256, false, false, EPI_STORE_BF16, 192>(a, mp, p, st);  // 6 stages
     return cudaErrorNotSupported;
   }
   if (cg == 2) {
     // deep ring (192 KB) unless kernels on the communication stream must co-reside (smem_kb hint)
     if (a.smem_kb == 160) {
       switch (BN) {
-        case 256: return dispatch<2, 256, 160>(a, ma, mb, p, st);
-        case 192: return dispatch<2, 192, 160>(a, ma, mb, p, st);
-        default: return dispatch<2, 128, 160>(a, ma, mb, p, st);
+        case 256: return dispatch<2, 256, 160>(a, mp, p, st);
+        case 192: return dispatch<2, 192, 160>(a, mp, p, st);
+        default: return dispatch<2, 128, 160>(a, mp, p, st);
       }
     }
     switch (BN) {
-      case 256: return dispatch<2, 256, 192>(a, ma, mb, p, st);
-      case 192: return dispatch<2, 192, 192>(a, ma, mb, p, st);
-      default: return dispatch<2, 128, 192>(a, ma, mb, p, st);
+      case 256: return dispatch<2, 256, 192>(a, mp, p, st);
+      case 192: return dispatch<2, 192, 192>(a, mp, p, st);
+      default: return dispatch<2, 128, 192>(a, mp, p, st);
     }
   }
-  return BN == 256 ? dispatch<1, 256, 192>(a, ma, mb, p, st) : dispatch<1, 128, 192>(a, ma, mb, p, st);
+  return BN == 256 ? dispatch<1, 256, 192>(a, mp, p, st) : dispatch<1, 128, 192>(a, mp, p, st);
 }
 
 }  // namespace mk

@@ -50,6 +50,24 @@ MK_DEV void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0
       : "memory");
 }
 
+// TMA store smem -> global (bulk async-group); the smem box must be complete and fenced
+// (fence.proxy.async) before the issuing thread calls this.
+MK_DEV void tma_store_2d(const CUtensorMap *map, const void *src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+MK_DEV void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+MK_DEV void tma_store_wait_read() {  // at most N groups may still be reading smem
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+MK_DEV void tma_store_wait() {  // at most N groups still in flight (writes complete otherwise)
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // ------------------------------------------------------------------ tcgen05
 template <uint32_t NCOLS>
 MK_DEV void tmem_alloc(uint32_t *slot_smem) {
