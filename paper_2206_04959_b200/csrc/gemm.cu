@@ -575,7 +575,9 @@ static int gemm_cg() {
 cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaErrorInvalidValue;
   const int cg = gemm_cg();
-  const int BN = a.epi >= 5 ? 256 : pick_bn(a, cg);
+  // measured: 256-wide tiles beat 192/128 on every layer shape despite the last-wave loss
+  // (4096x4800x1600: 1181 vs 991 TFLOP/s), so the wave-quantisation heuristic is off by default
+  const int BN = (a.epi >= 5 || !getenv("MERAK_GEMM_PICK_BN")) ? (a.N > 128 ? 256 : 128) : pick_bn(a, cg);
   const int bnc = BN / cg;  // B rows staged per CTA
   Maps mp;
   // A: K-major stored [M, K]; MN-major stored [K, M]
