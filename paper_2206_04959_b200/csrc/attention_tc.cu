@@ -34,7 +34,7 @@ struct FaCfg {
   static constexpr int Q_BYTES = NA * Q_ATOM;
   static constexpr int K_BYTES = NA * H_ATOM;       // K-major [64 keys][d]
   static constexpr int V_BYTES = NA * H_ATOM;       // MN-major: NA chunks of [64 keys][64 d-columns]
-  static constexpr int STAGES = (D <= 64) ? 3 : 2;
+  static constexpr int STAGES = (D <= 64) ? 3 : 2;  // 4 stages no longer fit two CTAs per SM
   static constexpr int P_BYTES = TQ * 128;          // [128 q][64 keys] bf16 = one atom
   static constexpr int SMEM = Q_BYTES + STAGES * (K_BYTES + V_BYTES) + 2 * P_BYTES + 1024 + 256;
   static constexpr uint32_t S_COL = 0;              // 2 x 64 fp32 columns
@@ -188,12 +188,13 @@ __global__ void __launch_bounds__(192, FaCfg<D>::MIN_CTAS)
       tmem_ld_wait();
       const int kj0 = j * TKH;
       const bool mask = (kj0 + TKH - 1 > qt * TQ) || (kj0 + TKH > s);
-      float mx = -INFINITY;
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent chains
 #pragma unroll
       for (int k = 0; k < 64; ++k) {
         const float x = __uint_as_float(v[k]);
-        if (!mask || (kj0 + k <= qi && kj0 + k < s)) mx = fmaxf(mx, x);
+        if (!mask || (kj0 + k <= qi && kj0 + k < s)) mx4[k & 3] = fmaxf(mx4[k & 3], x);
       }
+      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       // the max grew by more than 2^8: move to the new max, rescale O and l.  TMEM access is
       // warp-collective, so the whole warp enters when any row needs it (others scale by 1).
       const bool need = mx > m + thr;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(192, FaCfg<D>::MIN_CTAS)
       // P buffer b was last read by P_{j-2} V_{j-2}
       mbar_wait(&p_free[b], ((j >> 1) & 1) ^ 1);
       const float ms = m * sl2;
-      float rs = 0.f;
+      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
       uint8_t *prow = sP + b * C::P_BYTES + r * 128;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {
@@ -236,12 +237,12 @@ __global__ void __launch_bounds__(192, FaCfg<D>::MIN_CTAS)
             if (!(kj0 + k <= qi && kj0 + k < s)) p0 = 0.f;
             if (!(kj0 + k + 1 <= qi && kj0 + k + 1 < s)) p1 = 0.f;
           }
-          rs += p0 + p1;
+          rs4[u] += p0 + p1;
           pk[u] = pack_bf16(p0, p1);
         }
         *reinterpret_cast<uint4 *>(prow + ((ch ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
-      l += rs;
+      l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
       fence_proxy_async();  // generic-proxy P stores -> visible to the tensor core
       tc_fence_before();
       __syncwarp();
