@@ -505,13 +505,10 @@ static cudaError_t bwd_d(const AttnArgs &a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Implementation switches are read per call (a getenv is ~100 ns) so tests can cover both paths.
 static bool use_tc() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("MERAK_ATTN_TC");  // tcgen05 forward: opt-in until it beats mma.sync
-    v = (e && atoi(e) == 1) ? 1 : 0;
-  }
-  return v == 1;
+  const char *e = getenv("MERAK_ATTN_TC");  // tcgen05 forward: opt-in until it beats mma.sync
+  return e && atoi(e) == 1;
 }
 
 cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st) {
@@ -526,7 +523,13 @@ cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st) {
   return cudaErrorNotSupported;
 }
 
+static bool use_bwd_tc() {
+  const char *e = getenv("MERAK_ATTN_BWD_TC");  // tcgen05 backward is the default (1.6x the mma.sync one)
+  return !(e && atoi(e) == 0);
+}
+
 cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st) {
+  if (use_bwd_tc() && a.s % 4 == 0) return attn_bwd_tc(a, st);  // 1-D bulk copies of lse/delta need 16 B
   switch (a.d) {
     case 32: return bwd_d<32>(a, st);
     case 64: return bwd_d<64>(a, st);

@@ -577,7 +577,11 @@ cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   const int cg = gemm_cg();
   // measured: 256-wide tiles beat 192/128 on every layer shape despite the last-wave loss
   // (4096x4800x1600: 1181 vs 991 TFLOP/s), so the wave-quantisation heuristic is off by default
-  const int BN = (a.epi >= 5 || !getenv("MERAK_GEMM_PICK_BN")) ? (a.N > 128 ? 256 : 128) : pick_bn(a, cg);
+  int BN = (a.epi >= 5 || !getenv("MERAK_GEMM_PICK_BN")) ? (a.N > 128 ? 256 : 128) : pick_bn(a, cg);
+  if (const char *fb = getenv("MERAK_GEMM_BN")) {  // microbenchmark override (read per call)
+    const int v = atoi(fb);
+    if (v == 128 || v == 256 || (v == 192 && !a.a_mn && !a.b_mn)) BN = v;
+  }
   const int bnc = BN / cg;  // B rows staged per CTA
   Maps mp;
   // A: K-major stored [M, K]; MN-major stored [K, M]

@@ -65,6 +65,7 @@ struct AttnArgs {
 cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st);     // tcgen05 version if MERAK_ATTN_TC=1
 cudaError_t attn_fwd_tc(const AttnArgs &a, cudaStream_t st);  // attention_tc.cu
 cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st);  // 2 launches: dQ (+delta), then dK/dV
+cudaError_t attn_bwd_tc(const AttnArgs &a, cudaStream_t st);  // attention_bwd_tc.cu (MERAK_ATTN_BWD_TC=1)
 
 // ---------------------------------------------------------------- LN / all-reduce / reductions (ln_ar.cu)
 constexpr int MAX_T = 8;

@@ -50,6 +50,14 @@ MK_DEV void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0
       : "memory");
 }
 
+// 1-D bulk copy global -> smem (bytes multiple of 16, both addresses 16-B aligned), completing on `bar`
+MK_DEV void bulk_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // TMA store smem -> global (bulk async-group); the smem box must be complete and fenced
 // (fence.proxy.async) before the issuing thread calls this.
 MK_DEV void tma_store_2d(const CUtensorMap *map, const void *src, int c0, int c1) {
