@@ -106,6 +106,7 @@ struct merak_tmp {
   std::string err;
   ncclComm_t nccl = nullptr;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // watchdog (env MERAK_AR_TIMEOUT_MS)
+  bool two_shot = false;  // T >= 4: reduce-scatter + all-gather instead of one-shot (env MERAK_AR_TWO_SHOT)
 };
 
 static std::string g_init_err;
@@ -265,6 +266,34 @@ static merak_status sync_peers(merak_tmp_t *h, const PeerSync &ps) {
   return MERAK_OK;
 }
 
+// Two-shot all-reduce (SURVEY §8(e), T >= 4): each rank sums only the rows it owns,
+// [r*chunk, (r+1)*chunk), from all T slots (same arithmetic as one-shot, rounded once) and writes
+// them back into its own slot; after a second barrier the fused epilogue kernel reads every row
+// from its owner's slot ("gathered" mode).  NVLink bytes per rank: 2(T-1)/T of a slot instead of
+// (T-1) for one-shot.  Returns the chunk (rows per owner) for the epilogue kernel.
+static bool two_shot_on(merak_tmp_t *h, bool comm) { return comm && h->T > 1 && !h->nccl && h->two_shot; }
+static merak_status two_shot_rs(merak_tmp_t *h, int slot, size_t r0, int m, const bf16 *resid, const bf16 *bias,
+                                int *chunk) {
+  const int c = (m + h->T - 1) / h->T;
+  ArRsArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int q = 0; q < h->T; ++q) a.partial[q] = slot_ptr(h, q, slot) + r0 * h->h;
+  a.T = h->T; a.h = h->h;
+  a.row0 = h->r * c < m ? h->r * c : m;
+  a.row1 = (h->r + 1) * c < m ? (h->r + 1) * c : m;
+  a.resid = resid; a.bias = bias;
+  a.out = slot_ptr(h, h->r, slot) + r0 * h->h;
+  a.ctas = h->cfg.comm_ctas;
+  {
+    Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+    CK(h, ar_rs(a, h->ms));
+  }
+  PeerSync ps = make_sync(h, true);
+  TRY(sync_peers(h, ps));
+  *chunk = c;
+  return MERAK_OK;
+}
+
 static merak_status check_async_error(merak_tmp_t *h) {
   if (h->err_host && *(volatile int *)h->err_host)
     return fail(h, MERAK_ETIMEOUT,
@@ -357,6 +386,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.eps = h->eps; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 0, r0, m, xj, (const bf16 *)w->b_o, &a.chunk));
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
       CK(h, ar_fwd(a, ps, h->ms));
     }
@@ -387,6 +417,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.out = y + r0 * hh; a.do_ln = false; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 1, r0, m, a.resid, a.bias, &a.chunk));
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
       CK(h, ar_fwd(a, ps, h->ms));
     }
@@ -440,6 +471,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 2, r0, m, nullptr, nullptr, &a.chunk));
       {
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         CK(h, ar_bwd(a, ps, h->ms));
@@ -490,6 +522,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 3, r0, m, nullptr, nullptr, &a.chunk));
       {
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         CK(h, ar_bwd(a, ps, h->ms));
@@ -581,6 +614,8 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   h->dev = cfg->device;
   h->G = ar_bwd_group_rows(h->h);
   if (const char *t = getenv("MERAK_AR_TIMEOUT_MS")) h->timeout_ns = (uint64_t)atoll(t) * 1000000ull;
+  h->two_shot = h->T >= 4;
+  if (const char *t = getenv("MERAK_AR_TWO_SHOT")) h->two_shot = h->T > 1 && atoi(t) == 1;
   auto bail = [&](merak_status st) {
     g_init_err = h->err;
     release(h);

@@ -99,8 +99,24 @@ struct ArFwdArgs {
   float *mean, *rstd;
   float eps;
   int ctas;
+  // two-shot phase 2 ("gathered" mode, chunk > 0): row i was already reduced (sum + bias + resid,
+  // rounded once) by rank i / chunk into its slot; partial[q] is rank q's slot, bias/resid unused.
+  int chunk;
 };
 cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st);
+
+// Two-shot phase 1 (reduce-scatter, T >= 4): rows [row0, row1) of the sub-batch, owned by this
+// rank: v = sum_r partial[r] (rank order) [+ bias + resid], rounded once to bf16 and written IN
+// PLACE into this rank's own slot (out = partial[rank]).  Peers read those rows in phase 2.
+struct ArRsArgs {
+  const __nv_bfloat16 *partial[MAX_T];
+  int T, h, row0, row1;
+  const __nv_bfloat16 *resid;  // nullptr: plain sum (backward); else forward AR epilogue terms
+  const __nv_bfloat16 *bias;
+  __nv_bfloat16 *out;
+  int ctas;
+};
+cudaError_t ar_rs(const ArRsArgs &a, cudaStream_t st);
 // 1-warp kernel: publish ps.epoch to every peer and wait for theirs (no-op unless ps.enabled)
 cudaError_t peer_ready(const PeerSync &ps, cudaStream_t st);
 
@@ -116,6 +132,7 @@ struct ArBwdArgs {
   float *part_dg, *part_db;     // out: per-group column partials [m/G, h]
   int G;                        // rows per group (8; divides s)
   int ctas;
+  int chunk;                    // > 0: two-shot phase 2, row i reads the reduced du from partial[i / chunk]
 };
 cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st);
 int ar_bwd_group_rows(int h);

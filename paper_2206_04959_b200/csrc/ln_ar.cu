@@ -92,14 +92,17 @@ __global__ void __launch_bounds__(256) ar_fwd_kernel(ArFwdArgs a, PeerSync ps) {
     for (int row = blockIdx.x * nw + warp; row < a.m; row += gridDim.x * nw) {
       const size_t ro = (size_t)row * h;
       float sum = 0.f;
+      const __nv_bfloat16 *src0 = a.chunk > 0 ? a.partial[row / a.chunk] : a.partial[0];
       for (int c = lane; c < nc; c += 32) {
         float v[8];
-        load8(a.partial[0] + ro + c * 8, v);
+        load8(src0 + ro + c * 8, v);
+        if (a.chunk == 0) {
 #pragma unroll
-        for (int r = 1; r < MAX_T; ++r)
-          if (r < a.T) add8(a.partial[r] + ro + c * 8, v);  // rank order (R10)
-        add8(a.bias + c * 8, v);
-        add8(a.resid + ro + c * 8, v);
+          for (int r = 1; r < MAX_T; ++r)
+            if (r < a.T) add8(a.partial[r] + ro + c * 8, v);  // rank order (R10)
+          add8(a.bias + c * 8, v);
+          add8(a.resid + ro + c * 8, v);
+        }
         store8(a.out + ro + c * 8, v);
         if (a.do_ln) {
           float q[8];
@@ -135,6 +138,29 @@ __global__ void __launch_bounds__(256) ar_fwd_kernel(ArFwdArgs a, PeerSync ps) {
   }
 }
 
+// ------------------------------------------------------------------------------ two-shot phase 1
+// Same per-element arithmetic (and order) as the one-shot kernels above, so one-shot and two-shot
+// results are bit-identical.
+__global__ void __launch_bounds__(256) ar_rs_kernel(ArRsArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int h = a.h, nc = h >> 3;
+  for (int row = a.row0 + blockIdx.x * nw + warp; row < a.row1; row += gridDim.x * nw) {
+    const size_t ro = (size_t)row * h;
+    for (int c = lane; c < nc; c += 32) {
+      float v[8];
+      load8(a.partial[0] + ro + c * 8, v);
+#pragma unroll
+      for (int r = 1; r < MAX_T; ++r)
+        if (r < a.T) add8(a.partial[r] + ro + c * 8, v);
+      if (a.resid) {
+        add8(a.bias + c * 8, v);
+        add8(a.resid + ro + c * 8, v);
+      }
+      store8(a.out + ro + c * 8, v);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------ backward all-reduce
 template <int G>
 __global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
@@ -152,12 +178,17 @@ __global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
         const size_t ro = (size_t)row * h;
         const float mean = a.mean[row], rstd = a.rstd[row];
         float acc1 = 0.f, acc2 = 0.f;
+        const __nv_bfloat16 *src0 = a.chunk > 0 ? a.partial[row / a.chunk] : a.partial[0];
         for (int c = lane; c < nc; c += 32) {
           float du[8], x[8], gm[8];
-          load8(a.partial[0] + ro + c * 8, du);
+          load8(src0 + ro + c * 8, du);
+          if (a.chunk == 0) {
 #pragma unroll
-          for (int r = 1; r < MAX_T; ++r)
-            if (r < a.T) add8(a.partial[r] + ro + c * 8, du);
+            for (int r = 1; r < MAX_T; ++r)
+              if (r < a.T) add8(a.partial[r] + ro + c * 8, du);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) du[i] = bf16_round(du[i]);  // the AR result is rounded once (R10)
+          }
           float4 *ds = reinterpret_cast<float4 *>(du_s + ri * h + c * 8);
           ds[0] = make_float4(du[0], du[1], du[2], du[3]);
           ds[1] = make_float4(du[4], du[5], du[6], du[7]);
@@ -386,6 +417,15 @@ cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
 }
 
 int ar_bwd_group_rows(int h) { return 8; }
+
+cudaError_t ar_rs(const ArRsArgs &a, cudaStream_t st) {
+  if (a.row1 <= a.row0) return cudaSuccess;
+  static int resident = 0;
+  if (!resident) resident = resident_ctas((const void *)ar_rs_kernel, 256, 0);
+  const int grid = clamp_ctas(a.ctas, (a.row1 - a.row0 + 7) / 8, resident);
+  ar_rs_kernel<<<grid, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
   const size_t smem = (size_t)a.G * a.h * sizeof(float);

@@ -237,6 +237,7 @@ MK_DEV uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // RNE
   return *reinterpret_cast<uint32_t *>(&v);
 }
+MK_DEV float bf16_round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 MK_DEV float2 unpack_bf16(uint32_t u) {
   __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162 *>(&u);
   return __bfloat1622float2(v);

@@ -1,6 +1,7 @@
 """Multi-rank worker (launched by torchrun from tests/test_gpu_multi.py): the TMP layer on T = WORLD_SIZE
 GPUs through the C ABI, each rank holding its shard; checks vs the fp64 oracle's slices, cross-rank
-bit equality of the replicated outputs, and bit-identity of n = 1 vs n = 2 at T > 1.
+bit equality of the replicated outputs, bit-identity of n = 1 vs n = 2 at T > 1, and of the one-shot vs
+two-shot all-reduce.
 Exit code 0 = all checks passed."""
 import os
 import sys
@@ -61,6 +62,15 @@ def main():
         for k in out:
             if not torch.equal(out[k], out1[k]):
                 failures.append((name, f"{k}: n={cfg.n_sub} vs n=1 not bit-identical"))
+        # one-shot vs two-shot all-reduce (default: two-shot at T >= 4) must be bit-identical
+        os.environ["MERAK_AR_TWO_SHOT"] = "0" if T >= 4 else "1"
+        try:
+            out2 = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group)
+        finally:
+            del os.environ["MERAK_AR_TWO_SHOT"]
+        for k in out:
+            if not torch.equal(out[k], out2[k]):
+                failures.append((name, f"{k}: one-shot vs two-shot all-reduce not bit-identical"))
         # NCCL baseline (MERAK_COMM_NCCL): same kernels, ncclAllReduce instead of the peer kernel
         outn = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group, comm=1)
         errs, bad = compare_to_oracle(outn, y, dx, oracle_rank_slices(g, cfg, T, rank), cfg)
