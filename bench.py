@@ -212,36 +212,38 @@ def main():
         if world > 1:
             dist.barrier()
 
-    def step(flags=0, x_in=None, dy_in=None):
+    def step(flags=0, x_in=None, dy_in=None, lay=None):
         """K chained layers forward, then backward in reverse (overlap across layers): every
         call but the last passes MERAK_FLAG_CHAIN so layer k+1's sub-batch 0 starts while layer k's
         last all-reduce is in flight; the last backward joins the caller stream."""
         x_in = X if x_in is None else x_in
         dy_in = DY if dy_in is None else dy_in
+        lay = lay or layer
         for k in range(K):
-            layer.forward(ws[k], x_in if k == 0 else Ys[k - 1], Ys[k], saved[k], flags=flags | FLAG_CHAIN)
+            lay.forward(ws[k], x_in if k == 0 else Ys[k - 1], Ys[k], saved[k], flags=flags | FLAG_CHAIN)
         for k in reversed(range(K)):
-            layer.backward(ws[k], x_in if k == 0 else Ys[k - 1], saved[k], dy_in if k == K - 1 else DXs[k + 1],
+            lay.backward(ws[k], x_in if k == 0 else Ys[k - 1], saved[k], dy_in if k == K - 1 else DXs[k + 1],
                            DXs[k], grads[k], flags=flags | (FLAG_CHAIN if k > 0 else 0))
 
-    def timed(nsteps, flags=0, prof=False):
+    def timed(nsteps, flags=0, prof=False, lay=None):
+        lay = lay or layer
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(nsteps)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(nsteps)]
         if prof:
-            layer.set_profiling(True)
-        l0 = layer.launch_count()
+            lay.set_profiling(True)
+        l0 = lay.launch_count()
         barrier()
         for i in range(nsteps):
             flush.zero_()
             starts[i].record(stream)
-            step(flags)
+            step(flags, lay=lay)
             ends[i].record(stream)
         barrier()
-        launches = layer.launch_count() - l0
+        launches = lay.launch_count() - l0
         ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-        prof_d = layer.get_profile() if prof else None
+        prof_d = lay.get_profile() if prof else None
         if prof:
-            layer.set_profiling(False)
+            lay.set_profiling(False)
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -260,7 +262,7 @@ def main():
     barrier()
     stage("warmup done")
     with ClockSampler(local) as clk:
-        ms_step, launches, prof = timed(args.steps, prof=True)
+        ms_step, launches, _ = timed(args.steps)
     clocks = clk.summary()
     stage("timed done")
     fl = K * layer_flops(cfg)
@@ -316,7 +318,24 @@ def main():
                          "h2d_bytes_per_step": 2 * X.numel() * 2, "d2h_bytes_per_step": 2 * X.numel() * 2,
                          "ms_per_step": te.item()}
 
-    # roofline of the dominant kernel class (the tcgen05 GEMM), from live CUDA events on its stream
+    # roofline of the dominant kernel class (the tcgen05 GEMM), from CUDA events around every launch on
+    # its stream.  The timed run overlaps kernels of different sub-batches (and the wgrad filler), so
+    # per-launch event spans there include time shared with other kernels: the per-kernel numbers come
+    # from a profiling pass of a second handle with all compute on one stream (MERAK_STREAMS=1), the
+    # same kernels, shapes and order as the ncu launch list.
+    os.environ["MERAK_STREAMS"] = "1"
+    try:
+        layer_p = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, tmp_degree=T, tmp_rank=rank,
+                           n_sub=n_sub, comm_ctas=args.comm_ctas, device=local, group=group)
+    finally:
+        del os.environ["MERAK_STREAMS"]
+    for _ in range(2):
+        step(lay=layer_p)
+    nprof = max(3, args.steps // 2)
+    ms_serial, _, prof = timed(nprof, prof=True, lay=layer_p)
+    layer_p.close()
+    stage("profiling pass done")
+    extras["serialized_ms_per_step"] = ms_serial
     peak_burst, peak_sust, peak_src = measured_peaks()
     g = prof["gemm"]
     gemm_tflops = g["flops"] / (g["ms"] * 1e-3) / 1e12 if g["ms"] > 0 else 0.0
@@ -327,10 +346,11 @@ def main():
     share = {k: v["ms"] for k, v in prof.items()}
     roofline = {"bound": "tensor", "achieved": gemm_tflops, "peak": peak_burst, "unit": "TFLOP/s",
                 "frac": gemm_tflops / peak_burst, "traffic": traffic,
-                "kernel": "tcgen05 bf16 GEMM (all 12 layer GEMMs; FLOPs 2MNK per launch / event-timed duration)",
+                "kernel": "tcgen05 bf16 GEMM (all 12 layer GEMMs; FLOPs 2MNK per launch / event-timed duration, "
+                          "serialized profiling pass)",
                 "peak_source": f"{peak_src} bf16_tflops (burst); sustained {peak_sust}",
-                "gemm_launches": g["launches"], "gemm_ms_per_layer": g["ms"] / args.steps / K,
-                "class_ms_per_layer": {k: v / args.steps / K for k, v in share.items()},
+                "gemm_launches_per_step": g["launches"] / nprof, "gemm_ms_per_layer": g["ms"] / nprof / K,
+                "class_ms_per_layer": {k: v / nprof / K for k, v in share.items()},
                 "layer_frac_of_peak": value / world / peak_burst}
 
     if rank == 0:

@@ -75,7 +75,10 @@ struct merak_tmp {
   int h, H, s, B, T, r, n, f, d, Hr, hr, fr, e0, M;
   float eps;
   int dev;
-  cudaStream_t cs = nullptr, ms = nullptr;
+  // cs: compute stream of even sub-batches; cs1: odd sub-batches (so one sub-batch's kernels fill the
+  // wave-quantisation tails of the other's); cw: weight-gradient GEMMs (lowest priority filler);
+  // ms: all-reduces (highest priority).  With MERAK_STREAMS=1, cs1 and cw alias cs.
+  cudaStream_t cs = nullptr, cs1 = nullptr, cw = nullptr, ms = nullptr;
   // peer-visible memory: NSLOT slots of [M, h] bf16 followed by the flag array
   char *pv = nullptr;
   size_t slot_bytes = 0, flags_off = 0, pv_bytes = 0;
@@ -88,8 +91,12 @@ struct merak_tmp {
   float *delta = nullptr, *part_col = nullptr, *part_lng = nullptr, *part_lnb = nullptr;
   int G = 16;
   // events
-  cudaEvent_t ev_entry = nullptr, ev_cs_end = nullptr;
+  cudaEvent_t ev_entry = nullptr, ev_cs_end = nullptr, ev_cs1_end = nullptr, ev_cw_end = nullptr;
   bool have_prev = false;
+  // workspace hazards across calls: wgrads on cw read dz / dx1 / dqkv that the next backward rewrites
+  cudaEvent_t ev_w1 = nullptr, ev_wo = nullptr, ev_wqkv = nullptr;
+  bool have_wg = false;
+  cudaEvent_t ev_dz[MAXN] = {}, ev_dq[MAXN] = {};
   cudaEvent_t ev_p[MAXN] = {};
   cudaEvent_t ev_ar[NSLOT][MAXN] = {};
   bool ev_ar_valid[NSLOT][MAXN] = {};
@@ -159,7 +166,7 @@ struct Launch {
     if (h->prof) {
       cudaEvent_t b = pool_event(h);
       cudaEventRecord(b, st);
-      h->recs.push_back({cls, a, b, flops, st == h->ms ? 1 : 0});
+      h->recs.push_back({cls, a, b, flops, st == h->ms ? 1 : (st == h->cw && h->cw != h->cs) ? 2 : 0});
       h->prof_launch[cls] += nk;
     }
   }
@@ -218,14 +225,16 @@ static bf16 *slot_ptr(merak_tmp_t *h, int rank, int slot) {
 }
 
 // ------------------------------------------------------------------------------ kernel wrappers
-static merak_status run_gemm(merak_tmp_t *h, const GemmArgs &a0) {
+static merak_status run_gemm(merak_tmp_t *h, const GemmArgs &a0, cudaStream_t st) {
   GemmArgs a = a0;
   // T > 1: keep smem free on every SM for the all-reduce kernels that overlap the GEMMs
   a.smem_kb = h->T > 1 ? 160 : 192;
-  Launch L(h, MERAK_K_GEMM, h->cs, 2.0 * a.M * a.N * a.K);
-  CK(h, gemm(a, h->cs));
+  Launch L(h, MERAK_K_GEMM, st, 2.0 * a.M * a.N * a.K);
+  CK(h, gemm(a, st));
   return MERAK_OK;
 }
+// compute stream of sub-batch j
+static cudaStream_t sub_stream(merak_tmp_t *h, int j) { return (j & 1) ? h->cs1 : h->cs; }
 static GemmArgs gargs(const void *A, const void *B, int M, int N, int K, int lda, int ldb, bool a_mn, bool b_mn,
                       int epi) {
   GemmArgs a;
@@ -307,21 +316,34 @@ static merak_status enter(merak_tmp_t *h, cudaStream_t st) {
   TRY(check_async_error(h));
   CK(h, cudaSetDevice(h->dev));
   CK(h, cudaEventRecord(h->ev_entry, st));
-  CK(h, cudaStreamWaitEvent(h->cs, h->ev_entry, 0));
-  CK(h, cudaStreamWaitEvent(h->ms, h->ev_entry, 0));
-  // the comm stream may reuse workspace only after the previous call's compute work is done
-  if (h->have_prev) CK(h, cudaStreamWaitEvent(h->ms, h->ev_cs_end, 0));
+  for (cudaStream_t c : {h->cs, h->cs1, h->cw, h->ms}) CK(h, cudaStreamWaitEvent(c, h->ev_entry, 0));
+  // the comm stream rewrites dx1 (AR#3) only after the previous call's readers of it are done:
+  // the sub-batch streams (proj dgrad) and the W_o wgrad on cw
+  if (h->have_prev) {
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_cs_end, 0));
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_cs1_end, 0));
+  }
+  if (h->have_wg) CK(h, cudaStreamWaitEvent(h->ms, h->ev_wo, 0));
+  return MERAK_OK;
+}
+
+static merak_status wait_all(merak_tmp_t *h, cudaStream_t st) {
+  CK(h, cudaStreamWaitEvent(st, h->ev_cs_end, 0));
+  CK(h, cudaStreamWaitEvent(st, h->ev_cs1_end, 0));
+  CK(h, cudaStreamWaitEvent(st, h->ev_cw_end, 0));
   return MERAK_OK;
 }
 
 static merak_status leave(merak_tmp_t *h, cudaStream_t st, uint32_t flags, int last_slot) {
   CK(h, cudaEventRecord(h->ev_cs_end, h->cs));
+  CK(h, cudaEventRecord(h->ev_cs1_end, h->cs1));
+  CK(h, cudaEventRecord(h->ev_cw_end, h->cw));
   h->have_prev = true;
   for (int j = 0; j < h->n; ++j) h->prev_out[j] = h->ev_ar[last_slot][j];
   if (flags & MERAK_FLAG_CHAIN) {
     h->chain_open = true;
   } else {
-    CK(h, cudaStreamWaitEvent(st, h->ev_cs_end, 0));
+    TRY(wait_all(h, st));
     CK(h, cudaStreamWaitEvent(st, h->ev_ar[last_slot][h->n - 1], 0));
     h->chain_open = false;
   }
@@ -338,7 +360,8 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
   auto S = [&](size_t off) { return saved + off; };
   // ---- attention block, sub-batch j: LN1 -> QKV -> attention -> proj (partial into slot 0) -> AR#1
   for (int j = 0; j < n; ++j) {
-    if (h->chain_open) CK(h, cudaStreamWaitEvent(h->cs, h->prev_out[j], 0));
+    cudaStream_t cst = sub_stream(h, j);
+    if (h->chain_open) CK(h, cudaStreamWaitEvent(cst, h->prev_out[j], 0));
     const size_t r0 = (size_t)j * m;
     const bf16 *xj = x + r0 * hh;
     bf16 *u = (bf16 *)S(L.u) + r0 * L.ld_u;
@@ -354,25 +377,25 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       pad.ptr[1] = ctx; pad.ld[1] = L.ld_ctx; pad.col[1] = hr;
       pad.ptr[2] = (bf16 *)S(L.u2) + r0 * L.ld_u2; pad.ld[2] = L.ld_u2; pad.col[2] = hh;
       pad.ptr[3] = (bf16 *)S(L.g) + r0 * L.ld_g; pad.ld[3] = L.ld_g; pad.col[3] = fr;
-      Launch Lk(h, MERAK_K_LN, h->cs, 0.0);
+      Launch Lk(h, MERAK_K_LN, cst, 0.0);
       CK(h, ln_fwd(xj, (const bf16 *)w->ln1_g, (const bf16 *)w->ln1_b, u, L.ld_u, mean1, rstd1, m, hh, h->eps, pad,
-                   h->cs));
+                   cst));
     }
     GemmArgs g = gargs(u, w->w_qkv, m, 3 * hr, hh, L.ld_u, hh, false, false, EPI_BIAS_BF16);
     g.out = qkv; g.ldo = 3 * hr; g.bias = w->b_qkv;
-    TRY(run_gemm(h, g));
+    TRY(run_gemm(h, g, cst));
     {
       AttnArgs a;
       memset(&a, 0, sizeof(a));
       a.qkv = qkv; a.ctx = ctx; a.ld_ctx = L.ld_ctx; a.lse = lse; a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
-      Launch Lk(h, MERAK_K_ATTN_FWD, h->cs, 2.0 * b * hr * (double)h->s * (h->s + 1));
-      CK(h, attn_fwd(a, h->cs));
+      Launch Lk(h, MERAK_K_ATTN_FWD, cst, 2.0 * b * hr * (double)h->s * (h->s + 1));
+      CK(h, attn_fwd(a, cst));
     }
-    if (h->ev_ar_valid[0][j]) CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[0][j], 0));
+    if (h->ev_ar_valid[0][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[0][j], 0));
     g = gargs(ctx, w->w_o, m, hh, hr, L.ld_ctx, hr, false, false, EPI_STORE_BF16);
     g.out = slot_ptr(h, h->r, 0) + r0 * hh; g.ldo = hh;
-    TRY(run_gemm(h, g));
-    CK(h, cudaEventRecord(h->ev_p[j], h->cs));
+    TRY(run_gemm(h, g, cst));
+    CK(h, cudaEventRecord(h->ev_p[j], cst));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
     {
       ArFwdArgs a;
@@ -395,18 +418,19 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
   }
   // ---- FFN block, sub-batch j: fc1 (+bias+GeLU) -> fc2 (partial into slot 1) -> AR#2
   for (int j = 0; j < n; ++j) {
+    cudaStream_t cst = sub_stream(h, j);
     const size_t r0 = (size_t)j * m;
-    CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[0][j], 0));
+    CK(h, cudaStreamWaitEvent(cst, h->ev_ar[0][j], 0));
     bf16 *u2 = (bf16 *)S(L.u2) + r0 * L.ld_u2;
     bf16 *z = (bf16 *)S(L.z) + r0 * fr, *gg = (bf16 *)S(L.g) + r0 * L.ld_g;
     GemmArgs g = gargs(u2, w->w_1, m, fr, hh, L.ld_u2, hh, false, false, EPI_BIAS_GELU);
     g.out = z; g.ldo = fr; g.out2 = gg; g.ldo2 = L.ld_g; g.bias = w->b_1;
-    TRY(run_gemm(h, g));
-    if (h->ev_ar_valid[1][j]) CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[1][j], 0));
+    TRY(run_gemm(h, g, cst));
+    if (h->ev_ar_valid[1][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[1][j], 0));
     g = gargs(gg, w->w_2, m, hh, fr, L.ld_g, fr, false, false, EPI_STORE_BF16);
     g.out = slot_ptr(h, h->r, 1) + r0 * hh; g.ldo = hh;
-    TRY(run_gemm(h, g));
-    CK(h, cudaEventRecord(h->ev_p[j], h->cs));
+    TRY(run_gemm(h, g, cst));
+    CK(h, cudaEventRecord(h->ev_p[j], cst));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
     {
       ArFwdArgs a;
@@ -429,11 +453,12 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
 
 // wgrad: dW[M', N'] += A_s^T B_s over the sub-batch tokens, with the ones column of B_s giving the
 // bias gradient db[M'] in the same accumulation chain.
+// Runs on the filler stream cw (lowest priority), after the events that produce its operands.
 static merak_status run_wgrad(merak_tmp_t *h, const bf16 *A, int lda, int Mo, const void *B, int ldb, int No, int m,
                               float *dW, float *db) {
   GemmArgs g = gargs(A, B, Mo, No + 1, m, lda, ldb, true, true, EPI_ACC_F32);
   g.out32 = dW; g.ld32 = No; g.db32 = db;
-  return run_gemm(h, g);
+  return run_gemm(h, g, h->cw);
 }
 
 // ------------------------------------------------------------------------------ backward
@@ -445,20 +470,27 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
   const bool comm = !(flags & MERAK_FLAG_NO_COMM);
   TRY(enter(h, st));
   auto S = [&](size_t off) { return saved + off; };
+  // W2 / b2 grads need only dy and the saved g: they can fill from the start of the backward
+  if (h->chain_open)
+    for (int j = 0; j < n; ++j) CK(h, cudaStreamWaitEvent(h->cw, h->prev_out[j], 0));
+  TRY(run_wgrad(h, dy, hh, hh, (const bf16 *)S(L.g), L.ld_g, fr, h->M, gr->w_2, gr->b_2));
   // ---- FFN block: fc2 dgrad (x GeLU') -> fc1 dgrad (partial, slot 2) -> AR#3 ; wgrads fill the gap
   for (int j = 0; j < n; ++j) {
-    if (h->chain_open) CK(h, cudaStreamWaitEvent(h->cs, h->prev_out[j], 0));
+    cudaStream_t cst = sub_stream(h, j);
+    if (h->chain_open) CK(h, cudaStreamWaitEvent(cst, h->prev_out[j], 0));
+    if (h->have_wg) CK(h, cudaStreamWaitEvent(cst, h->ev_w1, 0));  // previous W1 wgrad read dz
     const size_t r0 = (size_t)j * m;
     const bf16 *dyj = dy + r0 * hh;
     bf16 *dz = h->dz + r0 * fr;
     GemmArgs g = gargs(dyj, w->w_2, m, fr, hh, hh, fr, false, true, EPI_GELU_BWD);
     g.out = dz; g.ldo = fr; g.aux = (const bf16 *)S(L.z) + r0 * fr; g.ld_aux = fr;
-    TRY(run_gemm(h, g));
-    if (h->ev_ar_valid[2][j]) CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[2][j], 0));
+    TRY(run_gemm(h, g, cst));
+    CK(h, cudaEventRecord(h->ev_dz[j], cst));
+    if (h->ev_ar_valid[2][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[2][j], 0));
     g = gargs(dz, w->w_1, m, hh, fr, fr, hh, false, true, EPI_STORE_BF16);
     g.out = slot_ptr(h, h->r, 2) + r0 * hh; g.ldo = hh;
-    TRY(run_gemm(h, g));
-    CK(h, cudaEventRecord(h->ev_p[j], h->cs));
+    TRY(run_gemm(h, g, cst));
+    CK(h, cudaEventRecord(h->ev_p[j], cst));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
     {
       ArBwdArgs a;
@@ -483,33 +515,38 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     CK(h, cudaEventRecord(h->ev_ar[2][j], h->ms));
     h->ev_ar_valid[2][j] = true;
   }
-  // weight + bias gradients of the FFN block over ALL tokens (overlapping AR#3 of the last
-  // sub-batch): one accumulation chain over tokens 0..B*s-1 -- the same MMA sequence as n = 1.
-  TRY(run_wgrad(h, dy, hh, hh, (const bf16 *)S(L.g), L.ld_g, fr, h->M, gr->w_2, gr->b_2));
+  // weight + bias gradients of the FFN block over ALL tokens: one accumulation chain over tokens
+  // 0..B*s-1 -- the same MMA sequence as n = 1 -- on the filler stream once every dz rows exist.
+  for (int j = 0; j < n; ++j) CK(h, cudaStreamWaitEvent(h->cw, h->ev_dz[j], 0));
   TRY(run_wgrad(h, h->dz, fr, fr, (const bf16 *)S(L.u2), L.ld_u2, hh, h->M, gr->w_1, gr->b_1));
+  CK(h, cudaEventRecord(h->ev_w1, h->cw));
   // ---- attention block: proj dgrad -> attention bwd -> QKV dgrad (partial, slot 3) -> AR#4
   for (int j = 0; j < n; ++j) {
+    cudaStream_t cst = sub_stream(h, j);
     const size_t r0 = (size_t)j * m;
-    CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[2][j], 0));
+    CK(h, cudaStreamWaitEvent(cst, h->ev_ar[2][j], 0));
     const bf16 *dx1 = h->dx1 + r0 * hh;
     bf16 *dctx = h->dctx + r0 * hr, *dqkv = h->dqkv + r0 * 3 * hr;
     const bf16 *qkv = (const bf16 *)S(L.qkv) + r0 * 3 * hr, *ctx = (const bf16 *)S(L.ctx) + r0 * L.ld_ctx;
     GemmArgs g = gargs(dx1, w->w_o, m, hr, hh, hh, hr, false, true, EPI_STORE_BF16);
     g.out = dctx; g.ldo = hr;
-    TRY(run_gemm(h, g));
+    TRY(run_gemm(h, g, cst));
+    if (h->have_wg) CK(h, cudaStreamWaitEvent(cst, h->ev_wqkv, 0));  // previous W_qkv wgrad read dqkv
     {
       AttnArgs a;
       memset(&a, 0, sizeof(a));
-      a.qkv = qkv; a.ctx = (void *)ctx; a.ld_ctx = L.ld_ctx; a.lse = (float *)S(L.lse) + (size_t)j * b * h->Hr * h->s;
-      a.dctx = dctx; a.dqkv = dqkv; a.delta = h->delta; a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
-      Launch Lk(h, MERAK_K_ATTN_BWD, h->cs, 4.0 * b * hr * (double)h->s * (h->s + 1), 2);
-      CK(h, attn_bwd(a, h->cs));
+      const size_t so = (size_t)j * b * h->Hr * h->s;  // per-sub-batch lse / delta rows
+      a.qkv = qkv; a.ctx = (void *)ctx; a.ld_ctx = L.ld_ctx; a.lse = (float *)S(L.lse) + so;
+      a.dctx = dctx; a.dqkv = dqkv; a.delta = h->delta + so; a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
+      Launch Lk(h, MERAK_K_ATTN_BWD, cst, 4.0 * b * hr * (double)h->s * (h->s + 1), 2);
+      CK(h, attn_bwd(a, cst));
     }
-    if (h->ev_ar_valid[3][j]) CK(h, cudaStreamWaitEvent(h->cs, h->ev_ar[3][j], 0));
+    CK(h, cudaEventRecord(h->ev_dq[j], cst));
+    if (h->ev_ar_valid[3][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[3][j], 0));
     g = gargs(dqkv, w->w_qkv, m, hh, 3 * hr, 3 * hr, hh, false, true, EPI_STORE_BF16);
     g.out = slot_ptr(h, h->r, 3) + r0 * hh; g.ldo = hh;
-    TRY(run_gemm(h, g));
-    CK(h, cudaEventRecord(h->ev_p[j], h->cs));
+    TRY(run_gemm(h, g, cst));
+    CK(h, cudaEventRecord(h->ev_p[j], cst));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
     {
       ArBwdArgs a;
@@ -534,9 +571,14 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     CK(h, cudaEventRecord(h->ev_ar[3][j], h->ms));
     h->ev_ar_valid[3][j] = true;
   }
-  // weight + bias gradients of the attention block over all tokens (overlapping the last AR#4)
+  // weight + bias gradients of the attention block over all tokens (filling behind the last AR#4)
+  CK(h, cudaStreamWaitEvent(h->cw, h->ev_ar[2][n - 1], 0));  // every dx1 row (AR#3 in order on ms)
   TRY(run_wgrad(h, h->dx1, hh, hh, (const bf16 *)S(L.ctx), L.ld_ctx, hr, h->M, gr->w_o, gr->b_o));
+  CK(h, cudaEventRecord(h->ev_wo, h->cw));
+  for (int j = 0; j < n; ++j) CK(h, cudaStreamWaitEvent(h->cw, h->ev_dq[j], 0));
   TRY(run_wgrad(h, h->dqkv, 3 * hr, 3 * hr, (const bf16 *)S(L.u), L.ld_u, hh, h->M, gr->w_qkv, gr->b_qkv));
+  CK(h, cudaEventRecord(h->ev_wqkv, h->cw));
+  h->have_wg = true;
   return leave(h, st, flags, 3);
 }
 
@@ -570,8 +612,8 @@ static merak_status validate(const merak_tmp_config *c) {
 static void release(merak_tmp_t *h) {
   if (!h) return;
   cudaSetDevice(h->dev);
-  if (h->cs) cudaStreamSynchronize(h->cs);
-  if (h->ms) cudaStreamSynchronize(h->ms);
+  for (cudaStream_t c : {h->cs, h->cs1, h->cw, h->ms})
+    if (c) cudaStreamSynchronize(c);
   for (int q = 0; q < MAX_T; ++q)
     if (h->peer_pv[q] && h->peer_pv[q] != h->pv) cudaIpcCloseMemHandle(h->peer_pv[q]);
   if (h->nccl) g_nccl.CommDestroy(h->nccl);
@@ -579,16 +621,25 @@ static void release(merak_tmp_t *h) {
   if (h->ws) cudaFree(h->ws);
   if (h->err_host) cudaFreeHost(h->err_host);
   for (auto e : h->evpool) cudaEventDestroy(e);
-  if (h->ev_entry) cudaEventDestroy(h->ev_entry);
-  if (h->ev_cs_end) cudaEventDestroy(h->ev_cs_end);
+  for (cudaEvent_t e : {h->ev_entry, h->ev_cs_end, h->ev_cs1_end, h->ev_cw_end, h->ev_w1, h->ev_wo, h->ev_wqkv})
+    if (e) cudaEventDestroy(e);
   for (int j = 0; j < MAXN; ++j) {
     if (h->ev_p[j]) cudaEventDestroy(h->ev_p[j]);
+    if (h->ev_dz[j]) cudaEventDestroy(h->ev_dz[j]);
+    if (h->ev_dq[j]) cudaEventDestroy(h->ev_dq[j]);
     for (int k = 0; k < NSLOT; ++k)
       if (h->ev_ar[k][j]) cudaEventDestroy(h->ev_ar[k][j]);
   }
+  if (h->cs1 && h->cs1 != h->cs) cudaStreamDestroy(h->cs1);
+  if (h->cw && h->cw != h->cs) cudaStreamDestroy(h->cw);
   if (h->cs) cudaStreamDestroy(h->cs);
   if (h->ms) cudaStreamDestroy(h->ms);
   delete h;
+}
+
+static merak_status sync_all(merak_tmp_t *h) {
+  for (cudaStream_t c : {h->cs, h->cs1, h->cw, h->ms}) CK(h, cudaStreamSynchronize(c));
+  return MERAK_OK;
 }
 
 extern "C" {
@@ -632,12 +683,23 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   CKI(cudaSetDevice(h->dev));
   int prio_lo = 0, prio_hi = 0;
   CKI(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-  CKI(cudaStreamCreateWithPriority(&h->cs, cudaStreamNonBlocking, prio_lo));
+  // priorities: comm > sub-batch compute > wgrad filler (greatest priority = numerically lowest)
+  const int prio_mid = prio_hi < prio_lo ? prio_hi + 1 : prio_lo;
+  CKI(cudaStreamCreateWithPriority(&h->cs, cudaStreamNonBlocking, prio_mid));
   CKI(cudaStreamCreateWithPriority(&h->ms, cudaStreamNonBlocking, prio_hi));  // comm first when both ready
-  CKI(cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming));
-  CKI(cudaEventCreateWithFlags(&h->ev_cs_end, cudaEventDisableTiming));
+  const char *ns = getenv("MERAK_STREAMS");
+  if (ns && atoi(ns) == 1) {
+    h->cs1 = h->cw = h->cs;
+  } else {
+    CKI(cudaStreamCreateWithPriority(&h->cs1, cudaStreamNonBlocking, prio_mid));
+    CKI(cudaStreamCreateWithPriority(&h->cw, cudaStreamNonBlocking, prio_lo));
+  }
+  for (cudaEvent_t *e : {&h->ev_entry, &h->ev_cs_end, &h->ev_cs1_end, &h->ev_cw_end, &h->ev_w1, &h->ev_wo, &h->ev_wqkv})
+    CKI(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   for (int j = 0; j < MAXN; ++j) {
     CKI(cudaEventCreateWithFlags(&h->ev_p[j], cudaEventDisableTiming));
+    CKI(cudaEventCreateWithFlags(&h->ev_dz[j], cudaEventDisableTiming));
+    CKI(cudaEventCreateWithFlags(&h->ev_dq[j], cudaEventDisableTiming));
     for (int k = 0; k < NSLOT; ++k) CKI(cudaEventCreateWithFlags(&h->ev_ar[k][j], cudaEventDisableTiming));
   }
   // peer-visible slots + flags
@@ -725,8 +787,7 @@ merak_status merak_tmp_set_subbatches(merak_tmp_t *h, int32_t n_sub) {
   if (n_sub <= 0 || n_sub > MAXN) return fail(h, MERAK_EINVAL, "n_sub out of range");
   if (h->B % n_sub) return fail(h, MERAK_EINDIVISIBLE, "microbatch %% n_sub != 0");
   // all outstanding work of the old split must finish before slot/event indices are reinterpreted
-  CK(h, cudaStreamSynchronize(h->cs));
-  CK(h, cudaStreamSynchronize(h->ms));
+  TRY(sync_all(h));
   memset(h->ev_ar_valid, 0, sizeof(h->ev_ar_valid));
   h->n = n_sub;
   h->cfg.n_sub = n_sub;
@@ -763,7 +824,7 @@ merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, con
 merak_status merak_tmp_join(merak_tmp_t *h, void *st) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
   if (!h->have_prev) return MERAK_OK;
-  CK(h, cudaStreamWaitEvent((cudaStream_t)st, h->ev_cs_end, 0));
+  TRY(wait_all(h, (cudaStream_t)st));
   for (int j = 0; j < h->n; ++j) CK(h, cudaStreamWaitEvent((cudaStream_t)st, h->prev_out[j], 0));
   h->chain_open = false;
   return MERAK_OK;
@@ -785,8 +846,7 @@ const char *merak_tmp_last_error(const merak_tmp_t *h) { return h ? h->err.c_str
 
 merak_status merak_tmp_set_profiling(merak_tmp_t *h, int32_t on) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
-  CK(h, cudaStreamSynchronize(h->cs));
-  CK(h, cudaStreamSynchronize(h->ms));
+  TRY(sync_all(h));
   h->prof = on != 0;
   h->recs.clear();
   h->evnext = 0;
@@ -800,8 +860,7 @@ merak_status merak_tmp_set_profiling(merak_tmp_t *h, int32_t on) {
 
 merak_status merak_tmp_get_profile(merak_tmp_t *h, double *ms, int64_t *launches, double *flops) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
-  CK(h, cudaStreamSynchronize(h->cs));
-  CK(h, cudaStreamSynchronize(h->ms));
+  TRY(sync_all(h));
   for (auto &r : h->recs) {
     float t = 0;
     CK(h, cudaEventElapsedTime(&t, r.a, r.b));
@@ -821,8 +880,7 @@ merak_status merak_tmp_get_profile(merak_tmp_t *h, double *ms, int64_t *launches
 merak_status merak_tmp_get_timeline(merak_tmp_t *h, int32_t cap, int32_t *count, int32_t *cls, int32_t *stream,
                                     float *t0, float *t1) {
   if (!h || !count) return fail(h, MERAK_EINVAL, "NULL argument");
-  CK(h, cudaStreamSynchronize(h->cs));
-  CK(h, cudaStreamSynchronize(h->ms));
+  TRY(sync_all(h));
   int32_t n = 0;
   if (!h->recs.empty()) {
     cudaEvent_t origin = h->recs.front().a;
