@@ -288,12 +288,15 @@ def main():
             extras["n1_ms_per_step"] = ms_n1
             extras["subpipelining_speedup_vs_n1"] = ms_n1 / ms_step
             stage("n=1 done")
-        # e2e through the public API with host buffers: H2D x, dy (pinned) -> K fwd -> K bwd -> D2H y, dx
+        # e2e through the public API with host buffers: H2D x, dy (pinned) -> K fwd -> K bwd -> D2H y, dx.
+        # dy's upload overlaps the forward and y's download overlaps the backward (copy stream); x's
+        # upload and dx's download are exposed.
         hx = X.cpu().pin_memory()
         hdy = DY.cpu().pin_memory()
         hy = torch.empty_like(hx).pin_memory()
         hdx = torch.empty_like(hx).pin_memory()
         Xe, DYe = torch.empty_like(X), torch.empty_like(DY)
+        cp = torch.cuda.Stream(device=dev)
         ne = max(3, args.steps // 2)
         barrier()
         s_ev = [torch.cuda.Event(enable_timing=True) for _ in range(ne)]
@@ -302,10 +305,23 @@ def main():
             flush.zero_()
             s_ev[i].record(stream)
             Xe.copy_(hx, non_blocking=True)
-            DYe.copy_(hdy, non_blocking=True)
-            step(0, Xe, DYe)
-            hy.copy_(Ys[K - 1], non_blocking=True)
+            cp.wait_event(s_ev[i])
+            with torch.cuda.stream(cp):
+                DYe.copy_(hdy, non_blocking=True)
+            ev_dy = cp.record_event()
+            for k in range(K):
+                # the last forward joins the caller stream, so y is complete when the copy stream reads it
+                layer.forward(ws[k], Xe if k == 0 else Ys[k - 1], Ys[k], saved[k], flags=FLAG_CHAIN if k < K - 1 else 0)
+            cp.wait_stream(stream)
+            with torch.cuda.stream(cp):
+                hy.copy_(Ys[K - 1], non_blocking=True)
+            ev_y = cp.record_event()
+            stream.wait_event(ev_dy)
+            for k in reversed(range(K)):
+                layer.backward(ws[k], Xe if k == 0 else Ys[k - 1], saved[k], DYe if k == K - 1 else DXs[k + 1],
+                               DXs[k], grads[k], flags=FLAG_CHAIN if k > 0 else 0)
             hdx.copy_(DXs[0], non_blocking=True)
+            stream.wait_event(ev_y)
             e_ev[i].record(stream)
             stage(f"e2e iter {i} issued")
         barrier()

@@ -55,6 +55,13 @@
  * bias and residual in fp32 and rounds once to bf16; every reduction over tokens (bias,
  * LN and weight gradients) runs in a fixed order that does not depend on n_sub, so the
  * sub-pipelined (n_sub > 1) and the non-sub-pipelined (n_sub = 1) runs are bit-identical.
+ *
+ * fp32 check mode (precision = MERAK_FP32_CHECK; SURVEY §8(a) "the fp32 check mode is fp32
+ * everywhere", north_star tolerance 1e-5): x, y, dx, dy, every weight and the saved buffer are
+ * fp32 (same shapes and layouts; merak_tmp_saved_bytes() returns the fp32 size); the all-reduces
+ * sum fp32 partials in rank order without rounding.  Same sharding, sub-batch loop and token-order
+ * reductions (n_sub-independent), simple FP32-pipe kernels, all on one internal stream: a
+ * numerical reference for the method, not a fast path.
  */
 #ifndef MERAK_TMP_H
 #define MERAK_TMP_H
@@ -103,7 +110,7 @@ typedef struct {
   int32_t n_sub;       /* sub-microbatches n (P:571 uses 2); 1 = Megatron baseline     */
   int32_t ffn_hidden;  /* f; 0 => 4h (reading R7)                                     */
   float ln_eps;        /* LayerNorm epsilon; 0 => 1e-5 (reading R3)                   */
-  int32_t precision;   /* MERAK_BF16 (MERAK_FP32_CHECK: reserved, returns EUNSUPPORTED)*/
+  int32_t precision;   /* MERAK_BF16 | MERAK_FP32_CHECK (see "fp32 check mode" above)   */
   int32_t comm;        /* MERAK_COMM_PEER | MERAK_COMM_NCCL                           */
   int32_t comm_ctas;   /* CTAs used by each all-reduce kernel; 0 => auto              */
   int32_t device;      /* CUDA device ordinal this handle lives on                    */

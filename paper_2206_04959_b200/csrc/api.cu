@@ -114,6 +114,10 @@ struct merak_tmp {
   ncclComm_t nccl = nullptr;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // watchdog (env MERAK_AR_TIMEOUT_MS)
   bool two_shot = false;  // T >= 4: reduce-scatter + all-gather instead of one-shot (env MERAK_AR_TWO_SHOT)
+  // fp32 check mode (MERAK_FP32_CHECK): fp32 workspace
+  bool f32 = false;
+  char *ws32 = nullptr;
+  float *dz32 = nullptr, *dx1_32 = nullptr, *dctx32 = nullptr, *dqkv32 = nullptr, *delta32 = nullptr, *du32 = nullptr;
 };
 
 static std::string g_init_err;
@@ -250,9 +254,11 @@ static GemmArgs gargs(const void *A, const void *B, int M, int N, int K, int lda
 
 // NCCL baseline: in-place sum of this rank's slot rows on the comm stream; the fused epilogue
 // kernel then runs with the single (already reduced) local partial.
-static merak_status nccl_allreduce(merak_tmp_t *h, bf16 *rows, size_t count) {
-  Launch L(h, MERAK_K_ALLREDUCE, h->ms, 0.0, 0);
-  ncclResult_t r = g_nccl.AllReduce(rows, rows, count, ncclBfloat16, ncclSum, h->nccl, h->ms);
+static merak_status nccl_allreduce(merak_tmp_t *h, void *rows, size_t count, bool f32 = false,
+                                   cudaStream_t st = nullptr) {
+  if (!st) st = h->ms;
+  Launch L(h, MERAK_K_ALLREDUCE, st, 0.0, 0);
+  ncclResult_t r = g_nccl.AllReduce(rows, rows, count, f32 ? ncclFloat32 : ncclBfloat16, ncclSum, h->nccl, st);
   if (r != ncclSuccess) return fail(h, MERAK_ECUDA, "ncclAllReduce: %s", g_nccl.GetErrorString(r));
   return MERAK_OK;
 }
@@ -582,6 +588,206 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
   return leave(h, st, flags, 3);
 }
 
+// ------------------------------------------------------------------------------ fp32 check mode
+// MERAK_FP32_CHECK: the same method (sharding, sub-batch loop, rank-ordered all-reduces, token-order
+// reductions) with every tensor fp32 and the simple kernels of check_f32.cu, all on the compute
+// stream (peer handshakes included).  x, y, dx, dy, weights and saved activations are fp32.
+struct SavedF32 {
+  size_t u, mean1, rstd1, qkv, ctx, lse, x1, mean2, rstd2, u2, z, g, total;
+};
+static SavedF32 saved_f32(const merak_tmp_t *h) {
+  SavedF32 L;
+  size_t o = 0;
+  auto take = [&](size_t elems) { size_t at = o; o += align256(elems * 4); return at; };
+  const size_t M = h->M;
+  L.u = take(M * h->h); L.mean1 = take(M); L.rstd1 = take(M);
+  L.qkv = take(M * 3 * h->hr); L.ctx = take(M * h->hr); L.lse = take((size_t)h->B * h->Hr * h->s);
+  L.x1 = take(M * h->h); L.mean2 = take(M); L.rstd2 = take(M); L.u2 = take(M * h->h);
+  L.z = take(M * h->fr); L.g = take(M * h->fr);
+  L.total = o;
+  return L;
+}
+
+static F32GemmArgs g32(const float *A, const float *B, int M, int N, int K, int lda, int ldb, bool a_mn, bool b_mn,
+                       int epi, float *C, int ldc) {
+  F32GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.A = A; a.B = B; a.M = M; a.N = N; a.K = K; a.lda = lda; a.ldb = ldb; a.a_mn = a_mn; a.b_mn = b_mn;
+  a.epi = epi; a.C = C; a.ldc = ldc;
+  return a;
+}
+static merak_status run_g32(merak_tmp_t *h, const F32GemmArgs &a) {
+  Launch L(h, MERAK_K_GEMM, h->cs, 2.0 * a.M * a.N * a.K);
+  CK(h, f32_gemm(a, h->cs));
+  return MERAK_OK;
+}
+static float *slot32(merak_tmp_t *h, int rank, int slot) {
+  return reinterpret_cast<float *>(h->peer_pv[rank] + (size_t)slot * h->slot_bytes);
+}
+// all-reduce prologue: NCCL sum or peer handshake; fills the rank-ordered partial pointers
+static merak_status ar32_prologue(merak_tmp_t *h, bool comm, int slot, size_t r0, int m, F32ArArgs &a) {
+  float *mine = slot32(h, h->r, slot) + r0 * h->h;
+  if (comm && h->T > 1 && h->nccl) TRY(nccl_allreduce(h, mine, (size_t)m * h->h, true, h->cs));
+  if (!comm || h->T == 1 || h->nccl) {
+    a.T = 1;
+    a.partial[0] = mine;
+  } else {
+    a.T = h->T;
+    for (int q = 0; q < h->T; ++q) a.partial[q] = slot32(h, q, slot) + r0 * h->h;
+    PeerSync ps = make_sync(h, comm);
+    Launch Lk(h, MERAK_K_ALLREDUCE, h->cs, 0.0);
+    CK(h, peer_ready(ps, h->cs));
+  }
+  a.m = m; a.h = h->h; a.eps = h->eps;
+  return MERAK_OK;
+}
+
+static merak_status layer_fwd_f32(merak_tmp_t *h, const merak_tmp_weights *w, const float *x, float *y, char *saved,
+                                  uint32_t flags, cudaStream_t st) {
+  const SavedF32 L = saved_f32(h);
+  const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr;
+  const bool comm = !(flags & MERAK_FLAG_NO_COMM);
+  cudaStream_t c = h->cs;
+  TRY(enter(h, st));
+  auto S = [&](size_t off) { return reinterpret_cast<float *>(saved + off); };
+  for (int j = 0; j < n; ++j) {  // attention block
+    if (h->chain_open) CK(h, cudaStreamWaitEvent(c, h->prev_out[j], 0));
+    const size_t r0 = (size_t)j * m;
+    const float *xj = x + r0 * hh;
+    float *u = S(L.u) + r0 * hh, *qkv = S(L.qkv) + r0 * 3 * hr, *ctx = S(L.ctx) + r0 * hr;
+    {
+      Launch Lk(h, MERAK_K_LN, c, 0.0);
+      CK(h, f32_ln_fwd(xj, (const float *)w->ln1_g, (const float *)w->ln1_b, u, S(L.mean1) + r0, S(L.rstd1) + r0, m,
+                       hh, h->eps, c));
+    }
+    F32GemmArgs g = g32(u, (const float *)w->w_qkv, m, 3 * hr, hh, hh, hh, false, false, EPI_BIAS_BF16, qkv, 3 * hr);
+    g.bias = (const float *)w->b_qkv;
+    TRY(run_g32(h, g));
+    {
+      F32AttnArgs a;
+      memset(&a, 0, sizeof(a));
+      a.qkv = qkv; a.ctx = ctx; a.lse = S(L.lse) + (size_t)j * b * h->Hr * h->s;
+      a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
+      Launch Lk(h, MERAK_K_ATTN_FWD, c, 2.0 * b * hr * (double)h->s * (h->s + 1));
+      CK(h, f32_attn_fwd(a, c));
+    }
+    TRY(run_g32(h, g32(ctx, (const float *)w->w_o, m, hh, hr, hr, hr, false, false, EPI_STORE_BF16,
+                       slot32(h, h->r, 0) + r0 * hh, hh)));
+    F32ArArgs a;
+    memset(&a, 0, sizeof(a));
+    TRY(ar32_prologue(h, comm, 0, r0, m, a));
+    a.resid = xj; a.bias = (const float *)w->b_o; a.out = S(L.x1) + r0 * hh;
+    a.ln_out = S(L.u2) + r0 * hh; a.gamma = (const float *)w->ln2_g; a.beta = (const float *)w->ln2_b;
+    a.mean = S(L.mean2) + r0; a.rstd = S(L.rstd2) + r0;
+    {
+      Launch Lk(h, MERAK_K_ALLREDUCE, c, 0.0);
+      CK(h, f32_ar_fwd(a, c));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[0][j], c));
+  }
+  for (int j = 0; j < n; ++j) {  // FFN block
+    const size_t r0 = (size_t)j * m;
+    F32GemmArgs g = g32(S(L.u2) + r0 * hh, (const float *)w->w_1, m, fr, hh, hh, hh, false, false, EPI_BIAS_GELU,
+                        S(L.z) + r0 * fr, fr);
+    g.C2 = S(L.g) + r0 * fr; g.ldc2 = fr; g.bias = (const float *)w->b_1;
+    TRY(run_g32(h, g));
+    TRY(run_g32(h, g32(S(L.g) + r0 * fr, (const float *)w->w_2, m, hh, fr, fr, fr, false, false, EPI_STORE_BF16,
+                       slot32(h, h->r, 1) + r0 * hh, hh)));
+    F32ArArgs a;
+    memset(&a, 0, sizeof(a));
+    TRY(ar32_prologue(h, comm, 1, r0, m, a));
+    a.resid = S(L.x1) + r0 * hh; a.bias = (const float *)w->b_2; a.out = y + r0 * hh;
+    {
+      Launch Lk(h, MERAK_K_ALLREDUCE, c, 0.0);
+      CK(h, f32_ar_fwd(a, c));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[1][j], c));
+  }
+  return leave(h, st, flags, 1);
+}
+
+static merak_status layer_bwd_f32(merak_tmp_t *h, const merak_tmp_weights *w, const float *x, const char *saved_c,
+                                  const float *dy, float *dx, const merak_tmp_grads *gr, uint32_t flags,
+                                  cudaStream_t st) {
+  char *saved = const_cast<char *>(saved_c);
+  const SavedF32 L = saved_f32(h);
+  const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr, M = h->M;
+  const bool comm = !(flags & MERAK_FLAG_NO_COMM);
+  cudaStream_t c = h->cs;
+  TRY(enter(h, st));
+  auto S = [&](size_t off) { return reinterpret_cast<float *>(saved + off); };
+  auto chain = [&](const float *X, int ld, int cols, float *out) -> merak_status {
+    Launch Lk(h, MERAK_K_REDUCE, c, 0.0);
+    CK(h, f32_colsum_chain(X, ld, M, cols, out, c));
+    return MERAK_OK;
+  };
+  for (int j = 0; j < n; ++j) {  // FFN block: fc2 dgrad (x GeLU') -> fc1 dgrad -> AR#3
+    if (h->chain_open) CK(h, cudaStreamWaitEvent(c, h->prev_out[j], 0));
+    const size_t r0 = (size_t)j * m;
+    F32GemmArgs g = g32(dy + r0 * hh, (const float *)w->w_2, m, fr, hh, hh, fr, false, true, EPI_GELU_BWD,
+                        h->dz32 + r0 * fr, fr);
+    g.aux = S(L.z) + r0 * fr; g.ld_aux = fr;
+    TRY(run_g32(h, g));
+    TRY(run_g32(h, g32(h->dz32 + r0 * fr, (const float *)w->w_1, m, hh, fr, fr, hh, false, true, EPI_STORE_BF16,
+                       slot32(h, h->r, 2) + r0 * hh, hh)));
+    F32ArArgs a;
+    memset(&a, 0, sizeof(a));
+    TRY(ar32_prologue(h, comm, 2, r0, m, a));
+    a.x_ln = S(L.x1) + r0 * hh; a.mean = S(L.mean2) + r0; a.rstd = S(L.rstd2) + r0;
+    a.gamma = (const float *)w->ln2_g; a.dres = dy + r0 * hh; a.out = h->dx1_32 + r0 * hh; a.du = h->du32 + r0 * hh;
+    {
+      Launch Lk(h, MERAK_K_ALLREDUCE, c, 0.0);
+      CK(h, f32_ar_bwd(a, c));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[2][j], c));
+  }
+  // FFN weight / bias / LN2 grads over all tokens in token order
+  TRY(run_g32(h, g32(dy, S(L.g), hh, fr, M, hh, fr, true, true, EPI_ACC_F32, gr->w_2, fr)));
+  TRY(chain(dy, hh, hh, gr->b_2));
+  TRY(run_g32(h, g32(h->dz32, S(L.u2), fr, hh, M, fr, hh, true, true, EPI_ACC_F32, gr->w_1, hh)));
+  TRY(chain(h->dz32, fr, fr, gr->b_1));
+  {
+    Launch Lk(h, MERAK_K_REDUCE, c, 0.0);
+    CK(h, f32_ln_grad_chain(h->du32, S(L.x1), S(L.mean2), S(L.rstd2), M, hh, gr->ln2_g, gr->ln2_b, c));
+  }
+  for (int j = 0; j < n; ++j) {  // attention block: proj dgrad -> attention bwd -> QKV dgrad -> AR#4
+    const size_t r0 = (size_t)j * m;
+    TRY(run_g32(h, g32(h->dx1_32 + r0 * hh, (const float *)w->w_o, m, hr, hh, hh, hr, false, true, EPI_STORE_BF16,
+                       h->dctx32 + r0 * hr, hr)));
+    {
+      F32AttnArgs a;
+      memset(&a, 0, sizeof(a));
+      const size_t so = (size_t)j * b * h->Hr * h->s;
+      a.qkv = S(L.qkv) + r0 * 3 * hr; a.ctx = S(L.ctx) + r0 * hr; a.lse = S(L.lse) + so;
+      a.dctx = h->dctx32 + r0 * hr; a.dqkv = h->dqkv32 + r0 * 3 * hr; a.delta = h->delta32 + so;
+      a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
+      Launch Lk(h, MERAK_K_ATTN_BWD, c, 4.0 * b * hr * (double)h->s * (h->s + 1), 2);
+      CK(h, f32_attn_bwd(a, c));
+    }
+    TRY(run_g32(h, g32(h->dqkv32 + r0 * 3 * hr, (const float *)w->w_qkv, m, hh, 3 * hr, 3 * hr, hh, false, true,
+                       EPI_STORE_BF16, slot32(h, h->r, 3) + r0 * hh, hh)));
+    F32ArArgs a;
+    memset(&a, 0, sizeof(a));
+    TRY(ar32_prologue(h, comm, 3, r0, m, a));
+    a.x_ln = x + r0 * hh; a.mean = S(L.mean1) + r0; a.rstd = S(L.rstd1) + r0;
+    a.gamma = (const float *)w->ln1_g; a.dres = h->dx1_32 + r0 * hh; a.out = dx + r0 * hh; a.du = h->du32 + r0 * hh;
+    {
+      Launch Lk(h, MERAK_K_ALLREDUCE, c, 0.0);
+      CK(h, f32_ar_bwd(a, c));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[3][j], c));
+  }
+  TRY(run_g32(h, g32(h->dx1_32, S(L.ctx), hh, hr, M, hh, hr, true, true, EPI_ACC_F32, gr->w_o, hr)));
+  TRY(chain(h->dx1_32, hh, hh, gr->b_o));
+  TRY(run_g32(h, g32(h->dqkv32, S(L.u), 3 * hr, hh, M, 3 * hr, hh, true, true, EPI_ACC_F32, gr->w_qkv, hh)));
+  TRY(chain(h->dqkv32, 3 * hr, 3 * hr, gr->b_qkv));
+  {
+    Launch Lk(h, MERAK_K_REDUCE, c, 0.0);
+    CK(h, f32_ln_grad_chain(h->du32, x, S(L.mean1), S(L.rstd1), M, hh, gr->ln1_g, gr->ln1_b, c));
+  }
+  return leave(h, st, flags, 3);
+}
+
 // ------------------------------------------------------------------------------ init / destroy
 static merak_status validate(const merak_tmp_config *c) {
   if (!c) return fail(nullptr, MERAK_EINVAL, "config is NULL");
@@ -605,7 +811,6 @@ static merak_status validate(const merak_tmp_config *c) {
   if (c->seq_len % 16) return fail(nullptr, MERAK_EUNSUPPORTED, "seq_len must be a multiple of 16");
   if (c->microbatch > 48) return fail(nullptr, MERAK_EUNSUPPORTED, "microbatch > 48");
   if (c->hidden % 8 || (f / T) % 8) return fail(nullptr, MERAK_EUNSUPPORTED, "h and f/T must be multiples of 8");
-  if (c->precision == MERAK_FP32_CHECK) return fail(nullptr, MERAK_EUNSUPPORTED, "fp32 check mode not built yet");
   return MERAK_OK;
 }
 
@@ -619,6 +824,7 @@ static void release(merak_tmp_t *h) {
   if (h->nccl) g_nccl.CommDestroy(h->nccl);
   if (h->pv) cudaFree(h->pv);
   if (h->ws) cudaFree(h->ws);
+  if (h->ws32) cudaFree(h->ws32);
   if (h->err_host) cudaFreeHost(h->err_host);
   for (auto e : h->evpool) cudaEventDestroy(e);
   for (cudaEvent_t e : {h->ev_entry, h->ev_cs_end, h->ev_cs1_end, h->ev_cw_end, h->ev_w1, h->ev_wo, h->ev_wqkv})
@@ -665,8 +871,9 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   h->dev = cfg->device;
   h->G = ar_bwd_group_rows(h->h);
   if (const char *t = getenv("MERAK_AR_TIMEOUT_MS")) h->timeout_ns = (uint64_t)atoll(t) * 1000000ull;
-  h->two_shot = h->T >= 4;
-  if (const char *t = getenv("MERAK_AR_TWO_SHOT")) h->two_shot = h->T > 1 && atoi(t) == 1;
+  h->f32 = cfg->precision == MERAK_FP32_CHECK;
+  h->two_shot = h->T >= 4 && !h->f32;
+  if (const char *t = getenv("MERAK_AR_TWO_SHOT")) h->two_shot = h->T > 1 && !h->f32 && atoi(t) == 1;
   auto bail = [&](merak_status st) {
     g_init_err = h->err;
     release(h);
@@ -703,7 +910,7 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
     for (int k = 0; k < NSLOT; ++k) CKI(cudaEventCreateWithFlags(&h->ev_ar[k][j], cudaEventDisableTiming));
   }
   // peer-visible slots + flags
-  h->slot_bytes = align256((size_t)h->M * h->h * 2);
+  h->slot_bytes = align256((size_t)h->M * h->h * (h->f32 ? 4 : 2));
   h->flags_off = NSLOT * h->slot_bytes;
   h->pv_bytes = h->flags_off + align256(2 * MAX_AR_CTAS * MAX_T * sizeof(uint32_t));
   CKI(cudaMalloc(&h->pv, h->pv_bytes));
@@ -725,6 +932,16 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
     h->dz = (bf16 *)(h->ws + o_dz); h->dx1 = (bf16 *)(h->ws + o_dx1); h->dctx = (bf16 *)(h->ws + o_dctx);
     h->dqkv = (bf16 *)(h->ws + o_dqkv); h->delta = (float *)(h->ws + o_delta);
     h->part_col = (float *)(h->ws + o_pc); h->part_lng = (float *)(h->ws + o_pg); h->part_lnb = (float *)(h->ws + o_pb);
+  }
+  if (h->f32) {
+    const size_t M = h->M;
+    size_t o = 0;
+    auto take = [&](size_t elems) { size_t at = o; o += align256(elems * 4); return at; };
+    const size_t a = take(M * h->fr), b = take(M * h->h), c = take(M * h->hr), d = take(M * 3 * h->hr);
+    const size_t e = take((size_t)h->B * h->Hr * h->s), f = take(M * h->h);
+    CKI(cudaMalloc(&h->ws32, o));
+    h->dz32 = (float *)(h->ws32 + a); h->dx1_32 = (float *)(h->ws32 + b); h->dctx32 = (float *)(h->ws32 + c);
+    h->dqkv32 = (float *)(h->ws32 + d); h->delta32 = (float *)(h->ws32 + e); h->du32 = (float *)(h->ws32 + f);
   }
   CKI(cudaDeviceSynchronize());
   for (int q = 0; q < MAX_T; ++q) h->peer_pv[q] = nullptr;
@@ -794,7 +1011,10 @@ merak_status merak_tmp_set_subbatches(merak_tmp_t *h, int32_t n_sub) {
   return MERAK_OK;
 }
 
-size_t merak_tmp_saved_bytes(const merak_tmp_t *h) { return h ? saved_layout(h).total : 0; }
+size_t merak_tmp_saved_bytes(const merak_tmp_t *h) {
+  if (!h) return 0;
+  return h->f32 ? saved_f32(h).total : saved_layout(h).total;
+}
 
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
@@ -805,6 +1025,7 @@ merak_status merak_tmp_layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, con
   const void *ps[] = {w->ln1_g, w->ln1_b, w->w_qkv, w->b_qkv, w->w_o, w->b_o, w->ln2_g, w->ln2_b, w->w_1, w->b_1, w->w_2, w->b_2, x, y, saved};
   for (const void *p : ps)
     if (!p || !aligned16(p)) return fail(h, MERAK_EINVAL, "NULL or non-16B-aligned pointer");
+  if (h->f32) return layer_fwd_f32(h, w, (const float *)x, (float *)y, (char *)saved, flags, (cudaStream_t)st);
   return layer_fwd(h, w, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st);
 }
 
@@ -817,6 +1038,9 @@ merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, con
                       g->ln2_g, g->ln2_b, g->w_1, g->b_1, g->w_2, g->b_2};
   for (const void *p : ps)
     if (!p || !aligned16(p)) return fail(h, MERAK_EINVAL, "NULL or non-16B-aligned pointer");
+  if (h->f32)
+    return layer_bwd_f32(h, w, (const float *)x, (const char *)saved, (const float *)dy, (float *)dx, g, flags,
+                         (cudaStream_t)st);
   return layer_bwd(h, w, (const bf16 *)x, (const char *)saved, (const bf16 *)dy, (bf16 *)dx, g, flags,
                    (cudaStream_t)st);
 }

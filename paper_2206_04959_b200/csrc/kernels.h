@@ -16,6 +16,8 @@ namespace mk {
 //   b_mn = true : B stored [K rows, N cols] (N contiguous), row stride ldb   (B = stored^T)
 // Reduction order per output element is fixed: K walked in 64-wide blocks in increasing order,
 // 16-wide MMA steps inside; it never depends on M (bit-identity across sub-batch counts).
+constexpr int MAX_T = 8;  // max TMP degree
+
 enum Epi : int {
   EPI_STORE_BF16 = 0,  // out = bf16(acc)
   EPI_BIAS_BF16 = 1,   // out = bf16(acc + bias[n])
@@ -67,8 +69,52 @@ cudaError_t attn_fwd_tc(const AttnArgs &a, cudaStream_t st);  // attention_tc.cu
 cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st);  // 2 launches: dQ (+delta), then dK/dV
 cudaError_t attn_bwd_tc(const AttnArgs &a, cudaStream_t st);  // attention_bwd_tc.cu (MERAK_ATTN_BWD_TC=1)
 
+// ---------------------------------------------------------------- fp32 check mode (check_f32.cu)
+struct F32GemmArgs {  // C[M,N] (epi) sum_k A(m,k) B(n,k); A(m,k) = a_mn ? A[k*lda+m] : A[m*lda+k], same for B
+  const float *A, *B;
+  int M, N, K, lda, ldb;
+  bool a_mn, b_mn;
+  int epi;  // EPI_STORE_BF16 (plain store), EPI_BIAS_BF16, EPI_BIAS_GELU (C = z, C2 = gelu z), EPI_GELU_BWD, EPI_ACC_F32
+  float *C;
+  int ldc;
+  float *C2;
+  int ldc2;
+  const float *bias, *aux;
+  int ld_aux;
+};
+cudaError_t f32_gemm(const F32GemmArgs &a, cudaStream_t st);
+cudaError_t f32_ln_fwd(const float *x, const float *g, const float *b, float *u, float *mean, float *rstd, int m,
+                       int h, float eps, cudaStream_t st);
+struct F32AttnArgs {
+  const float *qkv;  // [b*s, 3hr]
+  float *ctx;        // [b*s, hr]
+  float *lse;        // [b, H, s] natural-log LSE of the scaled scores
+  const float *dctx;
+  float *dqkv;
+  float *delta;
+  int b, s, heads, d;
+};
+cudaError_t f32_attn_fwd(const F32AttnArgs &a, cudaStream_t st);
+cudaError_t f32_attn_bwd(const F32AttnArgs &a, cudaStream_t st);
+struct F32ArArgs {
+  const float *partial[MAX_T];
+  int T, m, h;
+  const float *resid, *bias;  // forward: out = sum partials + bias + resid
+  float *out;                 // forward: x1 / y; backward: dx
+  float *ln_out;              // forward AR#1: LN2(x1) (nullptr otherwise)
+  const float *gamma, *beta;
+  float *mean, *rstd;         // forward: written; backward: read (saved LN stats)
+  float eps;
+  const float *x_ln, *dres;   // backward: LN input, residual-path gradient
+  float *du;                  // backward: the all-reduced gradient (kept for the LN weight grads)
+};
+cudaError_t f32_ar_fwd(const F32ArArgs &a, cudaStream_t st);
+cudaError_t f32_ar_bwd(const F32ArArgs &a, cudaStream_t st);
+cudaError_t f32_colsum_chain(const float *X, int ldx, int rows, int cols, float *out, cudaStream_t st);
+cudaError_t f32_ln_grad_chain(const float *du, const float *xln, const float *mean, const float *rstd, int rows, int h,
+                              float *dg, float *db, cudaStream_t st);
+
 // ---------------------------------------------------------------- LN / all-reduce / reductions (ln_ar.cu)
-constexpr int MAX_T = 8;
 constexpr int MAX_AR_CTAS = 1024;
 
 // Peer synchronisation for one all-reduce.  flags_local: this rank's flag array; flags_peer[r]:

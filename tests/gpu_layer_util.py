@@ -8,6 +8,7 @@ import torch
 from paper_2206_04959_b200 import PARAM_NAMES, TmpLayer, shard_weights, zero_grads_like
 
 TOL_BF16 = 2e-2  # north_star: relative Frobenius error <= 2e-2 for bf16 with fp32 accumulation
+TOL_FP32 = 1e-5  # north_star: <= 1e-5 for the fp32 check mode
 
 
 def rel_err(gpu, ref) -> float:
@@ -16,17 +17,19 @@ def rel_err(gpu, ref) -> float:
     return float(np.linalg.norm(g - r) / max(np.linalg.norm(r), 1e-300))
 
 
-def run_gpu_layer(cfg, params, x, dy, T=1, rank=0, n_sub=None, group=None, reps=1, flags=0, device=None, comm=0):
+def run_gpu_layer(cfg, params, x, dy, T=1, rank=0, n_sub=None, group=None, reps=1, flags=0, device=None, comm=0,
+                  precision=0):
     """Forward + backward through merak_tmp_layer_fwd/bwd.  Returns dict of torch tensors on device:
-    y, dx and the rank's fp32 gradient shards."""
+    y, dx and the rank's fp32 gradient shards.  precision=1: MERAK_FP32_CHECK (fp32 tensors)."""
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
     n = cfg.n_sub if n_sub is None else n_sub
     layer = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, tmp_degree=T, tmp_rank=rank, n_sub=n,
-                     device=dev.index, group=group, comm=comm)
-    w = shard_weights(params, cfg.heads, T, rank, dev)
+                     device=dev.index, group=group, comm=comm, precision=precision)
+    dt = torch.float32 if precision == 1 else torch.bfloat16
+    w = shard_weights(params, cfg.heads, T, rank, dev, dtype=dt)
     M, h = cfg.tokens, cfg.hidden
-    X = torch.as_tensor(np.asarray(x).reshape(M, h)).to(dev, torch.bfloat16)
-    DY = torch.as_tensor(np.asarray(dy).reshape(M, h)).to(dev, torch.bfloat16)
+    X = torch.as_tensor(np.asarray(x).reshape(M, h)).to(dev, dt)
+    DY = torch.as_tensor(np.asarray(dy).reshape(M, h)).to(dev, dt)
     Y = torch.empty_like(X)
     DX = torch.empty_like(X)
     saved = layer.new_saved()

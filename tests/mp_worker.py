@@ -14,7 +14,7 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
-from gpu_layer_util import compare_to_oracle, oracle_rank_slices, run_gpu_layer  # noqa: E402
+from gpu_layer_util import TOL_FP32, compare_to_oracle, oracle_rank_slices, run_gpu_layer  # noqa: E402
 from oracle import layer_fwd_bwd  # noqa: E402
 from synth import CONFIGS  # noqa: E402
 from synth import make_all  # noqa: E402
@@ -71,6 +71,13 @@ def main():
         for k in out:
             if not torch.equal(out[k], out2[k]):
                 failures.append((name, f"{k}: one-shot vs two-shot all-reduce not bit-identical"))
+        # fp32 check mode over the peer all-reduce (tolerance 1e-5)
+        if cfg.hidden <= 320:
+            out32 = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group, precision=1)
+            errs, bad = compare_to_oracle(out32, y, dx, oracle_rank_slices(g, cfg, T, rank), cfg, tol=TOL_FP32)
+            print(f"[rank {rank}] {name} T={T} fp32", {k: f"{v:.1e}" for k, v in errs.items()}, flush=True)
+            if bad:
+                failures.append((name + "/fp32", bad))
         # NCCL baseline (MERAK_COMM_NCCL): same kernels, ncclAllReduce instead of the peer kernel
         outn = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group, comm=1)
         errs, bad = compare_to_oracle(outn, y, dx, oracle_rank_slices(g, cfg, T, rank), cfg)
