@@ -132,6 +132,14 @@ def cpu_oracle_sample(cfg, target_s=12.0):
             "host_cores_visible": len(os.sched_getaffinity(0))}
 
 
+def arm_config(cfg, K, T, n_sub):
+    """The workload both arms report (the reference arm times a bounded sample of it)."""
+    return {"workload": f"{cfg.name} layer fwd+bwd x {K} chained layers: h={cfg.hidden}, H={cfg.heads}, "
+                        f"s={cfg.seq_len}, B={cfg.microbatch}, TMP={T}, n_sub={n_sub}",
+            "layers": K, "tmp_degree": T, "n_sub": n_sub,
+            "l2": "flushed between steps (256 MiB write, outside the timed events)"}
+
+
 def run_reference(args, cfg, rank, world):
     """--impl reference: the CPU oracle as it stands, each step a bounded sample (1 sample of the
     workload's layer).  Rank 0 only; other ranks exit without work."""
@@ -157,10 +165,10 @@ def run_reference(args, cfg, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name} layer fwd+bwd, bounded sample: 1 of {cfg.microbatch} samples "
-                                   f"per step (h={cfg.hidden}, H={cfg.heads}, s={cfg.seq_len})"},
+            "config": arm_config(cfg, args.layers, world, cfg.n_sub),
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-                             "sample": f"1 of {cfg.microbatch} samples per step"},
+                             "sample": f"bounded sample: each step = 1 of the {cfg.microbatch} samples of one "
+                                       f"layer fwd+bwd, unsharded, fp64 numpy (TFLOP/s of that sample)"},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -278,6 +286,23 @@ def main():
             stage("no-comm done")
         else:
             extras["exposed_allreduce_ms_per_layer"] = 0.0
+        # all-reduce alone on the comm stream (NVLink roofline of the reduction): one sub-batch message
+        if T > 1:
+            rows = cfg.tokens // n_sub
+            two = (T >= 4) if os.environ.get("MERAK_AR_TWO_SHOT") is None else os.environ["MERAK_AR_TWO_SHOT"] == "1"
+            t_f = layer.bench_allreduce(0, rows, 20)
+            t_b = layer.bench_allreduce(1, rows, 20)
+            t_h = layer.bench_allreduce(0, rows // 2, 20)  # half message: marginal rate without fixed costs
+            msg = rows * h * 2
+            nvl = (2 * (T - 1) / T if two else (T - 1)) * msg  # bytes each GPU pulls from its peers per AR
+            extras["allreduce"] = {"algorithm": "two-shot" if two else "one-shot", "rows": rows, "msg_bytes": msg,
+                                   "nvlink_bytes_in_per_gpu": nvl, "fwd_ar_us": t_f * 1e3, "bwd_ar_us": t_b * 1e3,
+                                   "achieved_GBps": nvl / (t_f * 1e-3) / 1e9, "peak_GBps": 900.0,
+                                   "frac": nvl / (t_f * 1e-3) / 900e9,
+                                   "marginal_GBps": (nvl / 2) / ((t_f - t_h) * 1e-3) / 1e9 if t_f > t_h else None,
+                                   "fixed_us": (2 * t_h - t_f) * 1e3,
+                                   "note": "forward AR#2 incl. handshake kernel(s); peak = NVLink 5 per direction"}
+            stage("allreduce bench done")
         # n = 1 (Megatron-style, no sub-pipelining) with the same kernels: fig:ablation_pipetp analog
         if n_sub != 1:
             layer.set_subbatches(1)
@@ -373,11 +398,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, synth/)",
-                "config": {"workload": f"{cfg.name} layer fwd+bwd x {K} chained layers: h={cfg.hidden}, "
-                                       f"H={cfg.heads}, s={cfg.seq_len}, B={cfg.microbatch}, TMP={T}, n_sub={n_sub}",
-                           "layers": K, "tmp_degree": T, "n_sub": n_sub, "flops_per_step": fl,
-                           "ms_per_layer": ms_step / K,
-                           "l2": "flushed between steps (256 MiB write, outside the timed events)"},
+                "config": arm_config(cfg, K, T, n_sub), "flops_per_step": fl, "ms_per_layer": ms_step / K,
                 "value_per_gpu": value / world, "tokens_per_s": K * cfg.tokens / (ms_step * 1e-3),
                 "roofline": roofline, "gpu_launches": launches, "clocks": clocks}
         line.update({k: v for k, v in extras.items() if k != "e2e"})

@@ -89,7 +89,11 @@ typedef enum {
 } merak_status;
 
 enum { MERAK_BF16 = 0, MERAK_FP32_CHECK = 1 };      /* merak_tmp_config.precision */
-enum { MERAK_COMM_PEER = 0, MERAK_COMM_NCCL = 1 };  /* merak_tmp_config.comm      */
+/* merak_tmp_config.comm.  MERAK_COMM_LOCAL is a measurement mode: one process emulates rank
+ * tmp_rank of a T-way group on its own (no peers, no callback needed); every all-reduce reads only
+ * the local partial, as with MERAK_FLAG_NO_COMM.  Used to time per-rank compute of T = 8 shapes
+ * on one GPU (SURVEY §8(d) "TMP=8" projection).  Results are NOT the layer's. */
+enum { MERAK_COMM_PEER = 0, MERAK_COMM_NCCL = 1, MERAK_COMM_LOCAL = 2 };
 
 /* flags for layer_fwd / layer_bwd */
 enum {
@@ -111,7 +115,7 @@ typedef struct {
   int32_t ffn_hidden;  /* f; 0 => 4h (reading R7)                                     */
   float ln_eps;        /* LayerNorm epsilon; 0 => 1e-5 (reading R3)                   */
   int32_t precision;   /* MERAK_BF16 | MERAK_FP32_CHECK (see "fp32 check mode" above)   */
-  int32_t comm;        /* MERAK_COMM_PEER | MERAK_COMM_NCCL                           */
+  int32_t comm;        /* MERAK_COMM_PEER | MERAK_COMM_NCCL | MERAK_COMM_LOCAL        */
   int32_t comm_ctas;   /* CTAs used by each all-reduce kernel; 0 => auto              */
   int32_t device;      /* CUDA device ordinal this handle lives on                    */
 } merak_tmp_config;
@@ -189,6 +193,15 @@ merak_status merak_tmp_get_timeline(merak_tmp_t *h, int32_t cap, int32_t *count,
 
 /* Total kernels this handle launched since init (all classes, profiling on or off). */
 int64_t merak_tmp_launch_count(const merak_tmp_t *h);
+
+/* All-reduce microbenchmark (NVLink roofline evidence; collective over the TMP group, T > 1, bf16).
+ * Runs `iters` back-to-back all-reduces of `rows` x h bf16 partials (rows <= B*s) through the same
+ * path the layer uses (handshake kernel + one-shot, or two-shot at T >= 4, + fused epilogue), on the
+ * communication stream with nothing else running, and writes the mean device time per all-reduce in
+ * milliseconds to *ms.  which = 0: forward epilogue (AR#2: + bias + residual), 1: backward epilogue
+ * (AR#3: LayerNorm backward + residual), 2: the cross-rank handshake kernel alone.  Partial
+ * contents are zeros.  Synchronises the handle. */
+merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t rows, int32_t iters, float *ms);
 
 #ifdef __cplusplus
 }

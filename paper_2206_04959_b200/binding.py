@@ -19,7 +19,7 @@ MERAK_ECUDA, MERAK_EPEER, MERAK_ENOMEM, MERAK_ETIMEOUT, MERAK_ESTATE = -4, -5, -
 STATUS_NAMES = {0: "OK", -1: "EINVAL", -2: "EINDIVISIBLE", -3: "EUNSUPPORTED", -4: "ECUDA", -5: "EPEER",
                 -6: "ENOMEM", -7: "ETIMEOUT", -8: "ESTATE"}
 MERAK_BF16, MERAK_FP32_CHECK = 0, 1
-MERAK_COMM_PEER, MERAK_COMM_NCCL = 0, 1
+MERAK_COMM_PEER, MERAK_COMM_NCCL, MERAK_COMM_LOCAL = 0, 1, 2
 FLAG_CHAIN, FLAG_NO_COMM = 1, 2
 KERNEL_CLASSES = ("gemm", "attn_fwd", "attn_bwd", "layernorm", "allreduce", "reduce")
 PARAM_NAMES = ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_o", "b_o", "ln2_g", "ln2_b", "w_1", "b_1", "w_2", "b_2")
@@ -78,6 +78,8 @@ def lib():
         L.merak_tmp_get_timeline.restype = ctypes.c_int
         L.merak_tmp_launch_count.argtypes = [P]
         L.merak_tmp_launch_count.restype = ctypes.c_int64
+        L.merak_tmp_bench_allreduce.argtypes = [P, I32, I32, I32, ctypes.POINTER(ctypes.c_float)]
+        L.merak_tmp_bench_allreduce.restype = ctypes.c_int
         for fn in ("merak_tmp_init", "merak_tmp_set_subbatches", "merak_tmp_layer_fwd", "merak_tmp_layer_bwd",
                    "merak_tmp_join", "merak_tmp_destroy", "merak_tmp_set_profiling", "merak_tmp_get_profile"):
             getattr(L, fn).restype = ctypes.c_int
@@ -181,7 +183,7 @@ class TmpLayer:
         self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
         self.cfg = Config(hidden, heads, seq_len, microbatch, tmp_degree, tmp_rank, n_sub, ffn_hidden, ln_eps,
                           precision, comm, comm_ctas, self.device.index or 0)
-        self._cb = ALLGATHER_FN(_make_allgather(group)) if tmp_degree > 1 else ALLGATHER_FN(0)
+        self._cb = ALLGATHER_FN(_make_allgather(group)) if tmp_degree > 1 and comm != MERAK_COMM_LOCAL else ALLGATHER_FN(0)
         h = ctypes.c_void_p()
         st = L.merak_tmp_init(ctypes.byref(self.cfg), self._cb, None, ctypes.byref(h))
         if st != MERAK_OK:
@@ -246,6 +248,12 @@ class TmpLayer:
         t0, t1 = (ctypes.c_float * cap)(), (ctypes.c_float * cap)()
         self._check(lib().merak_tmp_get_timeline(self.h, cap, ctypes.byref(n), cls, st, t0, t1))
         return [(KERNEL_CLASSES[cls[i]], "comm" if st[i] else "comp", t0[i], t1[i]) for i in range(n.value)]
+
+    def bench_allreduce(self, which: int, rows: int, iters: int = 20) -> float:
+        """Mean device ms of one all-reduce of rows x h (collective: every rank must call it)."""
+        t = ctypes.c_float()
+        self._check(lib().merak_tmp_bench_allreduce(self.h, which, rows, iters, ctypes.byref(t)))
+        return t.value
 
     def launch_count(self) -> int:
         return lib().merak_tmp_launch_count(self.h)

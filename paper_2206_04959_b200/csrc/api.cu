@@ -116,6 +116,7 @@ struct merak_tmp {
   bool two_shot = false;  // T >= 4: reduce-scatter + all-gather instead of one-shot (env MERAK_AR_TWO_SHOT)
   // fp32 check mode (MERAK_FP32_CHECK): fp32 workspace
   bool f32 = false;
+  bool local = false;  // MERAK_COMM_LOCAL: single-process emulation of one rank, no peers
   char *ws32 = nullptr;
   float *dz32 = nullptr, *dx1_32 = nullptr, *dctx32 = nullptr, *dqkv32 = nullptr, *delta32 = nullptr, *du32 = nullptr;
 };
@@ -361,7 +362,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
                               uint32_t flags, cudaStream_t st) {
   const SavedLayout L = saved_layout(h);
   const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr;
-  const bool comm = !(flags & MERAK_FLAG_NO_COMM);
+  const bool comm = !(flags & MERAK_FLAG_NO_COMM) && !h->local;
   TRY(enter(h, st));
   auto S = [&](size_t off) { return saved + off; };
   // ---- attention block, sub-batch j: LN1 -> QKV -> attention -> proj (partial into slot 0) -> AR#1
@@ -473,7 +474,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
   char *saved = const_cast<char *>(saved_c);
   const SavedLayout L = saved_layout(h);
   const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr;
-  const bool comm = !(flags & MERAK_FLAG_NO_COMM);
+  const bool comm = !(flags & MERAK_FLAG_NO_COMM) && !h->local;
   TRY(enter(h, st));
   auto S = [&](size_t off) { return saved + off; };
   // W2 / b2 grads need only dy and the saved g: they can fill from the start of the backward
@@ -646,7 +647,7 @@ static merak_status layer_fwd_f32(merak_tmp_t *h, const merak_tmp_weights *w, co
                                   uint32_t flags, cudaStream_t st) {
   const SavedF32 L = saved_f32(h);
   const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr;
-  const bool comm = !(flags & MERAK_FLAG_NO_COMM);
+  const bool comm = !(flags & MERAK_FLAG_NO_COMM) && !h->local;
   cudaStream_t c = h->cs;
   TRY(enter(h, st));
   auto S = [&](size_t off) { return reinterpret_cast<float *>(saved + off); };
@@ -712,7 +713,7 @@ static merak_status layer_bwd_f32(merak_tmp_t *h, const merak_tmp_weights *w, co
   char *saved = const_cast<char *>(saved_c);
   const SavedF32 L = saved_f32(h);
   const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr, M = h->M;
-  const bool comm = !(flags & MERAK_FLAG_NO_COMM);
+  const bool comm = !(flags & MERAK_FLAG_NO_COMM) && !h->local;
   cudaStream_t c = h->cs;
   TRY(enter(h, st));
   auto S = [&](size_t off) { return reinterpret_cast<float *>(saved + off); };
@@ -797,7 +798,8 @@ static merak_status validate(const merak_tmp_config *c) {
   if (c->tmp_rank < 0 || c->tmp_rank >= c->tmp_degree) return fail(nullptr, MERAK_EINVAL, "tmp_rank out of range");
   if (c->precision != MERAK_BF16 && c->precision != MERAK_FP32_CHECK)
     return fail(nullptr, MERAK_EINVAL, "bad precision");
-  if (c->comm != MERAK_COMM_PEER && c->comm != MERAK_COMM_NCCL) return fail(nullptr, MERAK_EINVAL, "bad comm");
+  if (c->comm != MERAK_COMM_PEER && c->comm != MERAK_COMM_NCCL && c->comm != MERAK_COMM_LOCAL)
+    return fail(nullptr, MERAK_EINVAL, "bad comm");
   const int T = c->tmp_degree, f = c->ffn_hidden ? c->ffn_hidden : 4 * c->hidden;
   if (c->hidden % c->heads) return fail(nullptr, MERAK_EINDIVISIBLE, "hidden %% heads != 0");
   if (c->heads < T) return fail(nullptr, MERAK_EINDIVISIBLE, "heads < tmp_degree");
@@ -854,7 +856,8 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   if (!out) return fail(nullptr, MERAK_EINVAL, "out is NULL");
   *out = nullptr;
   TRY(validate(cfg));
-  if (cfg->tmp_degree > 1 && !ag) return fail(nullptr, MERAK_EINVAL, "tmp_degree > 1 needs an allgather callback");
+  if (cfg->tmp_degree > 1 && !ag && cfg->comm != MERAK_COMM_LOCAL)
+    return fail(nullptr, MERAK_EINVAL, "tmp_degree > 1 needs an allgather callback");
   merak_tmp_t *h = new merak_tmp();
   h->cfg = *cfg;
   h->h = cfg->hidden; h->H = cfg->heads; h->s = cfg->seq_len; h->B = cfg->microbatch;
@@ -872,6 +875,7 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   h->G = ar_bwd_group_rows(h->h);
   if (const char *t = getenv("MERAK_AR_TIMEOUT_MS")) h->timeout_ns = (uint64_t)atoll(t) * 1000000ull;
   h->f32 = cfg->precision == MERAK_FP32_CHECK;
+  h->local = cfg->comm == MERAK_COMM_LOCAL;
   h->two_shot = h->T >= 4 && !h->f32;
   if (const char *t = getenv("MERAK_AR_TWO_SHOT")) h->two_shot = h->T > 1 && !h->f32 && atoi(t) == 1;
   auto bail = [&](merak_status st) {
@@ -946,7 +950,7 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   CKI(cudaDeviceSynchronize());
   for (int q = 0; q < MAX_T; ++q) h->peer_pv[q] = nullptr;
   h->peer_pv[h->r] = h->pv;
-  if (h->T > 1) {
+  if (h->T > 1 && !h->local) {
     cudaIpcMemHandle_t mine;
     CKI(cudaIpcGetMemHandle(&mine, h->pv));
     std::vector<cudaIpcMemHandle_t> all(h->T);
@@ -1055,7 +1059,7 @@ merak_status merak_tmp_join(merak_tmp_t *h, void *st) {
 }
 
 merak_status merak_tmp_destroy(merak_tmp_t *h) {
-  if (h && h->T > 1 && !h->nccl && h->ms) {
+  if (h && h->T > 1 && !h->nccl && !h->local && h->ms) {
     // final barrier: no rank frees its slots while a peer's last all-reduce may still read them
     cudaSetDevice(h->dev);
     PeerSync ps = make_sync(h, true);
@@ -1125,6 +1129,77 @@ merak_status merak_tmp_get_timeline(merak_tmp_t *h, int32_t cap, int32_t *count,
 }
 
 int64_t merak_tmp_launch_count(const merak_tmp_t *h) { return h ? h->launches : 0; }
+
+merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t rows, int32_t iters, float *ms) {
+  if (!h || !ms) return fail(h, MERAK_EINVAL, "NULL argument");
+  if (h->T < 2 || h->nccl || h->f32 || h->local) return fail(h, MERAK_EUNSUPPORTED, "needs T > 1, peer comm, bf16");
+  if (rows <= 0 || rows > h->M || iters <= 0 || which < 0 || which > 2 || rows % h->G)
+    return fail(h, MERAK_EINVAL, "bad rows / iters / which");
+  TRY(sync_all(h));
+  CK(h, cudaSetDevice(h->dev));
+  const size_t hh = h->h, nb = (size_t)rows * hh * 2;
+  char *tmp = nullptr;
+  CK(h, cudaMalloc(&tmp, 3 * nb + 4 * hh * 4 + 1024));
+  bf16 *resid = (bf16 *)tmp, *out = (bf16 *)(tmp + nb), *gam = (bf16 *)(tmp + 2 * nb);
+  float *mean = nullptr, *rstd = nullptr;  // LN stats of the backward epilogue (rows entries each)
+  merak_status st = MERAK_OK;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  float *stats = nullptr;
+  do {
+    if (cudaMalloc(&stats, 2 * (size_t)rows * 4) != cudaSuccess) { st = fail(h, MERAK_ENOMEM, "stats"); break; }
+    mean = stats; rstd = stats + rows;
+    if (cudaMemsetAsync(tmp, 0, 3 * nb + 4 * hh * 4, h->ms) != cudaSuccess ||
+        cudaMemsetAsync(stats, 0, 2 * (size_t)rows * 4, h->ms) != cudaSuccess ||
+        cudaMemsetAsync(h->pv + h->slot_bytes, 0, nb, h->ms) != cudaSuccess) {
+      st = fail(h, MERAK_ECUDA, "memset");
+      break;
+    }
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto one = [&]() -> merak_status {
+      PeerSync ps = make_sync(h, true);
+      TRY(sync_peers(h, ps));
+      if (which == 2) return MERAK_OK;  // handshake kernel only
+      if (which == 0) {
+        ArFwdArgs a;
+        memset(&a, 0, sizeof(a));
+        a.T = ar_partials(h, true, 1, 0, a.partial);
+        a.m = rows; a.h = (int)hh; a.resid = resid; a.bias = gam; a.out = out; a.ctas = h->cfg.comm_ctas;
+        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, resid, gam, &a.chunk));
+        Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+        CK(h, ar_fwd(a, ps, h->ms));
+      } else {
+        ArBwdArgs a;
+        memset(&a, 0, sizeof(a));
+        a.T = ar_partials(h, true, 1, 0, a.partial);
+        a.m = rows; a.h = (int)hh; a.x_ln = resid; a.mean = mean; a.rstd = rstd; a.gamma = gam; a.dres = resid;
+        a.dx = out; a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
+        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, nullptr, nullptr, &a.chunk));
+        Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+        CK(h, ar_bwd(a, ps, h->ms));
+      }
+      return MERAK_OK;
+    };
+    for (int i = 0; i < 3 && st == MERAK_OK; ++i) st = one();  // warm-up
+    if (st != MERAK_OK) break;
+    cudaEventRecord(e0, h->ms);
+    for (int i = 0; i < iters && st == MERAK_OK; ++i) st = one();
+    if (st != MERAK_OK) break;
+    cudaEventRecord(e1, h->ms);
+    if (cudaEventSynchronize(e1) != cudaSuccess) { st = fail(h, MERAK_ECUDA, "event sync"); break; }
+    float t = 0;
+    cudaEventElapsedTime(&t, e0, e1);
+    *ms = t / iters;
+    st = check_async_error(h);
+  } while (0);
+  cudaStreamSynchronize(h->ms);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (stats) cudaFree(stats);
+  cudaFree(tmp);
+  memset(h->ev_ar_valid, 0, sizeof(h->ev_ar_valid));
+  return st;
+}
 
 // ------------------------------------------------------------------------------ testing entry points
 int merak_test_gemm(const void *A, const void *B, int M, int N, int K, int lda, int ldb, int a_mn, int b_mn, int epi,

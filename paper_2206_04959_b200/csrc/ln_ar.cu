@@ -52,18 +52,20 @@ MK_DEV void store8(__nv_bfloat16 *p, const float (&v)[8]) {
 }
 
 // One warp: lane r < T publishes epoch e to peer r, then waits for the peers' epoch e.
-// err_word[0] = 1 on timeout; err_word[1..4] = epoch, 0, peer, last flag value seen.
+// err_word[0] = 1 on timeout; err_word[1..4] = epoch, 0, peer, last flag value seen.  The error word
+// lives in host-mapped memory (a PCIe read), so the spin loop reads it only every 256 polls.
 __global__ void peer_ready_kernel(PeerSync ps) {
   const int r = threadIdx.x;
   volatile int *err = ps.err_word;
   if (*err) return;
-  __threadfence_system();
+  // The partials were written by kernels that completed before this one (stream / event order);
+  // peers read them through this GPU's L2, so the release store of the epoch suffices.
   if (r < ps.T && r != ps.rank) st_release_sys(ps.flags_peer[r] + ps.rank, ps.epoch);
   if (r < ps.T && r != ps.rank) {
     const uint64_t t0 = globaltimer();
     uint32_t v;
-    while ((int)((v = ld_acquire_sys(ps.flags_local + r)) - ps.epoch) < 0) {
-      if (*err || globaltimer() - t0 > ps.timeout_ns) {
+    for (uint32_t it = 1; (int)((v = ld_acquire_sys(ps.flags_local + r)) - ps.epoch) < 0; ++it) {
+      if ((it & 255) == 0 && (*err || globaltimer() - t0 > ps.timeout_ns)) {
         if (atomicExch(ps.err_word, 1) == 0) {
           err[1] = (int)ps.epoch;
           err[2] = 0;
@@ -83,94 +85,143 @@ cudaError_t peer_ready(const PeerSync &ps, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------ rank-ordered row sums
+// A peer load over NVLink costs ~1-2 us; a per-chunk dependent chain would serialise them.  Each lane
+// therefore issues the loads of CH of its chunks (chunk c = c0 + 32 i, 8 bf16 each) from all NT
+// sources before any arithmetic; the sums keep the fixed rank order 0..NT-1 (reading R10).
+MK_DEV void unpack8(const uint4 &u, float (&v)[8]) {
+  float2 a = unpack_bf16(u.x), b = unpack_bf16(u.y), c = unpack_bf16(u.z), d = unpack_bf16(u.w);
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y; v[6] = d.x; v[7] = d.y;
+}
+template <int NT, int CH>
+MK_DEV void rank_sum(const __nv_bfloat16 *const (&src)[NT], size_t ro, int c0, int nc, float (&v)[CH][8]) {
+  uint4 raw[CH][NT];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    const int c = c0 + 32 * i;
+#pragma unroll
+    for (int r = 0; r < NT; ++r)
+      raw[i][r] = c < nc ? *reinterpret_cast<const uint4 *>(src[r] + ro + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    unpack8(raw[i][0], v[i]);
+#pragma unroll
+    for (int r = 1; r < NT; ++r) {
+      float t[8];
+      unpack8(raw[i][r], t);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[i][k] += t[k];
+    }
+  }
+}
+// sources of one row: the T rank-ordered partials, or (two-shot phase 2, NT = 1) the owner's slot
+template <int NT>
+MK_DEV void row_sources(const __nv_bfloat16 *const *partial, int chunk, int row, const __nv_bfloat16 *(&src)[NT]) {
+#pragma unroll
+  for (int r = 0; r < NT; ++r) src[r] = partial[r];
+  if (NT == 1 && chunk > 0) src[0] = partial[row / chunk];
+}
+__host__ __device__ constexpr int ar_ch(int nt) { return nt >= 8 ? 1 : nt >= 4 ? 2 : 4; }
+
 // ------------------------------------------------------------------------------ forward all-reduce
+template <int NT>
 __global__ void __launch_bounds__(256) ar_fwd_kernel(ArFwdArgs a, PeerSync ps) {
-  {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nw = blockDim.x >> 5;
-    const int h = a.h, nc = h >> 3;
-    for (int row = blockIdx.x * nw + warp; row < a.m; row += gridDim.x * nw) {
-      const size_t ro = (size_t)row * h;
-      float sum = 0.f;
-      const __nv_bfloat16 *src0 = a.chunk > 0 ? a.partial[row / a.chunk] : a.partial[0];
-      for (int c = lane; c < nc; c += 32) {
-        float v[8];
-        load8(src0 + ro + c * 8, v);
-        if (a.chunk == 0) {
+  constexpr int CH = ar_ch(NT);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  const int h = a.h, nc = h >> 3;
+  const bool gathered = a.chunk > 0;
+  for (int row = blockIdx.x * nw + warp; row < a.m; row += gridDim.x * nw) {
+    const size_t ro = (size_t)row * h;
+    float sum = 0.f;
+    const __nv_bfloat16 *src[NT];
+    row_sources<NT>(a.partial, a.chunk, row, src);
+    for (int c0 = lane; c0 < nc; c0 += 32 * CH) {
+      float v[CH][8];
+      rank_sum<NT, CH>(src, ro, c0, nc, v);
 #pragma unroll
-          for (int r = 1; r < MAX_T; ++r)
-            if (r < a.T) add8(a.partial[r] + ro + c * 8, v);  // rank order (R10)
-          add8(a.bias + c * 8, v);
-          add8(a.resid + ro + c * 8, v);
+      for (int i = 0; i < CH; ++i) {
+        const int c = c0 + 32 * i;
+        if (c >= nc) continue;
+        if (!gathered) {
+          add8(a.bias + c * 8, v[i]);
+          add8(a.resid + ro + c * 8, v[i]);
         }
-        store8(a.out + ro + c * 8, v);
+        store8(a.out + ro + c * 8, v[i]);
         if (a.do_ln) {
-          float q[8];
-          load8(a.out + ro + c * 8, q);  // LN2 reads the stored bf16 x1 (reading R12)
 #pragma unroll
-          for (int i = 0; i < 8; ++i) sum += q[i];
+          for (int k = 0; k < 8; ++k) sum += bf16_round(v[i][k]);  // LN2 of the stored bf16 x1 (R12)
         }
       }
-      if (!a.do_ln) continue;
-      const float mean = warp_sum(sum) / h;
-      float var = 0.f;
-      for (int c = lane; c < nc; c += 32) {
-        float q[8];
-        load8(a.out + ro + c * 8, q);
+    }
+    if (!a.do_ln) continue;
+    const float mean = warp_sum(sum) / h;
+    float var = 0.f;
+    for (int c = lane; c < nc; c += 32) {
+      float q[8];
+      load8(a.out + ro + c * 8, q);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) var += (q[i] - mean) * (q[i] - mean);
-      }
-      const float rstd = rsqrtf(warp_sum(var) / h + a.eps);
-      for (int c = lane; c < nc; c += 32) {
-        float q[8], gm[8], bt[8];
-        load8(a.out + ro + c * 8, q);
-        load8(a.gamma + c * 8, gm);
-        load8(a.beta + c * 8, bt);
+      for (int i = 0; i < 8; ++i) var += (q[i] - mean) * (q[i] - mean);
+    }
+    const float rstd = rsqrtf(warp_sum(var) / h + a.eps);
+    for (int c = lane; c < nc; c += 32) {
+      float q[8], gm[8], bt[8];
+      load8(a.out + ro + c * 8, q);
+      load8(a.gamma + c * 8, gm);
+      load8(a.beta + c * 8, bt);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) q[i] = (q[i] - mean) * rstd * gm[i] + bt[i];
-        store8(a.ln_out + (size_t)row * a.ld_ln + c * 8, q);
-      }
-      if (lane == 0) {
-        a.mean[row] = mean;
-        a.rstd[row] = rstd;
-      }
+      for (int i = 0; i < 8; ++i) q[i] = (q[i] - mean) * rstd * gm[i] + bt[i];
+      store8(a.ln_out + (size_t)row * a.ld_ln + c * 8, q);
+    }
+    if (lane == 0) {
+      a.mean[row] = mean;
+      a.rstd[row] = rstd;
     }
   }
 }
 
 // ------------------------------------------------------------------------------ two-shot phase 1
-// Same per-element arithmetic (and order) as the one-shot kernels above, so one-shot and two-shot
-// results are bit-identical.
+// Same per-element arithmetic (and order) as the one-shot kernels, so one-shot and two-shot results
+// are bit-identical.
+template <int NT>
 __global__ void __launch_bounds__(256) ar_rs_kernel(ArRsArgs a) {
+  constexpr int CH = ar_ch(NT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int h = a.h, nc = h >> 3;
+  const __nv_bfloat16 *src[NT];
+  row_sources<NT>(a.partial, 0, 0, src);
   for (int row = a.row0 + blockIdx.x * nw + warp; row < a.row1; row += gridDim.x * nw) {
     const size_t ro = (size_t)row * h;
-    for (int c = lane; c < nc; c += 32) {
-      float v[8];
-      load8(a.partial[0] + ro + c * 8, v);
+    for (int c0 = lane; c0 < nc; c0 += 32 * CH) {
+      float v[CH][8];
+      rank_sum<NT, CH>(src, ro, c0, nc, v);
 #pragma unroll
-      for (int r = 1; r < MAX_T; ++r)
-        if (r < a.T) add8(a.partial[r] + ro + c * 8, v);
-      if (a.resid) {
-        add8(a.bias + c * 8, v);
-        add8(a.resid + ro + c * 8, v);
+      for (int i = 0; i < CH; ++i) {
+        const int c = c0 + 32 * i;
+        if (c >= nc) continue;
+        if (a.resid) {
+          add8(a.bias + c * 8, v[i]);
+          add8(a.resid + ro + c * 8, v[i]);
+        }
+        store8(a.out + ro + c * 8, v[i]);
       }
-      store8(a.out + ro + c * 8, v);
     }
   }
 }
 
 // ------------------------------------------------------------------------------ backward all-reduce
-template <int G>
+template <int G, int NT>
 __global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
-  extern __shared__ __align__(16) float du_s[];  // [G][h] fp32 sum of the partials
+  constexpr int CH = ar_ch(NT);
+  extern __shared__ __align__(16) float du_s[];  // [G][h] the all-reduced gradient (bf16-rounded)
   __shared__ float s_mean[G], s_rstd[G];
   {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int h = a.h, nc = h >> 3;
     const float inv_h = 1.f / h;
     const int ngroups = a.m / G;
+    const bool gathered = a.chunk > 0;
     for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
       // phase 1: warp per row -- all-reduce, LN backward, residual
       for (int ri = warp; ri < G; ri += 8) {
@@ -178,27 +229,31 @@ __global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
         const size_t ro = (size_t)row * h;
         const float mean = a.mean[row], rstd = a.rstd[row];
         float acc1 = 0.f, acc2 = 0.f;
-        const __nv_bfloat16 *src0 = a.chunk > 0 ? a.partial[row / a.chunk] : a.partial[0];
-        for (int c = lane; c < nc; c += 32) {
-          float du[8], x[8], gm[8];
-          load8(src0 + ro + c * 8, du);
-          if (a.chunk == 0) {
+        const __nv_bfloat16 *src[NT];
+        row_sources<NT>(a.partial, a.chunk, row, src);
+        for (int c0 = lane; c0 < nc; c0 += 32 * CH) {
+          float dv[CH][8];
+          rank_sum<NT, CH>(src, ro, c0, nc, dv);
 #pragma unroll
-            for (int r = 1; r < MAX_T; ++r)
-              if (r < a.T) add8(a.partial[r] + ro + c * 8, du);
+          for (int i = 0; i < CH; ++i) {
+            const int c = c0 + 32 * i;
+            if (c >= nc) continue;
+            float x[8], gm[8];
+            if (!gathered) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) du[i] = bf16_round(du[i]);  // the AR result is rounded once (R10)
-          }
-          float4 *ds = reinterpret_cast<float4 *>(du_s + ri * h + c * 8);
-          ds[0] = make_float4(du[0], du[1], du[2], du[3]);
-          ds[1] = make_float4(du[4], du[5], du[6], du[7]);
-          load8(a.x_ln + ro + c * 8, x);
-          load8(a.gamma + c * 8, gm);
+              for (int k = 0; k < 8; ++k) dv[i][k] = bf16_round(dv[i][k]);  // AR result rounded once (R10)
+            }
+            float4 *ds = reinterpret_cast<float4 *>(du_s + ri * h + c * 8);
+            ds[0] = make_float4(dv[i][0], dv[i][1], dv[i][2], dv[i][3]);
+            ds[1] = make_float4(dv[i][4], dv[i][5], dv[i][6], dv[i][7]);
+            load8(a.x_ln + ro + c * 8, x);
+            load8(a.gamma + c * 8, gm);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float xh = (x[i] - mean) * rstd, dxh = du[i] * gm[i];
-            acc1 += dxh;
-            acc2 += dxh * xh;
+            for (int k = 0; k < 8; ++k) {
+              const float xh = (x[k] - mean) * rstd, dxh = dv[i][k] * gm[k];
+              acc1 += dxh;
+              acc2 += dxh * xh;
+            }
           }
         }
         const float m1 = warp_sum(acc1) * inv_h, m2 = warp_sum(acc2) * inv_h;
@@ -407,50 +462,74 @@ static int clamp_ctas(int want, int work, int resident) {
   return want < 1 ? 1 : want;
 }
 
-cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
-  // handshake CTA count must be identical on all ranks: it depends only on (m, ctas)
+template <int NT>
+static cudaError_t ar_fwd_t(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
   static int resident = 0;
-  if (!resident) resident = resident_ctas((const void *)ar_fwd_kernel, 256, 0);
+  if (!resident) resident = resident_ctas((const void *)ar_fwd_kernel<NT>, 256, 0);
   const int grid = clamp_ctas(a.ctas, (a.m + 7) / 8, resident);
-  ar_fwd_kernel<<<grid, 256, 0, st>>>(a, ps);
+  ar_fwd_kernel<NT><<<grid, 256, 0, st>>>(a, ps);
   return cudaGetLastError();
+}
+cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
+  switch (a.chunk > 0 ? 1 : a.T) {
+    case 1: return ar_fwd_t<1>(a, ps, st);
+    case 2: return ar_fwd_t<2>(a, ps, st);
+    case 4: return ar_fwd_t<4>(a, ps, st);
+    case 8: return ar_fwd_t<8>(a, ps, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 int ar_bwd_group_rows(int h) { return 8; }
 
-cudaError_t ar_rs(const ArRsArgs &a, cudaStream_t st) {
-  if (a.row1 <= a.row0) return cudaSuccess;
+template <int NT>
+static cudaError_t ar_rs_t(const ArRsArgs &a, cudaStream_t st) {
   static int resident = 0;
-  if (!resident) resident = resident_ctas((const void *)ar_rs_kernel, 256, 0);
+  if (!resident) resident = resident_ctas((const void *)ar_rs_kernel<NT>, 256, 0);
   const int grid = clamp_ctas(a.ctas, (a.row1 - a.row0 + 7) / 8, resident);
-  ar_rs_kernel<<<grid, 256, 0, st>>>(a);
+  ar_rs_kernel<NT><<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }
-
-cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
-  const size_t smem = (size_t)a.G * a.h * sizeof(float);
-  if (a.G == 16) {
-    static size_t attr16 = 0;
-    if (smem > attr16) {
-      cudaError_t e = cudaFuncSetAttribute(ar_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      attr16 = smem;
-    }
-    const int grid = clamp_ctas(a.ctas, a.m / a.G, resident_ctas((const void *)ar_bwd_kernel<16>, 256, smem));
-    ar_bwd_kernel<16><<<grid, 256, smem, st>>>(a, ps);
-  } else if (a.G == 8) {
-    static size_t attr8 = 0;
-    if (smem > attr8) {
-      cudaError_t e = cudaFuncSetAttribute(ar_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      attr8 = smem;
-    }
-    const int grid = clamp_ctas(a.ctas, a.m / a.G, resident_ctas((const void *)ar_bwd_kernel<8>, 256, smem));
-    ar_bwd_kernel<8><<<grid, 256, smem, st>>>(a, ps);
-  } else {
-    return cudaErrorInvalidValue;
+cudaError_t ar_rs(const ArRsArgs &a, cudaStream_t st) {
+  if (a.row1 <= a.row0) return cudaSuccess;
+  switch (a.T) {
+    case 1: return ar_rs_t<1>(a, st);
+    case 2: return ar_rs_t<2>(a, st);
+    case 4: return ar_rs_t<4>(a, st);
+    case 8: return ar_rs_t<8>(a, st);
   }
+  return cudaErrorInvalidValue;
+}
+
+template <int NT>
+static cudaError_t ar_bwd_t(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
+  constexpr int G = 8;
+  const size_t smem = (size_t)G * a.h * sizeof(float);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(ar_bwd_kernel<G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  static int resident = 0;
+  static size_t res_smem = 0;
+  if (!resident || res_smem != smem) {
+    resident = resident_ctas((const void *)ar_bwd_kernel<G, NT>, 256, smem);
+    res_smem = smem;
+  }
+  const int grid = clamp_ctas(a.ctas, a.m / G, resident);
+  ar_bwd_kernel<G, NT><<<grid, 256, smem, st>>>(a, ps);
   return cudaGetLastError();
+}
+cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
+  if (a.G != 8 || a.m % 8) return cudaErrorInvalidValue;
+  switch (a.chunk > 0 ? 1 : a.T) {
+    case 1: return ar_bwd_t<1>(a, ps, st);
+    case 2: return ar_bwd_t<2>(a, ps, st);
+    case 4: return ar_bwd_t<4>(a, ps, st);
+    case 8: return ar_bwd_t<8>(a, ps, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t ln_fwd(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bfloat16 *b, __nv_bfloat16 *u,
