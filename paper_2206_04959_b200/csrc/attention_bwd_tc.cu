@@ -1,7 +1,8 @@
 // attention_bwd_tc.cu -- causal attention backward on tcgen05 / TMEM.
 //
-// Deterministic (bit-identity rule ii): two kernels, no atomics, each 192 threads
-// (warp 0 TMA, warp 1 TMEM owner + MMA issuer, warps 2-5 element-wise, thread = TMEM lane):
+// Deterministic (bit-identity rule ii): two kernels, no atomics, each 320 threads
+// (warp 0 TMA, warp 1 TMEM owner + MMA issuer, warps 2-9 element-wise: thread = TMEM lane, the two
+// warpgroups split the 64 columns of every tile -- the element-wise work is the latency-bound part):
 //   dQ kernel   one CTA per 128-query tile; for each 64-key half tile j:
 //               S = Q K_j^T, dP = dO V_j^T (TMEM) -> P = exp2(S*scale*log2e - lse), dS = P (dP - delta)
 //               (bf16, swizzled smem) -> dQ += dS K_j (TMEM accumulator).  Also writes delta =
@@ -21,6 +22,8 @@ namespace {
 
 constexpr int TR = 128;  // rows per CTA (TMEM lanes)
 constexpr int TH = 64;   // half tile
+constexpr int NTHR = 320;  // 2 + 8 warps
+constexpr int NEW = 8;     // element-wise warps (two warpgroups)
 
 MK_DEV void tmem_ld16b(uint32_t taddr, uint32_t *r) {
   asm volatile(
@@ -38,8 +41,9 @@ struct BwdCfg {
   static constexpr int FULL = NA * F_ATOM;
   static constexpr int HALF = NA * H_ATOM;
   static constexpr int X_BYTES = TR * 128;  // [128 rows][64] bf16 element-wise result (one atom)
-  // dQ kernel: Q, dO (full) + 2 stages of K, V (half) + 2 dS buffers
-  static constexpr int DQ_SMEM = 2 * FULL + 2 * 2 * HALF + 2 * X_BYTES + 1024 + 256;
+  // dQ kernel: Q, dO (full) + KST stages of K, V (half) + one dS buffer
+  static constexpr int KST = (D <= 64) ? 3 : 2;
+  static constexpr int DQ_SMEM = 2 * FULL + KST * 2 * HALF + X_BYTES + 1024 + 256;
   // dK/dV kernel: K, V (full) + 2 stages of Q, dO (half) + lse/delta + P^T, dS^T
   static constexpr int DKV_SMEM = 2 * FULL + 2 * (2 * HALF + 512) + 2 * X_BYTES + 1024 + 256;
   static constexpr int DQ_TMEM = (128 + D <= 256) ? 256 : 512;
@@ -62,7 +66,7 @@ MK_DEV void put_row_chunk(uint8_t *row, int r, int c32, const uint32_t (&w)[16])
 
 // ------------------------------------------------------------------------------------------ dQ
 template <int D>
-__global__ void __launch_bounds__(192, BwdCfg<D>::DQ_MIN)
+__global__ void __launch_bounds__(NTHR, BwdCfg<D>::DQ_MIN)
     attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmo,
                           const __grid_constant__ CUtensorMap tmkv, AttnArgs a) {
   using C = BwdCfg<D>;
@@ -70,13 +74,14 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DQ_MIN)
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sQ = smem, *sO = sQ + C::FULL;
-  uint8_t *sK = sO + C::FULL;            // [2][HALF]
-  uint8_t *sV = sK + 2 * C::HALF;        // [2][HALF]
-  uint8_t *sX = sV + 2 * C::HALF;        // [2][X_BYTES] dS
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sX + 2 * C::X_BYTES);
-  uint64_t *qd_full = bar, *kv_full = bar + 1, *kv_empty = bar + 3, *sp_full = bar + 5, *sp_free = bar + 6;
-  uint64_t *x_full = bar + 7, *x_free = bar + 9;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 11);
+  constexpr int KST = C::KST;
+  uint8_t *sK = sO + C::FULL;            // [KST][HALF]
+  uint8_t *sV = sK + KST * C::HALF;      // [KST][HALF]
+  uint8_t *sX = sV + KST * C::HALF;      // [X_BYTES] dS
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sX + C::X_BYTES);
+  uint64_t *qd_full = bar, *kv_full = bar + 1, *kv_empty = bar + 1 + KST, *sp_full = bar + 1 + 2 * KST;
+  uint64_t *sp_free = sp_full + 1, *x_full = sp_full + 2, *x_free = sp_full + 3;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sp_full + 4);
   constexpr uint32_t S_COL = 0, DP_COL = 64, DQ_COL = 128;
 
   const int s = a.s, H = a.heads, hr = H * D;
@@ -91,14 +96,14 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DQ_MIN)
     tma_prefetch(&tmo);
     tma_prefetch(&tmkv);
     mbar_init(qd_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < KST; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
-      mbar_init(&x_full[i], 4);
-      mbar_init(&x_free[i], 1);
     }
+    mbar_init(x_full, NEW);
+    mbar_init(x_free, 1);
     mbar_init(sp_full, 1);
-    mbar_init(sp_free, 4);
+    mbar_init(sp_free, NEW);
     fence_mbar_init();
     fence_proxy_async();
   }
@@ -117,8 +122,8 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DQ_MIN)
       }
     }
     for (int j = 0; j < J; ++j) {
-      const int st = j & 1;
-      mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+      const int st = j % KST;
+      mbar_wait(&kv_empty[st], ((j / KST) & 1) ^ 1);
       if (lane == 0) {
         mbar_expect_tx(&kv_full[st], 2 * C::HALF);
         for (int c = 0; c < NA; ++c) {
@@ -135,8 +140,8 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DQ_MIN)
     mbar_wait(qd_full, 0);
     for (int j = 0; j <= J; ++j) {
       if (j < J) {
-        const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        const int st = j % KST;
+        mbar_wait(&kv_full[st], (j / KST) & 1);
         mbar_wait(sp_free, (j & 1) ^ 1);
         tc_fence_after();
         if (lane == 0) {
@@ -155,23 +160,23 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DQ_MIN)
         __syncwarp();
       }
       if (j >= 1) {
-        const int i = j - 1, st = i & 1, b = i & 1;
-        mbar_wait(&x_full[b], (i >> 1) & 1);
+        const int i = j - 1, st = i % KST;
+        mbar_wait(x_full, i & 1);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t x0 = smem_u32(sX + b * C::X_BYTES), k0 = smem_u32(sK + st * C::HALF);
+          const uint32_t x0 = smem_u32(sX), k0 = smem_u32(sK + st * C::HALF);
 #pragma unroll
           for (int kk = 0; kk < TH / 16; ++kk)
             tc_mma_f16(tmem + DQ_COL, sdesc_sw128(x0 + kk * 32, 16, 1024), sdesc_sw128(k0 + kk * 2048, C::H_ATOM, 1024),
                        idesc_q, (i > 0 || kk > 0) ? 1u : 0u);
-          tc_commit(&x_free[b]);
+          tc_commit(x_free);
           tc_commit(&kv_empty[st]);
         }
         __syncwarp();
       }
     }
   } else {
-    const int q = warp & 3, r = q * 32 + lane, qi = qt * TR + r;
+    const int q = warp & 3, r = q * 32 + lane, qi = qt * TR + r, cw = (warp - 2) >> 2;
     const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
     const float scale = 1.f / sqrtf((float)D), sl2 = 1.4426950408889634f * scale;
     const size_t srow = ((size_t)bi * H + head) * s;
@@ -192,25 +197,25 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DQ_MIN)
         acc[3] += o3.x * d3.x + o3.y * d3.y;
       }
       del = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-      a.delta[srow + qi] = del;
+      if (cw == 0) a.delta[srow + qi] = del;
     }
     const float ls = lse;
     for (int j = 0; j < J; ++j) {
-      const int b = j & 1;
       mbar_wait(sp_full, j & 1);
       tc_fence_after();
       const int kj0 = j * TH;
       const bool mask = (kj0 + TH - 1 > qt * TR) || (kj0 + TH > s);
-      uint32_t w[2][16];
+      uint32_t w[16];  // this warpgroup's 32 columns, bf16-packed
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        uint32_t sv[32], dv[32];
-        tmem_ld32(lb + S_COL + h2 * 32, sv);
-        tmem_ld32(lb + DP_COL + h2 * 32, dv);
+      for (int hc = 0; hc < 2; ++hc) {
+        const int col0 = cw * 32 + hc * 16;
+        uint32_t sv[16], dv[16];
+        tmem_ld16b(lb + S_COL + col0, sv);
+        tmem_ld16b(lb + DP_COL + col0, dv);
         tmem_ld_wait();
 #pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          const int kj = kj0 + h2 * 32 + k;
+        for (int k = 0; k < 16; k += 2) {
+          const int kj = kj0 + col0 + k;
           float p0 = fast_exp2(fmaf(__uint_as_float(sv[k]), sl2, -ls));
           float p1 = fast_exp2(fmaf(__uint_as_float(sv[k + 1]), sl2, -ls));
           float g0 = p0 * (__uint_as_float(dv[k]) - del), g1 = p1 * (__uint_as_float(dv[k + 1]) - del);
@@ -218,26 +223,25 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DQ_MIN)
             if (!(kj <= qi && kj < s)) g0 = 0.f;
             if (!(kj + 1 <= qi && kj + 1 < s)) g1 = 0.f;
           }
-          w[h2][k >> 1] = pack_bf16(g0, g1);
+          w[hc * 8 + (k >> 1)] = pack_bf16(g0, g1);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(sp_free);
-      mbar_wait(&x_free[b], ((j >> 1) & 1) ^ 1);  // dS buffer b was read by the MMA of j-2
-      uint8_t *row = sX + b * C::X_BYTES + r * 128;
-      put_row_chunk(row, r, 0, w[0]);
-      put_row_chunk(row, r, 1, w[1]);
+      mbar_wait(x_free, (j & 1) ^ 1);  // the dS buffer was read by the MMA of j-1
+      put_row_chunk(sX + r * 128, r, cw, w);
       fence_proxy_async();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&x_full[b]);
+      if (lane == 0) mbar_arrive(x_full);
     }
     const int last = J - 1;
-    mbar_wait(&x_free[last & 1], (last >> 1) & 1);
+    mbar_wait(x_free, last & 1);
     tc_fence_after();
     __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.dqkv) + (size_t)(tok0 + qi) * 3 * hr + head * D;
 #pragma unroll
     for (int c = 0; c < D / 16; ++c) {
+      if ((c & 1) != cw) continue;  // warp-uniform: the warpgroups take alternate 16-column chunks
       uint32_t o[16];
       tmem_ld16b(lb + DQ_COL + c * 16, o);
       tmem_ld_wait();
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DQ_MIN)
 
 // ------------------------------------------------------------------------------------------ dK / dV
 template <int D>
-__global__ void __launch_bounds__(192, BwdCfg<D>::DKV_MIN)
+__global__ void __launch_bounds__(NTHR, BwdCfg<D>::DKV_MIN)
     attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmf, const __grid_constant__ CUtensorMap tmh,
                             const __grid_constant__ CUtensorMap tmoh, AttnArgs a) {
   using C = BwdCfg<D>;
@@ -303,8 +307,8 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DKV_MIN)
       mbar_init(&q_empty[i], 1);
     }
     mbar_init(sp_full, 1);
-    mbar_init(sp_free, 4);
-    mbar_init(x_full, 4);
+    mbar_init(sp_free, NEW);
+    mbar_init(x_full, NEW);
     mbar_init(x_free, 1);
     fence_mbar_init();
     fence_proxy_async();
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DKV_MIN)
       }
     }
   } else {
-    const int q = warp & 3, r = q * 32 + lane, kj = kt * TR + r;
+    const int q = warp & 3, r = q * 32 + lane, kj = kt * TR + r, cw = (warp - 2) >> 2;
     const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
     const float scale = 1.f / sqrtf((float)D), sl2 = 1.4426950408889634f * scale;
     for (int ii = 0; ii < NI; ++ii) {
@@ -397,16 +401,17 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DKV_MIN)
       tc_fence_after();
       const bool mask = (qi0 < kt * TR + TR - 1) || (qi0 + TH > s);
       const float *L = sL + st * TH, *Dl = sD + st * TH;
-      uint32_t wp[2][16], ws[2][16];
+      uint32_t wp[16], ws[16];  // this warpgroup's 32 columns of P^T and dS^T, bf16-packed
 #pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        uint32_t sv[32], dv[32];
-        tmem_ld32(lb + ST_COL + h2 * 32, sv);
-        tmem_ld32(lb + DPT_COL + h2 * 32, dv);
+      for (int hc = 0; hc < 2; ++hc) {
+        const int col0 = cw * 32 + hc * 16;
+        uint32_t sv[16], dv[16];
+        tmem_ld16b(lb + ST_COL + col0, sv);
+        tmem_ld16b(lb + DPT_COL + col0, dv);
         tmem_ld_wait();
 #pragma unroll
-        for (int k = 0; k < 32; k += 2) {
-          const int c = h2 * 32 + k, qi = qi0 + c;
+        for (int k = 0; k < 16; k += 2) {
+          const int c = col0 + k, qi = qi0 + c;
           float p0 = fast_exp2(fmaf(__uint_as_float(sv[k]), sl2, -L[c]));
           float p1 = fast_exp2(fmaf(__uint_as_float(sv[k + 1]), sl2, -L[c + 1]));
           if (mask) {
@@ -414,19 +419,16 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DKV_MIN)
             if (!(kj <= qi + 1 && qi + 1 < s)) p1 = 0.f;
           }
           const float g0 = p0 * (__uint_as_float(dv[k]) - Dl[c]), g1 = p1 * (__uint_as_float(dv[k + 1]) - Dl[c + 1]);
-          wp[h2][k >> 1] = pack_bf16(p0, p1);
-          ws[h2][k >> 1] = pack_bf16(g0, g1);
+          wp[hc * 8 + (k >> 1)] = pack_bf16(p0, p1);
+          ws[hc * 8 + (k >> 1)] = pack_bf16(g0, g1);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(sp_free);
       mbar_wait(x_free, (ii & 1) ^ 1);  // P^T / dS^T were read by the MMAs of ii-1
-      uint8_t *rp = sP + r * 128, *rs = sS + r * 128;
-      put_row_chunk(rp, r, 0, wp[0]);
-      put_row_chunk(rp, r, 1, wp[1]);
-      put_row_chunk(rs, r, 0, ws[0]);
-      put_row_chunk(rs, r, 1, ws[1]);
+      put_row_chunk(sP + r * 128, r, cw, wp);
+      put_row_chunk(sS + r * 128, r, cw, ws);
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(x_full);
@@ -438,6 +440,7 @@ __global__ void __launch_bounds__(192, BwdCfg<D>::DKV_MIN)
     __nv_bfloat16 *dvp = dk + hr;
 #pragma unroll
     for (int c = 0; c < D / 16; ++c) {
+      if ((c & 1) != cw) continue;  // warp-uniform: alternate 16-column chunks per warpgroup
       uint32_t ov[16], ok[16];
       tmem_ld16b(lb + DV_COL + c * 16, ov);
       tmem_ld16b(lb + DK_COL + c * 16, ok);
@@ -511,10 +514,10 @@ static cudaError_t bwd_tc_d(const AttnArgs &a, cudaStream_t st) {
       !make_rows_map(&mo_full, a.dctx, tokens, hr, hr, TR) || !make_rows_map(&mo_half, a.dctx, tokens, hr, hr, TH))
     return cudaErrorInvalidValue;
   dim3 grid((a.s + TR - 1) / TR, a.heads, a.b);
-  attn_bwd_dq_tc_kernel<D><<<grid, 192, C::DQ_SMEM, st>>>(mq_full, mo_full, mq_half, a);
+  attn_bwd_dq_tc_kernel<D><<<grid, NTHR, C::DQ_SMEM, st>>>(mq_full, mo_full, mq_half, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  attn_bwd_dkdv_tc_kernel<D><<<grid, 192, C::DKV_SMEM, st>>>(mq_full, mq_half, mo_half, a);
+  attn_bwd_dkdv_tc_kernel<D><<<grid, NTHR, C::DKV_SMEM, st>>>(mq_full, mq_half, mo_half, a);
   return cudaGetLastError();
 }
 

@@ -43,7 +43,7 @@ def main():
         tb = t(lambda: lib().merak_test_attn_bwd(P(qkv), P(ctx), P(lse), P(dctx), P(dqkv), P(delta), b, s, H, d, st))
         res[f"b{b}_s{s}_H{H}_d{d}"] = {"fwd_us": round(tf * 1e3, 1), "fwd_tflops": round(fl / tf / 1e9, 1),
                                        "bwd_us": round(tb * 1e3, 1), "bwd_tflops": round(2 * fl / tb / 1e9, 1)}
-    print(json.dumps({"tc": os.environ.get("MERAK_ATTN_TC", "0"), "bwd_tc": os.environ.get("MERAK_ATTN_BWD_TC", "0"), "res": res}))
+    print(json.dumps({"fwd_tc": os.environ.get("MERAK_ATTN_TC", "0"), "bwd_tc": os.environ.get("MERAK_ATTN_BWD_TC", "1"), "res": res}))
 
 
 if __name__ == "__main__":
