@@ -59,3 +59,50 @@ def compare_to_oracle(out, y_ref, dx_ref, grads_ref_rank, cfg, tol=TOL_BF16):
         errs[k] = rel_err(out[k].cpu().numpy(), grads_ref_rank[k])
     bad = {k: v for k, v in errs.items() if not (v <= tol)}
     return errs, bad
+
+
+def run_gpu_chain(cfg, params_list, x, dy, T=1, rank=0, group=None, chain=True, n_sub=None):
+    """K stacked layers through the C ABI: forward 0..K-1, backward K-1..0.  chain=True passes
+    MERAK_FLAG_CHAIN on every call but the last backward (cross-layer overlap, the bench's mode), so
+    the library's cross-layer event hazards (workspace reuse between layers) are exercised.
+    Returns dict: y (last layer), dx (first layer), grads[k]."""
+    from paper_2206_04959_b200 import FLAG_CHAIN
+    dev = torch.device("cuda", torch.cuda.current_device())
+    K = len(params_list)
+    n = cfg.n_sub if n_sub is None else n_sub
+    layer = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, tmp_degree=T, tmp_rank=rank, n_sub=n,
+                     device=dev.index, group=group)
+    ws = [shard_weights(p, cfg.heads, T, rank, dev) for p in params_list]
+    M, h = cfg.tokens, cfg.hidden
+    X = torch.as_tensor(np.asarray(x).reshape(M, h)).to(dev, torch.bfloat16)
+    DY = torch.as_tensor(np.asarray(dy).reshape(M, h)).to(dev, torch.bfloat16)
+    Ys = [torch.empty_like(X) for _ in range(K)]
+    DXs = [torch.empty_like(X) for _ in range(K)]
+    grads = [zero_grads_like(w) for w in ws]
+    saved = [layer.new_saved() for _ in range(K)]
+    f = FLAG_CHAIN if chain else 0
+    for k in range(K):
+        layer.forward(ws[k], X if k == 0 else Ys[k - 1], Ys[k], saved[k], flags=f)
+    for k in reversed(range(K)):
+        layer.backward(ws[k], X if k == 0 else Ys[k - 1], saved[k], DY if k == K - 1 else DXs[k + 1], DXs[k],
+                       grads[k], flags=f if k > 0 else 0)
+    torch.cuda.synchronize()
+    out = {"y": Ys[K - 1].clone(), "dx": DXs[0].clone(), "grads": [{k: g[k].clone() for k in PARAM_NAMES}
+                                                                  for g in grads]}
+    layer.close()
+    return out
+
+
+def oracle_chain(params_list, x, dy, heads):
+    """fp64 composition of the oracle layer: forward through all layers, backward in reverse."""
+    from oracle.layer import layer_backward, layer_forward
+    caches, h_in = [], x
+    for p in params_list:
+        h_in, c = layer_forward(p, h_in, heads)
+        caches.append(c)
+    y = h_in
+    grads = [None] * len(params_list)
+    g = dy
+    for k in reversed(range(len(params_list))):
+        g, grads[k] = layer_backward(params_list[k], caches[k], g, heads)
+    return y, g, grads

@@ -84,6 +84,18 @@ def main():
         print(f"[rank {rank}] {name} T={T} nccl", {k: f"{v:.2e}" for k, v in errs.items()}, flush=True)
         if bad:
             failures.append((name + "/nccl", bad))
+    # chained stack (cross-layer overlap + workspace hazards across ranks): chained == unchained bitwise
+    from gpu_layer_util import run_gpu_chain
+    from synth import make_activations, make_params
+    ccfg = tiny.with_(hidden=256, heads=4, seq_len=128, microbatch=4, n_sub=2, tmp_degree=T)
+    cparams = [make_params(ccfg, layer=k) for k in range(3)]
+    cx, cdy = make_activations(ccfg)
+    ca = run_gpu_chain(ccfg, cparams, cx, cdy, T=T, rank=rank, group=group, chain=True)
+    cb = run_gpu_chain(ccfg, cparams, cx, cdy, T=T, rank=rank, group=group, chain=False)
+    if not (torch.equal(ca["y"], cb["y"]) and torch.equal(ca["dx"], cb["dx"]) and
+            all(torch.equal(ca["grads"][k][nm], cb["grads"][k][nm]) for k in range(3) for nm in ca["grads"][k])):
+        failures.append(("chain", "chained vs unchained not bit-identical"))
+    print(f"[rank {rank}] chain T={T} done", flush=True)
     dist.barrier()
     if failures:
         print(f"[rank {rank}] FAIL {failures}", flush=True)
