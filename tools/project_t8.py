@@ -23,7 +23,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-CONFIGS_T8 = ["gpt8.3b", "gpt20b", "gpt2.5b", "gpt1.5b"]
+CONFIGS_T8 = os.environ.get("T8_CONFIGS", "gpt8.3b,gpt20b,gpt2.5b,gpt1.5b").split(",")
 K = 4
 
 
@@ -32,16 +32,31 @@ def layer_flops(cfg):
     return 6.0 * B * s * (4 * h * h + 2 * f * h) + 6.0 * B * h * s * (s + 1)
 
 
+_PARAMS = {}
+
+
+def params_for(cfg, T, rank, dev):
+    """Weights of K layers, generated once per (config, T, rank) and reused across n_sub."""
+    from paper_2206_04959_b200 import shard_weights
+    from synth import make_params
+    key = (cfg.name, T, rank)
+    if key not in _PARAMS:
+        _PARAMS.clear()
+        _PARAMS[key] = [shard_weights(make_params(cfg.with_(tmp_degree=T), layer=k), cfg.heads, T, rank, dev)
+                        for k in range(K)]
+    return _PARAMS[key]
+
+
 def run_layers(cfg, T, rank, n_sub, comm, group, steps=6, warmup=3, flags=0):
     import torch
     import torch.distributed as dist
 
-    from paper_2206_04959_b200 import FLAG_CHAIN, TmpLayer, shard_weights, zero_grads_like
-    from synth import make_activations, make_params
+    from paper_2206_04959_b200 import FLAG_CHAIN, TmpLayer, zero_grads_like
+    from synth import make_activations
     dev = torch.device("cuda", torch.cuda.current_device())
     c = cfg.with_(tmp_degree=T, n_sub=n_sub)
     x, dy = make_activations(c)
-    ws = [shard_weights(make_params(c, layer=k), c.heads, T, rank, dev) for k in range(K)]
+    ws = params_for(cfg, T, rank, dev)
     M, h = c.tokens, c.hidden
     X = torch.as_tensor(x.reshape(M, h)).to(dev, torch.bfloat16)
     DY = torch.as_tensor(dy.reshape(M, h)).to(dev, torch.bfloat16)
