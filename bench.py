@@ -60,46 +60,60 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
-
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock, power and clock-event (throttle) reasons sampled every ~5 ms through NVML from a
+    background thread while the timed region runs (nvidia-smi -lms needs ~0.5 s to emit its first line,
+    longer than a short timed region)."""
 
     def __init__(self, index):
         self.index = index
-        self.p = None
+        self.rows = []
+        self._stop = None
+        self._t = None
 
     def __enter__(self):
+        import threading
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "20"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+            pynvml.nvmlInit()
+            # NVML enumerates every GPU; map the CUDA index through the visible-device order
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.index]) if vis and vis.split(",")[self.index].isdigit() else self.index
+            h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.p = None
+            return self
+        self._stop = threading.Event()
+        flags = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                 "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                 "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                 "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0
+                    self.rows.append((sm, [k for k, f in flags.items() if rs & f], pw))
+                except Exception:
+                    pass
+                self._stop.wait(0.005)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
         return self
 
     def __exit__(self, *a):
-        self.out = ""
-        if self.p:
-            self.p.terminate()
-            try:
-                self.out, _ = self.p.communicate(timeout=5)
-            except Exception:
-                self.p.kill()
+        if self._t:
+            self._stop.set()
+            self._t.join(timeout=2)
 
     def summary(self):
-        rows = [r.split(", ") for r in (self.out or "").strip().splitlines() if r.count(",") >= 8]
-        if not rows:
+        if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
-        sm = [float(r[1]) for r in rows]
-        reasons = set()
-        for r in rows:
-            for name, v in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), r[5:9]):
-                if v.strip().lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": sorted(reasons),
-                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+        reasons = sorted({r for row in self.rows for r in row[1]})
+        return {"sm_mhz": statistics.median([r[0] for r in self.rows]), "sm_max_mhz": float(self._max),
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(r[2] for r in self.rows),
+                "source": "NVML, ~5 ms period, timed region only"}
 
 
 def cpu_oracle_sample(cfg, target_s=12.0):
@@ -257,13 +271,15 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item() / nsteps, launches, prof_d
 
-    def stage(msg):
-        if os.environ.get("MERAK_BENCH_TRACE"):
-            print(f"[rank {rank}] {msg}", file=sys.stderr, flush=True)
+    t_start = time.time()
 
-    if os.environ.get("MERAK_BENCH_TRACE"):
-        import faulthandler
-        faulthandler.dump_traceback_later(int(os.environ.get("MERAK_BENCH_TRACE_S", "90")), exit=False)
+    def stage(msg):  # progress markers on stderr (multi-rank runs: evidence if a run ever stalls)
+        if world > 1 or os.environ.get("MERAK_BENCH_TRACE"):
+            print(f"[rank {rank} +{time.time() - t_start:.1f}s] {msg}", file=sys.stderr, flush=True)
+
+    # a stalled run dumps every Python thread's stack to stderr (diagnostics only; the run continues)
+    import faulthandler
+    faulthandler.dump_traceback_later(int(os.environ.get("MERAK_BENCH_TRACE_S", "240")), exit=False)
 
     for _ in range(args.warmup):
         step()
@@ -408,6 +424,7 @@ def main():
             line["cpu_baseline"] = cpu_oracle_sample(cfg)
         print(json.dumps(line), flush=True)
     layer.close()
+    faulthandler.cancel_dump_traceback_later()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
