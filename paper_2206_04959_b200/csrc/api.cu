@@ -117,6 +117,7 @@ struct merak_tmp {
   // fp32 check mode (MERAK_FP32_CHECK): fp32 workspace
   bool f32 = false;
   bool local = false;  // MERAK_COMM_LOCAL: single-process emulation of one rank, no peers
+  int *tile_ctr = nullptr;  // dynamic GEMM tile counters, one per compute stream (cs, cs1); MERAK_GEMM_DYN=1
   char *ws32 = nullptr;
   float *dz32 = nullptr, *dx1_32 = nullptr, *dctx32 = nullptr, *dqkv32 = nullptr, *delta32 = nullptr, *du32 = nullptr;
 };
@@ -234,6 +235,7 @@ static merak_status run_gemm(merak_tmp_t *h, const GemmArgs &a0, cudaStream_t st
   GemmArgs a = a0;
   // T > 1: keep smem free on every SM for the all-reduce kernels that overlap the GEMMs
   a.smem_kb = h->T > 1 ? 160 : 192;
+  if (h->tile_ctr && st != h->cw) a.tile_ctr = h->tile_ctr + (st == h->cs1 && h->cs1 != h->cs ? 1 : 0);
   Launch L(h, MERAK_K_GEMM, st, 2.0 * a.M * a.N * a.K);
   CK(h, gemm(a, st));
   return MERAK_OK;
@@ -932,7 +934,12 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
     const int ncol = std::max(std::max(3 * h->hr, h->fr), h->h);
     const size_t o_pc = take(2 * (size_t)h->B * ncol * 4);
     const size_t o_pg = take((M / h->G) * (size_t)h->h * 4), o_pb = take((M / h->G) * (size_t)h->h * 4);
+    const size_t o_ctr = take(64);
     CKI(cudaMalloc(&h->ws, o));
+    CKI(cudaMemset(h->ws + o_ctr, 0, 64));
+    // dynamic GEMM tile schedule: opt-in (measured no gain over the static schedule at gpt1.5b, T=1)
+    const char *dyn = getenv("MERAK_GEMM_DYN");
+    if (dyn && atoi(dyn) == 1) h->tile_ctr = (int *)(h->ws + o_ctr);
     h->dz = (bf16 *)(h->ws + o_dz); h->dx1 = (bf16 *)(h->ws + o_dx1); h->dctx = (bf16 *)(h->ws + o_dctx);
     h->dqkv = (bf16 *)(h->ws + o_dqkv); h->delta = (float *)(h->ws + o_delta);
     h->part_col = (float *)(h->ws + o_pc); h->part_lng = (float *)(h->ws + o_pg); h->part_lnb = (float *)(h->ws + o_pb);

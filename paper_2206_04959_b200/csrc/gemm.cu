@@ -55,6 +55,7 @@ struct EpiParams {
   int ld32;
   float *db32;  // EPI_ACC_F32: column n_main (the ones column of B) accumulates into db32[m]
   int n_main;
+  int *tile_ctr;  // dynamic tile scheduler counter (zero between launches), nullptr = static schedule
 };
 
 template <int EPI>
@@ -155,7 +156,9 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t *smB = smem + S * C::A_BYTES;
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S * C::STAGE_BYTES);
   uint64_t *full = bars, *empty = bars + S, *tfull = bars + 2 * S, *tfree = bars + 2 * S + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+  uint64_t *sched_full = bars + 2 * S + 4, *sched_empty = bars + 2 * S + 8;  // tile-id ring, 4 deep
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 12);
+  int *ring = reinterpret_cast<int *>(bars + 2 * S + 13);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -165,6 +168,47 @@ __global__ void __launch_bounds__(256, 1)
   const int tiles_n = (p.N + BN - 1) / BN;
   const int ntiles = tiles_m * tiles_n;
   const int nk = (p.K + BK - 1) / BK;
+  // Tile order.  Static: cluster cl takes tiles cl, cl + ncl, ...  Dynamic (p.tile_ctr): the leader's
+  // producer fetches the next tile index with an atomic and broadcasts it through a 4-deep smem ring
+  // to its MMA / epilogue warps and to the peer CTA, so clusters that start late (SMs still held by a
+  // kernel of the other sub-batch stream) simply take fewer tiles.  Every tile is still computed by
+  // one cluster in the fixed K order, so results do not depend on the order (bit-identity rule i).
+  const bool dyn = (EPI != EPI_ACC_F32) && p.tile_ctr != nullptr;
+  auto consume = [&](int lt) -> int {  // MMA, epilogue and peer-producer warps
+    if (!dyn) return cl + lt * ncl;
+    const int slot = lt & 3;
+    const uint32_t ph = (lt >> 2) & 1;
+    if (CG == 2 && rank == 1)
+      mbar_wait_cluster(&sched_full[slot], ph);
+    else
+      mbar_wait(&sched_full[slot], ph);
+    const int t = *reinterpret_cast<volatile int *>(&ring[slot]);
+    __syncwarp();
+    if (lane == 0) {
+      if (CG == 2 && rank == 1)
+        mbar_arrive_cluster(mapa_shared(&sched_empty[slot], 0));
+      else
+        mbar_arrive(&sched_empty[slot]);
+    }
+    return t;
+  };
+  auto fetch = [&](int lt) -> int {  // leader producer warp
+    if (!dyn) return cl + lt * ncl;
+    const int slot = lt & 3;
+    int t = 0;
+    if (lane == 0) {
+      mbar_wait(&sched_empty[slot], ((lt >> 2) & 1) ^ 1);
+      t = atomicAdd(p.tile_ctr, 1);
+      if (t == ntiles + ncl - 1) atomicExch(p.tile_ctr, 0);  // the launch's last fetch: reset for the next
+      ring[slot] = t;
+      if constexpr (CG == 2) {
+        st_shared_cluster_u32(mapa_shared(&ring[slot], 1), (uint32_t)t);
+        mbar_arrive_cluster(mapa_shared(&sched_full[slot], 1));
+      }
+      mbar_arrive(&sched_full[slot]);
+    }
+    return __shfl_sync(0xffffffffu, t, 0);
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -176,6 +220,10 @@ __global__ void __launch_bounds__(256, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tfree[i], 4 * CG);
+    }
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&sched_full[i], 1);
+      mbar_init(&sched_empty[i], CG == 2 ? 10 : 5);  // MMA + 4 epilogue warps (+ peer producer + 4)
     }
     fence_mbar_init();
     fence_proxy_async();
@@ -197,7 +245,9 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs of a pair load their own halves)
     int it = 0;
-    for (int tile = cl; tile < ntiles; tile += ncl) {
+    for (int lt = 0;; ++lt) {
+      const int tile = (rank == 0) ? fetch(lt) : consume(lt);
+      if (tile >= ntiles) break;
       const int tm = tile % tiles_m, tn = tile / tiles_m;
       const int row0 = tm * BMT + rank * BM;
       const int n0 = tn * BN + rank * C::BNC;
@@ -236,8 +286,10 @@ __global__ void __launch_bounds__(256, 1)
     constexpr uint32_t idesc = idesc_bf16(BMT, BN, A_MN, B_MN);
     constexpr uint32_t a_lbo = A_MN ? 8192u : 16u, a_sbo = 1024u, a_kstep = A_MN ? 2048u : 32u;
     constexpr uint32_t b_lbo = B_MN ? 8192u : 16u, b_sbo = 1024u, b_kstep = B_MN ? 2048u : 32u;
-    int it = 0, lt = 0;
-    for (int tile = cl; tile < ntiles; tile += ncl, ++lt) {
+    int it = 0;
+    for (int lt = 0;; ++lt) {
+      const int tile = consume(lt);
+      if (tile >= ntiles) break;
       const int buf = lt & 1;
       mbar_wait(&tfree[buf], (lt >> 1) & 1);
       tc_fence_after();
@@ -344,7 +396,9 @@ __global__ void __launch_bounds__(256, 1)
       }
       sbuf ^= 1;
     };
-    for (int tile = cl; tile < ntiles; tile += ncl, ++lt) {
+    for (;; ++lt) {
+      const int tile = consume(lt);
+      if (tile >= ntiles) break;
       const int buf = lt & 1;
       mbar_wait(&tfull[buf], (lt >> 1) & 1);
       tc_fence_after();
@@ -443,6 +497,8 @@ __global__ void __launch_bounds__(256, 1)
       tmem_dealloc<C::TMEM_COLS>(tmem_base);
   }
 }
+
+__device__ int g_test_tile_ctr = 0;  // dynamic-schedule counter of the test entry points (serial use)
 
 // ------------------------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -602,6 +658,15 @@ cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   p.aux = (const __nv_bfloat16 *)a.aux; p.ld_aux = a.ld_aux;
   p.out32 = a.out32; p.ld32 = a.ld32;
   p.db32 = a.db32;
+  p.tile_ctr = a.tile_ctr;
+  if (!p.tile_ctr) {  // test entry points: MERAK_GEMM_DYN=1 selects the dynamic schedule on a global counter
+    const char *e = getenv("MERAK_GEMM_DYN");
+    if (e && atoi(e) == 1) {
+      void *ptr = nullptr;
+      if (cudaGetSymbolAddress(&ptr, g_test_tile_ctr) != cudaSuccess) return cudaErrorInvalidValue;
+      p.tile_ctr = reinterpret_cast<int *>(ptr);
+    }
+  }
   p.n_main = a.db32 ? a.N - 1 : a.N;
   if (cg == 2 && a.epi >= 5 && !a.a_mn && !a.b_mn) {  // microbenchmark-only variants
     if (a.epi == 5) return launch<2, 256, false, false, 5>(a, mp, p, st);            // no stores

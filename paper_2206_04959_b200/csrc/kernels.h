@@ -47,6 +47,8 @@ struct GemmArgs {
   int max_ctas;      // persistent grid cap (0 = all SMs)
   int smem_kb;       // smem budget of the TMA ring: 192 (default) or 160 (leave room for co-resident
                      // all-reduce kernels when T > 1)
+  int *tile_ctr;     // dynamic tile scheduler: a device int that is 0 between launches and used by one
+                     // stream at a time (the kernel resets it); nullptr = static schedule
 };
 cudaError_t gemm(const GemmArgs &a, cudaStream_t st);
 int gemm_num_sms();

@@ -51,8 +51,10 @@ GEMM_SHAPES = [(16, 96, 64), (128, 128, 64), (256, 384, 320), (300, 200, 96), (5
                (4096, 1600, 6400)]
 
 
+@pytest.mark.parametrize("dyn", [0, 1])
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
-def test_gemm_forward_epilogues(M, N, K):
+def test_gemm_forward_epilogues(M, N, K, dyn, monkeypatch):
+    monkeypatch.setenv("MERAK_GEMM_DYN", str(dyn))  # static vs dynamic (atomic) tile schedule
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
     A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
     B = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
@@ -67,9 +69,11 @@ def test_gemm_forward_epilogues(M, N, K):
     assert rel(gl, gelu_ref(ref + bias.float())) < 5e-3
 
 
+@pytest.mark.parametrize("dyn", [0, 1])
 @pytest.mark.parametrize("M,N,K", GEMM_SHAPES)
-def test_gemm_dgrad(M, N, K):
+def test_gemm_dgrad(M, N, K, dyn, monkeypatch):
     """dgrad: B stored [K, N] (the weight [out, in] read MN-major)."""
+    monkeypatch.setenv("MERAK_GEMM_DYN", str(dyn))
     g = torch.Generator(device="cuda").manual_seed(M + 3 * N)
     A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
     Bs = (torch.randn(K, N, device="cuda", generator=g) * 0.05).bfloat16()
@@ -132,6 +136,20 @@ def test_gemm_reduction_order_independent_of_m():
     full, _ = run_gemm(A, B, 1024, 512, 640, False, False, 0)
     half, _ = run_gemm(A[512:].contiguous(), B, 512, 512, 640, False, False, 0, max_ctas=7)
     assert torch.equal(full[512:], half)
+
+
+def test_gemm_dynamic_schedule_bit_identical_to_static(monkeypatch):
+    """The dynamic tile order changes which cluster computes a tile, never a tile's K order; repeated
+    launches also check that the kernel leaves its counter at 0."""
+    g = torch.Generator(device="cuda").manual_seed(2)
+    A = torch.randn(4096, 1600, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(4800, 1600, device="cuda", generator=g) * 0.05).bfloat16()
+    monkeypatch.setenv("MERAK_GEMM_DYN", "0")
+    ref, _ = run_gemm(A, B, 4096, 4800, 1600, False, False, 0)
+    monkeypatch.setenv("MERAK_GEMM_DYN", "1")
+    for mc in (0, 0, 20, 7, 0):
+        out, _ = run_gemm(A, B, 4096, 4800, 1600, False, False, 0, max_ctas=mc)
+        assert torch.equal(out, ref), mc
 
 
 # ------------------------------------------------------------------------------------------- attention
