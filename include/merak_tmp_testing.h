@@ -26,6 +26,11 @@ int merak_test_attn_fwd(const void *qkv, void *ctx, float *lse, int b, int s, in
 int merak_test_attn_bwd(const void *qkv, const void *ctx, const float *lse, const void *dctx, void *dqkv, float *delta,
                         int b, int s, int heads, int d, void *stream);
 
+/* Same, with diagnostics: the tcgen05 backward kernels write per-CTA SM-clock stamps into dbg
+ * (64 x uint64 per CTA; the dQ kernel's CTAs, then the dK/dV kernel's; layout in attention_bwd_tc.cu). */
+int merak_test_attn_bwd_dbg(const void *qkv, const void *ctx, const float *lse, const void *dctx, void *dqkv,
+                            float *delta, int b, int s, int heads, int d, unsigned long long *dbg, void *stream);
+
 /* LayerNorm forward: u = LN(x) (bf16), mean/rstd fp32 [m]. */
 int merak_test_ln_fwd(const void *x, const void *gamma, const void *beta, void *u, float *mean, float *rstd, int m,
                       int h, float eps, void *stream);

@@ -1234,6 +1234,15 @@ int merak_test_attn_bwd(const void *qkv, const void *ctx, const float *lse, cons
   return (int)attn_bwd(a, (cudaStream_t)stream);
 }
 
+int merak_test_attn_bwd_dbg(const void *qkv, const void *ctx, const float *lse, const void *dctx, void *dqkv,
+                            float *delta, int b, int s, int heads, int d, unsigned long long *dbg, void *stream) {
+  AttnArgs a;
+  memset(&a, 0, sizeof(a));
+  a.qkv = qkv; a.ctx = (void *)ctx; a.lse = (float *)lse; a.dctx = dctx; a.dqkv = dqkv; a.delta = delta;
+  a.b = b; a.s = s; a.heads = heads; a.d = d; a.ld_ctx = heads * d; a.dbg = dbg;
+  return (int)attn_bwd_tc(a, (cudaStream_t)stream);
+}
+
 int merak_test_ln_fwd(const void *x, const void *gamma, const void *beta, void *u, float *mean, float *rstd, int m,
                       int h, float eps, void *stream) {
   OnesPad pad;

@@ -52,6 +52,25 @@ struct BwdCfg {
   static constexpr int DKV_MIN = (2 * (DKV_SMEM + 1024) <= 228 * 1024 && DKV_TMEM == 256) ? 2 : 1;
 };
 
+// Diagnostics (AttnArgs::dbg): one recording thread per CTA stores SM-clock stamps --
+// [0] entry, [1] prologue done, [2 + j] iteration j's scores ready (j < 54), [60] epilogue start,
+// [61] exit, [56]/[57] globaltimer at entry / exit, [62] SM id, [63] iteration count.
+MK_DEV unsigned long long *dbg_slot(unsigned long long *base) {
+  if (!base) return nullptr;
+  const size_t cta = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
+  return base + cta * 64;
+}
+MK_DEV unsigned long long clk64() {
+  unsigned long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+MK_DEV unsigned int smid() {
+  unsigned int r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
 // 32 scores of this thread's row -> 32 bf16 values packed in 16 words
 MK_DEV void put_row_chunk(uint8_t *row, int r, int c32, const uint32_t (&w)[16]) {
   // columns c32*32 .. +31 = 16-B chunks 4*c32 .. 4*c32+3 of the 128-B row (128-B swizzle)
@@ -66,9 +85,9 @@ MK_DEV void put_row_chunk(uint8_t *row, int r, int c32, const uint32_t (&w)[16])
 
 // ------------------------------------------------------------------------------------------ dQ
 template <int D>
-__global__ void __launch_bounds__(NTHR, BwdCfg<D>::DQ_MIN)
-    attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmo,
-                          const __grid_constant__ CUtensorMap tmkv, AttnArgs a) {
+__device__ __forceinline__ void dq_body(const CUtensorMap *tmq_p, const CUtensorMap *tmo_p, const CUtensorMap *tmkv_p,
+                                        const AttnArgs &a, const int tile) {
+  const CUtensorMap &tmq = *tmq_p, &tmo = *tmo_p, &tmkv = *tmkv_p;
   using C = BwdCfg<D>;
   constexpr int NA = C::NA;
   extern __shared__ uint8_t smem_raw[];
@@ -86,10 +105,17 @@ __global__ void __launch_bounds__(NTHR, BwdCfg<D>::DQ_MIN)
 
   const int s = a.s, H = a.heads, hr = H * D;
   const int nqt = (s + TR - 1) / TR;
-  const int qt = nqt - 1 - blockIdx.x;
+  const int qt = nqt - 1 - tile;  // heaviest (most key tiles) first
   const int head = blockIdx.y, bi = blockIdx.z, tok0 = bi * s;
   const int J = min(2 * (qt + 1), (s + TH - 1) / TH);
   const int warp = warp_id(), lane = lane_id();
+  unsigned long long *dbg = (warp == 2 && lane == 0) ? dbg_slot(a.dbg) : nullptr;
+  if (dbg) {
+    dbg[0] = clk64();
+    dbg[56] = globaltimer();
+    dbg[62] = smid();
+    dbg[63] = J;
+  }
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmq);
@@ -180,29 +206,14 @@ __global__ void __launch_bounds__(NTHR, BwdCfg<D>::DQ_MIN)
     const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
     const float scale = 1.f / sqrtf((float)D), sl2 = 1.4426950408889634f * scale;
     const size_t srow = ((size_t)bi * H + head) * s;
-    float lse = INFINITY, del = 0.f;
-    if (qi < s) {
-      lse = a.lse[srow + qi];
-      const __nv_bfloat16 *po = reinterpret_cast<const __nv_bfloat16 *>(a.ctx) + (size_t)(tok0 + qi) * a.ld_ctx + head * D;
-      const __nv_bfloat16 *pd = reinterpret_cast<const __nv_bfloat16 *>(a.dctx) + (size_t)(tok0 + qi) * hr + head * D;
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c = 0; c < D; c += 8) {
-        uint4 uo = *reinterpret_cast<const uint4 *>(po + c), ud = *reinterpret_cast<const uint4 *>(pd + c);
-        float2 o0 = unpack_bf16(uo.x), o1 = unpack_bf16(uo.y), o2 = unpack_bf16(uo.z), o3 = unpack_bf16(uo.w);
-        float2 d0 = unpack_bf16(ud.x), d1 = unpack_bf16(ud.y), d2 = unpack_bf16(ud.z), d3 = unpack_bf16(ud.w);
-        acc[0] += o0.x * d0.x + o0.y * d0.y;
-        acc[1] += o1.x * d1.x + o1.y * d1.y;
-        acc[2] += o2.x * d2.x + o2.y * d2.y;
-        acc[3] += o3.x * d3.x + o3.y * d3.y;
-      }
-      del = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-      if (cw == 0) a.delta[srow + qi] = del;
-    }
+    // delta = rowsum(dO * O) comes from attn_delta_kernel (launched first)
+    const float lse = qi < s ? a.lse[srow + qi] : INFINITY, del = qi < s ? a.delta[srow + qi] : 0.f;
     const float ls = lse;
+    if (dbg) dbg[1] = clk64();
     for (int j = 0; j < J; ++j) {
       mbar_wait(sp_full, j & 1);
       tc_fence_after();
+      if (dbg && j < 54) dbg[2 + j] = clk64();
       const int kj0 = j * TH;
       const bool mask = (kj0 + TH - 1 > qt * TR) || (kj0 + TH > s);
       uint32_t w[16];  // this warpgroup's 32 columns, bf16-packed
@@ -236,6 +247,7 @@ __global__ void __launch_bounds__(NTHR, BwdCfg<D>::DQ_MIN)
       if (lane == 0) mbar_arrive(x_full);
     }
     const int last = J - 1;
+    if (dbg) dbg[60] = clk64();
     mbar_wait(x_free, last & 1);
     tc_fence_after();
     __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.dqkv) + (size_t)(tok0 + qi) * 3 * hr + head * D;
@@ -260,6 +272,10 @@ __global__ void __launch_bounds__(NTHR, BwdCfg<D>::DQ_MIN)
       }
     }
   }
+  if (dbg) {
+    dbg[61] = clk64();
+    dbg[57] = globaltimer();
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -270,9 +286,9 @@ __global__ void __launch_bounds__(NTHR, BwdCfg<D>::DQ_MIN)
 
 // ------------------------------------------------------------------------------------------ dK / dV
 template <int D>
-__global__ void __launch_bounds__(NTHR, BwdCfg<D>::DKV_MIN)
-    attn_bwd_dkdv_tc_kernel(const __grid_constant__ CUtensorMap tmf, const __grid_constant__ CUtensorMap tmh,
-                            const __grid_constant__ CUtensorMap tmoh, AttnArgs a) {
+__device__ __forceinline__ void dkdv_body(const CUtensorMap *tmf_p, const CUtensorMap *tmh_p,
+                                          const CUtensorMap *tmoh_p, const AttnArgs &a, const int tile) {
+  const CUtensorMap &tmf = *tmf_p, &tmh = *tmh_p, &tmoh = *tmoh_p;
   using C = BwdCfg<D>;
   constexpr int NA = C::NA;
   extern __shared__ uint8_t smem_raw[];
@@ -291,11 +307,18 @@ __global__ void __launch_bounds__(NTHR, BwdCfg<D>::DKV_MIN)
   constexpr uint32_t ST_COL = 0, DPT_COL = 64, DV_COL = 128, DK_COL = 128 + D;
 
   const int s = a.s, H = a.heads, hr = H * D;
-  const int kt = blockIdx.x;
+  const int kt = tile;  // kt = 0 has the most query tiles: heaviest first
   const int head = blockIdx.y, bi = blockIdx.z, tok0 = bi * s;
   const int i0 = 2 * kt, NI = (s + TH - 1) / TH - i0;
   const size_t srow = ((size_t)bi * H + head) * s;
   const int warp = warp_id(), lane = lane_id();
+  unsigned long long *dbg = (warp == 2 && lane == 0) ? dbg_slot(a.dbg) : nullptr;
+  if (dbg) {
+    dbg[0] = clk64();
+    dbg[56] = globaltimer();
+    dbg[62] = smid();
+    dbg[63] = NI;
+  }
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmf);
@@ -393,12 +416,14 @@ __global__ void __launch_bounds__(NTHR, BwdCfg<D>::DKV_MIN)
     const int q = warp & 3, r = q * 32 + lane, kj = kt * TR + r, cw = (warp - 2) >> 2;
     const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
     const float scale = 1.f / sqrtf((float)D), sl2 = 1.4426950408889634f * scale;
+    if (dbg) dbg[1] = clk64();
     for (int ii = 0; ii < NI; ++ii) {
       const int i = i0 + ii, st = ii & 1;
       const int qi0 = i * TH;
       mbar_wait(&q_full[st], (ii >> 1) & 1);  // lse / delta of this half tile are in smem
       mbar_wait(sp_full, ii & 1);
       tc_fence_after();
+      if (dbg && ii < 54) dbg[2 + ii] = clk64();
       const bool mask = (qi0 < kt * TR + TR - 1) || (qi0 + TH > s);
       const float *L = sL + st * TH, *Dl = sD + st * TH;
       uint32_t wp[16], ws[16];  // this warpgroup's 32 columns of P^T and dS^T, bf16-packed
@@ -434,6 +459,7 @@ __global__ void __launch_bounds__(NTHR, BwdCfg<D>::DKV_MIN)
       if (lane == 0) mbar_arrive(x_full);
     }
     const int last = NI - 1;
+    if (dbg) dbg[60] = clk64();
     mbar_wait(x_free, last & 1);
     tc_fence_after();
     __nv_bfloat16 *dk = reinterpret_cast<__nv_bfloat16 *>(a.dqkv) + (size_t)(tok0 + kj) * 3 * hr + hr + head * D;
@@ -463,12 +489,56 @@ __global__ void __launch_bounds__(NTHR, BwdCfg<D>::DKV_MIN)
       }
     }
   }
+  if (dbg) {
+    dbg[61] = clk64();
+    dbg[57] = globaltimer();
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<C::DKV_TMEM>(tmem);
   }
+}
+
+// ------------------------------------------------------------------------------------------ kernels
+// delta = rowsum(dO * O) per (sample, head, query): one thread per (token, head), head fastest, so a
+// warp reads contiguous 128-B rows of O and dO.
+template <int D>
+__global__ void __launch_bounds__(256) attn_delta_kernel(AttnArgs a) {
+  const int H = a.heads, hr = H * D;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long)a.b * a.s * H) return;
+  const int t = (int)(idx / H), e = (int)(idx % H);
+  const __nv_bfloat16 *po = reinterpret_cast<const __nv_bfloat16 *>(a.ctx) + (size_t)t * a.ld_ctx + e * D;
+  const __nv_bfloat16 *pd = reinterpret_cast<const __nv_bfloat16 *>(a.dctx) + (size_t)t * hr + e * D;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int c = 0; c < D; c += 8) {
+    uint4 uo = *reinterpret_cast<const uint4 *>(po + c), ud = *reinterpret_cast<const uint4 *>(pd + c);
+    float2 o0 = unpack_bf16(uo.x), o1 = unpack_bf16(uo.y), o2 = unpack_bf16(uo.z), o3 = unpack_bf16(uo.w);
+    float2 d0 = unpack_bf16(ud.x), d1 = unpack_bf16(ud.y), d2 = unpack_bf16(ud.z), d3 = unpack_bf16(ud.w);
+    acc[0] += o0.x * d0.x + o0.y * d0.y;
+    acc[1] += o1.x * d1.x + o1.y * d1.y;
+    acc[2] += o2.x * d2.x + o2.y * d2.y;
+    acc[3] += o3.x * d3.x + o3.y * d3.y;
+  }
+  const int bi = t / a.s, i = t % a.s;
+  a.delta[((size_t)bi * H + e) * a.s + i] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+// One launch for both halves of the backward (independent once delta exists): even CTAs compute dQ
+// tiles, odd CTAs dK/dV tiles, both heaviest-first, so the causal imbalance of one fills the other.
+template <int D>
+__global__ void __launch_bounds__(NTHR, BwdCfg<D>::DQ_MIN < BwdCfg<D>::DKV_MIN ? BwdCfg<D>::DQ_MIN : BwdCfg<D>::DKV_MIN)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmq_full, const __grid_constant__ CUtensorMap tmq_half,
+                       const __grid_constant__ CUtensorMap tmo_full, const __grid_constant__ CUtensorMap tmo_half,
+                       AttnArgs a) {
+  const int tile = blockIdx.x >> 1;
+  if (blockIdx.x & 1)
+    dkdv_body<D>(&tmq_full, &tmq_half, &tmo_half, a, tile);
+  else
+    dq_body<D>(&tmq_full, &tmo_full, &tmq_half, a, tile);
 }
 
 // ------------------------------------------------------------------------------------------ host
@@ -498,12 +568,10 @@ static bool make_rows_map(CUtensorMap *m, const void *base, int rows, int cols, 
 template <int D>
 static cudaError_t bwd_tc_d(const AttnArgs &a, cudaStream_t st) {
   using C = BwdCfg<D>;
+  constexpr int SMEM = C::DQ_SMEM > C::DKV_SMEM ? C::DQ_SMEM : C::DKV_SMEM;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::DQ_SMEM);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(attn_bwd_dkdv_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::DKV_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -513,11 +581,12 @@ static cudaError_t bwd_tc_d(const AttnArgs &a, cudaStream_t st) {
       !make_rows_map(&mq_half, a.qkv, tokens, 3 * hr, 3 * hr, TH) ||
       !make_rows_map(&mo_full, a.dctx, tokens, hr, hr, TR) || !make_rows_map(&mo_half, a.dctx, tokens, hr, hr, TH))
     return cudaErrorInvalidValue;
-  dim3 grid((a.s + TR - 1) / TR, a.heads, a.b);
-  attn_bwd_dq_tc_kernel<D><<<grid, NTHR, C::DQ_SMEM, st>>>(mq_full, mo_full, mq_half, a);
+  const long nd = (long)tokens * a.heads;
+  attn_delta_kernel<D><<<(unsigned)((nd + 255) / 256), 256, 0, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  attn_bwd_dkdv_tc_kernel<D><<<grid, NTHR, C::DKV_SMEM, st>>>(mq_full, mq_half, mo_half, a);
+  dim3 grid(2 * ((a.s + TR - 1) / TR), a.heads, a.b);
+  attn_bwd_tc_kernel<D><<<grid, NTHR, SMEM, st>>>(mq_full, mq_half, mo_full, mo_half, a);
   return cudaGetLastError();
 }
 

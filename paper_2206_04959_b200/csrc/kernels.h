@@ -65,6 +65,7 @@ struct AttnArgs {
   float *delta;      // [b, H_r, s] rowsum(dO*O) workspace (bwd)
   int b, s, heads, d;
   int ld_ctx;        // row stride of ctx (elements; >= heads*d)
+  unsigned long long *dbg;  // diagnostics only (nullptr): per-CTA clock stamps of the tcgen05 backward
 };
 cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st);     // tcgen05 version if MERAK_ATTN_TC=1
 cudaError_t attn_fwd_tc(const AttnArgs &a, cudaStream_t st);  // attention_tc.cu
