@@ -128,10 +128,12 @@ __host__ __device__ constexpr int ar_ch(int nt) { return nt >= 8 ? 1 : nt >= 4 ?
 template <int NT>
 __global__ void __launch_bounds__(256) ar_fwd_kernel(ArFwdArgs a, PeerSync ps) {
   constexpr int CH = ar_ch(NT);
+  extern __shared__ uint4 row_s[];  // do_ln: per warp, the stored bf16 row (LN2 reads it, reading R12)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
   const int h = a.h, nc = h >> 3;
   const bool gathered = a.chunk > 0;
+  uint4 *rb = row_s + (size_t)warp * nc;
   for (int row = blockIdx.x * nw + warp; row < a.m; row += gridDim.x * nw) {
     const size_t ro = (size_t)row * h;
     float sum = 0.f;
@@ -148,26 +150,33 @@ __global__ void __launch_bounds__(256) ar_fwd_kernel(ArFwdArgs a, PeerSync ps) {
           add8(a.bias + c * 8, v[i]);
           add8(a.resid + ro + c * 8, v[i]);
         }
-        store8(a.out + ro + c * 8, v[i]);
+        uint4 pk;
+        pk.x = pack_bf16(v[i][0], v[i][1]); pk.y = pack_bf16(v[i][2], v[i][3]);
+        pk.z = pack_bf16(v[i][4], v[i][5]); pk.w = pack_bf16(v[i][6], v[i][7]);
+        *reinterpret_cast<uint4 *>(a.out + ro + c * 8) = pk;
         if (a.do_ln) {
+          rb[c] = pk;
+          float q[8];
+          unpack8(pk, q);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) sum += bf16_round(v[i][k]);  // LN2 of the stored bf16 x1 (R12)
+          for (int k = 0; k < 8; ++k) sum += q[k];  // LN2 of the stored bf16 x1 (R12)
         }
       }
     }
     if (!a.do_ln) continue;
+    __syncwarp();
     const float mean = warp_sum(sum) / h;
     float var = 0.f;
     for (int c = lane; c < nc; c += 32) {
       float q[8];
-      load8(a.out + ro + c * 8, q);
+      unpack8(rb[c], q);
 #pragma unroll
       for (int i = 0; i < 8; ++i) var += (q[i] - mean) * (q[i] - mean);
     }
     const float rstd = rsqrtf(warp_sum(var) / h + a.eps);
     for (int c = lane; c < nc; c += 32) {
       float q[8], gm[8], bt[8];
-      load8(a.out + ro + c * 8, q);
+      unpack8(rb[c], q);
       load8(a.gamma + c * 8, gm);
       load8(a.beta + c * 8, bt);
 #pragma unroll
@@ -211,11 +220,13 @@ __global__ void __launch_bounds__(256) ar_rs_kernel(ArRsArgs a) {
 }
 
 // ------------------------------------------------------------------------------ backward all-reduce
-template <int G, int NT>
+template <int G, int NT, bool STASH>
 __global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
   constexpr int CH = ar_ch(NT);
-  extern __shared__ __align__(16) float du_s[];  // [G][h] the all-reduced gradient (bf16-rounded)
+  extern __shared__ __align__(16) float du_s[];  // [G][h] the all-reduced gradient (bf16-rounded),
+                                                 // then [G][h/8] uint4 x_ln rows, [G][h/8] uint4 dres rows
   __shared__ float s_mean[G], s_rstd[G];
+  uint4 *xs = reinterpret_cast<uint4 *>(du_s + (size_t)G * a.h), *ds_res = xs + (size_t)G * (a.h >> 3);
   {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int h = a.h, nc = h >> 3;
@@ -246,7 +257,12 @@ __global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
             float4 *ds = reinterpret_cast<float4 *>(du_s + ri * h + c * 8);
             ds[0] = make_float4(dv[i][0], dv[i][1], dv[i][2], dv[i][3]);
             ds[1] = make_float4(dv[i][4], dv[i][5], dv[i][6], dv[i][7]);
-            load8(a.x_ln + ro + c * 8, x);
+            const uint4 xr = *reinterpret_cast<const uint4 *>(a.x_ln + ro + c * 8);
+            if constexpr (STASH) {
+              xs[ri * nc + c] = xr;
+              ds_res[ri * nc + c] = *reinterpret_cast<const uint4 *>(a.dres + ro + c * 8);
+            }
+            unpack8(xr, x);
             load8(a.gamma + c * 8, gm);
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -256,15 +272,21 @@ __global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
             }
           }
         }
+        __syncwarp();
         const float m1 = warp_sum(acc1) * inv_h, m2 = warp_sum(acc2) * inv_h;
         for (int c = lane; c < nc; c += 32) {
           float x[8], gm[8], dr[8], o[8];
           const float4 *ds = reinterpret_cast<const float4 *>(du_s + ri * h + c * 8);
           const float4 d0 = ds[0], d1 = ds[1];
           const float du[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-          load8(a.x_ln + ro + c * 8, x);
+          if constexpr (STASH) {
+            unpack8(xs[ri * nc + c], x);
+            unpack8(ds_res[ri * nc + c], dr);
+          } else {
+            load8(a.x_ln + ro + c * 8, x);
+            load8(a.dres + ro + c * 8, dr);
+          }
           load8(a.gamma + c * 8, gm);
-          load8(a.dres + ro + c * 8, dr);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float xh = (x[i] - mean) * rstd, dxh = du[i] * gm[i];
@@ -284,9 +306,11 @@ __global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) sg[i] = sb[i] = 0.f;
         for (int i = 0; i < G; ++i) {
-          const size_t ro = (size_t)(grp * G + i) * h;
           float x[8];
-          load8(a.x_ln + ro + cc * 8, x);
+          if constexpr (STASH)
+            unpack8(xs[i * nc + cc], x);
+          else
+            load8(a.x_ln + (size_t)(grp * G + i) * h + cc * 8, x);
           const float4 *ds = reinterpret_cast<const float4 *>(du_s + i * h + cc * 8);
           const float4 d0 = ds[0], d1 = ds[1];
           const float du[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
@@ -313,30 +337,36 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16 *x, con
                                                      const __nv_bfloat16 *beta, __nv_bfloat16 *u, int ld_u,
                                                      float *mean_out, float *rstd_out, int m, int h, float eps,
                                                      OnesPad pad) {
+  extern __shared__ uint4 row_s[];  // per warp: the x row (one global read; passes 2-3 from smem)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int row = blockIdx.x * nw + warp;
   if (row >= m) return;
   const int nc = h >> 3;
   const size_t ro = (size_t)row * h;
+  uint4 *rb = row_s + (size_t)warp * nc;
   float sum = 0.f;
+#pragma unroll 4
   for (int c = lane; c < nc; c += 32) {
+    const uint4 u4 = *reinterpret_cast<const uint4 *>(x + ro + c * 8);
+    rb[c] = u4;
     float q[8];
-    load8(x + ro + c * 8, q);
+    unpack8(u4, q);
 #pragma unroll
     for (int i = 0; i < 8; ++i) sum += q[i];
   }
+  __syncwarp();
   const float mean = warp_sum(sum) / h;
   float var = 0.f;
   for (int c = lane; c < nc; c += 32) {
     float q[8];
-    load8(x + ro + c * 8, q);
+    unpack8(rb[c], q);
 #pragma unroll
     for (int i = 0; i < 8; ++i) var += (q[i] - mean) * (q[i] - mean);
   }
   const float rstd = rsqrtf(warp_sum(var) / h + eps);
   for (int c = lane; c < nc; c += 32) {
     float q[8], gm[8], bt[8];
-    load8(x + ro + c * 8, q);
+    unpack8(rb[c], q);
     load8(gamma + c * 8, gm);
     load8(beta + c * 8, bt);
 #pragma unroll
@@ -464,10 +494,20 @@ static int clamp_ctas(int want, int work, int resident) {
 
 template <int NT>
 static cudaError_t ar_fwd_t(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
+  const size_t smem = a.do_ln ? (size_t)8 * a.h * 2 : 0;  // 8 warps x one bf16 row
   static int resident = 0;
-  if (!resident) resident = resident_ctas((const void *)ar_fwd_kernel<NT>, 256, 0);
+  static size_t res_smem = ~size_t(0), attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(ar_fwd_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  if (res_smem != smem) {
+    resident = resident_ctas((const void *)ar_fwd_kernel<NT>, 256, smem);
+    res_smem = smem;
+  }
   const int grid = clamp_ctas(a.ctas, (a.m + 7) / 8, resident);
-  ar_fwd_kernel<NT><<<grid, 256, 0, st>>>(a, ps);
+  ar_fwd_kernel<NT><<<grid, 256, smem, st>>>(a, ps);
   return cudaGetLastError();
 }
 cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
@@ -501,40 +541,50 @@ cudaError_t ar_rs(const ArRsArgs &a, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
-template <int NT>
+template <int NT, bool STASH>
 static cudaError_t ar_bwd_t(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
   constexpr int G = 8;
-  const size_t smem = (size_t)G * a.h * sizeof(float);
+  // du fp32 rows, plus (STASH) the x_ln and dres bf16 rows so the later passes read smem, not HBM
+  const size_t smem = (size_t)G * a.h * (sizeof(float) + (STASH ? 4 : 0));
   static size_t attr = 0;
   if (smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(ar_bwd_kernel<G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(ar_bwd_kernel<G, NT, STASH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = smem;
   }
   static int resident = 0;
   static size_t res_smem = 0;
   if (!resident || res_smem != smem) {
-    resident = resident_ctas((const void *)ar_bwd_kernel<G, NT>, 256, smem);
+    resident = resident_ctas((const void *)ar_bwd_kernel<G, NT, STASH>, 256, smem);
     res_smem = smem;
   }
   const int grid = clamp_ctas(a.ctas, a.m / G, resident);
-  ar_bwd_kernel<G, NT><<<grid, 256, smem, st>>>(a, ps);
+  ar_bwd_kernel<G, NT, STASH><<<grid, 256, smem, st>>>(a, ps);
   return cudaGetLastError();
 }
 cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
   if (a.G != 8 || a.m % 8) return cudaErrorInvalidValue;
+  const bool stash = (size_t)8 * a.h * 8 <= 160 * 1024;  // h <= 2560
   switch (a.chunk > 0 ? 1 : a.T) {
-    case 1: return ar_bwd_t<1>(a, ps, st);
-    case 2: return ar_bwd_t<2>(a, ps, st);
-    case 4: return ar_bwd_t<4>(a, ps, st);
-    case 8: return ar_bwd_t<8>(a, ps, st);
+    case 1: return stash ? ar_bwd_t<1, true>(a, ps, st) : ar_bwd_t<1, false>(a, ps, st);
+    case 2: return stash ? ar_bwd_t<2, true>(a, ps, st) : ar_bwd_t<2, false>(a, ps, st);
+    case 4: return stash ? ar_bwd_t<4, true>(a, ps, st) : ar_bwd_t<4, false>(a, ps, st);
+    case 8: return stash ? ar_bwd_t<8, true>(a, ps, st) : ar_bwd_t<8, false>(a, ps, st);
   }
   return cudaErrorInvalidValue;
 }
 
 cudaError_t ln_fwd(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bfloat16 *b, __nv_bfloat16 *u,
                    int ld_u, float *mean, float *rstd, int m, int h, float eps, const OnesPad &pad, cudaStream_t st) {
-  ln_fwd_kernel<<<(m + 7) / 8, 256, 0, st>>>(x, g, b, u, ld_u, mean, rstd, m, h, eps, pad);
+  const size_t smem = (size_t)8 * h * 2;
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(ln_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  ln_fwd_kernel<<<(m + 7) / 8, 256, smem, st>>>(x, g, b, u, ld_u, mean, rstd, m, h, eps, pad);
   return cudaGetLastError();
 }
 
