@@ -74,8 +74,10 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(AttnArgs a) {
 
   const int s = a.s, H = a.heads;
   const int nqt = (s + ABQ - 1) / ABQ;
-  const int qt = nqt - 1 - blockIdx.x;  // heaviest tiles first
-  const int head = blockIdx.y, bi = blockIdx.z;
+  // grid (heads, b, q tiles): the tile index is the slowest-varying dimension, so CTAs are dispatched
+  // globally heaviest-first (longest-processing-time order over every sample and head)
+  const int qt = nqt - 1 - blockIdx.z;
+  const int head = blockIdx.x, bi = blockIdx.y;
   const int hr = H * D, ld = 3 * hr;
   const __nv_bfloat16 *base = reinterpret_cast<const __nv_bfloat16 *>(a.qkv) + (size_t)bi * s * ld;
   const int cq = head * D, ck = hr + head * D, cv = 2 * hr + head * D;
@@ -480,7 +482,7 @@ static cudaError_t fwd_d(const AttnArgs &a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((a.s + ABQ - 1) / ABQ, a.heads, a.b);
+  dim3 grid(a.heads, a.b, (a.s + ABQ - 1) / ABQ);
   attn_fwd_kernel<D><<<grid, 128, smem, st>>>(a);
   return cudaGetLastError();
 }

@@ -106,7 +106,7 @@ __device__ __forceinline__ void dq_body(const CUtensorMap *tmq_p, const CUtensor
   const int s = a.s, H = a.heads, hr = H * D;
   const int nqt = (s + TR - 1) / TR;
   const int qt = nqt - 1 - tile;  // heaviest (most key tiles) first
-  const int head = blockIdx.y, bi = blockIdx.z, tok0 = bi * s;
+  const int head = blockIdx.x, bi = blockIdx.y, tok0 = bi * s;
   const int J = min(2 * (qt + 1), (s + TH - 1) / TH);
   const int warp = warp_id(), lane = lane_id();
   unsigned long long *dbg = (warp == 2 && lane == 0) ? dbg_slot(a.dbg) : nullptr;
@@ -308,7 +308,7 @@ __device__ __forceinline__ void dkdv_body(const CUtensorMap *tmf_p, const CUtens
 
   const int s = a.s, H = a.heads, hr = H * D;
   const int kt = tile;  // kt = 0 has the most query tiles: heaviest first
-  const int head = blockIdx.y, bi = blockIdx.z, tok0 = bi * s;
+  const int head = blockIdx.x, bi = blockIdx.y, tok0 = bi * s;
   const int i0 = 2 * kt, NI = (s + TH - 1) / TH - i0;
   const size_t srow = ((size_t)bi * H + head) * s;
   const int warp = warp_id(), lane = lane_id();
@@ -527,15 +527,16 @@ __global__ void __launch_bounds__(256) attn_delta_kernel(AttnArgs a) {
   a.delta[((size_t)bi * H + e) * a.s + i] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
-// One launch for both halves of the backward (independent once delta exists): even CTAs compute dQ
-// tiles, odd CTAs dK/dV tiles, both heaviest-first, so the causal imbalance of one fills the other.
+// One launch for both halves of the backward (independent once delta exists): grid (heads, b, 2 x
+// tiles) with the tile slot slowest, so dispatch is globally heaviest-first; even slots compute dQ
+// tiles, odd slots dK/dV tiles, and the causal imbalance of one fills the other.
 template <int D>
 __global__ void __launch_bounds__(NTHR, BwdCfg<D>::DQ_MIN < BwdCfg<D>::DKV_MIN ? BwdCfg<D>::DQ_MIN : BwdCfg<D>::DKV_MIN)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmq_full, const __grid_constant__ CUtensorMap tmq_half,
                        const __grid_constant__ CUtensorMap tmo_full, const __grid_constant__ CUtensorMap tmo_half,
                        AttnArgs a) {
-  const int tile = blockIdx.x >> 1;
-  if (blockIdx.x & 1)
+  const int tile = blockIdx.z >> 1;
+  if (blockIdx.z & 1)
     dkdv_body<D>(&tmq_full, &tmq_half, &tmo_half, a, tile);
   else
     dq_body<D>(&tmq_full, &tmo_full, &tmq_half, a, tile);
@@ -585,7 +586,7 @@ static cudaError_t bwd_tc_d(const AttnArgs &a, cudaStream_t st) {
   attn_delta_kernel<D><<<(unsigned)((nd + 255) / 256), 256, 0, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  dim3 grid(2 * ((a.s + TR - 1) / TR), a.heads, a.b);
+  dim3 grid(a.heads, a.b, 2 * ((a.s + TR - 1) / TR));
   attn_bwd_tc_kernel<D><<<grid, NTHR, SMEM, st>>>(mq_full, mq_half, mo_full, mo_half, a);
   return cudaGetLastError();
 }

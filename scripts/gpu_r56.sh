@@ -1,0 +1,8 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+for c in "2 100 3 64" "4 1024 4 64" "2 208 5 64" "2 16 2 32" "1 256 2 80" "1 192 2 128"; do
+  timeout 60 python tools/attn_bwd_case.py $c >> gpurun_out/r56_cases.log 2>&1 || echo "case $c FAILED rc=$?" >> gpurun_out/r56_cases.log
+done
+timeout 120 python tools/attn_bench.py > gpurun_out/r56_attn.json 2>&1
+timeout 120 python tools/attn_dbg.py > gpurun_out/r56_dbg.json 2>&1
+grep case gpurun_out/r56_cases.log; cat gpurun_out/r56_attn.json gpurun_out/r56_dbg.json

@@ -33,9 +33,9 @@ def main():
     for _ in range(3):
         assert L.merak_test_attn_bwd_dbg(P(qkv), P(ctx), P(lse), P(dctx), P(dqkv), P(delta), b, s, H, d, P(dbg), st) == 0
     torch.cuda.synchronize()
-    # one merged launch: CTA linear index parity = role (even: dQ, odd: dK/dV)
-    A = dbg.cpu().numpy().astype(np.int64).reshape(2 * ncta, 64)
-    D = [A[0::2], A[1::2]]
+    # one merged launch, grid (H, b, 2 x tiles): role = z & 1 (even: dQ, odd: dK/dV)
+    A = dbg.cpu().numpy().astype(np.int64).reshape(2 * nq, H * b, 64)
+    D = [A[0::2].reshape(-1, 64), A[1::2].reshape(-1, 64)]
     out = {}
     for k, name in enumerate(("dq", "dkdv")):
         X = D[k]
