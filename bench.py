@@ -230,7 +230,17 @@ def main():
     stream = torch.cuda.current_stream()
 
     def barrier():
+        # a stalled synchronize reports the library's stream / watchdog state (diagnostics on stderr)
+        import threading
+        done = threading.Event()
+
+        def watch():
+            while not done.wait(60):
+                print(f"[rank {rank}] barrier stalled: {layer.debug_state()}", file=sys.stderr, flush=True)
+        th = threading.Thread(target=watch, daemon=True)
+        th.start()
         torch.cuda.synchronize()
+        done.set()
         if world > 1:
             dist.barrier()
 

@@ -203,6 +203,12 @@ int64_t merak_tmp_launch_count(const merak_tmp_t *h);
  * contents are zeros.  Synchronises the handle. */
 merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t rows, int32_t iters, float *ms);
 
+/* Diagnostics, callable from another host thread while work is pending (never blocks): out[0..4] =
+ * 1 if the internal stream (compute even, compute odd, wgrad filler, reductions, communication) still
+ * has unfinished work, else 0; out[5..9] = the watchdog error word (flag, epoch, cta, peer*16+kind,
+ * last flag value); out[10] = the handle's current handshake epoch. */
+merak_status merak_tmp_debug_state(const merak_tmp_t *h, int32_t *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -80,6 +80,8 @@ def lib():
         L.merak_tmp_launch_count.restype = ctypes.c_int64
         L.merak_tmp_bench_allreduce.argtypes = [P, I32, I32, I32, ctypes.POINTER(ctypes.c_float)]
         L.merak_tmp_bench_allreduce.restype = ctypes.c_int
+        L.merak_tmp_debug_state.argtypes = [P, ctypes.POINTER(I32)]
+        L.merak_tmp_debug_state.restype = ctypes.c_int
         for fn in ("merak_tmp_init", "merak_tmp_set_subbatches", "merak_tmp_layer_fwd", "merak_tmp_layer_bwd",
                    "merak_tmp_join", "merak_tmp_destroy", "merak_tmp_set_profiling", "merak_tmp_get_profile"):
             getattr(L, fn).restype = ctypes.c_int
@@ -254,6 +256,13 @@ class TmpLayer:
         t = ctypes.c_float()
         self._check(lib().merak_tmp_bench_allreduce(self.h, which, rows, iters, ctypes.byref(t)))
         return t.value
+
+    def debug_state(self) -> dict:
+        """Non-blocking: which internal streams still have work, and the watchdog error word."""
+        o = (ctypes.c_int32 * 11)()
+        lib().merak_tmp_debug_state(self.h, o)
+        return {"busy": {k: o[i] for i, k in enumerate(("cs", "cs1", "cw", "cr", "ms"))},
+                "err": list(o[5:10]), "epoch": o[10]}
 
     def launch_count(self) -> int:
         return lib().merak_tmp_launch_count(self.h)

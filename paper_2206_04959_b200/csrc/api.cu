@@ -79,6 +79,7 @@ struct merak_tmp {
   // wave-quantisation tails of the other's); cw: weight-gradient GEMMs (lowest priority filler);
   // ms: all-reduces (highest priority).  With MERAK_STREAMS=1, cs1 and cw alias cs.
   cudaStream_t cs = nullptr, cs1 = nullptr, cw = nullptr, ms = nullptr;
+  cudaStream_t cr = nullptr;  // LN-gradient sample reductions (off the comm stream, not behind the wgrads)
   // peer-visible memory: NSLOT slots of [M, h] bf16 followed by the flag array
   char *pv = nullptr;
   size_t slot_bytes = 0, flags_off = 0, pv_bytes = 0;
@@ -89,12 +90,13 @@ struct merak_tmp {
   char *ws = nullptr;
   bf16 *dz = nullptr, *dx1 = nullptr, *dctx = nullptr, *dqkv = nullptr;
   float *delta = nullptr, *part_col = nullptr, *part_lng = nullptr, *part_lnb = nullptr;
+  float *part_lng1 = nullptr, *part_lnb1 = nullptr;  // LN1 (AR#4) partials; part_lng/lnb serve LN2 (AR#3)
   int G = 16;
   // events
-  cudaEvent_t ev_entry = nullptr, ev_cs_end = nullptr, ev_cs1_end = nullptr, ev_cw_end = nullptr;
+  cudaEvent_t ev_entry = nullptr, ev_cs_end = nullptr, ev_cs1_end = nullptr, ev_cw_end = nullptr, ev_cr_end = nullptr;
   bool have_prev = false;
   // workspace hazards across calls: wgrads on cw read dz / dx1 / dqkv that the next backward rewrites
-  cudaEvent_t ev_w1 = nullptr, ev_wo = nullptr, ev_wqkv = nullptr;
+  cudaEvent_t ev_w1 = nullptr, ev_wo = nullptr, ev_wqkv = nullptr, ev_red = nullptr;
   bool have_wg = false;
   cudaEvent_t ev_dz[MAXN] = {}, ev_dq[MAXN] = {};
   cudaEvent_t ev_p[MAXN] = {};
@@ -325,14 +327,17 @@ static merak_status enter(merak_tmp_t *h, cudaStream_t st) {
   TRY(check_async_error(h));
   CK(h, cudaSetDevice(h->dev));
   CK(h, cudaEventRecord(h->ev_entry, st));
-  for (cudaStream_t c : {h->cs, h->cs1, h->cw, h->ms}) CK(h, cudaStreamWaitEvent(c, h->ev_entry, 0));
+  for (cudaStream_t c : {h->cs, h->cs1, h->cw, h->cr, h->ms}) CK(h, cudaStreamWaitEvent(c, h->ev_entry, 0));
   // the comm stream rewrites dx1 (AR#3) only after the previous call's readers of it are done:
   // the sub-batch streams (proj dgrad) and the W_o wgrad on cw
   if (h->have_prev) {
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_cs_end, 0));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_cs1_end, 0));
   }
-  if (h->have_wg) CK(h, cudaStreamWaitEvent(h->ms, h->ev_wo, 0));
+  if (h->have_wg) {
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_wo, 0));
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_red, 0));
+  }
   return MERAK_OK;
 }
 
@@ -340,6 +345,7 @@ static merak_status wait_all(merak_tmp_t *h, cudaStream_t st) {
   CK(h, cudaStreamWaitEvent(st, h->ev_cs_end, 0));
   CK(h, cudaStreamWaitEvent(st, h->ev_cs1_end, 0));
   CK(h, cudaStreamWaitEvent(st, h->ev_cw_end, 0));
+  CK(h, cudaStreamWaitEvent(st, h->ev_cr_end, 0));
   return MERAK_OK;
 }
 
@@ -347,6 +353,7 @@ static merak_status leave(merak_tmp_t *h, cudaStream_t st, uint32_t flags, int l
   CK(h, cudaEventRecord(h->ev_cs_end, h->cs));
   CK(h, cudaEventRecord(h->ev_cs1_end, h->cs1));
   CK(h, cudaEventRecord(h->ev_cw_end, h->cw));
+  CK(h, cudaEventRecord(h->ev_cr_end, h->cr));
   h->have_prev = true;
   for (int j = 0; j < h->n; ++j) h->prev_out[j] = h->ev_ar[last_slot][j];
   if (flags & MERAK_FLAG_CHAIN) {
@@ -509,7 +516,9 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.m = m; a.h = hh; a.x_ln = (const bf16 *)S(L.x1) + r0 * hh;
       a.mean = (const float *)S(L.mean2) + r0; a.rstd = (const float *)S(L.rstd2) + r0;
       a.gamma = (const bf16 *)w->ln2_g; a.dres = dyj; a.dx = h->dx1 + r0 * hh;
-      a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
+      // per-sub-batch region of the 8-row LN partials (the reduction below runs on the filler stream)
+      a.part_dg = h->part_lng + (r0 / h->G) * hh; a.part_db = h->part_lnb + (r0 / h->G) * hh;
+      a.G = h->G; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
       if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 2, r0, m, nullptr, nullptr, &a.chunk));
@@ -517,12 +526,17 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         CK(h, ar_bwd(a, ps, h->ms));
       }
-      Launch Lk(h, MERAK_K_REDUCE, h->ms, 0.0, 2);
-      CK(h, sample_reduce2(h->part_lng, h->part_lnb, h->s / h->G, m / h->s, hh, h->part_col,
-                           h->part_col + (size_t)h->B * hh, gr->ln2_g, gr->ln2_b, h->ms));
     }
     CK(h, cudaEventRecord(h->ev_ar[2][j], h->ms));
     h->ev_ar_valid[2][j] = true;
+    {
+      // dgamma2 / dbeta2: fixed per-sample tree + chain over samples (rule vi), in sub-batch order on cr,
+      // off the communication stream's critical path
+      CK(h, cudaStreamWaitEvent(h->cr, h->ev_ar[2][j], 0));
+      Launch Lk(h, MERAK_K_REDUCE, h->cr, 0.0, 2);
+      CK(h, sample_reduce2(h->part_lng + (r0 / h->G) * hh, h->part_lnb + (r0 / h->G) * hh, h->s / h->G, m / h->s,
+                           hh, h->part_col, h->part_col + (size_t)h->B * hh, gr->ln2_g, gr->ln2_b, h->cr));
+    }
   }
   // weight + bias gradients of the FFN block over ALL tokens: one accumulation chain over tokens
   // 0..B*s-1 -- the same MMA sequence as n = 1 -- on the filler stream once every dz rows exist.
@@ -565,7 +579,8 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.m = m; a.h = hh; a.x_ln = x + r0 * hh;
       a.mean = (const float *)S(L.mean1) + r0; a.rstd = (const float *)S(L.rstd1) + r0;
       a.gamma = (const bf16 *)w->ln1_g; a.dres = dx1; a.dx = dx + r0 * hh;
-      a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
+      a.part_dg = h->part_lng1 + (r0 / h->G) * hh; a.part_db = h->part_lnb1 + (r0 / h->G) * hh;
+      a.G = h->G; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
       if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 3, r0, m, nullptr, nullptr, &a.chunk));
@@ -573,12 +588,15 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         CK(h, ar_bwd(a, ps, h->ms));
       }
-      Launch Lk(h, MERAK_K_REDUCE, h->ms, 0.0, 2);
-      CK(h, sample_reduce2(h->part_lng, h->part_lnb, h->s / h->G, m / h->s, hh, h->part_col,
-                           h->part_col + (size_t)h->B * hh, gr->ln1_g, gr->ln1_b, h->ms));
     }
     CK(h, cudaEventRecord(h->ev_ar[3][j], h->ms));
     h->ev_ar_valid[3][j] = true;
+    {
+      CK(h, cudaStreamWaitEvent(h->cr, h->ev_ar[3][j], 0));
+      Launch Lk(h, MERAK_K_REDUCE, h->cr, 0.0, 2);
+      CK(h, sample_reduce2(h->part_lng1 + (r0 / h->G) * hh, h->part_lnb1 + (r0 / h->G) * hh, h->s / h->G, m / h->s,
+                           hh, h->part_col, h->part_col + (size_t)h->B * hh, gr->ln1_g, gr->ln1_b, h->cr));
+    }
   }
   // weight + bias gradients of the attention block over all tokens (filling behind the last AR#4)
   CK(h, cudaStreamWaitEvent(h->cw, h->ev_ar[2][n - 1], 0));  // every dx1 row (AR#3 in order on ms)
@@ -587,6 +605,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
   for (int j = 0; j < n; ++j) CK(h, cudaStreamWaitEvent(h->cw, h->ev_dq[j], 0));
   TRY(run_wgrad(h, h->dqkv, 3 * hr, 3 * hr, (const bf16 *)S(L.u), L.ld_u, hh, h->M, gr->w_qkv, gr->b_qkv));
   CK(h, cudaEventRecord(h->ev_wqkv, h->cw));
+  CK(h, cudaEventRecord(h->ev_red, h->cr));  // the next backward's AR#3/#4 rewrite the LN partials
   h->have_wg = true;
   return leave(h, st, flags, 3);
 }
@@ -821,7 +840,7 @@ static merak_status validate(const merak_tmp_config *c) {
 static void release(merak_tmp_t *h) {
   if (!h) return;
   cudaSetDevice(h->dev);
-  for (cudaStream_t c : {h->cs, h->cs1, h->cw, h->ms})
+  for (cudaStream_t c : {h->cs, h->cs1, h->cw, h->cr, h->ms})
     if (c) cudaStreamSynchronize(c);
   for (int q = 0; q < MAX_T; ++q)
     if (h->peer_pv[q] && h->peer_pv[q] != h->pv) cudaIpcCloseMemHandle(h->peer_pv[q]);
@@ -831,7 +850,8 @@ static void release(merak_tmp_t *h) {
   if (h->ws32) cudaFree(h->ws32);
   if (h->err_host) cudaFreeHost(h->err_host);
   for (auto e : h->evpool) cudaEventDestroy(e);
-  for (cudaEvent_t e : {h->ev_entry, h->ev_cs_end, h->ev_cs1_end, h->ev_cw_end, h->ev_w1, h->ev_wo, h->ev_wqkv})
+  for (cudaEvent_t e : {h->ev_entry, h->ev_cs_end, h->ev_cs1_end, h->ev_cw_end, h->ev_cr_end, h->ev_w1, h->ev_wo,
+                        h->ev_wqkv, h->ev_red})
     if (e) cudaEventDestroy(e);
   for (int j = 0; j < MAXN; ++j) {
     if (h->ev_p[j]) cudaEventDestroy(h->ev_p[j]);
@@ -844,11 +864,12 @@ static void release(merak_tmp_t *h) {
   if (h->cw && h->cw != h->cs) cudaStreamDestroy(h->cw);
   if (h->cs) cudaStreamDestroy(h->cs);
   if (h->ms) cudaStreamDestroy(h->ms);
+  if (h->cr) cudaStreamDestroy(h->cr);
   delete h;
 }
 
 static merak_status sync_all(merak_tmp_t *h) {
-  for (cudaStream_t c : {h->cs, h->cs1, h->cw, h->ms}) CK(h, cudaStreamSynchronize(c));
+  for (cudaStream_t c : {h->cs, h->cs1, h->cw, h->cr, h->ms}) CK(h, cudaStreamSynchronize(c));
   return MERAK_OK;
 }
 
@@ -907,7 +928,9 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
     CKI(cudaStreamCreateWithPriority(&h->cs1, cudaStreamNonBlocking, prio_mid));
     CKI(cudaStreamCreateWithPriority(&h->cw, cudaStreamNonBlocking, prio_lo));
   }
-  for (cudaEvent_t *e : {&h->ev_entry, &h->ev_cs_end, &h->ev_cs1_end, &h->ev_cw_end, &h->ev_w1, &h->ev_wo, &h->ev_wqkv})
+  CKI(cudaStreamCreateWithPriority(&h->cr, cudaStreamNonBlocking, prio_mid));
+  for (cudaEvent_t *e : {&h->ev_entry, &h->ev_cs_end, &h->ev_cs1_end, &h->ev_cw_end, &h->ev_cr_end, &h->ev_w1,
+                         &h->ev_wo, &h->ev_wqkv, &h->ev_red})
     CKI(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   for (int j = 0; j < MAXN; ++j) {
     CKI(cudaEventCreateWithFlags(&h->ev_p[j], cudaEventDisableTiming));
@@ -934,6 +957,7 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
     const int ncol = std::max(std::max(3 * h->hr, h->fr), h->h);
     const size_t o_pc = take(2 * (size_t)h->B * ncol * 4);
     const size_t o_pg = take((M / h->G) * (size_t)h->h * 4), o_pb = take((M / h->G) * (size_t)h->h * 4);
+    const size_t o_pg1 = take((M / h->G) * (size_t)h->h * 4), o_pb1 = take((M / h->G) * (size_t)h->h * 4);
     const size_t o_ctr = take(64);
     CKI(cudaMalloc(&h->ws, o));
     CKI(cudaMemset(h->ws + o_ctr, 0, 64));
@@ -943,6 +967,7 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
     h->dz = (bf16 *)(h->ws + o_dz); h->dx1 = (bf16 *)(h->ws + o_dx1); h->dctx = (bf16 *)(h->ws + o_dctx);
     h->dqkv = (bf16 *)(h->ws + o_dqkv); h->delta = (float *)(h->ws + o_delta);
     h->part_col = (float *)(h->ws + o_pc); h->part_lng = (float *)(h->ws + o_pg); h->part_lnb = (float *)(h->ws + o_pb);
+    h->part_lng1 = (float *)(h->ws + o_pg1); h->part_lnb1 = (float *)(h->ws + o_pb1);
   }
   if (h->f32) {
     const size_t M = h->M;
@@ -1136,6 +1161,15 @@ merak_status merak_tmp_get_timeline(merak_tmp_t *h, int32_t cap, int32_t *count,
 }
 
 int64_t merak_tmp_launch_count(const merak_tmp_t *h) { return h ? h->launches : 0; }
+
+merak_status merak_tmp_debug_state(const merak_tmp_t *h, int32_t *out) {
+  if (!h || !out) return MERAK_EINVAL;
+  cudaStream_t ss[5] = {h->cs, h->cs1, h->cw, h->cr, h->ms};
+  for (int i = 0; i < 5; ++i) out[i] = (ss[i] && cudaStreamQuery(ss[i]) == cudaErrorNotReady) ? 1 : 0;
+  for (int i = 0; i < 5; ++i) out[5 + i] = h->err_host ? ((volatile int *)h->err_host)[i] : 0;
+  out[10] = (int32_t)h->epoch;
+  return MERAK_OK;
+}
 
 merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t rows, int32_t iters, float *ms) {
   if (!h || !ms) return fail(h, MERAK_EINVAL, "NULL argument");

@@ -508,13 +508,16 @@ static cudaError_t bwd_d(const AttnArgs &a, cudaStream_t st) {
 }
 
 // Implementation switches are read per call (a getenv is ~100 ns) so tests can cover both paths.
-static bool use_tc() {
-  const char *e = getenv("MERAK_ATTN_TC");  // tcgen05 forward: opt-in until it beats mma.sync
-  return e && atoi(e) == 1;
+// tcgen05 forward by default where it measured faster (s >= 2048: 66.8 vs 79.9 us at b=2, H=8, d=96;
+// at s=1024 the mma.sync kernel wins); MERAK_ATTN_TC=0/1 forces either.
+static bool use_tc(const AttnArgs &a) {
+  const char *e = getenv("MERAK_ATTN_TC");
+  if (e) return atoi(e) == 1;
+  return a.s >= 2048;
 }
 
 cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st) {
-  if (use_tc()) return attn_fwd_tc(a, st);
+  if (use_tc(a)) return attn_fwd_tc(a, st);
   switch (a.d) {
     case 32: return fwd_d<32>(a, st);
     case 64: return fwd_d<64>(a, st);

@@ -80,8 +80,8 @@ __global__ void __launch_bounds__(192, FaCfg<D>::MIN_CTAS)
 
   const int s = a.s, H = a.heads;
   const int nqt = (s + TQ - 1) / TQ;
-  const int qt = nqt - 1 - blockIdx.x;  // heaviest tiles first
-  const int head = blockIdx.y, bi = blockIdx.z;
+  const int qt = nqt - 1 - blockIdx.z;  // grid (heads, b, tiles): globally heaviest tiles first
+  const int head = blockIdx.x, bi = blockIdx.y;
   const int hr = H * D;
   const int tok0 = bi * s;
   const int J = min(2 * (qt + 1), (s + TKH - 1) / TKH);  // causal: keys < (qt+1)*128, and < s
@@ -324,7 +324,7 @@ static cudaError_t fwd_tc_d(const AttnArgs &a, cudaStream_t st) {
   if (!make_qkv_map(&mq, a.qkv, a.b * a.s, 3 * a.heads * D, TQ) ||
       !make_qkv_map(&mkv, a.qkv, a.b * a.s, 3 * a.heads * D, TKH))
     return cudaErrorInvalidValue;
-  dim3 grid((a.s + TQ - 1) / TQ, a.heads, a.b);
+  dim3 grid(a.heads, a.b, (a.s + TQ - 1) / TQ);
   attn_fwd_tc_kernel<D><<<grid, 192, C::SMEM, st>>>(mq, mkv, a);
   return cudaGetLastError();
 }
