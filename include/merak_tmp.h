@@ -186,7 +186,7 @@ merak_status merak_tmp_set_profiling(merak_tmp_t *h, int32_t on);
 merak_status merak_tmp_get_profile(merak_tmp_t *h, double *ms, int64_t *launches, double *flops);
 
 /* Per-launch timeline since set_profiling(1) (call before get_profile, which consumes it): for up to
- * `cap` launches, the kernel class, the stream (0 = compute, 1 = communication) and start / end in ms
+ * `cap` launches, the kernel class, the stream (0 = compute (sub-batch or reduction streams), 1 = communication, 2 = wgrad filler) and start / end in ms
  * relative to the first recorded launch; *count receives the number written.  Synchronises. */
 merak_status merak_tmp_get_timeline(merak_tmp_t *h, int32_t cap, int32_t *count, int32_t *cls, int32_t *stream,
                                     float *t0, float *t1);

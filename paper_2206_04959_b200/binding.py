@@ -249,7 +249,8 @@ class TmpLayer:
         cls, st = (ctypes.c_int32 * cap)(), (ctypes.c_int32 * cap)()
         t0, t1 = (ctypes.c_float * cap)(), (ctypes.c_float * cap)()
         self._check(lib().merak_tmp_get_timeline(self.h, cap, ctypes.byref(n), cls, st, t0, t1))
-        return [(KERNEL_CLASSES[cls[i]], "comm" if st[i] else "comp", t0[i], t1[i]) for i in range(n.value)]
+        names = {0: "comp", 1: "comm", 2: "wgrad"}  # compute streams, communication stream, wgrad filler stream
+        return [(KERNEL_CLASSES[cls[i]], names.get(st[i], "comp"), t0[i], t1[i]) for i in range(n.value)]
 
     def bench_allreduce(self, which: int, rows: int, iters: int = 20) -> float:
         """Mean device ms of one all-reduce of rows x h (collective: every rank must call it)."""

@@ -75,7 +75,7 @@ def main():
     step()
     tl = layer.get_timeline()
     layer.set_profiling(False)
-    comp = union([[a, b] for c, s, a, b in tl if s == "comp"])
+    comp = union([[a, b] for c, s, a, b in tl if s in ("comp", "wgrad")])
     comm = union([[a, b] for c, s, a, b in tl if s == "comm" and c == "allreduce"])
     span = max(b for _, _, _, b in tl)
     busy_comp = sum(b - a for a, b in comp)
@@ -89,7 +89,7 @@ def main():
         # ASCII Gantt of the first layer's forward (both streams)
         width = 160
         end = max(b for c, s, a, b in tl[: len(tl) // (2 * K)] if True) if tl else 1.0
-        for name in ("comp", "comm"):
+        for name in ("comp", "wgrad", "comm"):
             row = [" "] * width
             for c, s, a, b in tl:
                 if s != name or a > end:
