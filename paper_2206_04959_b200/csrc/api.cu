@@ -116,6 +116,7 @@ struct merak_tmp {
   ncclComm_t nccl = nullptr;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // watchdog (env MERAK_AR_TIMEOUT_MS)
   bool two_shot = false;  // T >= 4: reduce-scatter + all-gather instead of one-shot (env MERAK_AR_TWO_SHOT)
+  bool pdl = false;       // programmatic dependent launch along the all-reduce kernel chain (env MERAK_AR_PDL)
   // fp32 check mode (MERAK_FP32_CHECK): fp32 workspace
   bool f32 = false;
   bool local = false;  // MERAK_COMM_LOCAL: single-process emulation of one rank, no peers
@@ -304,11 +305,13 @@ static merak_status two_shot_rs(merak_tmp_t *h, int slot, size_t r0, int m, cons
   a.resid = resid; a.bias = bias;
   a.out = slot_ptr(h, h->r, slot) + r0 * h->h;
   a.ctas = h->cfg.comm_ctas;
+  a.pdl = h->pdl && !h->prof;  // (profiling events between launches would break the PDL pairing)
   {
     Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
     CK(h, ar_rs(a, h->ms));
   }
   PeerSync ps = make_sync(h, true);
+  ps.pdl = h->pdl && !h->prof;
   TRY(sync_peers(h, ps));
   *chunk = c;
   return MERAK_OK;
@@ -427,6 +430,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       TRY(sync_peers(h, ps));
       if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 0, r0, m, xj, (const bf16 *)w->b_o, &a.chunk));
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+      a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
       CK(h, ar_fwd(a, ps, h->ms));
     }
     CK(h, cudaEventRecord(h->ev_ar[0][j], h->ms));
@@ -459,6 +463,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       TRY(sync_peers(h, ps));
       if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 1, r0, m, a.resid, a.bias, &a.chunk));
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+      a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
       CK(h, ar_fwd(a, ps, h->ms));
     }
     CK(h, cudaEventRecord(h->ev_ar[1][j], h->ms));
@@ -524,6 +529,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 2, r0, m, nullptr, nullptr, &a.chunk));
       {
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+        a.pdl = h->pdl && !h->prof && ps.enabled;
         CK(h, ar_bwd(a, ps, h->ms));
       }
     }
@@ -586,6 +592,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 3, r0, m, nullptr, nullptr, &a.chunk));
       {
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+        a.pdl = h->pdl && !h->prof && ps.enabled;
         CK(h, ar_bwd(a, ps, h->ms));
       }
     }
@@ -900,6 +907,7 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   h->f32 = cfg->precision == MERAK_FP32_CHECK;
   h->local = cfg->comm == MERAK_COMM_LOCAL;
   h->two_shot = h->T >= 4 && !h->f32;
+  if (const char *t = getenv("MERAK_AR_PDL")) h->pdl = atoi(t) == 1;
   if (const char *t = getenv("MERAK_AR_TWO_SHOT")) h->two_shot = h->T > 1 && !h->f32 && atoi(t) == 1;
   auto bail = [&](merak_status st) {
     g_init_err = h->err;
@@ -1208,7 +1216,8 @@ merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t ro
         a.m = rows; a.h = (int)hh; a.resid = resid; a.bias = gam; a.out = out; a.ctas = h->cfg.comm_ctas;
         if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, resid, gam, &a.chunk));
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
-        CK(h, ar_fwd(a, ps, h->ms));
+        a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
+      CK(h, ar_fwd(a, ps, h->ms));
       } else {
         ArBwdArgs a;
         memset(&a, 0, sizeof(a));
@@ -1217,6 +1226,7 @@ merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t ro
         a.dx = out; a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
         if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, nullptr, nullptr, &a.chunk));
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+        a.pdl = h->pdl && !h->prof && ps.enabled;
         CK(h, ar_bwd(a, ps, h->ms));
       }
       return MERAK_OK;

@@ -131,6 +131,7 @@ struct PeerSync {
   uint32_t *flags_peer[MAX_T];
   int *err_word;              // device word set to 1 on watchdog timeout
   uint64_t timeout_ns;
+  bool pdl;                   // host: launch as a programmatic dependent of the previous kernel
 };
 
 struct ArFwdArgs {
@@ -151,6 +152,7 @@ struct ArFwdArgs {
   // two-shot phase 2 ("gathered" mode, chunk > 0): row i was already reduced (sum + bias + resid,
   // rounded once) by rank i / chunk into its slot; partial[q] is rank q's slot, bias/resid unused.
   int chunk;
+  bool pdl;  // host: launch as a programmatic dependent of the handshake kernel before it
 };
 cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st);
 
@@ -164,6 +166,7 @@ struct ArRsArgs {
   const __nv_bfloat16 *bias;
   __nv_bfloat16 *out;
   int ctas;
+  bool pdl;
 };
 cudaError_t ar_rs(const ArRsArgs &a, cudaStream_t st);
 // 1-warp kernel: publish ps.epoch to every peer and wait for theirs (no-op unless ps.enabled)
@@ -182,6 +185,7 @@ struct ArBwdArgs {
   int G;                        // rows per group (8; divides s)
   int ctas;
   int chunk;                    // > 0: two-shot phase 2, row i reads the reduced du from partial[i / chunk]
+  bool pdl;
 };
 cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st);
 int ar_bwd_group_rows(int h);

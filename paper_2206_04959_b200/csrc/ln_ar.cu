@@ -23,6 +23,8 @@
 // call) and later waits fail fast.
 #include <math.h>
 
+#include <utility>
+
 #include "kernels.h"
 #include "ptx.cuh"
 
@@ -57,6 +59,8 @@ MK_DEV void store8(__nv_bfloat16 *p, const float (&v)[8]) {
 __global__ void peer_ready_kernel(PeerSync ps) {
   const int r = threadIdx.x;
   volatile int *err = ps.err_word;
+  griddep_wait();    // PDL (second two-shot handshake): the reduce-scatter kernel before it has finished
+  griddep_launch();  // let the data kernel after this one launch while this warp spins
   if (*err) return;
   // The partials were written by kernels that completed before this one (stream / event order);
   // peers read them through this GPU's L2, so the release store of the epoch suffices.
@@ -79,10 +83,27 @@ __global__ void peer_ready_kernel(PeerSync ps) {
   __syncwarp();
 }
 
+// Launch with an optional programmatic-dependent-launch attribute (hides the launch latency of the
+// next kernel of the all-reduce chain behind the previous one; the kernels call griddep_wait first).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl,
+                            Args &&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 cudaError_t peer_ready(const PeerSync &ps, cudaStream_t st) {
   if (!ps.enabled) return cudaSuccess;
-  peer_ready_kernel<<<1, 32, 0, st>>>(ps);
-  return cudaGetLastError();
+  return launch_k(peer_ready_kernel, dim3(1), dim3(32), 0, st, ps.pdl, ps);
 }
 
 // ------------------------------------------------------------------------------ rank-ordered row sums
@@ -128,6 +149,8 @@ __host__ __device__ constexpr int ar_ch(int nt) { return nt >= 8 ? 1 : nt >= 4 ?
 template <int NT>
 __global__ void __launch_bounds__(256) ar_fwd_kernel(ArFwdArgs a, PeerSync ps) {
   constexpr int CH = ar_ch(NT);
+  griddep_wait();  // PDL: the handshake before this kernel has completed (peers' data is ready)
+  griddep_launch();
   extern __shared__ uint4 row_s[];  // do_ln: per warp, the stored bf16 row (LN2 reads it, reading R12)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
@@ -196,6 +219,8 @@ __global__ void __launch_bounds__(256) ar_fwd_kernel(ArFwdArgs a, PeerSync ps) {
 template <int NT>
 __global__ void __launch_bounds__(256) ar_rs_kernel(ArRsArgs a) {
   constexpr int CH = ar_ch(NT);
+  griddep_wait();
+  griddep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int h = a.h, nc = h >> 3;
   const __nv_bfloat16 *src[NT];
@@ -223,6 +248,8 @@ __global__ void __launch_bounds__(256) ar_rs_kernel(ArRsArgs a) {
 template <int G, int NT, bool STASH>
 __global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
   constexpr int CH = ar_ch(NT);
+  griddep_wait();
+  griddep_launch();
   extern __shared__ __align__(16) float du_s[];  // [G][h] the all-reduced gradient (bf16-rounded),
                                                  // then [G][h/8] uint4 x_ln rows, [G][h/8] uint4 dres rows
   __shared__ float s_mean[G], s_rstd[G];
@@ -507,8 +534,7 @@ static cudaError_t ar_fwd_t(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t
     res_smem = smem;
   }
   const int grid = clamp_ctas(a.ctas, (a.m + 7) / 8, resident);
-  ar_fwd_kernel<NT><<<grid, 256, smem, st>>>(a, ps);
-  return cudaGetLastError();
+  return launch_k(ar_fwd_kernel<NT>, dim3(grid), dim3(256), smem, st, a.pdl, a, ps);
 }
 cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
   switch (a.chunk > 0 ? 1 : a.T) {
@@ -527,8 +553,7 @@ static cudaError_t ar_rs_t(const ArRsArgs &a, cudaStream_t st) {
   static int resident = 0;
   if (!resident) resident = resident_ctas((const void *)ar_rs_kernel<NT>, 256, 0);
   const int grid = clamp_ctas(a.ctas, (a.row1 - a.row0 + 7) / 8, resident);
-  ar_rs_kernel<NT><<<grid, 256, 0, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(ar_rs_kernel<NT>, dim3(grid), dim3(256), 0, st, a.pdl, a);
 }
 cudaError_t ar_rs(const ArRsArgs &a, cudaStream_t st) {
   if (a.row1 <= a.row0) return cudaSuccess;
@@ -560,8 +585,7 @@ static cudaError_t ar_bwd_t(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t
     res_smem = smem;
   }
   const int grid = clamp_ctas(a.ctas, a.m / G, resident);
-  ar_bwd_kernel<G, NT, STASH><<<grid, 256, smem, st>>>(a, ps);
-  return cudaGetLastError();
+  return launch_k(ar_bwd_kernel<G, NT, STASH>, dim3(grid), dim3(256), smem, st, a.pdl, a, ps);
 }
 cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
   if (a.G != 8 || a.m % 8) return cudaErrorInvalidValue;

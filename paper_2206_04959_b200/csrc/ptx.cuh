@@ -53,6 +53,11 @@ MK_DEV void st_shared_cluster_u32(uint32_t cluster_addr, uint32_t v) {
   asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
 }
 
+// programmatic dependent launch: no-ops unless the kernel was launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization
+MK_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+MK_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------------------------------ TMA
 MK_DEV void tma_prefetch(const CUtensorMap *map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
