@@ -116,11 +116,21 @@ class ClockSampler:
                 "source": "NVML, ~5 ms period, timed region only"}
 
 
+def _use_host_cores():
+    """torchrun sets OMP_NUM_THREADS=1; the oracle is timed on all of the host cores this process may use."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(len(os.sched_getaffinity(0)))
+    except Exception:
+        pass
+
+
 def cpu_oracle_sample(cfg, target_s=12.0):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload: b samples of the same
     layer shape (fwd+bwd), growing b until ~target_s of CPU work.  Returns the cpu_baseline dict."""
     import numpy as np  # noqa: F401
 
+    _use_host_cores()
     from oracle import layer_flops as oflops, layer_fwd_bwd
     from synth import make_all
     b = 1
@@ -159,6 +169,7 @@ def run_reference(args, cfg, rank, world):
     workload's layer).  Rank 0 only; other ranks exit without work."""
     if rank != 0:
         return
+    _use_host_cores()
     from oracle import layer_flops as oflops, layer_fwd_bwd
     from synth import make_all
     sub = cfg.with_(microbatch=1)
