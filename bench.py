@@ -119,6 +119,7 @@ class ClockSampler:
 def _use_host_cores():
     """torchrun sets OMP_NUM_THREADS=1; the oracle is timed on all of the host cores this process may use."""
     try:
+        import numpy  # noqa: F401  (load the BLAS first, then raise its thread limit)
         from threadpoolctl import threadpool_limits
         threadpool_limits(len(os.sched_getaffinity(0)))
     except Exception:
