@@ -355,11 +355,25 @@ def main():
         # every step uploads its x and dy from pinned host memory and downloads y and dx (all inside the
         # timed region, on a copy stream), double-buffered so step i+1's upload and step i's downloads
         # overlap compute; only the first upload and the last download are exposed.
-        hx = X.cpu().pin_memory()
-        hdy = DY.cpu().pin_memory()
+        # x, dy, y, dx are replicated on the T ranks: each rank moves only its 1/T row slice over PCIe and
+        # the slices are all-gathered over NVLink (NCCL) -- the way a TMP input pipeline shares one batch.
+        rows = M // world
+        r0 = rank * rows
+        hx = X[r0:r0 + rows].cpu().pin_memory()
+        hdy = DY[r0:r0 + rows].cpu().pin_memory()
         hy = torch.empty_like(hx).pin_memory()
         hdx = torch.empty_like(hx).pin_memory()
         Xb, DYb = [torch.empty_like(X) for _ in range(2)], [torch.empty_like(DY) for _ in range(2)]
+
+        def upload(bi_):
+            if world == 1:
+                Xb[bi_].copy_(hx, non_blocking=True)
+                DYb[bi_].copy_(hdy, non_blocking=True)
+                return
+            Xb[bi_][r0:r0 + rows].copy_(hx, non_blocking=True)
+            DYb[bi_][r0:r0 + rows].copy_(hdy, non_blocking=True)
+            dist.all_gather_into_tensor(Xb[bi_], Xb[bi_][r0:r0 + rows])
+            dist.all_gather_into_tensor(DYb[bi_], DYb[bi_][r0:r0 + rows])
         cp = torch.cuda.Stream(device=dev)    # uploads (H2D copy engine)
         cpo = torch.cuda.Stream(device=dev)   # downloads (D2H copy engine)
         ne = max(3, args.steps // 2)
@@ -369,8 +383,7 @@ def main():
         cp.wait_stream(stream)
         ev_in, ev_free, ev_y, ev_dx = [None, None], [None, None], None, None
         with torch.cuda.stream(cp):
-            Xb[0].copy_(hx, non_blocking=True)
-            DYb[0].copy_(hdy, non_blocking=True)
+            upload(0)
         ev_in[0] = cp.record_event()
         for i in range(ne):
             bb = i & 1
@@ -379,8 +392,7 @@ def main():
                 if ev_free[1 - bb] is not None:
                     cp.wait_event(ev_free[1 - bb])
                 with torch.cuda.stream(cp):
-                    Xb[1 - bb].copy_(hx, non_blocking=True)
-                    DYb[1 - bb].copy_(hdy, non_blocking=True)
+                    upload(1 - bb)
                 ev_in[1 - bb] = cp.record_event()
             flush.zero_()  # L2 flush between steps, counted inside the e2e time (conservative)
             if ev_y is not None:
@@ -391,7 +403,7 @@ def main():
                               flags=FLAG_CHAIN if k < K - 1 else 0)
             cpo.wait_stream(stream)
             with torch.cuda.stream(cpo):
-                hy.copy_(Ys[K - 1], non_blocking=True)
+                hy.copy_(Ys[K - 1][r0:r0 + rows], non_blocking=True)
             ev_y = cpo.record_event()
             if ev_dx is not None:
                 stream.wait_event(ev_dx)  # the previous dx download has read DXs[0]
@@ -401,7 +413,7 @@ def main():
             ev_free[bb] = stream.record_event()
             cpo.wait_event(ev_free[bb])
             with torch.cuda.stream(cpo):
-                hdx.copy_(DXs[0], non_blocking=True)
+                hdx.copy_(DXs[0][r0:r0 + rows], non_blocking=True)
             ev_dx = cpo.record_event()
             stage(f"e2e iter {i} issued")
         stream.wait_stream(cp)
@@ -413,11 +425,12 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         stage("e2e done")
         extras["e2e"] = {"value": fl / (te.item() * 1e-3) / 1e12, "unit": "TFLOP/s",
-                         "h2d_bytes_per_step": 2 * X.numel() * 2, "d2h_bytes_per_step": 2 * X.numel() * 2,
+                         "h2d_bytes_per_step": 2 * hx.numel() * 2, "d2h_bytes_per_step": 2 * hx.numel() * 2,
                          "ms_per_step": te.item(), "steps": ne,
                          "note": "pinned-host x, dy up and y, dx down every step (upload and download copy streams), "
                                  "double-buffered like an input pipeline; the L2 flush between steps is inside the "
-                                 "timed region"}
+                                 "timed region; at T > 1 each rank moves its 1/T row slice over PCIe and the inputs "
+                                 "are all-gathered over NVLink (NCCL); bytes are per GPU"}
 
     # roofline of the dominant kernel class (the tcgen05 GEMM), from CUDA events around every launch on
     # its stream.  The timed run overlaps kernels of different sub-batches (and the wgrad filler), so
