@@ -71,6 +71,15 @@ def main():
         for k in out:
             if not torch.equal(out[k], out2[k]):
                 failures.append((name, f"{k}: one-shot vs two-shot all-reduce not bit-identical"))
+        # programmatic dependent launch along the all-reduce chain (opt-in) must not change a bit
+        os.environ["MERAK_AR_PDL"] = "1"
+        try:
+            outp = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group)
+        finally:
+            del os.environ["MERAK_AR_PDL"]
+        for k in out:
+            if not torch.equal(out[k], outp[k]):
+                failures.append((name, f"{k}: PDL all-reduce chain not bit-identical"))
         # fp32 check mode over the peer all-reduce (tolerance 1e-5)
         if cfg.hidden <= 320:
             out32 = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group, precision=1)
