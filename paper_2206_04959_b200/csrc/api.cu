@@ -117,6 +117,7 @@ struct merak_tmp {
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // watchdog (env MERAK_AR_TIMEOUT_MS)
   bool two_shot = false;  // T >= 4: reduce-scatter + all-gather instead of one-shot (env MERAK_AR_TWO_SHOT)
   bool pdl = false;       // programmatic dependent launch along the all-reduce kernel chain (env MERAK_AR_PDL)
+  int gemm_smem_kb = 192;  // GEMM TMA ring: 160 KB at T > 1 leaves smem for co-resident all-reduce kernels
   // fp32 check mode (MERAK_FP32_CHECK): fp32 workspace
   bool f32 = false;
   bool local = false;  // MERAK_COMM_LOCAL: single-process emulation of one rank, no peers
@@ -237,7 +238,7 @@ static bf16 *slot_ptr(merak_tmp_t *h, int rank, int slot) {
 static merak_status run_gemm(merak_tmp_t *h, const GemmArgs &a0, cudaStream_t st) {
   GemmArgs a = a0;
   // T > 1: keep smem free on every SM for the all-reduce kernels that overlap the GEMMs
-  a.smem_kb = h->T > 1 ? 160 : 192;
+  a.smem_kb = h->gemm_smem_kb;
   if (h->tile_ctr && st != h->cw) a.tile_ctr = h->tile_ctr + (st == h->cs1 && h->cs1 != h->cs ? 1 : 0);
   Launch L(h, MERAK_K_GEMM, st, 2.0 * a.M * a.N * a.K);
   CK(h, gemm(a, st));
@@ -908,6 +909,8 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   h->local = cfg->comm == MERAK_COMM_LOCAL;
   h->two_shot = h->T >= 4 && !h->f32;
   if (const char *t = getenv("MERAK_AR_PDL")) h->pdl = atoi(t) == 1;
+  h->gemm_smem_kb = h->T > 1 ? 160 : 192;
+  if (const char *t = getenv("MERAK_GEMM_SMEM_KB")) h->gemm_smem_kb = atoi(t) == 160 ? 160 : 192;
   if (const char *t = getenv("MERAK_AR_TWO_SHOT")) h->two_shot = h->T > 1 && !h->f32 && atoi(t) == 1;
   auto bail = [&](merak_status st) {
     g_init_err = h->err;
