@@ -241,20 +241,30 @@ def main():
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
 
-    def barrier():
-        # a stalled synchronize reports the library's stream / watchdog state (diagnostics on stderr)
-        import threading
-        done = threading.Event()
+    # stall watchdog (diagnostics on stderr): if the host makes no progress for STALL_S seconds -- blocked in
+    # a synchronize or in a launch whose queue is full -- print the library's stream / watchdog state
+    import threading
+    progress = [time.time()]
+    stall_s = float(os.environ.get("MERAK_BENCH_STALL_S", "5"))
 
-        def watch():
-            while not done.wait(60):
-                print(f"[rank {rank}] barrier stalled: {layer.debug_state()}", file=sys.stderr, flush=True)
-        th = threading.Thread(target=watch, daemon=True)
-        th.start()
+    def watchdog():
+        while True:
+            time.sleep(1.0)
+            if time.time() - progress[0] > stall_s:
+                # host-only state first (cannot block), then the CUDA-side state from a helper thread
+                print(f"[rank {rank}] stalled {time.time() - progress[0]:.0f}s host: {layer.debug_host()}",
+                      file=sys.stderr, flush=True)
+                threading.Thread(target=lambda: print(f"[rank {rank}] device: {layer.debug_state()}",
+                                                      file=sys.stderr, flush=True), daemon=True).start()
+                progress[0] = time.time()
+    threading.Thread(target=watchdog, daemon=True).start()
+
+    def barrier():
         torch.cuda.synchronize()
-        done.set()
+        progress[0] = time.time()
         if world > 1:
             dist.barrier()
+        progress[0] = time.time()
 
     def step(flags=0, x_in=None, dy_in=None, lay=None):
         """K chained layers forward, then backward in reverse (overlap across layers): every
@@ -282,6 +292,7 @@ def main():
             starts[i].record(stream)
             step(flags, lay=lay)
             ends[i].record(stream)
+            progress[0] = time.time()
         barrier()
         launches = lay.launch_count() - l0
         ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
@@ -296,6 +307,7 @@ def main():
     t_start = time.time()
 
     def stage(msg):  # progress markers on stderr (multi-rank runs: evidence if a run ever stalls)
+        progress[0] = time.time()
         if world > 1 or os.environ.get("MERAK_BENCH_TRACE"):
             print(f"[rank {rank} +{time.time() - t_start:.1f}s] {msg}", file=sys.stderr, flush=True)
 
@@ -478,7 +490,9 @@ def main():
         if "e2e" in extras:
             line["e2e"] = extras["e2e"]
         if not args.no_cpu_baseline and world == 1:
+            progress[0] = time.time() + 1e9  # CPU work: not a GPU stall
             line["cpu_baseline"] = cpu_oracle_sample(cfg)
+            progress[0] = time.time()
         print(json.dumps(line), flush=True)
     layer.close()
     faulthandler.cancel_dump_traceback_later()

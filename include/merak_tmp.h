@@ -206,8 +206,15 @@ merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t ro
 /* Diagnostics, callable from another host thread while work is pending (never blocks): out[0..4] =
  * 1 if the internal stream (compute even, compute odd, wgrad filler, reductions, communication) still
  * has unfinished work, else 0; out[5..9] = the watchdog error word (flag, epoch, cta, peer*16+kind,
- * last flag value); out[10] = the handle's current handshake epoch. */
+ * last flag value); out[10] = the handle's current handshake epoch; with MERAK_DEBUG_TRACE=1 set at init,
+ * out[11..15] = the kernel class (MERAK_K_*) of the first unfinished launch on each of those streams
+ * and out[16..20] its launch sequence number (-1 when none / tracing off).  out has 21 entries. */
 merak_status merak_tmp_debug_state(const merak_tmp_t *h, int32_t *out);
+
+/* Host-memory-only part of the diagnostics (no CUDA call, so it cannot block behind a launch):
+ * out[0..4] = watchdog error word, out[5] = handshake epoch, out[6] = launches enqueued so far,
+ * out[7..11] = traced launches enqueued per stream (cs, cs1, cw, cr, ms; MERAK_DEBUG_TRACE=1). */
+merak_status merak_tmp_debug_host(const merak_tmp_t *h, int32_t *out);
 
 #ifdef __cplusplus
 }

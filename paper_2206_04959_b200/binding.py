@@ -82,6 +82,8 @@ def lib():
         L.merak_tmp_bench_allreduce.restype = ctypes.c_int
         L.merak_tmp_debug_state.argtypes = [P, ctypes.POINTER(I32)]
         L.merak_tmp_debug_state.restype = ctypes.c_int
+        L.merak_tmp_debug_host.argtypes = [P, ctypes.POINTER(I32)]
+        L.merak_tmp_debug_host.restype = ctypes.c_int
         for fn in ("merak_tmp_init", "merak_tmp_set_subbatches", "merak_tmp_layer_fwd", "merak_tmp_layer_bwd",
                    "merak_tmp_join", "merak_tmp_destroy", "merak_tmp_set_profiling", "merak_tmp_get_profile"):
             getattr(L, fn).restype = ctypes.c_int
@@ -260,10 +262,19 @@ class TmpLayer:
 
     def debug_state(self) -> dict:
         """Non-blocking: which internal streams still have work, and the watchdog error word."""
-        o = (ctypes.c_int32 * 11)()
+        o = (ctypes.c_int32 * 21)()
         lib().merak_tmp_debug_state(self.h, o)
-        return {"busy": {k: o[i] for i, k in enumerate(("cs", "cs1", "cw", "cr", "ms"))},
-                "err": list(o[5:10]), "epoch": o[10]}
+        names = ("cs", "cs1", "cw", "cr", "ms")
+        return {"busy": {k: o[i] for i, k in enumerate(names)}, "err": list(o[5:10]), "epoch": o[10],
+                "first_unfinished": {k: (KERNEL_CLASSES[o[11 + i]] if 0 <= o[11 + i] < len(KERNEL_CLASSES) else None,
+                                         o[16 + i]) for i, k in enumerate(names)}}
+
+    def debug_host(self) -> dict:
+        """Host-memory-only diagnostics (never blocks)."""
+        o = (ctypes.c_int32 * 12)()
+        lib().merak_tmp_debug_host(self.h, o)
+        return {"err": list(o[0:5]), "epoch": o[5], "launches": o[6],
+                "traced": dict(zip(("cs", "cs1", "cw", "cr", "ms"), list(o[7:12])))}
 
     def launch_count(self) -> int:
         return lib().merak_tmp_launch_count(self.h)

@@ -118,6 +118,13 @@ struct merak_tmp {
   bool two_shot = false;  // T >= 4: reduce-scatter + all-gather instead of one-shot (env MERAK_AR_TWO_SHOT)
   bool pdl = false;       // programmatic dependent launch along the all-reduce kernel chain (env MERAK_AR_PDL)
   int gemm_smem_kb = 192;  // GEMM TMA ring: 160 KB at T > 1 leaves smem for co-resident all-reduce kernels
+  // MERAK_DEBUG_TRACE=1: an event after every launch, per stream (cs, cs1, cw, cr, ms), in a 64-deep ring, so
+  // merak_tmp_debug_state can name the first unfinished kernel of a stalled stream
+  bool trace = false;
+  cudaEvent_t tr_ev[5][64] = {};
+  int tr_cls[5][64] = {};
+  int64_t tr_seq[5][64] = {};
+  int64_t tr_n[5] = {};
   // fp32 check mode (MERAK_FP32_CHECK): fp32 workspace
   bool f32 = false;
   bool local = false;  // MERAK_COMM_LOCAL: single-process emulation of one rank, no peers
@@ -173,6 +180,18 @@ struct Launch {
   }
   ~Launch() {
     h->launches += nk;
+    if (h->trace) {
+      const cudaStream_t ss[5] = {h->cs, h->cs1, h->cw, h->cr, h->ms};
+      for (int i = 0; i < 5; ++i)
+        if (ss[i] == st) {
+          const int k = (int)(h->tr_n[i] % 64);
+          cudaEventRecord(h->tr_ev[i][k], st);
+          h->tr_cls[i][k] = cls;
+          h->tr_seq[i][k] = h->launches;
+          ++h->tr_n[i];
+          break;
+        }
+    }
     if (h->prof) {
       cudaEvent_t b = pool_event(h);
       cudaEventRecord(b, st);
@@ -861,6 +880,9 @@ static void release(merak_tmp_t *h) {
   for (cudaEvent_t e : {h->ev_entry, h->ev_cs_end, h->ev_cs1_end, h->ev_cw_end, h->ev_cr_end, h->ev_w1, h->ev_wo,
                         h->ev_wqkv, h->ev_red})
     if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 5; ++i)
+    for (int k = 0; k < 64; ++k)
+      if (h->tr_ev[i][k]) cudaEventDestroy(h->tr_ev[i][k]);
   for (int j = 0; j < MAXN; ++j) {
     if (h->ev_p[j]) cudaEventDestroy(h->ev_p[j]);
     if (h->ev_dz[j]) cudaEventDestroy(h->ev_dz[j]);
@@ -911,6 +933,7 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   if (const char *t = getenv("MERAK_AR_PDL")) h->pdl = atoi(t) == 1;
   h->gemm_smem_kb = h->T > 1 ? 160 : 192;
   if (const char *t = getenv("MERAK_GEMM_SMEM_KB")) h->gemm_smem_kb = atoi(t) == 160 ? 160 : 192;
+  if (const char *t = getenv("MERAK_DEBUG_TRACE")) h->trace = atoi(t) == 1;
   if (const char *t = getenv("MERAK_AR_TWO_SHOT")) h->two_shot = h->T > 1 && !h->f32 && atoi(t) == 1;
   auto bail = [&](merak_status st) {
     g_init_err = h->err;
@@ -943,6 +966,9 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   for (cudaEvent_t *e : {&h->ev_entry, &h->ev_cs_end, &h->ev_cs1_end, &h->ev_cw_end, &h->ev_cr_end, &h->ev_w1,
                          &h->ev_wo, &h->ev_wqkv, &h->ev_red})
     CKI(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  if (h->trace)
+    for (int i = 0; i < 5; ++i)
+      for (int k = 0; k < 64; ++k) CKI(cudaEventCreateWithFlags(&h->tr_ev[i][k], cudaEventDisableTiming));
   for (int j = 0; j < MAXN; ++j) {
     CKI(cudaEventCreateWithFlags(&h->ev_p[j], cudaEventDisableTiming));
     CKI(cudaEventCreateWithFlags(&h->ev_dz[j], cudaEventDisableTiming));
@@ -1173,12 +1199,35 @@ merak_status merak_tmp_get_timeline(merak_tmp_t *h, int32_t cap, int32_t *count,
 
 int64_t merak_tmp_launch_count(const merak_tmp_t *h) { return h ? h->launches : 0; }
 
+merak_status merak_tmp_debug_host(const merak_tmp_t *h, int32_t *out) {
+  if (!h || !out) return MERAK_EINVAL;
+  for (int i = 0; i < 5; ++i) out[i] = h->err_host ? ((volatile int *)h->err_host)[i] : 0;
+  out[5] = (int32_t)h->epoch;
+  out[6] = (int32_t)h->launches;
+  for (int i = 0; i < 5; ++i) out[7 + i] = (int32_t)h->tr_n[i];
+  return MERAK_OK;
+}
+
 merak_status merak_tmp_debug_state(const merak_tmp_t *h, int32_t *out) {
   if (!h || !out) return MERAK_EINVAL;
   cudaStream_t ss[5] = {h->cs, h->cs1, h->cw, h->cr, h->ms};
   for (int i = 0; i < 5; ++i) out[i] = (ss[i] && cudaStreamQuery(ss[i]) == cudaErrorNotReady) ? 1 : 0;
   for (int i = 0; i < 5; ++i) out[5 + i] = h->err_host ? ((volatile int *)h->err_host)[i] : 0;
   out[10] = (int32_t)h->epoch;
+  for (int i = 0; i < 5; ++i) {  // first unfinished traced launch per stream (MERAK_DEBUG_TRACE=1), else -1
+    out[11 + i] = -1;
+    out[16 + i] = -1;
+    if (!h->trace) continue;
+    const int64_t n = h->tr_n[i], lo = n > 64 ? n - 64 : 0;
+    for (int64_t q = lo; q < n; ++q) {
+      const int k = (int)(q % 64);
+      if (cudaEventQuery(h->tr_ev[i][k]) == cudaErrorNotReady) {
+        out[11 + i] = h->tr_cls[i][k];
+        out[16 + i] = (int32_t)h->tr_seq[i][k];
+        break;
+      }
+    }
+  }
   return MERAK_OK;
 }
 
