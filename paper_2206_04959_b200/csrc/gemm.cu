@@ -228,6 +228,9 @@ __global__ void __launch_bounds__(256, 1)
     fence_mbar_init();
     fence_proxy_async();
   }
+  // 2-CTA: both CTAs of the pair are synchronised BEFORE the paired TMEM allocation (as well as after it
+  // and before teardown), the documented protocol for tcgen05.alloc.cta_group::2
+  if constexpr (CG == 2) cluster_sync();
   if (warp == 2) {
     if constexpr (CG == 2)
       tmem_alloc2<C::TMEM_COLS>(tmem_slot);
