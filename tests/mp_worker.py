@@ -36,6 +36,8 @@ def main():
         "tiny": tiny.with_(tmp_degree=T),
         "h320_H5_uneven": tiny.with_(hidden=320, heads=5, seq_len=64, microbatch=4, tmp_degree=T),
         "h256_H8_s128_n4": tiny.with_(hidden=256, heads=8, seq_len=128, microbatch=4, n_sub=4, tmp_degree=T),
+        "h320_H4_d80": tiny.with_(hidden=320, heads=4, seq_len=96, microbatch=2, tmp_degree=T),
+        "h384_H4_d96": tiny.with_(hidden=384, heads=4, seq_len=64, microbatch=4, n_sub=2, tmp_degree=T),
     }
     if os.environ.get("MERAK_TEST_FULL", "0") == "1":
         cases["gpt1.5b"] = CONFIGS["gpt1.5b"].with_(tmp_degree=T)
