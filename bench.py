@@ -20,7 +20,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -213,7 +212,6 @@ def main():
         run_reference(args, cfg, rank, world)
         return
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
