@@ -508,12 +508,13 @@ static cudaError_t bwd_d(const AttnArgs &a, cudaStream_t st) {
 }
 
 // Implementation switches are read per call (a getenv is ~100 ns) so tests can cover both paths.
-// tcgen05 forward by default where it measured faster (s >= 2048: 66.8 vs 79.9 us at b=2, H=8, d=96;
-// at s=1024 the mma.sync kernel wins); MERAK_ATTN_TC=0/1 forces either.
+// tcgen05 forward (two softmax warpgroups) by default: faster than the mma.sync kernel at every measured
+// shape (68.9 vs 71.0 us at b=4, s=1024, H=25, d=64; 54.6 vs 80.8 us at b=2, s=2048, H=8, d=96);
+// MERAK_ATTN_TC=0 forces the mma.sync kernel.
 static bool use_tc(const AttnArgs &a) {
   const char *e = getenv("MERAK_ATTN_TC");
   if (e) return atoi(e) == 1;
-  return a.s >= 2048;
+  return true;
 }
 
 cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st) {

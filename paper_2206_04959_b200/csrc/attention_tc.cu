@@ -36,7 +36,8 @@ struct FaCfg {
   static constexpr int V_BYTES = NA * H_ATOM;       // MN-major: NA chunks of [64 keys][64 d-columns]
   static constexpr int STAGES = (D <= 64) ? 3 : 2;  // 4 stages no longer fit two CTAs per SM
   static constexpr int P_BYTES = TQ * 128;          // [128 q][64 keys] bf16 = one atom
-  static constexpr int SMEM = Q_BYTES + STAGES * (K_BYTES + V_BYTES) + 2 * P_BYTES + 1024 + 256;
+  static constexpr int XCH_BYTES = (2 * 2 * TQ + 2 * TQ) * 4;  // row partial max [2][2][128], row sum [2][128]
+  static constexpr int SMEM = Q_BYTES + STAGES * (K_BYTES + V_BYTES) + 2 * P_BYTES + XCH_BYTES + 1024 + 256;
   static constexpr uint32_t S_COL = 0;              // 2 x 64 fp32 columns
   static constexpr uint32_t O_COL = 128;            // D fp32 columns
   static constexpr int TMEM_COLS = (128 + D <= 256) ? 256 : 512;
@@ -61,8 +62,10 @@ MK_DEV void tmem_st16(uint32_t taddr, const uint32_t *r) {
 
 }  // namespace
 
+// 320 threads: warp 0 TMA, warp 1 TMEM + MMA, warps 2-9 softmax (thread = query row; the two warpgroups
+// split each 64-key tile's columns and exchange the row max through shared memory)
 template <int D>
-__global__ void __launch_bounds__(192, FaCfg<D>::MIN_CTAS)
+__global__ void __launch_bounds__(320, FaCfg<D>::MIN_CTAS)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmkv, AttnArgs a) {
   using C = FaCfg<D>;
   constexpr int NA = C::NA, ST = C::STAGES;
@@ -72,7 +75,9 @@ __global__ void __launch_bounds__(192, FaCfg<D>::MIN_CTAS)
   uint8_t *sK = sQ + C::Q_BYTES;                 // [ST][K_BYTES]
   uint8_t *sV = sK + ST * C::K_BYTES;            // [ST][V_BYTES]
   uint8_t *sP = sV + ST * C::V_BYTES;            // [2][P_BYTES]
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sP + 2 * C::P_BYTES);
+  float *xmax = reinterpret_cast<float *>(sP + 2 * C::P_BYTES);  // [2 (tile parity)][2 (warpgroup)][128]
+  float *xsum = xmax + 4 * TQ;                                    // [2 (warpgroup)][128]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sP + 2 * C::P_BYTES + C::XCH_BYTES);
   uint64_t *q_full = bar;
   uint64_t *kv_full = bar + 1, *kv_empty = bar + 1 + ST;
   uint64_t *s_full = bar + 1 + 2 * ST, *s_free = s_full + 2, *p_full = s_full + 4, *p_free = s_full + 6;
@@ -97,8 +102,8 @@ __global__ void __launch_bounds__(192, FaCfg<D>::MIN_CTAS)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&s_free[i], 8);
+      mbar_init(&p_full[i], 8);
       mbar_init(&p_free[i], 1);
     }
     fence_mbar_init();
@@ -170,33 +175,36 @@ __global__ void __launch_bounds__(192, FaCfg<D>::MIN_CTAS)
       }
     }
   } else {
-    // ------------------------------------------------------------ softmax (thread = row)
-    const int q = warp & 3;
+    // ------------------------------------------------------------ softmax (thread = row, half the columns)
+    const int q = warp & 3, cw = (warp - 2) >> 2;
     const int r = q * 32 + lane;
     const int qi = qt * TQ + r;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     const float sl2 = 1.4426950408889634f / sqrtf((float)D);
     const float thr = 8.0f / sl2;  // lazy rescale threshold (2^8) in raw score units
-    float m = -INFINITY, l = 0.f;
+    float m = -INFINITY, l = 0.f;  // m is identical in both warpgroups; l is this warpgroup's partial
     for (int j = 0; j < J; ++j) {
       const int b = j & 1;
       mbar_wait(&s_full[b], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t v[64];
-      tmem_ld32(lane_base + C::S_COL + b * TKH, *reinterpret_cast<uint32_t(*)[32]>(v));
-      tmem_ld32(lane_base + C::S_COL + b * TKH + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+      uint32_t v[32];
+      tmem_ld32(lane_base + C::S_COL + b * TKH + cw * 32, v);
       tmem_ld_wait();
-      const int kj0 = j * TKH;
-      const bool mask = (kj0 + TKH - 1 > qt * TQ) || (kj0 + TKH > s);
+      const int kj0 = j * TKH + cw * 32;  // this warpgroup's first key
+      const bool mask = (j * TKH + TKH - 1 > qt * TQ) || (j * TKH + TKH > s);
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent chains
 #pragma unroll
-      for (int k = 0; k < 64; ++k) {
+      for (int k = 0; k < 32; ++k) {
         const float x = __uint_as_float(v[k]);
         if (!mask || (kj0 + k <= qi && kj0 + k < s)) mx4[k & 3] = fmaxf(mx4[k & 3], x);
       }
-      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      const float pmx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      xmax[(b * 2 + cw) * TQ + r] = pmx;
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 softmax warps
+      const float mx = fmaxf(pmx, xmax[(b * 2 + (cw ^ 1)) * TQ + r]);
       // the max grew by more than 2^8: move to the new max, rescale O and l.  TMEM access is
-      // warp-collective, so the whole warp enters when any row needs it (others scale by 1).
+      // warp-collective, so the whole warp enters when any row needs it (others scale by 1); the two
+      // warpgroups rescale alternate 16-column chunks of O.
       const bool need = mx > m + thr;
       if (__any_sync(0xffffffffu, need)) {
         const float corr = need ? fast_exp2((m - mx) * sl2) : 1.f;
@@ -206,6 +214,7 @@ __global__ void __launch_bounds__(192, FaCfg<D>::MIN_CTAS)
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < D / 16; ++c) {
+            if ((c & 1) != cw) continue;
             uint32_t o[16];
             tmem_ld16(lane_base + C::O_COL + c * 16, o);
             tmem_ld_wait();
@@ -226,11 +235,12 @@ __global__ void __launch_bounds__(192, FaCfg<D>::MIN_CTAS)
       float rs4[4] = {0.f, 0.f, 0.f, 0.f};
       uint8_t *prow = sP + b * C::P_BYTES + r * 128;
 #pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const int ch = cw * 4 + c4;  // 16-B chunk of the 128-B P row
         uint32_t pk[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int k = ch * 8 + u * 2;
+          const int k = c4 * 8 + u * 2;
           float p0 = fast_exp2(fmaf(__uint_as_float(v[k]), sl2, -ms));
           float p1 = fast_exp2(fmaf(__uint_as_float(v[k + 1]), sl2, -ms));
           if (mask) {
@@ -251,15 +261,20 @@ __global__ void __launch_bounds__(192, FaCfg<D>::MIN_CTAS)
         mbar_arrive(&p_full[b]);
       }
     }
+    // row sum: the two warpgroups' partials, added in a fixed order
+    xsum[cw * TQ + r] = l;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const float lt = xsum[r] + xsum[TQ + r];
     // the last P V has completed when its commit arrived on p_free
     const int last = J - 1;
     mbar_wait(&p_free[last & 1], (last >> 1) & 1);
     tc_fence_after();
     // tcgen05.ld is warp-collective (.sync.aligned): load converged, store only rows < s
-    const float inv = 1.f / l;
+    const float inv = 1.f / lt;
     __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.ctx) + (size_t)(tok0 + qi) * a.ld_ctx + head * D;
 #pragma unroll
     for (int c = 0; c < D / 16; ++c) {
+      if ((c & 1) != cw) continue;
       uint32_t o[16];
       tmem_ld16(lane_base + C::O_COL + c * 16, o);
       tmem_ld_wait();
@@ -277,7 +292,7 @@ __global__ void __launch_bounds__(192, FaCfg<D>::MIN_CTAS)
         *reinterpret_cast<uint4 *>(dst + c * 16 + 8) = u1;
       }
     }
-    if (qi < s) a.lse[((size_t)bi * H + head) * s + qi] = m * sl2 + log2f(l);
+    if (cw == 0 && qi < s) a.lse[((size_t)bi * H + head) * s + qi] = m * sl2 + log2f(lt);
   }
   tc_fence_before();
   __syncthreads();
@@ -325,7 +340,7 @@ static cudaError_t fwd_tc_d(const AttnArgs &a, cudaStream_t st) {
       !make_qkv_map(&mkv, a.qkv, a.b * a.s, 3 * a.heads * D, TKH))
     return cudaErrorInvalidValue;
   dim3 grid(a.heads, a.b, (a.s + TQ - 1) / TQ);
-  attn_fwd_tc_kernel<D><<<grid, 192, C::SMEM, st>>>(mq, mkv, a);
+  attn_fwd_tc_kernel<D><<<grid, 320, C::SMEM, st>>>(mq, mkv, a);
   return cudaGetLastError();
 }
 

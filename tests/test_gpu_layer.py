@@ -67,7 +67,7 @@ def test_no_comm_flag_is_identity_at_t1():
         assert torch.equal(a[k], b[k]), k
 
 
-@pytest.mark.parametrize("env", [{"MERAK_STREAMS": "1"}, {"MERAK_GEMM_DYN": "1"}, {"MERAK_ATTN_TC": "1"},
+@pytest.mark.parametrize("env", [{"MERAK_STREAMS": "1"}, {"MERAK_GEMM_DYN": "1"}, {"MERAK_ATTN_TC": "0"},
                                  {"MERAK_ATTN_BWD_TC": "0"}])
 def test_schedule_and_kernel_switches(env, monkeypatch):
     """Env-selected variants of the product path.  Schedule-only switches (single compute stream, dynamic
