@@ -65,3 +65,18 @@ def test_null_handle_calls(lib):
     assert lib.merak_tmp_saved_bytes(None) == 0
     assert lib.merak_tmp_destroy(None) == 0
     assert lib.merak_tmp_launch_count(None) == 0
+    assert lib.merak_tmp_join(None, None) == -1
+
+
+def test_null_handle_measurement_hooks(lib):
+    """The measurement / diagnostics hooks reject a NULL handle without touching the device."""
+    i32 = ctypes.c_int32
+    out = (i32 * 21)()
+    assert lib.merak_tmp_debug_state(None, out) == -1
+    assert lib.merak_tmp_debug_host(None, out) == -1
+    t = ctypes.c_float()
+    assert lib.merak_tmp_bench_allreduce(None, 0, 16, 1, ctypes.byref(t)) == -1
+    n = i32()
+    assert lib.merak_tmp_get_timeline(None, 0, ctypes.byref(n), None, None, None, None) == -1
+    assert lib.merak_tmp_set_profiling(None, 1) == -1
+    assert lib.merak_tmp_get_profile(None, None, None, None) == -1
