@@ -93,7 +93,12 @@ enum { MERAK_BF16 = 0, MERAK_FP32_CHECK = 1 };      /* merak_tmp_config.precisio
  * tmp_rank of a T-way group on its own (no peers, no callback needed); every all-reduce reads only
  * the local partial, as with MERAK_FLAG_NO_COMM.  Used to time per-rank compute of T = 8 shapes
  * on one GPU (SURVEY §8(d) "TMP=8" projection).  Results are NOT the layer's. */
-enum { MERAK_COMM_PEER = 0, MERAK_COMM_NCCL = 1, MERAK_COMM_LOCAL = 2 };
+/* MERAK_COMM_INPROC: the T ranks of the group are T handles of ONE process on ONE device, created
+ * together by merak_tmp_init_group; every all-reduce reads the peers' partials straight from their
+ * slots (same context, no CUDA IPC), with the same handshake, kernels and arithmetic as MERAK_COMM_PEER.
+ * It exists so that T > 1 runs of the method (P:107 partial sums over T ranks, P:571 sub-batch overlap)
+ * can be checked against the oracle on a single GPU.  Not for throughput (the ranks share one GPU). */
+enum { MERAK_COMM_PEER = 0, MERAK_COMM_NCCL = 1, MERAK_COMM_LOCAL = 2, MERAK_COMM_INPROC = 3 };
 
 /* flags for layer_fwd / layer_bwd */
 enum {
@@ -142,6 +147,16 @@ typedef struct {
  * On success *out owns everything; release with merak_tmp_destroy. */
 merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, void *ag_ctx,
                             merak_tmp_t **out);
+
+/* Create all T = cfg->tmp_degree ranks of a TMP group as handles of this process on cfg->device
+ * (MERAK_COMM_INPROC above; cfg->comm must be MERAK_COMM_PEER or MERAK_COMM_INPROC, cfg->tmp_rank is
+ * ignored).  out[0..T-1] (host array of T handles) receives rank 0..T-1; same validation and errors as
+ * merak_tmp_init; on failure no handle is left allocated.  The layer calls of the ranks never block the
+ * host, so one host thread may issue rank 0's call, then rank 1's, ...; every rank must issue the same
+ * sequence of collective calls.  merak_tmp_destroy of a member synchronises the device (all ranks' work),
+ * so destroy members only after every rank has issued its last call; merak_tmp_bench_allreduce blocks the
+ * calling thread and is therefore not usable from a single thread in this mode. */
+merak_status merak_tmp_init_group(const merak_tmp_config *cfg, merak_tmp_t **out);
 
 /* Change the number of sub-microbatches.  Requires B % n_sub == 0 (EINDIVISIBLE) and no
  * open chain (ESTATE).  Takes effect for the next layer_fwd/layer_bwd; all ranks must agree. */

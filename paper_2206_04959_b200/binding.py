@@ -19,7 +19,7 @@ MERAK_ECUDA, MERAK_EPEER, MERAK_ENOMEM, MERAK_ETIMEOUT, MERAK_ESTATE = -4, -5, -
 STATUS_NAMES = {0: "OK", -1: "EINVAL", -2: "EINDIVISIBLE", -3: "EUNSUPPORTED", -4: "ECUDA", -5: "EPEER",
                 -6: "ENOMEM", -7: "ETIMEOUT", -8: "ESTATE"}
 MERAK_BF16, MERAK_FP32_CHECK = 0, 1
-MERAK_COMM_PEER, MERAK_COMM_NCCL, MERAK_COMM_LOCAL = 0, 1, 2
+MERAK_COMM_PEER, MERAK_COMM_NCCL, MERAK_COMM_LOCAL, MERAK_COMM_INPROC = 0, 1, 2, 3
 FLAG_CHAIN, FLAG_NO_COMM = 1, 2
 KERNEL_CLASSES = ("gemm", "attn_fwd", "attn_bwd", "layernorm", "allreduce", "reduce")
 PARAM_NAMES = ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_o", "b_o", "ln2_g", "ln2_b", "w_1", "b_1", "w_2", "b_2")
@@ -61,6 +61,8 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         P, I32, U32, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint32, ctypes.c_size_t
         L.merak_tmp_init.argtypes = [ctypes.POINTER(Config), ALLGATHER_FN, P, ctypes.POINTER(P)]
+        L.merak_tmp_init_group.argtypes = [ctypes.POINTER(Config), ctypes.POINTER(P)]
+        L.merak_tmp_init_group.restype = ctypes.c_int
         L.merak_tmp_set_subbatches.argtypes = [P, I32]
         L.merak_tmp_saved_bytes.argtypes = [P]
         L.merak_tmp_saved_bytes.restype = SZ
@@ -194,6 +196,34 @@ class TmpLayer:
             raise MerakError(st, L.merak_tmp_last_error(None).decode())
         self.h = h
 
+    @classmethod
+    def group(cls, hidden, heads, seq_len, microbatch, tmp_degree, n_sub=2, ffn_hidden=0, ln_eps=1e-5, comm_ctas=0,
+              device=None, precision=MERAK_BF16):
+        """All T ranks of a TMP group as handles of this process on ONE device (merak_tmp_init_group,
+        MERAK_COMM_INPROC): rank r's all-reduces read the other ranks' partials straight from their slots.
+        Returns [rank 0, ..., rank T-1].  Issue every collective call on every rank (in any order from
+        one thread: the layer calls never block the host)."""
+        L = lib()
+        if device is None:
+            device = torch.cuda.current_device()
+        dev = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        cfg = Config(hidden, heads, seq_len, microbatch, tmp_degree, 0, n_sub, ffn_hidden, ln_eps, precision,
+                     MERAK_COMM_INPROC, comm_ctas, dev.index or 0)
+        hs = (ctypes.c_void_p * tmp_degree)()
+        st = L.merak_tmp_init_group(ctypes.byref(cfg), hs)
+        if st != MERAK_OK:
+            raise MerakError(st, L.merak_tmp_last_error(None).decode())
+        out = []
+        for r in range(tmp_degree):
+            o = cls.__new__(cls)
+            o.device = dev
+            o.cfg = Config(hidden, heads, seq_len, microbatch, tmp_degree, r, n_sub, ffn_hidden, ln_eps, precision,
+                           MERAK_COMM_INPROC, comm_ctas, dev.index or 0)
+            o._cb = ALLGATHER_FN(0)
+            o.h = ctypes.c_void_p(hs[r])
+            out.append(o)
+        return out
+
     # -- helpers
     def _check(self, st):
         if st != MERAK_OK:
@@ -281,8 +311,10 @@ class TmpLayer:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().merak_tmp_destroy(self.h)
-            self.h = None
+            h, self.h = self.h, None
+            st = lib().merak_tmp_destroy(h)
+            if st != MERAK_OK:
+                raise MerakError(st, lib().merak_tmp_last_error(None).decode())
 
     def __del__(self):
         try:

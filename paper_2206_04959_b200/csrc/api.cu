@@ -128,6 +128,8 @@ struct merak_tmp {
   // fp32 check mode (MERAK_FP32_CHECK): fp32 workspace
   bool f32 = false;
   bool local = false;  // MERAK_COMM_LOCAL: single-process emulation of one rank, no peers
+  bool broken = false;  // a layer call failed after advancing the handshake epoch: peers are out of step
+  bool inproc = false;  // MERAK_COMM_INPROC: the T ranks are handles of one process on one device (init_group)
   int *tile_ctr = nullptr;  // dynamic GEMM tile counters, one per compute stream (cs, cs1); MERAK_GEMM_DYN=1
   char *ws32 = nullptr;
   float *dz32 = nullptr, *dx1_32 = nullptr, *dctx32 = nullptr, *dqkv32 = nullptr, *delta32 = nullptr, *du32 = nullptr;
@@ -346,7 +348,7 @@ static merak_status check_async_error(merak_tmp_t *h) {
   return MERAK_OK;
 }
 
-static merak_status enter(merak_tmp_t *h, cudaStream_t st) {
+static merak_status enter(merak_tmp_t *h, cudaStream_t st, bool fwd) {
   TRY(check_async_error(h));
   CK(h, cudaSetDevice(h->dev));
   CK(h, cudaEventRecord(h->ev_entry, st));
@@ -360,6 +362,11 @@ static merak_status enter(merak_tmp_t *h, cudaStream_t st) {
   if (h->have_wg) {
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_wo, 0));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_red, 0));
+    // a forward rewrites saved activations (u, ctx, x1, u2, z, g) that the previous backward's weight
+    // gradients on cw read; the caller may pass the same `saved` buffer again (e.g. a gradient-
+    // accumulation loop chained across microbatches), so every writer waits for the filler stream
+    if (fwd)
+      for (cudaStream_t c : {h->cs, h->cs1, h->ms}) CK(h, cudaStreamWaitEvent(c, h->ev_cw_end, 0));
   }
   return MERAK_OK;
 }
@@ -395,7 +402,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
   const SavedLayout L = saved_layout(h);
   const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr;
   const bool comm = !(flags & MERAK_FLAG_NO_COMM) && !h->local;
-  TRY(enter(h, st));
+  TRY(enter(h, st, true));
   auto S = [&](size_t off) { return saved + off; };
   // ---- attention block, sub-batch j: LN1 -> QKV -> attention -> proj (partial into slot 0) -> AR#1
   for (int j = 0; j < n; ++j) {
@@ -509,7 +516,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
   const SavedLayout L = saved_layout(h);
   const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr;
   const bool comm = !(flags & MERAK_FLAG_NO_COMM) && !h->local;
-  TRY(enter(h, st));
+  TRY(enter(h, st, false));
   auto S = [&](size_t off) { return saved + off; };
   // W2 / b2 grads need only dy and the saved g: they can fill from the start of the backward
   if (h->chain_open)
@@ -697,7 +704,7 @@ static merak_status layer_fwd_f32(merak_tmp_t *h, const merak_tmp_weights *w, co
   const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr;
   const bool comm = !(flags & MERAK_FLAG_NO_COMM) && !h->local;
   cudaStream_t c = h->cs;
-  TRY(enter(h, st));
+  TRY(enter(h, st, true));
   auto S = [&](size_t off) { return reinterpret_cast<float *>(saved + off); };
   for (int j = 0; j < n; ++j) {  // attention block
     if (h->chain_open) CK(h, cudaStreamWaitEvent(c, h->prev_out[j], 0));
@@ -763,7 +770,7 @@ static merak_status layer_bwd_f32(merak_tmp_t *h, const merak_tmp_weights *w, co
   const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr, M = h->M;
   const bool comm = !(flags & MERAK_FLAG_NO_COMM) && !h->local;
   cudaStream_t c = h->cs;
-  TRY(enter(h, st));
+  TRY(enter(h, st, false));
   auto S = [&](size_t off) { return reinterpret_cast<float *>(saved + off); };
   auto chain = [&](const float *X, int ld, int cols, float *out) -> merak_status {
     Launch Lk(h, MERAK_K_REDUCE, c, 0.0);
@@ -846,7 +853,8 @@ static merak_status validate(const merak_tmp_config *c) {
   if (c->tmp_rank < 0 || c->tmp_rank >= c->tmp_degree) return fail(nullptr, MERAK_EINVAL, "tmp_rank out of range");
   if (c->precision != MERAK_BF16 && c->precision != MERAK_FP32_CHECK)
     return fail(nullptr, MERAK_EINVAL, "bad precision");
-  if (c->comm != MERAK_COMM_PEER && c->comm != MERAK_COMM_NCCL && c->comm != MERAK_COMM_LOCAL)
+  if (c->comm != MERAK_COMM_PEER && c->comm != MERAK_COMM_NCCL && c->comm != MERAK_COMM_LOCAL &&
+      c->comm != MERAK_COMM_INPROC)
     return fail(nullptr, MERAK_EINVAL, "bad comm");
   const int T = c->tmp_degree, f = c->ffn_hidden ? c->ffn_hidden : 4 * c->hidden;
   if (c->hidden % c->heads) return fail(nullptr, MERAK_EINDIVISIBLE, "hidden %% heads != 0");
@@ -870,7 +878,7 @@ static void release(merak_tmp_t *h) {
   for (cudaStream_t c : {h->cs, h->cs1, h->cw, h->cr, h->ms})
     if (c) cudaStreamSynchronize(c);
   for (int q = 0; q < MAX_T; ++q)
-    if (h->peer_pv[q] && h->peer_pv[q] != h->pv) cudaIpcCloseMemHandle(h->peer_pv[q]);
+    if (!h->inproc && h->peer_pv[q] && h->peer_pv[q] != h->pv) cudaIpcCloseMemHandle(h->peer_pv[q]);
   if (h->nccl) g_nccl.CommDestroy(h->nccl);
   if (h->pv) cudaFree(h->pv);
   if (h->ws) cudaFree(h->ws);
@@ -905,12 +913,8 @@ static merak_status sync_all(merak_tmp_t *h) {
 
 extern "C" {
 
-merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, void *ag_ctx, merak_tmp_t **out) {
-  if (!out) return fail(nullptr, MERAK_EINVAL, "out is NULL");
-  *out = nullptr;
-  TRY(validate(cfg));
-  if (cfg->tmp_degree > 1 && !ag && cfg->comm != MERAK_COMM_LOCAL)
-    return fail(nullptr, MERAK_EINVAL, "tmp_degree > 1 needs an allgather callback");
+// Everything a handle owns that does not involve its peers: streams, events, slots, workspace.
+static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out) {
   merak_tmp_t *h = new merak_tmp();
   h->cfg = *cfg;
   h->h = cfg->hidden; h->H = cfg->heads; h->s = cfg->seq_len; h->B = cfg->microbatch;
@@ -929,6 +933,7 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   if (const char *t = getenv("MERAK_AR_TIMEOUT_MS")) h->timeout_ns = (uint64_t)atoll(t) * 1000000ull;
   h->f32 = cfg->precision == MERAK_FP32_CHECK;
   h->local = cfg->comm == MERAK_COMM_LOCAL;
+  h->inproc = cfg->comm == MERAK_COMM_INPROC;
   h->two_shot = h->T >= 4 && !h->f32;
   if (const char *t = getenv("MERAK_AR_PDL")) h->pdl = atoi(t) == 1;
   h->gemm_smem_kb = h->T > 1 ? 160 : 192;
@@ -1019,6 +1024,34 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   CKI(cudaDeviceSynchronize());
   for (int q = 0; q < MAX_T; ++q) h->peer_pv[q] = nullptr;
   h->peer_pv[h->r] = h->pv;
+#undef CKI
+  *out = h;
+  return MERAK_OK;
+}
+
+merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, void *ag_ctx, merak_tmp_t **out) {
+  if (!out) return fail(nullptr, MERAK_EINVAL, "out is NULL");
+  *out = nullptr;
+  TRY(validate(cfg));
+  if (cfg->comm == MERAK_COMM_INPROC)
+    return fail(nullptr, MERAK_EINVAL, "MERAK_COMM_INPROC handles are created by merak_tmp_init_group");
+  if (cfg->tmp_degree > 1 && !ag && cfg->comm != MERAK_COMM_LOCAL)
+    return fail(nullptr, MERAK_EINVAL, "tmp_degree > 1 needs an allgather callback");
+  merak_tmp_t *h = nullptr;
+  TRY(create_local(cfg, &h));
+  auto bail = [&](merak_status st) {
+    g_init_err = h->err;
+    release(h);
+    return st;
+  };
+#define CKI(call)                                                                                          \
+  do {                                                                                                     \
+    cudaError_t _e = (call);                                                                               \
+    if (_e != cudaSuccess) {                                                                               \
+      fail(h, _e == cudaErrorMemoryAllocation ? MERAK_ENOMEM : MERAK_ECUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+      return bail(_e == cudaErrorMemoryAllocation ? MERAK_ENOMEM : MERAK_ECUDA);                          \
+    }                                                                                                      \
+  } while (0)
   if (h->T > 1 && !h->local) {
     cudaIpcMemHandle_t mine;
     CKI(cudaIpcGetMemHandle(&mine, h->pv));
@@ -1071,6 +1104,34 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   return MERAK_OK;
 }
 
+merak_status merak_tmp_init_group(const merak_tmp_config *cfg, merak_tmp_t **out) {
+  if (!out) return fail(nullptr, MERAK_EINVAL, "out is NULL");
+  TRY(validate(cfg));
+  if (cfg->comm != MERAK_COMM_PEER && cfg->comm != MERAK_COMM_INPROC)
+    return fail(nullptr, MERAK_EUNSUPPORTED, "init_group: comm must be MERAK_COMM_PEER or MERAK_COMM_INPROC");
+  const int T = cfg->tmp_degree;
+  for (int q = 0; q < T; ++q) out[q] = nullptr;
+  for (int q = 0; q < T; ++q) {
+    merak_tmp_config c = *cfg;
+    c.tmp_rank = q;
+    c.comm = MERAK_COMM_INPROC;
+    merak_status st = create_local(&c, &out[q]);
+    if (st != MERAK_OK) {
+      const std::string e = g_init_err;
+      for (int p = 0; p < q; ++p) {
+        release(out[p]);
+        out[p] = nullptr;
+      }
+      g_init_err = e;
+      return st;
+    }
+  }
+  // every rank maps every peer's peer-visible buffer directly: same process, same device, same context
+  for (int q = 0; q < T; ++q)
+    for (int p = 0; p < T; ++p) out[q]->peer_pv[p] = out[p]->pv;
+  return MERAK_OK;
+}
+
 merak_status merak_tmp_set_subbatches(merak_tmp_t *h, int32_t n_sub) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
   if (h->chain_open) return fail(h, MERAK_ESTATE, "set_subbatches while a MERAK_FLAG_CHAIN sequence is open");
@@ -1098,8 +1159,12 @@ merak_status merak_tmp_layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, con
   const void *ps[] = {w->ln1_g, w->ln1_b, w->w_qkv, w->b_qkv, w->w_o, w->b_o, w->ln2_g, w->ln2_b, w->w_1, w->b_1, w->w_2, w->b_2, x, y, saved};
   for (const void *p : ps)
     if (!p || !aligned16(p)) return fail(h, MERAK_EINVAL, "NULL or non-16B-aligned pointer");
-  if (h->f32) return layer_fwd_f32(h, w, (const float *)x, (float *)y, (char *)saved, flags, (cudaStream_t)st);
-  return layer_fwd(h, w, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st);
+  if (h->broken) return fail(h, MERAK_ESTATE, "handle unusable after an earlier failure: %s", h->err.c_str());
+  const uint32_t e0 = h->epoch;
+  const merak_status s = h->f32 ? layer_fwd_f32(h, w, (const float *)x, (float *)y, (char *)saved, flags, (cudaStream_t)st)
+                                : layer_fwd(h, w, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st);
+  if (s != MERAK_OK && (h->epoch != e0 || s == MERAK_ETIMEOUT)) h->broken = true;
+  return s;
 }
 
 merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const void *x, const void *saved,
@@ -1111,11 +1176,15 @@ merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, con
                       g->ln2_g, g->ln2_b, g->w_1, g->b_1, g->w_2, g->b_2};
   for (const void *p : ps)
     if (!p || !aligned16(p)) return fail(h, MERAK_EINVAL, "NULL or non-16B-aligned pointer");
-  if (h->f32)
-    return layer_bwd_f32(h, w, (const float *)x, (const char *)saved, (const float *)dy, (float *)dx, g, flags,
+  if (h->broken) return fail(h, MERAK_ESTATE, "handle unusable after an earlier failure: %s", h->err.c_str());
+  const uint32_t e0 = h->epoch;
+  const merak_status s =
+      h->f32 ? layer_bwd_f32(h, w, (const float *)x, (const char *)saved, (const float *)dy, (float *)dx, g, flags,
+                             (cudaStream_t)st)
+             : layer_bwd(h, w, (const bf16 *)x, (const char *)saved, (const bf16 *)dy, (bf16 *)dx, g, flags,
                          (cudaStream_t)st);
-  return layer_bwd(h, w, (const bf16 *)x, (const char *)saved, (const bf16 *)dy, (bf16 *)dx, g, flags,
-                   (cudaStream_t)st);
+  if (s != MERAK_OK && (h->epoch != e0 || s == MERAK_ETIMEOUT)) h->broken = true;
+  return s;
 }
 
 merak_status merak_tmp_join(merak_tmp_t *h, void *st) {
@@ -1124,19 +1193,31 @@ merak_status merak_tmp_join(merak_tmp_t *h, void *st) {
   TRY(wait_all(h, (cudaStream_t)st));
   for (int j = 0; j < h->n; ++j) CK(h, cudaStreamWaitEvent((cudaStream_t)st, h->prev_out[j], 0));
   h->chain_open = false;
-  return MERAK_OK;
+  return check_async_error(h);  // a watchdog that already fired (the word is host-mapped; no sync here)
 }
 
 merak_status merak_tmp_destroy(merak_tmp_t *h) {
-  if (h && h->T > 1 && !h->nccl && !h->local && h->ms) {
+  if (h && h->inproc) {
+    // every rank of the group has enqueued its collective calls (they never block the host), so the
+    // shared device drains: no rank frees its slots while a peer's all-reduce may still read them
+    cudaSetDevice(h->dev);
+    cudaDeviceSynchronize();
+  } else if (h && h->T > 1 && !h->nccl && !h->local && h->ms) {
     // final barrier: no rank frees its slots while a peer's last all-reduce may still read them
     cudaSetDevice(h->dev);
     PeerSync ps = make_sync(h, true);
     peer_ready(ps, h->ms);
     cudaStreamSynchronize(h->ms);
   }
+  if (!h) return MERAK_OK;
+  for (cudaStream_t c : {h->cs, h->cs1, h->cw, h->cr, h->ms})
+    if (c) cudaStreamSynchronize(c);
+  // the watchdog word after every stream drained: a handshake that timed out in the last calls
+  // (after which those calls' outputs are garbage) is reported here rather than lost
+  const merak_status st = check_async_error(h);
+  if (st != MERAK_OK) g_init_err = h->err;
   release(h);
-  return MERAK_OK;
+  return st;
 }
 
 const char *merak_tmp_last_error(const merak_tmp_t *h) { return h ? h->err.c_str() : g_init_err.c_str(); }
@@ -1249,6 +1330,11 @@ merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t ro
   do {
     if (cudaMalloc(&stats, 2 * (size_t)rows * 4) != cudaSuccess) { st = fail(h, MERAK_ENOMEM, "stats"); break; }
     mean = stats; rstd = stats + rows;
+    {
+      // no rank zeroes its slot while a peer's earlier all-reduce may still be reading it
+      PeerSync ps0 = make_sync(h, true);
+      if ((st = sync_peers(h, ps0)) != MERAK_OK) break;
+    }
     if (cudaMemsetAsync(tmp, 0, 3 * nb + 4 * hh * 4, h->ms) != cudaSuccess ||
         cudaMemsetAsync(stats, 0, 2 * (size_t)rows * 4, h->ms) != cudaSuccess ||
         cudaMemsetAsync(h->pv + h->slot_bytes, 0, nb, h->ms) != cudaSuccess) {
@@ -1336,7 +1422,7 @@ int merak_test_attn_bwd_dbg(const void *qkv, const void *ctx, const float *lse, 
   memset(&a, 0, sizeof(a));
   a.qkv = qkv; a.ctx = (void *)ctx; a.lse = (float *)lse; a.dctx = dctx; a.dqkv = dqkv; a.delta = delta;
   a.b = b; a.s = s; a.heads = heads; a.d = d; a.ld_ctx = heads * d; a.dbg = dbg;
-  return (int)attn_bwd_tc(a, (cudaStream_t)stream);
+  return (int)attn_bwd(a, (cudaStream_t)stream);
 }
 
 int merak_test_ln_fwd(const void *x, const void *gamma, const void *beta, void *u, float *mean, float *rstd, int m,

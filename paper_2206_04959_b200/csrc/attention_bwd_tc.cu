@@ -570,11 +570,12 @@ template <int D>
 static cudaError_t bwd_tc_d(const AttnArgs &a, cudaStream_t st) {
   using C = BwdCfg<D>;
   constexpr int SMEM = C::DQ_SMEM > C::DKV_SMEM ? C::DQ_SMEM : C::DKV_SMEM;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[MAX_DEV] = {};
+  const int dev = cur_device();
+  if (!attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[dev] = true;
   }
   const int tokens = a.b * a.s, hr = a.heads * D;
   CUtensorMap mq_full, mq_half, mo_full, mo_half;
@@ -591,7 +592,7 @@ static cudaError_t bwd_tc_d(const AttnArgs &a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t attn_bwd_tc(const AttnArgs &a, cudaStream_t st) {
+cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st) {
   switch (a.d) {
     case 32: return bwd_tc_d<32>(a, st);
     case 64: return bwd_tc_d<64>(a, st);

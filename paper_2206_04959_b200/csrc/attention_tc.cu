@@ -329,11 +329,12 @@ static bool make_qkv_map(CUtensorMap *m, const void *qkv, int tokens, int cols, 
 template <int D>
 static cudaError_t fwd_tc_d(const AttnArgs &a, cudaStream_t st) {
   using C = FaCfg<D>;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[MAX_DEV] = {};
+  const int dev = cur_device();
+  if (!attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[dev] = true;
   }
   CUtensorMap mq, mkv;
   if (!make_qkv_map(&mq, a.qkv, a.b * a.s, 3 * a.heads * D, TQ) ||
@@ -344,7 +345,7 @@ static cudaError_t fwd_tc_d(const AttnArgs &a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t attn_fwd_tc(const AttnArgs &a, cudaStream_t st) {
+cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st) {
   switch (a.d) {
     case 32: return fwd_tc_d<32>(a, st);
     case 64: return fwd_tc_d<64>(a, st);

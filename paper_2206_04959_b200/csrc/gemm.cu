@@ -539,13 +539,10 @@ struct Maps {
 };
 
 int gemm_num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
+  static int n[MAX_DEV] = {};
+  const int dev = cur_device();
+  if (!n[dev]) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+  return n[dev];
 }
 
 template <int CG, int BN, bool A_MN, bool B_MN, int EPI, int SMEM_KB = (CG == 2 ? 160 : 192)>
@@ -553,11 +550,12 @@ static cudaError_t launch(const GemmArgs &a, const Maps &mp, const EpiParams &p,
                           cudaStream_t st) {
   using C = GemmCfg<CG, BN, SMEM_KB>;
   auto kern = gemm_kernel<CG, BN, A_MN, B_MN, EPI, SMEM_KB>;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[MAX_DEV] = {};
+  const int dev = cur_device();
+  if (!attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr[dev] = true;
   }
   const int ntiles = ((a.M + BM * CG - 1) / (BM * CG)) * ((a.N + BN - 1) / BN);
   int clusters = (a.max_ctas > 0 ? a.max_ctas : gemm_num_sms()) / CG;

@@ -18,6 +18,15 @@ namespace mk {
 // 16-wide MMA steps inside; it never depends on M (bit-identity across sub-batch counts).
 constexpr int MAX_T = 8;  // max TMP degree
 
+// Function attributes (max dynamic smem) and occupancy are per device: host-side caches of them are
+// indexed by the current device ordinal, so handles on several devices in one process stay correct.
+constexpr int MAX_DEV = 64;
+inline int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d >= 0 && d < MAX_DEV ? d : MAX_DEV - 1;
+}
+
 enum Epi : int {
   EPI_STORE_BF16 = 0,  // out = bf16(acc)
   EPI_BIAS_BF16 = 1,   // out = bf16(acc + bias[n])
@@ -53,9 +62,10 @@ struct GemmArgs {
 cudaError_t gemm(const GemmArgs &a, cudaStream_t st);
 int gemm_num_sms();
 
-// ---------------------------------------------------------------- attention (attention.cu)
+// ---------------------------------------------------------------- attention (attention_tc.cu, attention_bwd_tc.cu)
 // Causal flash attention over packed qkv [tokens, 3*hr] (q | k | v column blocks, head e at
 // columns e*d..e*d+d-1 of each block), b samples of s tokens, H_r local heads of dim d.
+// tcgen05/TMEM/TMA kernels only (no alternate backend).
 struct AttnArgs {
   const void *qkv;   // bf16 [b*s, 3*hr]
   void *ctx;         // bf16 [b*s, hr]          (fwd out / bwd in as O)
@@ -65,12 +75,10 @@ struct AttnArgs {
   float *delta;      // [b, H_r, s] rowsum(dO*O) workspace (bwd)
   int b, s, heads, d;
   int ld_ctx;        // row stride of ctx (elements; >= heads*d)
-  unsigned long long *dbg;  // diagnostics only (nullptr): per-CTA clock stamps of the tcgen05 backward
+  unsigned long long *dbg;  // diagnostics only (nullptr): per-CTA clock stamps of the backward
 };
-cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st);     // tcgen05 version if MERAK_ATTN_TC=1
-cudaError_t attn_fwd_tc(const AttnArgs &a, cudaStream_t st);  // attention_tc.cu
-cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st);  // 2 launches: dQ (+delta), then dK/dV
-cudaError_t attn_bwd_tc(const AttnArgs &a, cudaStream_t st);  // attention_bwd_tc.cu (MERAK_ATTN_BWD_TC=1)
+cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st);  // attention_tc.cu
+cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st);  // attention_bwd_tc.cu: delta kernel, then dQ + dK/dV tiles
 
 // ---------------------------------------------------------------- fp32 check mode (check_f32.cu)
 struct F32GemmArgs {  // C[M,N] (epi) sum_k A(m,k) B(n,k); A(m,k) = a_mn ? A[k*lda+m] : A[m*lda+k], same for B

@@ -522,18 +522,21 @@ static int clamp_ctas(int want, int work, int resident) {
 template <int NT>
 static cudaError_t ar_fwd_t(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
   const size_t smem = a.do_ln ? (size_t)8 * a.h * 2 : 0;  // 8 warps x one bf16 row
-  static int resident = 0;
-  static size_t res_smem = ~size_t(0), attr = 0;
-  if (smem > attr) {
+  static int resident[MAX_DEV] = {};
+  static size_t res_smem[MAX_DEV], attr[MAX_DEV] = {};
+  static bool init[MAX_DEV] = {};
+  const int dev = cur_device();
+  if (smem > attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(ar_fwd_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[dev] = smem;
   }
-  if (res_smem != smem) {
-    resident = resident_ctas((const void *)ar_fwd_kernel<NT>, 256, smem);
-    res_smem = smem;
+  if (!init[dev] || res_smem[dev] != smem) {
+    resident[dev] = resident_ctas((const void *)ar_fwd_kernel<NT>, 256, smem);
+    res_smem[dev] = smem;
+    init[dev] = true;
   }
-  const int grid = clamp_ctas(a.ctas, (a.m + 7) / 8, resident);
+  const int grid = clamp_ctas(a.ctas, (a.m + 7) / 8, resident[dev]);
   return launch_k(ar_fwd_kernel<NT>, dim3(grid), dim3(256), smem, st, a.pdl, a, ps);
 }
 cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
@@ -550,9 +553,10 @@ int ar_bwd_group_rows(int h) { return 8; }
 
 template <int NT>
 static cudaError_t ar_rs_t(const ArRsArgs &a, cudaStream_t st) {
-  static int resident = 0;
-  if (!resident) resident = resident_ctas((const void *)ar_rs_kernel<NT>, 256, 0);
-  const int grid = clamp_ctas(a.ctas, (a.row1 - a.row0 + 7) / 8, resident);
+  static int resident[MAX_DEV] = {};
+  const int dev = cur_device();
+  if (!resident[dev]) resident[dev] = resident_ctas((const void *)ar_rs_kernel<NT>, 256, 0);
+  const int grid = clamp_ctas(a.ctas, (a.row1 - a.row0 + 7) / 8, resident[dev]);
   return launch_k(ar_rs_kernel<NT>, dim3(grid), dim3(256), 0, st, a.pdl, a);
 }
 cudaError_t ar_rs(const ArRsArgs &a, cudaStream_t st) {
@@ -571,20 +575,21 @@ static cudaError_t ar_bwd_t(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t
   constexpr int G = 8;
   // du fp32 rows, plus (STASH) the x_ln and dres bf16 rows so the later passes read smem, not HBM
   const size_t smem = (size_t)G * a.h * (sizeof(float) + (STASH ? 4 : 0));
-  static size_t attr = 0;
-  if (smem > attr) {
+  static size_t attr[MAX_DEV] = {};
+  const int dev = cur_device();
+  if (smem > attr[dev]) {
     cudaError_t e =
         cudaFuncSetAttribute(ar_bwd_kernel<G, NT, STASH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[dev] = smem;
   }
-  static int resident = 0;
-  static size_t res_smem = 0;
-  if (!resident || res_smem != smem) {
-    resident = resident_ctas((const void *)ar_bwd_kernel<G, NT, STASH>, 256, smem);
-    res_smem = smem;
+  static int resident[MAX_DEV] = {};
+  static size_t res_smem[MAX_DEV] = {};
+  if (!resident[dev] || res_smem[dev] != smem) {
+    resident[dev] = resident_ctas((const void *)ar_bwd_kernel<G, NT, STASH>, 256, smem);
+    res_smem[dev] = smem;
   }
-  const int grid = clamp_ctas(a.ctas, a.m / G, resident);
+  const int grid = clamp_ctas(a.ctas, a.m / G, resident[dev]);
   return launch_k(ar_bwd_kernel<G, NT, STASH>, dim3(grid), dim3(256), smem, st, a.pdl, a, ps);
 }
 cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
@@ -605,11 +610,12 @@ cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
 cudaError_t ln_fwd(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bfloat16 *b, __nv_bfloat16 *u,
                    int ld_u, float *mean, float *rstd, int m, int h, float eps, const OnesPad &pad, cudaStream_t st) {
   const size_t smem = (size_t)8 * h * 2;
-  static size_t attr = 0;
-  if (smem > attr) {
+  static size_t attr[MAX_DEV] = {};
+  const int dev = cur_device();
+  if (smem > attr[dev]) {
     cudaError_t e = cudaFuncSetAttribute(ln_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[dev] = smem;
   }
   ln_fwd_kernel<<<(m + 7) / 8, 256, smem, st>>>(x, g, b, u, ld_u, mean, rstd, m, h, eps, pad);
   return cudaGetLastError();

@@ -106,3 +106,54 @@ def oracle_chain(params_list, x, dy, heads):
     for k in reversed(range(len(params_list))):
         g, grads[k] = layer_backward(params_list[k], caches[k], g, heads)
     return y, g, grads
+
+
+def run_gpu_group(cfg, params, x, dy, T, n_sub=None, precision=0, flags=0, chain_params=None, chain=True):
+    """The T ranks of a TMP group as handles of this process on one GPU (merak_tmp_init_group,
+    MERAK_COMM_INPROC): each rank holds its own weight shard and outputs, every all-reduce sums the T
+    ranks' partials through the peer kernels.  Each rank issues its calls on its own caller stream (a
+    shared caller stream would serialise rank r+1 behind rank r's join, while rank r's all-reduce waits
+    for rank r+1).  chain_params: list of per-layer params -> K chained layers (MERAK_FLAG_CHAIN on every
+    call but the last backward; chain=False: no chaining), else one layer with `params`.
+    Returns [per-rank dict]: y, dx and the rank's gradient shards (grads[k] per layer when chained)."""
+    from paper_2206_04959_b200 import FLAG_CHAIN
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n = cfg.n_sub if n_sub is None else n_sub
+    ranks = TmpLayer.group(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, T, n_sub=n, device=dev.index,
+                           precision=precision)
+    dt = torch.float32 if precision == 1 else torch.bfloat16
+    plist = chain_params if chain_params is not None else [params]
+    K = len(plist)
+    ws = [[shard_weights(p, cfg.heads, T, r, dev, dtype=dt) for p in plist] for r in range(T)]
+    M, h = cfg.tokens, cfg.hidden
+    X = torch.as_tensor(np.asarray(x).reshape(M, h)).to(dev, dt)
+    DY = torch.as_tensor(np.asarray(dy).reshape(M, h)).to(dev, dt)
+    Ys = [[torch.empty_like(X) for _ in range(K)] for _ in range(T)]
+    DXs = [[torch.empty_like(X) for _ in range(K)] for _ in range(T)]
+    grads = [[zero_grads_like(w) for w in ws[r]] for r in range(T)]
+    saved = [[ranks[r].new_saved() for _ in range(K)] for r in range(T)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(T)]
+    for s in streams:
+        s.wait_stream(torch.cuda.current_stream())
+    cf = FLAG_CHAIN if chain_params is not None and chain else 0
+    for k in range(K):
+        for r in range(T):
+            ranks[r].forward(ws[r][k], X if k == 0 else Ys[r][k - 1], Ys[r][k], saved[r][k], flags=flags | cf,
+                             stream=streams[r])
+    for k in reversed(range(K)):
+        for r in range(T):
+            ranks[r].backward(ws[r][k], X if k == 0 else Ys[r][k - 1], saved[r][k],
+                              DY if k == K - 1 else DXs[r][k + 1], DXs[r][k], grads[r][k],
+                              flags=flags | (cf if k > 0 else 0), stream=streams[r])
+    torch.cuda.synchronize()
+    outs = []
+    for r in range(T):
+        o = {"y": Ys[r][K - 1].clone(), "dx": DXs[r][0].clone()}
+        if chain_params is None:
+            o.update({k: grads[r][0][k].clone() for k in PARAM_NAMES})
+        else:
+            o["grads"] = [{k: g[k].clone() for k in PARAM_NAMES} for g in grads[r]]
+        outs.append(o)
+    for lay in ranks:
+        lay.close()
+    return outs

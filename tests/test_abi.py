@@ -80,3 +80,25 @@ def test_null_handle_measurement_hooks(lib):
     assert lib.merak_tmp_get_timeline(None, 0, ctypes.byref(n), None, None, None, None) == -1
     assert lib.merak_tmp_set_profiling(None, 1) == -1
     assert lib.merak_tmp_get_profile(None, None, None, None) == -1
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(hidden=0), -1), (dict(microbatch=3, n_sub=2), -2), (dict(heads=2, tmp_degree=4), -2),
+    (dict(hidden=96, heads=2), -3), (dict(comm=1, tmp_degree=2), -3), (dict(comm=2, tmp_degree=2), -3),
+])
+def test_init_group_validation(lib, kw, status):
+    """merak_tmp_init_group (in-process TMP group) validates like merak_tmp_init and leaves no handle."""
+    T = kw.get("tmp_degree", 2)
+    kw = dict(kw, tmp_degree=T)
+    hs = (ctypes.c_void_p * T)()
+    st = lib.merak_tmp_init_group(ctypes.byref(_cfg(**kw)), hs)
+    assert st == status, (kw, st, lib.merak_tmp_last_error(None))
+    assert all(not v for v in hs)
+
+
+def test_init_rejects_inproc_comm(lib):
+    """MERAK_COMM_INPROC handles come only from merak_tmp_init_group."""
+    from paper_2206_04959_b200.binding import ALLGATHER_FN
+    h = ctypes.c_void_p()
+    st = lib.merak_tmp_init(ctypes.byref(_cfg(comm=3, tmp_degree=2)), ALLGATHER_FN(0), None, ctypes.byref(h))
+    assert st == -1 and not h.value

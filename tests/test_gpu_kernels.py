@@ -164,13 +164,10 @@ def attn_ref(qkv, b, s, H, d):
     return o.permute(0, 2, 1, 3).reshape(b * s, hr)
 
 
-@pytest.mark.parametrize("impl", ["mma_sync", "tcgen05"])
 @pytest.mark.parametrize("b,s,H,d", [(2, 16, 2, 32), (2, 100, 3, 64), (1, 256, 2, 80), (2, 1024, 2, 96),
-                                     (1, 192, 2, 128), (4, 1024, 4, 64), (2, 208, 5, 64)])
-def test_attention_fwd_bwd(b, s, H, d, impl, monkeypatch):
-    # the forward and backward switches are read per launch (csrc/attention.cu use_tc / use_bwd_tc)
-    monkeypatch.setenv("MERAK_ATTN_TC", "1" if impl == "tcgen05" else "0")
-    monkeypatch.setenv("MERAK_ATTN_BWD_TC", "1" if impl == "tcgen05" else "0")
+                                     (1, 192, 2, 128), (4, 1024, 4, 64), (2, 208, 5, 64), (1, 2048, 2, 96),
+                                     (3, 144, 3, 128), (2, 272, 2, 32)])
+def test_attention_fwd_bwd(b, s, H, d):
     g = torch.Generator(device="cuda").manual_seed(s * d + H)
     hr = H * d
     qkv = torch.randn(b * s, 3 * hr, device="cuda", generator=g).bfloat16()

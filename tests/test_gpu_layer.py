@@ -67,26 +67,18 @@ def test_no_comm_flag_is_identity_at_t1():
         assert torch.equal(a[k], b[k]), k
 
 
-@pytest.mark.parametrize("env", [{"MERAK_STREAMS": "1"}, {"MERAK_GEMM_DYN": "1"}, {"MERAK_ATTN_TC": "0"},
-                                 {"MERAK_ATTN_BWD_TC": "0"}])
-def test_schedule_and_kernel_switches(env, monkeypatch):
-    """Env-selected variants of the product path.  Schedule-only switches (single compute stream, dynamic
-    GEMM tile order) must be bit-identical to the default; kernel switches (attention implementations)
-    must stay within the bf16 tolerance of the oracle."""
-    from gpu_layer_util import compare_to_oracle, oracle_rank_slices
+@pytest.mark.parametrize("env", [{"MERAK_STREAMS": "1"}, {"MERAK_GEMM_DYN": "1"}])
+def test_schedule_switches(env, monkeypatch):
+    """Env-selected schedules of the product path (single compute stream, dynamic GEMM tile order) run the
+    same kernels in another order: bit-identical to the default."""
     cfg = TINY.with_(hidden=256, heads=4, seq_len=128, microbatch=4, n_sub=2, tmp_degree=1)
     params, x, dy = make_all(cfg, seed=81)
     ref = run_gpu_layer(cfg, params, x, dy)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     out = run_gpu_layer(cfg, params, x, dy)
-    if "MERAK_STREAMS" in env or "MERAK_GEMM_DYN" in env:
-        for k in ref:
-            assert torch.equal(ref[k], out[k]), k
-    else:
-        y, dx, g = layer_fwd_bwd(params, x, dy, cfg.heads)
-        errs, bad = compare_to_oracle(out, y, dx, oracle_rank_slices(g, cfg, 1, 0), cfg)
-        assert not bad, bad
+    for k in ref:
+        assert torch.equal(ref[k], out[k]), k
 
 
 def test_full_size_gpt15b_t1():

@@ -213,13 +213,14 @@ def test_head_partition():
         head_partition(2, 4)
 
 
-@pytest.mark.parametrize("T,n", [(1, 1), (2, 1), (2, 2), (4, 2), (3, 4)])
-def test_invariant_sharded_equals_unsharded(T, n):
+@pytest.mark.parametrize("T,n,h,H", [(1, 1, 80, 5), (2, 1, 80, 5), (2, 2, 80, 5), (4, 2, 80, 5), (3, 4, 96, 6),
+                                     (4, 4, 96, 6), (3, 2, 120, 5)])
+def test_invariant_sharded_equals_unsharded(T, n, h, H):
     """(1) sum of row-parallel partials over ranks == unsharded layer, incl. uneven head
-    splits (H=5); (2) sub-batching leaves outputs and grads unchanged."""
-    cfg = TINY.with_(hidden=80, heads=5, seq_len=12, microbatch=4)
-    if cfg.ffn % T:
-        pytest.skip("f % T")
+    splits (H=5 at T=2: 3/2, T=4: 2/1/1/1; H=6 at T=4: 2/2/1/1; H=5 at T=3: 2/2/1);
+    (2) sub-batching leaves outputs and grads unchanged."""
+    cfg = TINY.with_(hidden=h, heads=H, seq_len=12, microbatch=4)
+    assert cfg.ffn % T == 0 and cfg.hidden % cfg.heads == 0
     params, x, dy = make_all(cfg, seed=99)
     y, dx, g = layer_fwd_bwd(params, x, dy, cfg.heads)
     ys, dxs, gs, _ = sharded_fwd_bwd(params, x, dy, cfg.heads, T, n)
@@ -252,3 +253,24 @@ def test_shard_params_layout():
     assert np.array_equal(s["w_qkv"][32:64], params["w_qkv"][h + 48:h + 80])
     assert np.array_equal(s["w_o"], params["w_o"][:, 48:80])
     assert np.array_equal(s["w_1"], params["w_1"][160:320])
+
+
+def test_layer_flops_pin():
+    """oracle.layer_flops against an independent tally: every GEMM of the layer enumerated by its
+    (M, N, K) (forward QKV / proj / fc1 / fc2, each also as dgrad and wgrad in the backward), and the
+    causal attention products counted pair by pair (key j <= query i, diagonal included, reading R4):
+    QK^T and PV forward, dV, dP, dQ, dK backward, d multiply-adds each.  Also the closed form
+    72 B s h^2 + 6 B h s (s+1) at the BASELINE shapes (the per-GPU values SURVEY §8 tabulates x T)."""
+    from oracle import layer_flops
+    for (B, s, h, H) in [(2, 16, 64, 2), (3, 20, 96, 6), (1, 33, 80, 5)]:
+        f, M, d = 4 * h, B * s, h // H
+        fwd = [(M, 3 * h, h), (M, h, h), (M, f, h), (M, h, f)]
+        gemm = sum(2 * m * nn * k for (m, nn, k) in fwd) * 3  # fwd + dgrad + wgrad: same M*N*K each
+        pairs = sum(1 for i in range(s) for j in range(s) if j <= i)
+        attn = 2 * d * pairs * (2 + 4) * H * B
+        assert layer_flops(B, s, h, H) == gemm + attn, (B, s, h, H)
+    for (B, s, h, H, T, per_gpu_tf) in [(8, 1024, 1600, 25, 2, 0.795), (8, 1024, 2560, 32, 4, 0.999),
+                                        (8, 1024, 3072, 32, 8, 0.715), (4, 2048, 6144, 64, 8, 2.861)]:
+        closed = 72.0 * B * s * h * h + 6.0 * B * h * s * (s + 1)
+        assert layer_flops(B, s, h, H) == closed
+        assert abs(closed / T / 1e12 - per_gpu_tf) < 6e-4, (h, closed / T / 1e12)
