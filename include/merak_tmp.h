@@ -155,7 +155,10 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
  * host, so one host thread may issue rank 0's call, then rank 1's, ...; every rank must issue the same
  * sequence of collective calls.  merak_tmp_destroy of a member synchronises the device (all ranks' work),
  * so destroy members only after every rank has issued its last call; merak_tmp_bench_allreduce blocks the
- * calling thread and is therefore not usable from a single thread in this mode. */
+ * calling thread and is therefore not usable from a single thread in this mode.  The ranks' internal
+ * streams share one context: set CUDA_DEVICE_MAX_CONNECTIONS=32 before CUDA initialises, so that no
+ * rank's compute stream shares a hardware queue with (and waits behind) another rank's spinning handshake;
+ * at T = 8 each member runs all non-communication kernels on one stream to stay within 32 queues. */
 merak_status merak_tmp_init_group(const merak_tmp_config *cfg, merak_tmp_t **out);
 
 /* Change the number of sub-microbatches.  Requires B % n_sub == 0 (EINDIVISIBLE) and no

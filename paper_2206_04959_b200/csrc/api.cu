@@ -900,9 +900,9 @@ static void release(merak_tmp_t *h) {
   }
   if (h->cs1 && h->cs1 != h->cs) cudaStreamDestroy(h->cs1);
   if (h->cw && h->cw != h->cs) cudaStreamDestroy(h->cw);
+  if (h->cr && h->cr != h->cs) cudaStreamDestroy(h->cr);
   if (h->cs) cudaStreamDestroy(h->cs);
   if (h->ms) cudaStreamDestroy(h->ms);
-  if (h->cr) cudaStreamDestroy(h->cr);
   delete h;
 }
 
@@ -961,13 +961,19 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
   CKI(cudaStreamCreateWithPriority(&h->cs, cudaStreamNonBlocking, prio_mid));
   CKI(cudaStreamCreateWithPriority(&h->ms, cudaStreamNonBlocking, prio_hi));  // comm first when both ready
   const char *ns = getenv("MERAK_STREAMS");
-  if (ns && atoi(ns) == 1) {
+  // In-process groups put T ranks' streams in one context.  Streams beyond CUDA_DEVICE_MAX_CONNECTIONS (<= 32)
+  // share hardware queues, and a rank's compute queued behind another rank's spinning handshake deadlocks
+  // until the watchdog fires; at T = 8 each rank therefore runs everything but the all-reduces on one stream.
+  if ((ns && atoi(ns) == 1) || (h->inproc && h->T >= 8)) {
     h->cs1 = h->cw = h->cs;
   } else {
     CKI(cudaStreamCreateWithPriority(&h->cs1, cudaStreamNonBlocking, prio_mid));
     CKI(cudaStreamCreateWithPriority(&h->cw, cudaStreamNonBlocking, prio_lo));
   }
-  CKI(cudaStreamCreateWithPriority(&h->cr, cudaStreamNonBlocking, prio_mid));
+  if (h->inproc && h->T >= 8)
+    h->cr = h->cs;
+  else
+    CKI(cudaStreamCreateWithPriority(&h->cr, cudaStreamNonBlocking, prio_mid));
   for (cudaEvent_t *e : {&h->ev_entry, &h->ev_cs_end, &h->ev_cs1_end, &h->ev_cw_end, &h->ev_cr_end, &h->ev_w1,
                          &h->ev_wo, &h->ev_wqkv, &h->ev_red})
     CKI(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -1021,6 +1027,10 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
     h->dz32 = (float *)(h->ws32 + a); h->dx1_32 = (float *)(h->ws32 + b); h->dctx32 = (float *)(h->ws32 + c);
     h->dqkv32 = (float *)(h->ws32 + d); h->delta32 = (float *)(h->ws32 + e); h->du32 = (float *)(h->ws32 + f);
   }
+  // load every kernel this handle can launch now, not at a first launch inside a layer call (kernels.h)
+  CKI(h->f32 ? f32_preload() : gemm_preload());
+  if (!h->f32) CKI(attn_preload(h->d));
+  CKI(ln_ar_preload());
   CKI(cudaDeviceSynchronize());
   for (int q = 0; q < MAX_T; ++q) h->peer_pv[q] = nullptr;
   h->peer_pv[h->r] = h->pv;

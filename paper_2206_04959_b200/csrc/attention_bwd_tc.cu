@@ -603,4 +603,21 @@ cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st) {
   return cudaErrorNotSupported;
 }
 
+template <int D>
+static cudaError_t bwd_preload() {
+  cudaError_t e = touch_kernel((const void *)attn_delta_kernel<D>);
+  return e != cudaSuccess ? e : touch_kernel((const void *)attn_bwd_tc_kernel<D>);
+}
+
+cudaError_t attn_bwd_preload_d(int d) {
+  switch (d) {
+    case 32: return bwd_preload<32>();
+    case 64: return bwd_preload<64>();
+    case 80: return bwd_preload<80>();
+    case 96: return bwd_preload<96>();
+    case 128: return bwd_preload<128>();
+  }
+  return cudaErrorNotSupported;
+}
+
 }  // namespace mk

@@ -356,4 +356,21 @@ cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st) {
   return cudaErrorNotSupported;
 }
 
+template <int D>
+cudaError_t attn_preload_d() {
+  cudaError_t e = touch_kernel((const void *)attn_fwd_tc_kernel<D>);
+  return e != cudaSuccess ? e : attn_bwd_preload_d(D);
+}
+
+cudaError_t attn_preload(int d) {
+  switch (d) {
+    case 32: return attn_preload_d<32>();
+    case 64: return attn_preload_d<64>();
+    case 80: return attn_preload_d<80>();
+    case 96: return attn_preload_d<96>();
+    case 128: return attn_preload_d<128>();
+  }
+  return cudaErrorNotSupported;
+}
+
 }  // namespace mk

@@ -355,4 +355,16 @@ cudaError_t f32_ln_grad_chain(const float *du, const float *xln, const float *me
   return cudaGetLastError();
 }
 
+cudaError_t f32_preload() {
+  const void *ks[] = {(const void *)f32_gemm_kernel, (const void *)f32_ln_kernel, (const void *)f32_attn_fwd_kernel,
+                      (const void *)f32_attn_dq_kernel, (const void *)f32_attn_dkdv_kernel,
+                      (const void *)f32_ar_fwd_kernel, (const void *)f32_ar_bwd_kernel,
+                      (const void *)f32_colsum_chain_kernel, (const void *)f32_ln_grad_chain_kernel};
+  for (const void *k : ks) {
+    cudaError_t e = touch_kernel(k);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace mk

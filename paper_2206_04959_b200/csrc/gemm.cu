@@ -629,6 +629,34 @@ static int gemm_cg() {
   return cg;
 }
 
+template <int CG, int BN, int KB>
+static cudaError_t preload_cfg() {
+  const void *ks[] = {
+      (const void *)gemm_kernel<CG, BN, false, false, EPI_STORE_BF16, KB>,
+      (const void *)gemm_kernel<CG, BN, false, false, EPI_BIAS_BF16, KB>,
+      (const void *)gemm_kernel<CG, BN, false, false, EPI_BIAS_GELU, KB>,
+      (const void *)gemm_kernel<CG, BN, false, true, EPI_STORE_BF16, KB>,
+      (const void *)gemm_kernel<CG, BN, false, true, EPI_GELU_BWD, KB>,
+      (const void *)gemm_kernel<CG, BN, true, true, EPI_ACC_F32, KB>};
+  for (const void *k : ks) {
+    cudaError_t e = touch_kernel(k);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t gemm_preload() {
+  cudaError_t e;
+  if ((e = preload_cfg<2, 256, 160>()) != cudaSuccess) return e;
+  if ((e = preload_cfg<2, 192, 160>()) != cudaSuccess) return e;
+  if ((e = preload_cfg<2, 128, 160>()) != cudaSuccess) return e;
+  if ((e = preload_cfg<2, 256, 192>()) != cudaSuccess) return e;
+  if ((e = preload_cfg<2, 192, 192>()) != cudaSuccess) return e;
+  if ((e = preload_cfg<2, 128, 192>()) != cudaSuccess) return e;
+  if ((e = preload_cfg<1, 256, 192>()) != cudaSuccess) return e;
+  return preload_cfg<1, 128, 192>();
+}
+
 cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return cudaErrorInvalidValue;
   const int cg = gemm_cg();

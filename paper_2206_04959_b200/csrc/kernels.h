@@ -27,6 +27,21 @@ inline int cur_device() {
   return d >= 0 && d < MAX_DEV ? d : MAX_DEV - 1;
 }
 
+// Module preloading.  With CUDA's lazy loading a kernel's first launch loads it, and a load may need a
+// context-wide synchronisation; if another stream of this context is then running a handshake kernel that
+// waits for a peer whose work this host thread has not enqueued yet (an in-process group), the two block
+// each other.  Every handle therefore loads each kernel it can launch at init (cudaFuncGetAttributes forces
+// the load), so no layer call ever loads a module.
+inline cudaError_t touch_kernel(const void *f) {
+  cudaFuncAttributes at;
+  return cudaFuncGetAttributes(&at, f);
+}
+cudaError_t gemm_preload();
+cudaError_t attn_preload(int d);
+cudaError_t attn_bwd_preload_d(int d);
+cudaError_t ln_ar_preload();
+cudaError_t f32_preload();
+
 enum Epi : int {
   EPI_STORE_BF16 = 0,  // out = bf16(acc)
   EPI_BIAS_BF16 = 1,   // out = bf16(acc + bias[n])

@@ -638,4 +638,29 @@ cudaError_t sample_reduce2(const float *p0, const float *p1, int gps, int b, int
   return cudaGetLastError();
 }
 
+template <int NT>
+static cudaError_t ar_preload_t() {
+  const void *ks[] = {(const void *)ar_fwd_kernel<NT>, (const void *)ar_rs_kernel<NT>,
+                      (const void *)ar_bwd_kernel<8, NT, false>, (const void *)ar_bwd_kernel<8, NT, true>};
+  for (const void *k : ks) {
+    cudaError_t e = touch_kernel(k);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t ln_ar_preload() {
+  const void *ks[] = {(const void *)peer_ready_kernel, (const void *)ln_fwd_kernel, (const void *)colsum_sample_kernel,
+                      (const void *)sample_sum_kernel, (const void *)sample_chain_kernel};
+  for (const void *k : ks) {
+    cudaError_t e = touch_kernel(k);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e;
+  if ((e = ar_preload_t<1>()) != cudaSuccess) return e;
+  if ((e = ar_preload_t<2>()) != cudaSuccess) return e;
+  if ((e = ar_preload_t<4>()) != cudaSuccess) return e;
+  return ar_preload_t<8>();
+}
+
 }  // namespace mk
