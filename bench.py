@@ -4,15 +4,16 @@
 python bench.py --gpus N --steps K --warmup W            (N > 1: launched by torchrun, one rank per GPU)
 python bench.py --impl reference ...                      (the fp64 CPU oracle as the reference arm)
 
-One step = forward + backward of a stack of K (default 4) chained layers with distinct weights (every
-SURVEY §8(a) row: LN1, QKV, attention, proj, AR#1 + LN2, fc1 + GeLU, fc2, AR#2, and the backward
-mirror with AR#3/AR#4 and all weight gradients), so the all-reduce of one layer overlaps the next
-layer's first sub-batch, over one microbatch of the BASELINE.json configs[1] workload
-(GPT-1.5B-shaped layer: h=1600, H=25, s=1024, B=8) with the TMP degree T = N (rank r holds shard r;
-strong scaling: the model is fixed).
-Inputs are synthetic (synth/), resident in HBM; L2 is flushed (256 MiB write) between timed steps,
-outside the timed events.  value = whole-job algorithmic TFLOP/s of the layer ((72Bsh^2 +
-6Bhs(s+1)) x K FLOPs per step / device time, max over ranks).  Rank 0 prints ONE JSON line.
+One step = forward + backward of a stack of L (default 4) chained layers with distinct weights (every
+SURVEY §8(a) row: LN1, QKV, attention, proj, AR#1 + LN2, fc1 + GeLU, fc2, AR#2, and the backward mirror
+with AR#3 / AR#4 and all weight gradients), so the all-reduce of one layer overlaps the next layer's first
+sub-batch, over one microbatch of the headline workload: the GPT-20B-shaped layer of
+BASELINE.json configs[4] (h=6144, H=64, s=2048, B=4, n=2 sub-batches), the largest configuration, which
+fits one GPU at T = 1.  The TMP degree is T = N (rank r holds shard r; strong scaling, the model is fixed).
+Inputs are synthetic (synth/, seeded), resident in HBM; the per-step working set (weights, gradients,
+saved activations: > 10 GB at T = 1) is far larger than the 126 MB L2, so no flush is needed.
+value = algorithmic TFLOP/s PER GPU of the layer ((72Bsh^2 + 6Bhs(s+1)) x L FLOPs per step / N / device
+time, max over ranks), as BASELINE.json's metric states.  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -33,18 +34,21 @@ def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--layers", type=int, default=4, help="K chained layers per step (distinct weights)")
+    ap.add_argument("--layers", type=int, default=4, help="L chained layers per step (distinct weights)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="merak", choices=["merak", "reference"])
-    ap.add_argument("--config", default="gpt1.5b")
+    ap.add_argument("--config", default="gpt20b")
     ap.add_argument("--n-sub", type=int, default=None)
     ap.add_argument("--comm-ctas", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extras", action="store_true", help="skip the n=1 / no-comm / e2e passes")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the n=1 / no-comm / e2e / side-workload / profiling passes")
     return ap.parse_args()
 
 
 def layer_flops(cfg):
+    """Algorithmic fwd+bwd FLOPs of one unsharded layer: 72 B s h^2 (GEMMs, f = 4h) + 6 B h s (s+1)
+    (causal attention) -- DESIGN.md §5, pinned in tests/test_oracle_pins.py::test_layer_flops_pin."""
     B, s, h = cfg.microbatch, cfg.seq_len, cfg.hidden
     f = cfg.ffn
     return 6.0 * B * s * (4 * h * h + 2 * f * h) + 6.0 * B * h * s * (s + 1)
@@ -60,8 +64,7 @@ def measured_peaks():
 
 class ClockSampler:
     """SM clock, power and clock-event (throttle) reasons sampled every ~5 ms through NVML from a
-    background thread while the timed region runs (nvidia-smi -lms needs ~0.5 s to emit its first line,
-    longer than a short timed region)."""
+    background thread while the timed region runs."""
 
     def __init__(self, index):
         self.index = index
@@ -74,7 +77,6 @@ class ClockSampler:
         try:
             import pynvml
             pynvml.nvmlInit()
-            # NVML enumerates every GPU; map the CUDA index through the visible-device order
             vis = os.environ.get("CUDA_VISIBLE_DEVICES")
             idx = int(vis.split(",")[self.index]) if vis and vis.split(",")[self.index].isdigit() else self.index
             h = pynvml.nvmlDeviceGetHandleByIndex(idx)
@@ -125,77 +127,114 @@ def _use_host_cores():
         pass
 
 
-def cpu_oracle_sample(cfg, target_s=12.0):
-    """Time the fp64 oracle (as it stands) on a bounded sample of the workload: b samples of the same
-    layer shape (fwd+bwd), growing b until ~target_s of CPU work.  Returns the cpu_baseline dict."""
-    import numpy as np  # noqa: F401
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads") or 1 for i in threadpool_info()] or [1])
+    except Exception:
+        return os.cpu_count()
 
+
+def oracle_sample(cfg, tokens):
+    """The bounded oracle sample: ONE sample of the workload's layer (full h, H, weights), restricted to its
+    first `tokens` positions.  Attention is causal, so these positions' outputs do not depend on later ones:
+    the sample is exactly a prefix of the workload's computation.  Returns (seconds, FLOPs)."""
     _use_host_cores()
     from oracle import layer_flops as oflops, layer_fwd_bwd
     from synth import make_all
-    b = 1
-    while True:
-        sub = cfg.with_(microbatch=b)
-        params, x, dy = make_all(sub)
-        t0 = time.perf_counter()
-        layer_fwd_bwd(params, x, dy, sub.heads)
-        dt = time.perf_counter() - t0
-        if dt >= target_s / 2 or b >= cfg.microbatch:
-            break
-        b = min(cfg.microbatch, b * 2)
-    fl = oflops(b, sub.seq_len, sub.hidden, sub.heads)
-    try:
-        from threadpoolctl import threadpool_info
-        blas = [{"api": i.get("internal_api"), "threads": i.get("num_threads")} for i in threadpool_info()]
-        threads = max([i["threads"] or 1 for i in blas] or [1])
-    except Exception:
-        blas, threads = [], os.cpu_count()
-    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
-            "sample": f"{b} of {cfg.microbatch} samples of the {cfg.name} layer fwd+bwd in fp64 (numpy), "
-                      f"{dt:.2f} s, {fl / 1e9:.1f} GFLOP", "seconds": dt, "blas": blas,
-            "host_cores_visible": len(os.sched_getaffinity(0))}
+    sub = cfg.with_(microbatch=1, seq_len=tokens)
+    params, x, dy = make_all(sub)
+    t0 = time.perf_counter()
+    layer_fwd_bwd(params, x, dy, sub.heads)
+    dt = time.perf_counter() - t0
+    return dt, oflops(1, tokens, sub.hidden, sub.heads)
 
 
-def arm_config(cfg, K, T, n_sub):
+def cpu_oracle_baseline(cfg, tokens=512):
+    dt, fl = oracle_sample(cfg, tokens)
+    return {"value": fl / dt / 1e12, "unit": "TFLOP/s", "cores": _blas_threads(), "kind": "oracle",
+            "sample": f"1 of the {cfg.microbatch} samples of the {cfg.name} layer (h={cfg.hidden}, H={cfg.heads}), "
+                      f"its first {tokens} of {cfg.seq_len} positions (a causal prefix), fwd+bwd, unsharded, fp64 "
+                      f"numpy: {dt:.2f} s, {fl / 1e9:.0f} GFLOP",
+            "seconds": dt, "host_cores_visible": len(os.sched_getaffinity(0))}
+
+
+def arm_config(cfg, L, T, n_sub):
     """The workload both arms report (the reference arm times a bounded sample of it)."""
-    return {"workload": f"{cfg.name} layer fwd+bwd x {K} chained layers: h={cfg.hidden}, H={cfg.heads}, "
+    return {"workload": f"{cfg.name} layer fwd+bwd x {L} chained layers: h={cfg.hidden}, H={cfg.heads}, "
                         f"s={cfg.seq_len}, B={cfg.microbatch}, TMP={T}, n_sub={n_sub}",
-            "layers": K, "tmp_degree": T, "n_sub": n_sub,
-            "l2": "flushed between steps (256 MiB write, outside the timed events)"}
+            "layers": L, "tmp_degree": T, "n_sub": n_sub, "hidden": cfg.hidden, "heads": cfg.heads,
+            "seq_len": cfg.seq_len, "microbatch": cfg.microbatch,
+            "l2": "not flushed: the per-step working set (weights, fp32 grads, saved activations) is >> 126 MB L2"}
 
 
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the CPU oracle as it stands, each step a bounded sample (1 sample of the
-    workload's layer).  Rank 0 only; other ranks exit without work."""
+    """--impl reference: the CPU oracle as it stands; each step a bounded sample of the workload (one sample,
+    a causal prefix of 128 positions, full h).  Rank 0 only; other ranks exit without work."""
     if rank != 0:
         return
-    _use_host_cores()
-    from oracle import layer_flops as oflops, layer_fwd_bwd
-    from synth import make_all
-    sub = cfg.with_(microbatch=1)
-    params, x, dy = make_all(sub)
+    tokens = 128
     for _ in range(args.warmup):
-        layer_fwd_bwd(params, x, dy, sub.heads)
-    t0 = time.perf_counter()
+        oracle_sample(cfg, tokens)
+    tot, fl = 0.0, 0.0
     for _ in range(args.steps):
-        layer_fwd_bwd(params, x, dy, sub.heads)
-    dt = (time.perf_counter() - t0) / args.steps
-    fl = oflops(1, sub.seq_len, sub.hidden, sub.heads)
-    v = fl / dt / 1e12
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads") or 1 for i in threadpool_info()] or [1])
-    except Exception:
-        threads = os.cpu_count()
+        dt, f = oracle_sample(cfg, tokens)
+        tot += dt
+        fl += f
+    v = fl / tot / 1e12
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": arm_config(cfg, args.layers, world, cfg.n_sub),
-            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": arm_config(cfg, args.layers, world, cfg.n_sub),
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": _blas_threads(), "kind": "oracle",
                              "sample": f"bounded sample: each step = 1 of the {cfg.microbatch} samples of one "
-                                       f"layer fwd+bwd, unsharded, fp64 numpy (TFLOP/s of that sample)"},
+                                       f"{cfg.name} layer, its first {tokens} positions (causal prefix), fwd+bwd, "
+                                       f"unsharded, fp64 numpy"},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+class Stack:
+    """L chained layers of one rank (weights, grads, saved activations, outputs) on one TmpLayer handle."""
+
+    def __init__(self, cfg, L, T, rank, dev, group, n_sub, comm=0, comm_ctas=0, streams1=False):
+        import torch
+
+        from paper_2206_04959_b200 import TmpLayer, shard_weights, zero_grads_like
+        from synth import make_activations_torch, make_params_torch
+        self.cfg, self.L, self.T, self.dev = cfg, L, T, dev
+        self.X, self.DY = make_activations_torch(cfg, dev)
+        self.ws = [shard_weights(make_params_torch(cfg, dev, layer=k), cfg.heads, T, rank, dev) for k in range(L)]
+        self.Ys = [torch.empty_like(self.X) for _ in range(L)]
+        self.DXs = [torch.empty_like(self.X) for _ in range(L)]
+        self.grads = [zero_grads_like(w) for w in self.ws]
+        if streams1:
+            os.environ["MERAK_STREAMS"] = "1"
+        try:
+            self.layer = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, tmp_degree=T, tmp_rank=rank,
+                                  n_sub=n_sub, comm=comm, comm_ctas=comm_ctas, device=dev.index, group=group)
+        finally:
+            if streams1:
+                del os.environ["MERAK_STREAMS"]
+        self.saved = [self.layer.new_saved() for _ in range(L)]
+
+    def step(self, flags=0, X=None, DY=None):
+        """L layers forward, then backward in reverse (overlap across layers): every call but the last
+        backward passes MERAK_FLAG_CHAIN, so layer k+1's sub-batch 0 starts while layer k's last all-reduce is
+        in flight; the last backward joins the caller stream."""
+        from paper_2206_04959_b200 import FLAG_CHAIN
+        X = self.X if X is None else X
+        DY = self.DY if DY is None else DY
+        L, lay = self.L, self.layer
+        for k in range(L):
+            lay.forward(self.ws[k], X if k == 0 else self.Ys[k - 1], self.Ys[k], self.saved[k], flags=flags | FLAG_CHAIN)
+        for k in reversed(range(L)):
+            lay.backward(self.ws[k], X if k == 0 else self.Ys[k - 1], self.saved[k],
+                         DY if k == L - 1 else self.DXs[k + 1], self.DXs[k], self.grads[k],
+                         flags=flags | (FLAG_CHAIN if k > 0 else 0))
+
+    def close(self):
+        self.layer.close()
 
 
 def main():
@@ -215,7 +254,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2206_04959_b200 import FLAG_CHAIN, FLAG_NO_COMM, TmpLayer, shard_weights, zero_grads_like
+    from paper_2206_04959_b200 import FLAG_NO_COMM
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -223,125 +262,75 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
-    K = args.layers
-    from synth import make_activations, make_params
-    x, dy = make_activations(cfg)
-    ws = [shard_weights(make_params(cfg, layer=k), cfg.heads, T, rank, dev) for k in range(K)]
-    M, h = cfg.tokens, cfg.hidden
-    X = torch.as_tensor(x.reshape(M, h)).to(dev, torch.bfloat16)
-    DY = torch.as_tensor(dy.reshape(M, h)).to(dev, torch.bfloat16)
-    Ys = [torch.empty_like(X) for _ in range(K)]      # Ys[k] = output of layer k = input of layer k+1
-    DXs = [torch.empty_like(X) for _ in range(K)]     # DXs[k] = dL/d(input of layer k)
-    grads = [zero_grads_like(w) for w in ws]
-    layer = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, tmp_degree=T, tmp_rank=rank, n_sub=n_sub,
-                     comm_ctas=args.comm_ctas, device=local, group=group)
-    saved = [layer.new_saved() for _ in range(K)]
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    L = args.layers
+    stack = Stack(cfg, L, T, rank, dev, group, n_sub, comm_ctas=args.comm_ctas)
     stream = torch.cuda.current_stream()
-
-    # stall watchdog (diagnostics on stderr): if the host makes no progress for STALL_S seconds -- blocked in
-    # a synchronize or in a launch whose queue is full -- print the library's stream / watchdog state
-    import threading
-    progress = [time.time()]
-    stall_s = float(os.environ.get("MERAK_BENCH_STALL_S", "5"))
-
-    def watchdog():
-        while True:
-            time.sleep(1.0)
-            if time.time() - progress[0] > stall_s:
-                # host-only state first (cannot block), then the CUDA-side state from a helper thread
-                print(f"[rank {rank}] stalled {time.time() - progress[0]:.0f}s host: {layer.debug_host()}",
-                      file=sys.stderr, flush=True)
-                threading.Thread(target=lambda: print(f"[rank {rank}] device: {layer.debug_state()}",
-                                                      file=sys.stderr, flush=True), daemon=True).start()
-                progress[0] = time.time()
-    threading.Thread(target=watchdog, daemon=True).start()
-
-    def barrier():
-        torch.cuda.synchronize()
-        progress[0] = time.time()
-        if world > 1:
-            dist.barrier()
-        progress[0] = time.time()
-
-    def step(flags=0, x_in=None, dy_in=None, lay=None):
-        """K chained layers forward, then backward in reverse (overlap across layers): every
-        call but the last passes MERAK_FLAG_CHAIN so layer k+1's sub-batch 0 starts while layer k's
-        last all-reduce is in flight; the last backward joins the caller stream."""
-        x_in = X if x_in is None else x_in
-        dy_in = DY if dy_in is None else dy_in
-        lay = lay or layer
-        for k in range(K):
-            lay.forward(ws[k], x_in if k == 0 else Ys[k - 1], Ys[k], saved[k], flags=flags | FLAG_CHAIN)
-        for k in reversed(range(K)):
-            lay.backward(ws[k], x_in if k == 0 else Ys[k - 1], saved[k], dy_in if k == K - 1 else DXs[k + 1],
-                           DXs[k], grads[k], flags=flags | (FLAG_CHAIN if k > 0 else 0))
-
-    def timed(nsteps, flags=0, prof=False, lay=None):
-        lay = lay or layer
-        starts = [torch.cuda.Event(enable_timing=True) for _ in range(nsteps)]
-        ends = [torch.cuda.Event(enable_timing=True) for _ in range(nsteps)]
-        if prof:
-            lay.set_profiling(True)
-        l0 = lay.launch_count()
-        barrier()
-        for i in range(nsteps):
-            flush.zero_()
-            starts[i].record(stream)
-            step(flags, lay=lay)
-            ends[i].record(stream)
-            progress[0] = time.time()
-        barrier()
-        launches = lay.launch_count() - l0
-        ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-        prof_d = lay.get_profile() if prof else None
-        if prof:
-            lay.set_profiling(False)
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return t.item() / nsteps, launches, prof_d
-
     t_start = time.time()
 
     def stage(msg):  # progress markers on stderr (multi-rank runs: evidence if a run ever stalls)
-        progress[0] = time.time()
         if world > 1 or os.environ.get("MERAK_BENCH_TRACE"):
             print(f"[rank {rank} +{time.time() - t_start:.1f}s] {msg}", file=sys.stderr, flush=True)
 
-    # a stalled run dumps every Python thread's stack to stderr (diagnostics only; the run continues)
     import faulthandler
-    faulthandler.dump_traceback_later(int(os.environ.get("MERAK_BENCH_TRACE_S", "240")), exit=False)
+    faulthandler.dump_traceback_later(int(os.environ.get("MERAK_BENCH_TRACE_S", "300")), exit=False)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def timed(st, nsteps, flags=0, prof=False):
+        """nsteps back-to-back steps between one pair of CUDA events on the caller stream, bracketed by
+        synchronize + barrier; returns (max-over-ranks ms per step, kernel launches, profile)."""
+        if prof:
+            st.layer.set_profiling(True)
+        l0 = st.layer.launch_count()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        for _ in range(nsteps):
+            st.step(flags)
+        e1.record(stream)
+        barrier()
+        launches = st.layer.launch_count() - l0
+        prof_d = st.layer.get_profile() if prof else None
+        if prof:
+            st.layer.set_profiling(False)
+        return max_over_ranks(e0.elapsed_time(e1) / nsteps), launches, prof_d
 
     for _ in range(args.warmup):
-        step()
+        stack.step()
     barrier()
     stage("warmup done")
     with ClockSampler(local) as clk:
-        ms_step, launches, _ = timed(args.steps)
+        ms_step, launches, _ = timed(stack, args.steps)
     clocks = clk.summary()
     stage("timed done")
-    fl = K * layer_flops(cfg)
-    value = fl / (ms_step * 1e-3) / 1e12
+    fl = L * layer_flops(cfg)
+    value = fl / world / (ms_step * 1e-3) / 1e12  # per GPU (BASELINE.json metric)
 
     extras = {}
     if not args.no_extras:
+        nx = max(3, args.steps // 2)
         # exposed communication: same kernels with every all-reduce reading only the local partial
         if T > 1:
-            ms_nc, _, _ = timed(max(3, args.steps // 2), flags=FLAG_NO_COMM)
-            extras["exposed_allreduce_ms_per_layer"] = (ms_step - ms_nc) / K
+            ms_nc, _, _ = timed(stack, nx, flags=FLAG_NO_COMM)
+            extras["exposed_allreduce_ms_per_layer"] = (ms_step - ms_nc) / L
+            extras["exposed_allreduce_frac"] = (ms_step - ms_nc) / ms_step
             extras["no_comm_ms_per_step"] = ms_nc
             stage("no-comm done")
-        else:
-            extras["exposed_allreduce_ms_per_layer"] = 0.0
-        # all-reduce alone on the comm stream (NVLink roofline of the reduction): one sub-batch message
-        if T > 1:
             rows = cfg.tokens // n_sub
             two = (T >= 4) if os.environ.get("MERAK_AR_TWO_SHOT") is None else os.environ["MERAK_AR_TWO_SHOT"] == "1"
-            t_f = layer.bench_allreduce(0, rows, 20)
-            t_b = layer.bench_allreduce(1, rows, 20)
-            t_h = layer.bench_allreduce(0, rows // 2, 20)  # half message: marginal rate without fixed costs
-            msg = rows * h * 2
+            t_f = stack.layer.bench_allreduce(0, rows, 20)
+            t_b = stack.layer.bench_allreduce(1, rows, 20)
+            t_h = stack.layer.bench_allreduce(0, rows // 2, 20)
+            msg = rows * cfg.hidden * 2
             nvl = (2 * (T - 1) / T if two else (T - 1)) * msg  # bytes each GPU pulls from its peers per AR
             extras["allreduce"] = {"algorithm": "two-shot" if two else "one-shot", "rows": rows, "msg_bytes": msg,
                                    "nvlink_bytes_in_per_gpu": nvl, "fwd_ar_us": t_f * 1e3, "bwd_ar_us": t_b * 1e3,
@@ -349,154 +338,191 @@ def main():
                                    "frac": nvl / (t_f * 1e-3) / 900e9,
                                    "marginal_GBps": (nvl / 2) / ((t_f - t_h) * 1e-3) / 1e9 if t_f > t_h else None,
                                    "fixed_us": (2 * t_h - t_f) * 1e3,
-                                   "note": "forward AR#2 incl. handshake kernel(s); peak = NVLink 5 per direction"}
+                                   "note": "forward AR#2 alone on the comm stream incl. handshake kernel(s); "
+                                           "peak = NVLink 5 per direction"}
             stage("allreduce bench done")
+        else:
+            extras["exposed_allreduce_ms_per_layer"] = 0.0
         # n = 1 (Megatron-style, no sub-pipelining) with the same kernels: fig:ablation_pipetp analog
         if n_sub != 1:
-            layer.set_subbatches(1)
-            for _ in range(2):
-                step()
-            ms_n1, _, _ = timed(max(3, args.steps // 2))
-            layer.set_subbatches(n_sub)
+            stack.layer.set_subbatches(1)
+            stack.step()
+            ms_n1, _, _ = timed(stack, nx)
+            stack.layer.set_subbatches(n_sub)
+            stack.step()
             extras["n1_ms_per_step"] = ms_n1
             extras["subpipelining_speedup_vs_n1"] = ms_n1 / ms_step
             stage("n=1 done")
-        # e2e through the public API with host buffers, pipelined as a training input pipeline would be:
-        # every step uploads its x and dy from pinned host memory and downloads y and dx (all inside the
-        # timed region, on a copy stream), double-buffered so step i+1's upload and step i's downloads
-        # overlap compute; only the first upload and the last download are exposed.
-        # x, dy, y, dx are replicated on the T ranks: each rank moves only its 1/T row slice over PCIe and
-        # the slices are all-gathered over NVLink (NCCL) -- the way a TMP input pipeline shares one batch.
-        rows = M // world
-        r0 = rank * rows
-        hx = X[r0:r0 + rows].cpu().pin_memory()
-        hdy = DY[r0:r0 + rows].cpu().pin_memory()
-        hy = torch.empty_like(hx).pin_memory()
-        hdx = torch.empty_like(hx).pin_memory()
-        Xb, DYb = [torch.empty_like(X) for _ in range(2)], [torch.empty_like(DY) for _ in range(2)]
-
-        def upload(bi_):
-            if world == 1:
-                Xb[bi_].copy_(hx, non_blocking=True)
-                DYb[bi_].copy_(hdy, non_blocking=True)
-                return
-            Xb[bi_][r0:r0 + rows].copy_(hx, non_blocking=True)
-            DYb[bi_][r0:r0 + rows].copy_(hdy, non_blocking=True)
-            dist.all_gather_into_tensor(Xb[bi_], Xb[bi_][r0:r0 + rows])
-            dist.all_gather_into_tensor(DYb[bi_], DYb[bi_][r0:r0 + rows])
-        cp = torch.cuda.Stream(device=dev)    # uploads (H2D copy engine)
-        cpo = torch.cuda.Stream(device=dev)   # downloads (D2H copy engine)
-        ne = max(3, args.steps // 2)
-        barrier()
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
-        cp.wait_stream(stream)
-        ev_in, ev_free, ev_y, ev_dx = [None, None], [None, None], None, None
-        with torch.cuda.stream(cp):
-            upload(0)
-        ev_in[0] = cp.record_event()
-        for i in range(ne):
-            bb = i & 1
-            stream.wait_event(ev_in[bb])
-            if i + 1 < ne:  # prefetch the next step's inputs once their buffer's last use (step i-1) is done
-                if ev_free[1 - bb] is not None:
-                    cp.wait_event(ev_free[1 - bb])
-                with torch.cuda.stream(cp):
-                    upload(1 - bb)
-                ev_in[1 - bb] = cp.record_event()
-            flush.zero_()  # L2 flush between steps, counted inside the e2e time (conservative)
-            if ev_y is not None:
-                stream.wait_event(ev_y)  # the previous y download has read Ys[K-1]
-            for k in range(K):
-                # the last forward joins the caller stream, so y is complete when the copy stream reads it
-                layer.forward(ws[k], Xb[bb] if k == 0 else Ys[k - 1], Ys[k], saved[k],
-                              flags=FLAG_CHAIN if k < K - 1 else 0)
-            cpo.wait_stream(stream)
-            with torch.cuda.stream(cpo):
-                hy.copy_(Ys[K - 1][r0:r0 + rows], non_blocking=True)
-            ev_y = cpo.record_event()
-            if ev_dx is not None:
-                stream.wait_event(ev_dx)  # the previous dx download has read DXs[0]
-            for k in reversed(range(K)):
-                layer.backward(ws[k], Xb[bb] if k == 0 else Ys[k - 1], saved[k], DYb[bb] if k == K - 1 else DXs[k + 1],
-                               DXs[k], grads[k], flags=FLAG_CHAIN if k > 0 else 0)
-            ev_free[bb] = stream.record_event()
-            cpo.wait_event(ev_free[bb])
-            with torch.cuda.stream(cpo):
-                hdx.copy_(DXs[0][r0:r0 + rows], non_blocking=True)
-            ev_dx = cpo.record_event()
-            stage(f"e2e iter {i} issued")
-        stream.wait_stream(cp)
-        stream.wait_stream(cpo)
-        t1.record(stream)
-        barrier()
-        te = torch.tensor([t0.elapsed_time(t1) / ne], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        extras["e2e"] = e2e_pass(stack, nx, world, rank, dev, fl, dist, barrier, max_over_ranks)
         stage("e2e done")
-        extras["e2e"] = {"value": fl / (te.item() * 1e-3) / 1e12, "unit": "TFLOP/s",
-                         "h2d_bytes_per_step": 2 * hx.numel() * 2, "d2h_bytes_per_step": 2 * hx.numel() * 2,
-                         "ms_per_step": te.item(), "steps": ne,
-                         "note": "pinned-host x, dy up and y, dx down every step (upload and download copy streams), "
-                                 "double-buffered like an input pipeline; the L2 flush between steps is inside the "
-                                 "timed region; at T > 1 each rank moves its 1/T row slice over PCIe and the inputs "
-                                 "are all-gathered over NVLink (NCCL); bytes are per GPU"}
-
-    # roofline of the dominant kernel class (the tcgen05 GEMM), from CUDA events around every launch on
-    # its stream.  The timed run overlaps kernels of different sub-batches (and the wgrad filler), so
-    # per-launch event spans there include time shared with other kernels: the per-kernel numbers come
-    # from a profiling pass of a second handle with all compute on one stream (MERAK_STREAMS=1), the
-    # same kernels, shapes and order as the ncu launch list.
-    os.environ["MERAK_STREAMS"] = "1"
-    try:
-        layer_p = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, tmp_degree=T, tmp_rank=rank,
-                           n_sub=n_sub, comm_ctas=args.comm_ctas, device=local, group=group)
-    finally:
-        del os.environ["MERAK_STREAMS"]
-    for _ in range(2):
-        step(lay=layer_p)
-    nprof = max(3, args.steps // 2)
-    ms_serial, _, prof = timed(nprof, prof=True, lay=layer_p)
-    layer_p.close()
-    stage("profiling pass done")
-    extras["serialized_ms_per_step"] = ms_serial
-    peak_burst, peak_sust, peak_src = measured_peaks()
-    g = prof["gemm"]
-    gemm_tflops = g["flops"] / (g["ms"] * 1e-3) / 1e12 if g["ms"] > 0 else 0.0
-    traffic = None
-    tr_path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tr_path):
-        traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
-    share = {k: v["ms"] for k, v in prof.items()}
-    roofline = {"bound": "tensor", "achieved": gemm_tflops, "peak": peak_burst, "unit": "TFLOP/s",
-                "frac": gemm_tflops / peak_burst, "traffic": traffic,
-                "kernel": "tcgen05 bf16 GEMM (all 12 layer GEMMs; FLOPs 2MNK per launch / event-timed duration, "
-                          "serialized profiling pass)",
-                "peak_source": f"{peak_src} bf16_tflops (burst); sustained {peak_sust}",
-                "gemm_launches_per_step": g["launches"] / nprof, "gemm_ms_per_layer": g["ms"] / nprof / K,
-                "class_ms_per_layer": {k: v / nprof / K for k, v in share.items()},
-                "layer_frac_of_peak": value / world / peak_burst}
+        extras["roofline"], extras["serialized_ms_per_step"] = roofline_pass(cfg, L, T, rank, dev, group, n_sub, args,
+                                                                             timed, value)
+        stage("profiling pass done")
+        extras["side_workloads"] = side_workloads(args, T, rank, dev, group, timed, stack)
+        stage("side workloads done")
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded, synth/)",
-                "config": arm_config(cfg, K, T, n_sub), "flops_per_step": fl, "ms_per_layer": ms_step / K,
-                "value_per_gpu": value / world, "tokens_per_s": K * cfg.tokens / (ms_step * 1e-3),
-                "roofline": roofline, "gpu_launches": launches, "clocks": clocks}
-        line.update({k: v for k, v in extras.items() if k != "e2e"})
-        if "e2e" in extras:
-            line["e2e"] = extras["e2e"]
+                "config": arm_config(cfg, L, T, n_sub), "flops_per_step": fl, "ms_per_layer": ms_step / L,
+                "value_whole_job": value * world, "tokens_per_s": L * cfg.tokens / (ms_step * 1e-3),
+                "gpu_launches": launches, "clocks": clocks}
+        for k in ("roofline", "e2e"):
+            if k in extras:
+                line[k] = extras[k]
+        line.update({k: v for k, v in extras.items() if k not in ("roofline", "e2e")})
         if not args.no_cpu_baseline and world == 1:
-            progress[0] = time.time() + 1e9  # CPU work: not a GPU stall
-            line["cpu_baseline"] = cpu_oracle_sample(cfg)
-            progress[0] = time.time()
+            line["cpu_baseline"] = cpu_oracle_baseline(cfg)
         print(json.dumps(line), flush=True)
-    layer.close()
+    stack.close()
     faulthandler.cancel_dump_traceback_later()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def e2e_pass(stack, ne, world, rank, dev, fl, dist, barrier, max_over_ranks):
+    """The same metric through the public API with HOST buffers: every step uploads its x and dy from pinned
+    host memory and downloads y and dx (all inside the timed region, on copy streams), double-buffered as an
+    input pipeline would be.  x, dy, y, dx are replicated on the T ranks: each rank moves its 1/T row slice
+    over PCIe and the slices are all-gathered over NVLink (NCCL)."""
+    import torch
+
+    from paper_2206_04959_b200 import FLAG_CHAIN
+    X, DY, L = stack.X, stack.DY, stack.L
+    M = X.shape[0]
+    rows = M // world
+    r0 = rank * rows
+    hx = X[r0:r0 + rows].cpu().pin_memory()
+    hdy = DY[r0:r0 + rows].cpu().pin_memory()
+    hy = torch.empty_like(hx).pin_memory()
+    hdx = torch.empty_like(hx).pin_memory()
+    Xb, DYb = [torch.empty_like(X) for _ in range(2)], [torch.empty_like(DY) for _ in range(2)]
+    stream = torch.cuda.current_stream()
+
+    def upload(bi_):
+        if world == 1:
+            Xb[bi_].copy_(hx, non_blocking=True)
+            DYb[bi_].copy_(hdy, non_blocking=True)
+            return
+        Xb[bi_][r0:r0 + rows].copy_(hx, non_blocking=True)
+        DYb[bi_][r0:r0 + rows].copy_(hdy, non_blocking=True)
+        dist.all_gather_into_tensor(Xb[bi_], Xb[bi_][r0:r0 + rows])
+        dist.all_gather_into_tensor(DYb[bi_], DYb[bi_][r0:r0 + rows])
+    cp = torch.cuda.Stream(device=dev)    # uploads (H2D copy engine)
+    cpo = torch.cuda.Stream(device=dev)   # downloads (D2H copy engine)
+    lay, ws, Ys, DXs, saved, grads = stack.layer, stack.ws, stack.Ys, stack.DXs, stack.saved, stack.grads
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    cp.wait_stream(stream)
+    ev_in, ev_free, ev_y, ev_dx = [None, None], [None, None], None, None
+    with torch.cuda.stream(cp):
+        upload(0)
+    ev_in[0] = cp.record_event()
+    for i in range(ne):
+        bb = i & 1
+        stream.wait_event(ev_in[bb])
+        if i + 1 < ne:  # prefetch the next step's inputs once their buffer's last use (step i-1) is done
+            if ev_free[1 - bb] is not None:
+                cp.wait_event(ev_free[1 - bb])
+            with torch.cuda.stream(cp):
+                upload(1 - bb)
+            ev_in[1 - bb] = cp.record_event()
+        if ev_y is not None:
+            stream.wait_event(ev_y)  # the previous y download has read Ys[L-1]
+        for k in range(L):
+            # the last forward joins the caller stream, so y is complete when the copy stream reads it
+            lay.forward(ws[k], Xb[bb] if k == 0 else Ys[k - 1], Ys[k], saved[k], flags=FLAG_CHAIN if k < L - 1 else 0)
+        cpo.wait_stream(stream)
+        with torch.cuda.stream(cpo):
+            hy.copy_(Ys[L - 1][r0:r0 + rows], non_blocking=True)
+        ev_y = cpo.record_event()
+        if ev_dx is not None:
+            stream.wait_event(ev_dx)  # the previous dx download has read DXs[0]
+        for k in reversed(range(L)):
+            lay.backward(ws[k], Xb[bb] if k == 0 else Ys[k - 1], saved[k], DYb[bb] if k == L - 1 else DXs[k + 1],
+                         DXs[k], grads[k], flags=FLAG_CHAIN if k > 0 else 0)
+        ev_free[bb] = stream.record_event()
+        cpo.wait_event(ev_free[bb])
+        with torch.cuda.stream(cpo):
+            hdx.copy_(DXs[0][r0:r0 + rows], non_blocking=True)
+        ev_dx = cpo.record_event()
+    stream.wait_stream(cp)
+    stream.wait_stream(cpo)
+    t1.record(stream)
+    barrier()
+    te = max_over_ranks(t0.elapsed_time(t1) / ne)
+    return {"value": fl / world / (te * 1e-3) / 1e12, "unit": "TFLOP/s",
+            "h2d_bytes_per_step": 2 * hx.numel() * 2, "d2h_bytes_per_step": 2 * hx.numel() * 2,
+            "ms_per_step": te, "steps": ne,
+            "note": "per GPU; pinned-host x, dy up and y, dx down every step (upload and download copy streams), "
+                    "double-buffered like an input pipeline, timed with the same event structure as `value` "
+                    "(one event pair around back-to-back steps); the extra join after the last forward (y must be "
+                    "complete before its download) is the only schedule difference; at T > 1 each rank moves its "
+                    "1/T row slice over PCIe and the inputs are all-gathered over NVLink (NCCL); bytes are per GPU"}
+
+
+def roofline_pass(cfg, L, T, rank, dev, group, n_sub, args, timed, value):
+    """Roofline of the dominant kernel class (the tcgen05 GEMM): algorithmic FLOPs (2MNK per launch) over the
+    CUDA-event durations of every GEMM launch, recorded on the stream that launches it.  The timed run overlaps
+    kernels of different sub-batches (and the wgrad filler), so per-launch spans there include time shared with
+    other kernels: this pass uses a second handle with all compute on one stream (MERAK_STREAMS=1): the same
+    kernels, shapes and order as the ncu launch list."""
+    st = Stack(cfg, L, T, rank, dev, group, n_sub, comm_ctas=args.comm_ctas, streams1=True)
+    for _ in range(2):
+        st.step()
+    nprof = max(3, args.steps // 4)
+    ms_serial, _, prof = timed(st, nprof, prof=True)
+    st.close()
+    peak_burst, peak_sust, peak_src = measured_peaks()
+    g = prof["gemm"]
+    gemm_tflops = g["flops"] / (g["ms"] * 1e-3) / 1e12 if g["ms"] > 0 else 0.0
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", f"gemm_traffic_{cfg.name}_T{T}.json")
+    if os.path.exists(tr_path):
+        traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
+    share = {k: v["ms"] / nprof / L for k, v in prof.items()}
+    attn = {k: prof[k]["flops"] / (prof[k]["ms"] * 1e-3) / 1e12 if prof[k]["ms"] > 0 else None
+            for k in ("attn_fwd", "attn_bwd")}
+    return ({"bound": "tensor", "achieved": gemm_tflops, "peak": peak_burst, "unit": "TFLOP/s",
+             "frac": gemm_tflops / peak_burst, "traffic": traffic,
+             "kernel": "tcgen05 bf16 GEMM (all 12 layer GEMMs; FLOPs 2MNK per launch / event-timed duration, "
+                       "serialized profiling pass)",
+             "peak_source": f"{peak_src} bf16_tflops (burst); sustained {peak_sust}",
+             "gemm_launches_per_step": g["launches"] / nprof, "gemm_ms_per_layer": g["ms"] / nprof / L,
+             "class_ms_per_layer": share,
+             "class_share_of_kernel_time": {k: v / max(sum(share.values()), 1e-9) for k, v in share.items()},
+             "attention_tflops": attn,
+             "layer_frac_of_peak": value / peak_burst}, ms_serial)
+
+
+def side_workloads(args, T, rank, dev, group, timed, main_stack):
+    """Extra measured keys: the gpt1.5b stack at the same T = N, and (N = 1 only) the per-rank compute of the
+    TMP = 8 shards of gpt8.3b and gpt20b (MERAK_COMM_LOCAL: one process runs rank 0 of an 8-way group; every
+    all-reduce reads the local partial, so this is per-GPU compute only, not the layer's result)."""
+    from paper_2206_04959_b200 import MERAK_COMM_LOCAL
+    from synth import CONFIGS
+    out = {}
+    nx = max(3, args.steps // 2)
+    jobs = []
+    if args.config != "gpt1.5b":
+        jobs.append(("gpt1.5b", CONFIGS["gpt1.5b"].with_(tmp_degree=T), T, 0))
+    if T == 1:
+        jobs.append(("gpt8.3b_T8_rank_shard", CONFIGS["gpt8.3b"], 8, MERAK_COMM_LOCAL))
+        jobs.append(("gpt20b_T8_rank_shard", CONFIGS["gpt20b"], 8, MERAK_COMM_LOCAL))
+    for name, c, tt, comm in jobs:
+        st = Stack(c, args.layers, tt, 0 if comm else rank, dev, None if comm else group, c.n_sub, comm=comm)
+        for _ in range(3):
+            st.step()
+        ms, _, _ = timed(st, nx)
+        st.close()
+        fl = args.layers * layer_flops(c) / tt
+        out[name] = {"tflops_per_gpu": fl / (ms * 1e-3) / 1e12, "ms_per_step": ms, "ms_per_layer": ms / args.layers,
+                     "tmp_degree": tt, "n_sub": c.n_sub, "layers": args.layers,
+                     "mode": "per-rank compute only (MERAK_COMM_LOCAL)" if comm else f"full layer at T={tt}"}
+    return out
 
 
 if __name__ == "__main__":

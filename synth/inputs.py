@@ -134,3 +134,44 @@ def make_all(cfg: LayerConfig, seed: int = SEED) -> tuple:
     """(params, x, dy) for one layer."""
     x, dy = make_activations(cfg, seed)
     return make_params(cfg, seed), x, dy
+
+
+def make_params_torch(cfg: LayerConfig, device, seed: int = SEED, layer: int = 0) -> dict:
+    """Same shapes and value distributions as make_params, drawn with torch's
+    seeded device generator and RNE-rounded to bf16 on the device: used by bench.py, whose full-size
+    weights (0.9 GB per gpt20b layer) numpy's Philox would take ~20 s per layer to draw.  The values are
+    NOT those of make_params (different generator); parity tests use make_params."""
+    import torch
+
+    h, f = cfg.hidden, cfg.ffn
+    base = 100 * (layer + 1)
+    gen = torch.Generator(device=device)
+
+    def normal(idx, shape, std):
+        gen.manual_seed(seed + base + idx)
+        return (torch.randn(shape, generator=gen, device=device) * std).to(torch.bfloat16)
+
+    def uniform(idx, shape, lo, hi):
+        gen.manual_seed(seed + base + idx)
+        return (torch.rand(shape, generator=gen, device=device) * (hi - lo) + lo).to(torch.bfloat16)
+
+    return {
+        "ln1_g": uniform(0, (h,), 0.5, 1.5), "ln1_b": normal(1, (h,), 0.1),
+        "w_qkv": normal(2, (3 * h, h), 0.02), "b_qkv": normal(3, (3 * h,), 0.02),
+        "w_o": normal(4, (h, h), 0.02), "b_o": normal(5, (h,), 0.02),
+        "ln2_g": uniform(6, (h,), 0.5, 1.5), "ln2_b": normal(7, (h,), 0.1),
+        "w_1": normal(8, (f, h), 0.02), "b_1": normal(9, (f,), 0.02),
+        "w_2": normal(10, (h, f), 0.02), "b_2": normal(11, (h,), 0.02),
+    }
+
+
+def make_activations_torch(cfg: LayerConfig, device, seed: int = SEED) -> tuple:
+    """x, dy ~ N(0, 1) as [B*s, h] bf16 device tensors (bench.py; see make_params_torch)."""
+    import torch
+
+    gen = torch.Generator(device=device)
+    out = []
+    for idx in (10, 11):
+        gen.manual_seed(seed + idx)
+        out.append(torch.randn((cfg.tokens, cfg.hidden), generator=gen, device=device).to(torch.bfloat16))
+    return tuple(out)
