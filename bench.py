@@ -135,6 +135,9 @@ def _blas_threads():
         return os.cpu_count()
 
 
+_SAMPLES = {}
+
+
 def oracle_sample(cfg, tokens):
     """The bounded oracle sample: ONE sample of the workload's layer (full h, H, weights), restricted to its
     first `tokens` positions.  Attention is causal, so these positions' outputs do not depend on later ones:
@@ -143,7 +146,10 @@ def oracle_sample(cfg, tokens):
     from oracle import layer_flops as oflops, layer_fwd_bwd
     from synth import make_all
     sub = cfg.with_(microbatch=1, seq_len=tokens)
-    params, x, dy = make_all(sub)
+    key = (sub.name, sub.hidden, tokens)
+    if key not in _SAMPLES:  # drawing a full-h layer's weights takes ~20 s: once per sample shape
+        _SAMPLES[key] = make_all(sub)
+    params, x, dy = _SAMPLES[key]
     t0 = time.perf_counter()
     layer_fwd_bwd(params, x, dy, sub.heads)
     dt = time.perf_counter() - t0

@@ -197,7 +197,7 @@ struct Launch {
     if (h->prof) {
       cudaEvent_t b = pool_event(h);
       cudaEventRecord(b, st);
-      h->recs.push_back({cls, a, b, flops, st == h->ms ? 1 : (st == h->cw && h->cw != h->cs) ? 2 : 0});
+      h->recs.push_back({cls, a, b, flops, (st == h->ms && h->ms != h->cs) ? 1 : (st == h->cw && h->cw != h->cs) ? 2 : 0});
       h->prof_launch[cls] += nk;
     }
   }
@@ -901,8 +901,8 @@ static void release(merak_tmp_t *h) {
   if (h->cs1 && h->cs1 != h->cs) cudaStreamDestroy(h->cs1);
   if (h->cw && h->cw != h->cs) cudaStreamDestroy(h->cw);
   if (h->cr && h->cr != h->cs) cudaStreamDestroy(h->cr);
+  if (h->ms && h->ms != h->cs) cudaStreamDestroy(h->ms);
   if (h->cs) cudaStreamDestroy(h->cs);
-  if (h->ms) cudaStreamDestroy(h->ms);
   delete h;
 }
 
@@ -959,18 +959,24 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
   // priorities: comm > sub-batch compute > wgrad filler (greatest priority = numerically lowest)
   const int prio_mid = prio_hi < prio_lo ? prio_hi + 1 : prio_lo;
   CKI(cudaStreamCreateWithPriority(&h->cs, cudaStreamNonBlocking, prio_mid));
-  CKI(cudaStreamCreateWithPriority(&h->ms, cudaStreamNonBlocking, prio_hi));  // comm first when both ready
   const char *ns = getenv("MERAK_STREAMS");
+  // MERAK_STREAMS=1 (measurement): every kernel of the handle on ONE stream, in issue order -- the serialised
+  // schedule whose per-launch event spans are kernel durations (bench.py's roofline pass, ncu launch lists)
+  const bool one_stream = ns && atoi(ns) == 1;
+  if (one_stream)
+    h->ms = h->cs;
+  else
+    CKI(cudaStreamCreateWithPriority(&h->ms, cudaStreamNonBlocking, prio_hi));  // comm first when both ready
   // In-process groups put T ranks' streams in one context.  Streams beyond CUDA_DEVICE_MAX_CONNECTIONS (<= 32)
   // share hardware queues, and a rank's compute queued behind another rank's spinning handshake deadlocks
   // until the watchdog fires; at T = 8 each rank therefore runs everything but the all-reduces on one stream.
-  if ((ns && atoi(ns) == 1) || (h->inproc && h->T >= 8)) {
+  if (one_stream || (h->inproc && h->T >= 8)) {
     h->cs1 = h->cw = h->cs;
   } else {
     CKI(cudaStreamCreateWithPriority(&h->cs1, cudaStreamNonBlocking, prio_mid));
     CKI(cudaStreamCreateWithPriority(&h->cw, cudaStreamNonBlocking, prio_lo));
   }
-  if (h->inproc && h->T >= 8)
+  if (one_stream || (h->inproc && h->T >= 8))
     h->cr = h->cs;
   else
     CKI(cudaStreamCreateWithPriority(&h->cr, cudaStreamNonBlocking, prio_mid));
