@@ -3,17 +3,20 @@
 // per (sample, local head e): S = Q_e K_e^T / sqrt(d), causal mask (reading R4),
 // P = softmax(S), ctx = P V_e; lse2 = log2 sum exp2(S * scale * log2e) saved for the backward.
 //
-// One CTA = one 128-row query tile of one (sample, head); 192 threads; two CTAs per SM for d <= 64.
-//   warp 0    TMA producer: Q once, then 64-key half tiles K_j / V_j through a 3-stage ring
-//   warp 1    TMEM owner + MMA issuer: S_j = Q K_j^T into one of two TMEM S buffers, then
-//             O += P_{j-1} V_{j-1} into the TMEM output accumulator (S_{j+1} is queued before
-//             P_j V_j, so the tensor core works while the softmax warps run)
-//   warps 2-5 softmax, thread = query row (= TMEM lane): S_j row -> registers, exp2, row sum, bf16
-//             P_j into a 128-B-swizzled smem tile (double-buffered) for the next MMA.
-// The running max is updated lazily (only when it grows by more than 2^8, as in FlashAttention-4):
-// then O (in TMEM) is rescaled in place after P_{j-1} V_{j-1} completed; otherwise probabilities
-// are taken relative to the stale max (<= 2^8, exact after the final 1 / l).
-// Operands: Q, K K-major; V MN-major (its rows are keys); P K-major in smem.
+// One CTA = TWO adjacent 128-row query tiles (A = 2p, B = 2p + 1) of one (sample, head), 320 threads,
+// one CTA per SM (all 512 TMEM columns):
+//   warp 0     TMA producer: Q_A, Q_B once, then 128-key tiles K_j / V_j (shared by both query tiles)
+//   warp 1     TMEM owner + MMA issuer, ping-pong between the tiles: while softmax group A works on S_A(j)
+//              the tensor core runs S_B(j) and P_B(j-1) V_j-1, and vice versa
+//   warps 2-5  softmax of tile A, warps 6-9 softmax of tile B: thread = query row = TMEM lane, the whole
+//              128-key row in registers (no cross-warp exchange).  P (bf16) is written back into the TMEM
+//              columns of S and read from there as the A operand of O += P V (tcgen05.mma with A in TMEM),
+//              so P never touches shared memory.
+// TMEM: S_A [0,128), S_B [128,256), O_A [256, 256+D), O_B [384, 384+D) (fp32 columns).
+// The running max is updated lazily (only when it grows by more than 2^8, as in FlashAttention-4): then O
+// (in TMEM) is rescaled in place after the previous P V completed; otherwise probabilities are taken
+// relative to the stale max (<= 2^8, exact after the final 1 / l).
+// Operands: Q, K K-major; V MN-major (its rows are keys); P K-major in TMEM.
 #include <math.h>
 
 #include "kernels.h"
@@ -23,25 +26,20 @@ namespace mk {
 
 namespace {
 
-constexpr int TQ = 128;   // query rows per CTA (TMEM lanes)
-constexpr int TKH = 64;   // keys per half tile
+constexpr int TQ = 128;  // query rows per tile (TMEM lanes)
+constexpr int TK = 128;  // keys per K/V tile
 
 template <int D>
 struct FaCfg {
   static constexpr int NA = (D + 63) / 64;          // 64-wide swizzle atoms along d
-  static constexpr int Q_ATOM = TQ * 128;           // [128 rows][64] bf16
-  static constexpr int H_ATOM = TKH * 128;          // [64 rows][64] bf16
-  static constexpr int Q_BYTES = NA * Q_ATOM;
-  static constexpr int K_BYTES = NA * H_ATOM;       // K-major [64 keys][d]
-  static constexpr int V_BYTES = NA * H_ATOM;       // MN-major: NA chunks of [64 keys][64 d-columns]
-  static constexpr int STAGES = (D <= 64) ? 3 : 2;  // 4 stages no longer fit two CTAs per SM
-  static constexpr int P_BYTES = TQ * 128;          // [128 q][64 keys] bf16 = one atom
-  static constexpr int XCH_BYTES = (2 * 2 * TQ + 2 * TQ) * 4;  // row partial max [2][2][128], row sum [2][128]
-  static constexpr int SMEM = Q_BYTES + STAGES * (K_BYTES + V_BYTES) + 2 * P_BYTES + XCH_BYTES + 1024 + 256;
-  static constexpr uint32_t S_COL = 0;              // 2 x 64 fp32 columns
-  static constexpr uint32_t O_COL = 128;            // D fp32 columns
-  static constexpr int TMEM_COLS = (128 + D <= 256) ? 256 : 512;
-  static constexpr int MIN_CTAS = (D <= 64) ? 2 : 1;
+  static constexpr int ATOM = 128 * 128;            // [128 rows][64] bf16
+  static constexpr int Q_BYTES = NA * ATOM;         // one query tile
+  static constexpr int K_BYTES = NA * ATOM;         // K-major [128 keys][d]
+  static constexpr int V_BYTES = NA * ATOM;         // MN-major: NA chunks of [128 keys][64 d-columns]
+  static constexpr int STAGES = (D <= 64) ? 3 : 2;
+  static constexpr int SMEM = 2 * Q_BYTES + STAGES * (K_BYTES + V_BYTES) + 1024 + 256;
+  static constexpr uint32_t S_COL = 0;              // + 128 * tile
+  static constexpr uint32_t O_COL = 256;            // + 128 * tile
 };
 
 MK_DEV void tmem_ld16(uint32_t taddr, uint32_t *r) {
@@ -59,37 +57,65 @@ MK_DEV void tmem_st16(uint32_t taddr, const uint32_t *r) {
       "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem desc]^T, kind::f16; A (M x K, K-major) read from TMEM: lane = row,
+// bf16 pairs packed along K in consecutive 32-bit columns
+MK_DEV void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// packed fp32 pairs (FFMA2 / FADD2 on sm_100): lo = first element
+MK_DEV uint64_t pack_u64(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
+MK_DEV uint64_t f32x2(float lo, float hi) { return pack_u64(__float_as_uint(lo), __float_as_uint(hi)); }
+MK_DEV uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+MK_DEV uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+MK_DEV float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
 
 }  // namespace
 
-// 320 threads: warp 0 TMA, warp 1 TMEM + MMA, warps 2-9 softmax (thread = query row; the two warpgroups
-// split each 64-key tile's columns and exchange the row max through shared memory)
 template <int D>
-__global__ void __launch_bounds__(320, FaCfg<D>::MIN_CTAS)
+__global__ void __launch_bounds__(320, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmkv, AttnArgs a) {
   using C = FaCfg<D>;
   constexpr int NA = C::NA, ST = C::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sQ = smem;
-  uint8_t *sK = sQ + C::Q_BYTES;                 // [ST][K_BYTES]
+  uint8_t *sQ = smem;                            // [2][Q_BYTES]
+  uint8_t *sK = sQ + 2 * C::Q_BYTES;             // [ST][K_BYTES]
   uint8_t *sV = sK + ST * C::K_BYTES;            // [ST][V_BYTES]
-  uint8_t *sP = sV + ST * C::V_BYTES;            // [2][P_BYTES]
-  float *xmax = reinterpret_cast<float *>(sP + 2 * C::P_BYTES);  // [2 (tile parity)][2 (warpgroup)][128]
-  float *xsum = xmax + 4 * TQ;                                    // [2 (warpgroup)][128]
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sP + 2 * C::P_BYTES + C::XCH_BYTES);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sV + ST * C::V_BYTES);
   uint64_t *q_full = bar;
   uint64_t *kv_full = bar + 1, *kv_empty = bar + 1 + ST;
-  uint64_t *s_full = bar + 1 + 2 * ST, *s_free = s_full + 2, *p_full = s_full + 4, *p_free = s_full + 6;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(s_full + 8);
+  uint64_t *s_full = bar + 1 + 2 * ST, *p_full = s_full + 2, *o_done = s_full + 4;  // [2] each: tile A, B
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(s_full + 6);
 
   const int s = a.s, H = a.heads;
-  const int nqt = (s + TQ - 1) / TQ;
-  const int qt = nqt - 1 - blockIdx.z;  // grid (heads, b, tiles): globally heaviest tiles first
+  const int nqt = (s + TQ - 1) / TQ, nkt = (s + TK - 1) / TK;
+  const int np = (nqt + 1) / 2;
+  const int p = np - 1 - blockIdx.z;  // grid (heads, b, pairs): globally heaviest pairs first
   const int head = blockIdx.x, bi = blockIdx.y;
   const int hr = H * D;
   const int tok0 = bi * s;
-  const int J = min(2 * (qt + 1), (s + TKH - 1) / TKH);  // causal: keys < (qt+1)*128, and < s
+  const int ntile = (2 * p + 1 < nqt) ? 2 : 1;       // the last pair may hold one tile
+  const int J0 = min(2 * p + 1, nkt);                 // key tiles of query tile A / B (causal)
+  const int J1 = ntile == 2 ? min(2 * p + 2, nkt) : 0;
+  const int Jmax = max(J0, J1);
   const int warp = warp_id(), lane = lane_id();
 
   if (warp == 0 && lane == 0) {
@@ -102,14 +128,13 @@ __global__ void __launch_bounds__(320, FaCfg<D>::MIN_CTAS)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 8);
-      mbar_init(&p_full[i], 8);
-      mbar_init(&p_free[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_done[i], 1);
     }
     fence_mbar_init();
     fence_proxy_async();
   }
-  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -118,109 +143,117 @@ __global__ void __launch_bounds__(320, FaCfg<D>::MIN_CTAS)
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      mbar_expect_tx(q_full, C::Q_BYTES);
-      for (int c = 0; c < NA; ++c) tma_load_2d(sQ + c * C::Q_ATOM, &tmq, q_full, head * D + c * 64, tok0 + qt * TQ);
+      mbar_expect_tx(q_full, ntile * C::Q_BYTES);
+      for (int t = 0; t < ntile; ++t)
+        for (int c = 0; c < NA; ++c)
+          tma_load_2d(sQ + t * C::Q_BYTES + c * C::ATOM, &tmq, q_full, head * D + c * 64, tok0 + (2 * p + t) * TQ);
     }
-    for (int j = 0; j < J; ++j) {
+    for (int j = 0; j < Jmax; ++j) {
       const int st = j % ST;
       mbar_wait(&kv_empty[st], ((j / ST) & 1) ^ 1);
       if (lane == 0) {
         mbar_expect_tx(&kv_full[st], C::K_BYTES + C::V_BYTES);
         for (int c = 0; c < NA; ++c) {
-          tma_load_2d(sK + st * C::K_BYTES + c * C::H_ATOM, &tmkv, &kv_full[st], hr + head * D + c * 64,
-                      tok0 + j * TKH);
-          tma_load_2d(sV + st * C::V_BYTES + c * C::H_ATOM, &tmkv, &kv_full[st], 2 * hr + head * D + c * 64,
-                      tok0 + j * TKH);
+          tma_load_2d(sK + st * C::K_BYTES + c * C::ATOM, &tmkv, &kv_full[st], hr + head * D + c * 64, tok0 + j * TK);
+          tma_load_2d(sV + st * C::V_BYTES + c * C::ATOM, &tmkv, &kv_full[st], 2 * hr + head * D + c * 64,
+                      tok0 + j * TK);
         }
       }
       __syncwarp();
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc_s = idesc_bf16(TQ, TKH, false, false);  // Q K^T: both K-major
-    constexpr uint32_t idesc_o = idesc_bf16(TQ, D, false, true);     // P V: V is MN-major
+    constexpr uint32_t idesc_s = idesc_bf16(TQ, TK, false, false);  // Q K^T: both K-major
+    constexpr uint32_t idesc_o = idesc_bf16(TQ, D, false, true);    // P V: P K-major (TMEM), V MN-major
     mbar_wait(q_full, 0);
-    for (int j = 0; j <= J; ++j) {
-      if (j < J) {
-        const int st = j % ST, b = j & 1;
-        mbar_wait(&kv_full[st], (j / ST) & 1);
-        mbar_wait(&s_free[b], ((j >> 1) & 1) ^ 1);
+    for (int j = 0; j <= Jmax; ++j) {
+      if (j < Jmax) {
+        mbar_wait(&kv_full[j % ST], (j / ST) & 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK + st * C::K_BYTES);
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            tc_mma_f16(tmem + C::S_COL + b * TKH, sdesc_sw128(q0 + (kk >> 2) * C::Q_ATOM + (kk & 3) * 32, 16, 1024),
-                       sdesc_sw128(k0 + (kk >> 2) * C::H_ATOM + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-          }
-          tc_commit(&s_full[b]);
-        }
-        __syncwarp();
       }
-      if (j >= 1) {
-        const int i = j - 1, st = i % ST, pb = i & 1;
-        mbar_wait(&p_full[pb], (i >> 1) & 1);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t p0 = smem_u32(sP + pb * C::P_BYTES), v0 = smem_u32(sV + st * C::V_BYTES);
+      for (int t = 0; t < ntile; ++t) {
+        // O_t += P_t(j-1) V_{j-1}: P_t(j-1) sits in S_t's columns (written by softmax group t)
+        if (j >= 1 && j - 1 < (t ? J1 : J0)) {
+          const int i = j - 1, st = i % ST;
+          mbar_wait(&p_full[t], i & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t v0 = smem_u32(sV + st * C::V_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < TKH / 16; ++kk) {
-            tc_mma_f16(tmem + C::O_COL, sdesc_sw128(p0 + kk * 32, 16, 1024),
-                       sdesc_sw128(v0 + kk * 2048, C::H_ATOM, 1024), idesc_o, (i > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < TK / 16; ++kk)
+              tc_mma_f16_ts(tmem + C::O_COL + 128 * t, tmem + C::S_COL + 128 * t + kk * 8,
+                            sdesc_sw128(v0 + kk * 2048, C::ATOM, 1024), idesc_o, (i > 0 || kk > 0) ? 1u : 0u);
+            tc_commit(&o_done[t]);
           }
-          tc_commit(&p_free[pb]);
-          tc_commit(&kv_empty[st]);
+          __syncwarp();
         }
-        __syncwarp();
+        // S_t(j) = Q_t K_j^T into S_t's columns (issued after the P V that reads them: in-order execution)
+        if (j < (t ? J1 : J0)) {
+          if (lane == 0) {
+            const uint32_t q0 = smem_u32(sQ + t * C::Q_BYTES), k0 = smem_u32(sK + (j % ST) * C::K_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+              tc_mma_f16(tmem + C::S_COL + 128 * t, sdesc_sw128(q0 + (kk >> 2) * C::ATOM + (kk & 3) * 32, 16, 1024),
+                         sdesc_sw128(k0 + (kk >> 2) * C::ATOM + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
+            tc_commit(&s_full[t]);
+          }
+          __syncwarp();
+        }
       }
+      // K/V stage of j-1 is free once both tiles' P V of j-1 have completed
+      if (j >= 1 && lane == 0) tc_commit(&kv_empty[(j - 1) % ST]);
+      __syncwarp();
     }
   } else {
-    // ------------------------------------------------------------ softmax (thread = row, half the columns)
-    const int q = warp & 3, cw = (warp - 2) >> 2;
+    // ------------------------------------------------------------ softmax (thread = query row)
+    const int t = (warp - 2) >> 2;  // query tile of this warpgroup
+    const int q = warp & 3;         // TMEM lane quarter this warp may access
     const int r = q * 32 + lane;
+    const int qt = 2 * p + t;
     const int qi = qt * TQ + r;
+    const int J = t ? J1 : J0;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t s_col = lane_base + C::S_COL + 128 * t, o_col = lane_base + C::O_COL + 128 * t;
     const float sl2 = 1.4426950408889634f / sqrtf((float)D);
     const float thr = 8.0f / sl2;  // lazy rescale threshold (2^8) in raw score units
-    float m = -INFINITY, l = 0.f;  // m is identical in both warpgroups; l is this warpgroup's partial
+    float m = -INFINITY, l = 0.f;
     for (int j = 0; j < J; ++j) {
-      const int b = j & 1;
-      mbar_wait(&s_full[b], (j >> 1) & 1);
+      mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      uint32_t v[32];
-      tmem_ld32(lane_base + C::S_COL + b * TKH + cw * 32, v);
-      tmem_ld_wait();
-      const int kj0 = j * TKH + cw * 32;  // this warpgroup's first key
-      const bool mask = (j * TKH + TKH - 1 > qt * TQ) || (j * TKH + TKH > s);
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // 4 independent chains
+      uint32_t v[128];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const float x = __uint_as_float(v[k]);
-        if (!mask || (kj0 + k <= qi && kj0 + k < s)) mx4[k & 3] = fmaxf(mx4[k & 3], x);
+      for (int c = 0; c < 4; ++c) tmem_ld32(s_col + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * c]));
+      tmem_ld_wait();
+      const int kj0 = j * TK;
+      const bool mask = (kj0 + TK - 1 > qi) || (kj0 + TK > s);
+      if (mask) {  // diagonal / ragged tile: keys kj0 + k with k > lim are invisible to this row -> -inf
+        const int lim = min(qi, s - 1) - kj0;
+#pragma unroll
+        for (int k = 0; k < 128; ++k)
+          if (k > lim) v[k] = 0xff800000u;
       }
-      const float pmx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-      xmax[(b * 2 + cw) * TQ + r] = pmx;
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 softmax warps
-      const float mx = fmaxf(pmx, xmax[(b * 2 + (cw ^ 1)) * TQ + r]);
-      // the max grew by more than 2^8: move to the new max, rescale O and l.  TMEM access is
-      // warp-collective, so the whole warp enters when any row needs it (others scale by 1); the two
-      // warpgroups rescale alternate 16-column chunks of O.
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // independent chains, 3-input max
+#pragma unroll
+      for (int k = 0; k < 128; k += 8)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) mx4[c] = fmax3(mx4[c], __uint_as_float(v[k + 2 * c]), __uint_as_float(v[k + 2 * c + 1]));
+      const float mx = fmaxf(m, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])));
+      // the max grew by more than 2^8: move to the new max, rescale O and l.  TMEM access is warp-collective,
+      // so the whole warp enters when any row needs it (the others scale by 1).
       const bool need = mx > m + thr;
       if (__any_sync(0xffffffffu, need)) {
         const float corr = need ? fast_exp2((m - mx) * sl2) : 1.f;
         if (j >= 1) {
-          const int pi = j - 1;
-          mbar_wait(&p_free[pi & 1], (pi >> 1) & 1);  // P_{j-1} V_{j-1} has landed in O
+          mbar_wait(&o_done[t], (j - 1) & 1);  // P(j-1) V(j-1) has landed in O
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < D / 16; ++c) {
-            if ((c & 1) != cw) continue;
             uint32_t o[16];
-            tmem_ld16(lane_base + C::O_COL + c * 16, o);
+            tmem_ld16(o_col + c * 16, o);
             tmem_ld_wait();
 #pragma unroll
             for (int k = 0; k < 16; ++k) o[k] = __float_as_uint(__uint_as_float(o[k]) * corr);
-            tmem_st16(lane_base + C::O_COL + c * 16, o);
+            tmem_st16(o_col + c * 16, o);
           }
           tmem_st_wait();
         }
@@ -229,54 +262,37 @@ __global__ void __launch_bounds__(320, FaCfg<D>::MIN_CTAS)
           m = mx;
         }
       }
-      // P buffer b was last read by P_{j-2} V_{j-2}
-      mbar_wait(&p_free[b], ((j >> 1) & 1) ^ 1);
       const float ms = m * sl2;
-      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
-      uint8_t *prow = sP + b * C::P_BYTES + r * 128;
+      // p = exp2(s * sl2 - m * sl2): packed FFMA2 for the argument, MUFU.EX2, packed FADD2 for the row sum
+      const uint64_t sc2 = f32x2(sl2, sl2), nm2 = f32x2(-ms, -ms);
+      uint64_t rs2[4] = {0, 0, 0, 0};
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {
-        const int ch = cw * 4 + c4;  // 16-B chunk of the 128-B P row
-        uint32_t pk[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = c4 * 8 + u * 2;
-          float p0 = fast_exp2(fmaf(__uint_as_float(v[k]), sl2, -ms));
-          float p1 = fast_exp2(fmaf(__uint_as_float(v[k + 1]), sl2, -ms));
-          if (mask) {
-            if (!(kj0 + k <= qi && kj0 + k < s)) p0 = 0.f;
-            if (!(kj0 + k + 1 <= qi && kj0 + k + 1 < s)) p1 = 0.f;
-          }
-          rs4[u] += p0 + p1;
-          pk[u] = pack_bf16(p0, p1);
-        }
-        *reinterpret_cast<uint4 *>(prow + ((ch ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      for (int k = 0; k < 128; k += 2) {
+        const uint64_t x = ffma2(pack_u64(v[k], v[k + 1]), sc2, nm2);
+        const float p0 = fast_exp2(__uint_as_float((uint32_t)x)), p1 = fast_exp2(__uint_as_float((uint32_t)(x >> 32)));
+        rs2[(k >> 1) & 3] = fadd2(rs2[(k >> 1) & 3], f32x2(p0, p1));
+        v[k >> 1] = pack_bf16(p0, p1);  // P packed into v[0..63] (v[k], v[k+1] already consumed)
       }
-      l += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
-      fence_proxy_async();  // generic-proxy P stores -> visible to the tensor core
+      const uint64_t rs = fadd2(fadd2(rs2[0], rs2[1]), fadd2(rs2[2], rs2[3]));
+      l += __uint_as_float((uint32_t)rs) + __uint_as_float((uint32_t)(rs >> 32));
+      // P (bf16 pairs) over the first 64 columns of S: the A operand of O += P V
+      tmem_st32(s_col, *reinterpret_cast<const uint32_t(*)[32]>(&v[0]));
+      tmem_st32(s_col + 32, *reinterpret_cast<const uint32_t(*)[32]>(&v[32]));
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_free[b]);
-        mbar_arrive(&p_full[b]);
-      }
+      if (lane == 0) mbar_arrive(&p_full[t]);
     }
-    // row sum: the two warpgroups' partials, added in a fixed order
-    xsum[cw * TQ + r] = l;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    const float lt = xsum[r] + xsum[TQ + r];
-    // the last P V has completed when its commit arrived on p_free
-    const int last = J - 1;
-    mbar_wait(&p_free[last & 1], (last >> 1) & 1);
+    // the last P V has completed when its commit arrived on o_done
+    mbar_wait(&o_done[t], (J - 1) & 1);
     tc_fence_after();
     // tcgen05.ld is warp-collective (.sync.aligned): load converged, store only rows < s
-    const float inv = 1.f / lt;
+    const float inv = 1.f / l;
     __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.ctx) + (size_t)(tok0 + qi) * a.ld_ctx + head * D;
 #pragma unroll
     for (int c = 0; c < D / 16; ++c) {
-      if ((c & 1) != cw) continue;
       uint32_t o[16];
-      tmem_ld16(lane_base + C::O_COL + c * 16, o);
+      tmem_ld16(o_col + c * 16, o);
       tmem_ld_wait();
       if (qi < s) {
         uint4 u0, u1;
@@ -292,13 +308,13 @@ __global__ void __launch_bounds__(320, FaCfg<D>::MIN_CTAS)
         *reinterpret_cast<uint4 *>(dst + c * 16 + 8) = u1;
       }
     }
-    if (cw == 0 && qi < s) a.lse[((size_t)bi * H + head) * s + qi] = m * sl2 + log2f(lt);
+    if (qi < s) a.lse[((size_t)bi * H + head) * s + qi] = m * sl2 + log2f(l);
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<C::TMEM_COLS>(tmem);
+    tmem_dealloc<512>(tmem);
   }
 }
 
@@ -338,9 +354,9 @@ static cudaError_t fwd_tc_d(const AttnArgs &a, cudaStream_t st) {
   }
   CUtensorMap mq, mkv;
   if (!make_qkv_map(&mq, a.qkv, a.b * a.s, 3 * a.heads * D, TQ) ||
-      !make_qkv_map(&mkv, a.qkv, a.b * a.s, 3 * a.heads * D, TKH))
+      !make_qkv_map(&mkv, a.qkv, a.b * a.s, 3 * a.heads * D, TK))
     return cudaErrorInvalidValue;
-  dim3 grid(a.heads, a.b, (a.s + TQ - 1) / TQ);
+  dim3 grid(a.heads, a.b, ((a.s + TQ - 1) / TQ + 1) / 2);
   attn_fwd_tc_kernel<D><<<grid, 320, C::SMEM, st>>>(mq, mkv, a);
   return cudaGetLastError();
 }

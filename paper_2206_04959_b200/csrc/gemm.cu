@@ -143,6 +143,20 @@ MK_DEV void epi_store_chunk(const EpiParams &p, int gm, int gn0, const uint32_t 
   }
 }
 
+// Tile raster: bands of GROUP_M m-tiles, n-major inside a band (m fastest within a group column), so the
+// ~74 tiles a persistent wave runs at once cover a compact block of about 8 x 9 tiles and share their A and B
+// k-slabs in L2 (m-fastest order over all of M made every wave of the wgrad GEMMs -- M' = 24576 rows -- stream
+// 74 distinct A panels: 4x the algorithmic DRAM bytes).  The order never changes a tile's K reduction.
+constexpr int GROUP_M = 8;
+MK_DEV void tile_coords(int tile, int tiles_m, int tiles_n, int &tm, int &tn) {
+  const int band = tile / (GROUP_M * tiles_n);
+  const int m0 = band * GROUP_M;
+  const int gm = min(GROUP_M, tiles_m - m0);  // last band may be narrower
+  const int r = tile - band * GROUP_M * tiles_n;
+  tm = m0 + r % gm;
+  tn = r / gm;
+}
+
 template <int CG, int BN, bool A_MN, bool B_MN, int EPI, int SMEM_KB>
 __global__ void __launch_bounds__(256, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -251,7 +265,8 @@ __global__ void __launch_bounds__(256, 1)
     for (int lt = 0;; ++lt) {
       const int tile = (rank == 0) ? fetch(lt) : consume(lt);
       if (tile >= ntiles) break;
-      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      int tm, tn;
+      tile_coords(tile, tiles_m, tiles_n, tm, tn);
       const int row0 = tm * BMT + rank * BM;
       const int n0 = tn * BN + rank * C::BNC;
       for (int kb = 0; kb < nk; ++kb, ++it) {
@@ -342,7 +357,8 @@ __global__ void __launch_bounds__(256, 1)
       }
     };
     auto preload = [&](int tile, int buf) {
-      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      int tm, tn;
+      tile_coords(tile, tiles_m, tiles_n, tm, tn);
       const int gm = tm * BMT + rank * BM + q * 32 + lane;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
@@ -405,7 +421,8 @@ __global__ void __launch_bounds__(256, 1)
       const int buf = lt & 1;
       mbar_wait(&tfull[buf], (lt >> 1) & 1);
       tc_fence_after();
-      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      int tm, tn;
+      tile_coords(tile, tiles_m, tiles_n, tm, tn);
       const int gm = tm * BMT + rank * BM + q * 32 + lane;
       if constexpr (EPI == EPI_ACC_F32 || EPI == 5) {
 #pragma unroll 1
