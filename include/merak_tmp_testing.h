@@ -6,6 +6,7 @@
  */
 #ifndef MERAK_TMP_TESTING_H
 #define MERAK_TMP_TESTING_H
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -22,14 +23,11 @@ int merak_test_gemm(const void *A, const void *B, int M, int N, int K, int lda, 
 
 /* Causal attention forward over packed qkv [b*s, 3*heads*d] -> ctx [b*s, heads*d], lse [b,heads,s] fp32. */
 int merak_test_attn_fwd(const void *qkv, void *ctx, float *lse, int b, int s, int heads, int d, void *stream);
-/* Backward -> dqkv [b*s, 3*heads*d]; delta: fp32 workspace [b, heads, s]. */
-int merak_test_attn_bwd(const void *qkv, const void *ctx, const float *lse, const void *dctx, void *dqkv, float *delta,
+/* Backward -> dqkv [b*s, 3*heads*d]; ws: device workspace of merak_test_attn_bwd_ws_bytes() bytes, ZEROED
+ * before its first use (it holds the dQ ordering counters, which every call leaves zero). */
+size_t merak_test_attn_bwd_ws_bytes(int b, int s, int heads, int d);
+int merak_test_attn_bwd(const void *qkv, const void *ctx, const float *lse, const void *dctx, void *dqkv, void *ws,
                         int b, int s, int heads, int d, void *stream);
-
-/* Same, with diagnostics: the tcgen05 backward kernels write per-CTA SM-clock stamps into dbg
- * (64 x uint64 per CTA; the dQ kernel's CTAs, then the dK/dV kernel's; layout in attention_bwd_tc.cu). */
-int merak_test_attn_bwd_dbg(const void *qkv, const void *ctx, const float *lse, const void *dctx, void *dqkv,
-                            float *delta, int b, int s, int heads, int d, unsigned long long *dbg, void *stream);
 
 /* LayerNorm forward: u = LN(x) (bf16), mean/rstd fp32 [m]. */
 int merak_test_ln_fwd(const void *x, const void *gamma, const void *beta, void *u, float *mean, float *rstd, int m,

@@ -94,6 +94,8 @@ def lib():
                                                                       P]
         L.merak_test_attn_fwd.argtypes = [P, P, P] + [ctypes.c_int] * 4 + [P]
         L.merak_test_attn_bwd.argtypes = [P, P, P, P, P, P] + [ctypes.c_int] * 4 + [P]
+        L.merak_test_attn_bwd_ws_bytes.argtypes = [ctypes.c_int] * 4
+        L.merak_test_attn_bwd_ws_bytes.restype = ctypes.c_size_t
         L.merak_test_ln_fwd.argtypes = [P, P, P, P, P, P, ctypes.c_int, ctypes.c_int, ctypes.c_float, P]
         L.merak_test_ar_fwd.argtypes = [ctypes.POINTER(P), ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P,
                                         ctypes.c_int, P, P, P, P, P, ctypes.c_float, ctypes.c_int, P]

@@ -90,6 +90,8 @@ struct merak_tmp {
   char *ws = nullptr;
   bf16 *dz = nullptr, *dx1 = nullptr, *dctx = nullptr, *dqkv = nullptr;
   float *delta = nullptr, *part_col = nullptr, *part_lng = nullptr, *part_lnb = nullptr;
+  float *dq_acc = nullptr;  // attention backward: fp32 dQ accumulator and its ordering counters
+  int *dq_sem = nullptr;
   float *part_lng1 = nullptr, *part_lnb1 = nullptr;  // LN1 (AR#4) partials; part_lng/lnb serve LN2 (AR#3)
   int G = 16;
   // events
@@ -594,6 +596,8 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       const size_t so = (size_t)j * b * h->Hr * h->s;  // per-sub-batch lse / delta rows
       a.qkv = qkv; a.ctx = (void *)ctx; a.ld_ctx = L.ld_ctx; a.lse = (float *)S(L.lse) + so;
       a.dctx = dctx; a.dqkv = dqkv; a.delta = h->delta + so; a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
+      a.dq_acc = h->dq_acc + so * h->d;
+      a.dq_sem = h->dq_sem + (size_t)j * b * h->Hr * ((h->s + 63) / 64);
       Launch Lk(h, MERAK_K_ATTN_BWD, cst, 4.0 * b * hr * (double)h->s * (h->s + 1), 2);
       CK(h, attn_bwd(a, cst));
     }
@@ -1007,7 +1011,7 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
     size_t o = 0;
     auto take = [&](size_t bytes) { size_t at = o; o += align256(bytes); return at; };
     const size_t o_dz = take(M * h->fr * 2), o_dx1 = take(M * h->h * 2), o_dctx = take(M * h->hr * 2);
-    const size_t o_dqkv = take(M * 3 * h->hr * 2), o_delta = take((size_t)h->B * h->Hr * h->s * 4);
+    const size_t o_dqkv = take(M * 3 * h->hr * 2), o_delta = take(attn_bwd_ws_floats(h->B, h->s, h->Hr, h->d) * 4);
     const int ncol = std::max(std::max(3 * h->hr, h->fr), h->h);
     const size_t o_pc = take(2 * (size_t)h->B * ncol * 4);
     const size_t o_pg = take((M / h->G) * (size_t)h->h * 4), o_pb = take((M / h->G) * (size_t)h->h * 4);
@@ -1015,11 +1019,14 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
     const size_t o_ctr = take(64);
     CKI(cudaMalloc(&h->ws, o));
     CKI(cudaMemset(h->ws + o_ctr, 0, 64));
+    CKI(cudaMemset(h->ws + o_delta, 0, attn_bwd_ws_floats(h->B, h->s, h->Hr, h->d) * 4));  // dQ counters start at 0
     // dynamic GEMM tile schedule: opt-in (measured no gain over the static schedule at gpt1.5b, T=1)
     const char *dyn = getenv("MERAK_GEMM_DYN");
     if (dyn && atoi(dyn) == 1) h->tile_ctr = (int *)(h->ws + o_ctr);
     h->dz = (bf16 *)(h->ws + o_dz); h->dx1 = (bf16 *)(h->ws + o_dx1); h->dctx = (bf16 *)(h->ws + o_dctx);
     h->dqkv = (bf16 *)(h->ws + o_dqkv); h->delta = (float *)(h->ws + o_delta);
+    h->dq_acc = h->delta + (size_t)h->B * h->Hr * h->s;
+    h->dq_sem = (int *)(h->dq_acc + (size_t)h->B * h->Hr * h->s * h->d);
     h->part_col = (float *)(h->ws + o_pc); h->part_lng = (float *)(h->ws + o_pg); h->part_lnb = (float *)(h->ws + o_pb);
     h->part_lng1 = (float *)(h->ws + o_pg1); h->part_lnb1 = (float *)(h->ws + o_pb1);
   }
@@ -1423,21 +1430,29 @@ int merak_test_attn_fwd(const void *qkv, void *ctx, float *lse, int b, int s, in
   return (int)attn_fwd(a, (cudaStream_t)stream);
 }
 
-int merak_test_attn_bwd(const void *qkv, const void *ctx, const float *lse, const void *dctx, void *dqkv, float *delta,
-                        int b, int s, int heads, int d, void *stream) {
+int merak_test_attn_bwd_dbg(const void *qkv, const void *ctx, const float *lse, const void *dctx, void *dqkv, void *ws,
+                            int b, int s, int heads, int d, unsigned long long *dbg, void *stream) {
   AttnArgs a;
   memset(&a, 0, sizeof(a));
-  a.qkv = qkv; a.ctx = (void *)ctx; a.lse = (float *)lse; a.dctx = dctx; a.dqkv = dqkv; a.delta = delta;
-  a.b = b; a.s = s; a.heads = heads; a.d = d; a.ld_ctx = heads * d;
+  a.qkv = qkv; a.ctx = (void *)ctx; a.lse = (float *)lse; a.dctx = dctx; a.dqkv = dqkv;
+  a.delta = (float *)ws;
+  a.dq_acc = a.delta + (size_t)b * heads * s;
+  a.dq_sem = (int *)(a.dq_acc + (size_t)b * heads * s * d);
+  a.b = b; a.s = s; a.heads = heads; a.d = d; a.ld_ctx = heads * d; a.dbg = dbg;
   return (int)attn_bwd(a, (cudaStream_t)stream);
 }
 
-int merak_test_attn_bwd_dbg(const void *qkv, const void *ctx, const float *lse, const void *dctx, void *dqkv,
-                            float *delta, int b, int s, int heads, int d, unsigned long long *dbg, void *stream) {
+size_t merak_test_attn_bwd_ws_bytes(int b, int s, int heads, int d) { return attn_bwd_ws_floats(b, s, heads, d) * 4; }
+
+int merak_test_attn_bwd(const void *qkv, const void *ctx, const float *lse, const void *dctx, void *dqkv, void *ws,
+                        int b, int s, int heads, int d, void *stream) {
   AttnArgs a;
   memset(&a, 0, sizeof(a));
-  a.qkv = qkv; a.ctx = (void *)ctx; a.lse = (float *)lse; a.dctx = dctx; a.dqkv = dqkv; a.delta = delta;
-  a.b = b; a.s = s; a.heads = heads; a.d = d; a.ld_ctx = heads * d; a.dbg = dbg;
+  a.qkv = qkv; a.ctx = (void *)ctx; a.lse = (float *)lse; a.dctx = dctx; a.dqkv = dqkv;
+  a.delta = (float *)ws;
+  a.dq_acc = a.delta + (size_t)b * heads * s;
+  a.dq_sem = (int *)(a.dq_acc + (size_t)b * heads * s * d);
+  a.b = b; a.s = s; a.heads = heads; a.d = d; a.ld_ctx = heads * d;
   return (int)attn_bwd(a, (cudaStream_t)stream);
 }
 

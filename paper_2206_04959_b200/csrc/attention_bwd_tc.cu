@@ -1,17 +1,32 @@
 // attention_bwd_tc.cu -- causal attention backward on tcgen05 / TMEM.
 //
-// Deterministic (bit-identity rule ii): two kernels, no atomics, each 320 threads
-// (warp 0 TMA, warp 1 TMEM owner + MMA issuer, warps 2-9 element-wise: thread = TMEM lane, the two
-// warpgroups split the 64 columns of every tile -- the element-wise work is the latency-bound part):
-//   dQ kernel   one CTA per 128-query tile; for each 64-key half tile j:
-//               S = Q K_j^T, dP = dO V_j^T (TMEM) -> P = exp2(S*scale*log2e - lse), dS = P (dP - delta)
-//               (bf16, swizzled smem) -> dQ += dS K_j (TMEM accumulator).  Also writes delta =
-//               rowsum(dO * O) for the second kernel.
-//   dK/dV kernel one CTA per 128-key tile; for each 64-query half tile i (from the diagonal on):
-//               S^T = K Q_i^T, dP^T = V dO_i^T -> P^T, dS^T (smem) -> dV += P^T dO_i, dK += dS^T Q_i.
-// Q / dO / K / V tiles serve as K-major operands for the score products and, unchanged, as MN-major
-// operands for the accumulations (rows of 128 B in the 128-B swizzle are both canonical layouts).
+// Per (sample, local head e), with P = softmax(Q K^T / sqrt(d) + causal mask) recomputed from the saved
+// base-2 LSE and delta = rowsum(dO * O):
+//   dV = P^T dO,  dP = dO V^T,  dS = P (dP - delta),  dQ = dS K / sqrt(d),  dK = dS^T Q / sqrt(d).
+//
+// One CTA per 128-key tile (TMEM lanes = keys), iterating over the 64-query half-blocks i that see those
+// keys (causal: from the diagonal on).  Five MMAs per (key tile, half-block), nothing recomputed twice:
+//   S^T  = K Q_i^T      (M 128 keys, N 64 queries, K d)        -> TMEM, double-buffered
+//   dP^T = V dO_i^T     (same shape)                            -> TMEM, double-buffered
+//   dV  += P^T dO_i     (A = P^T read from TMEM: bf16 written over S^T by the element-wise warps)
+//   dK  += dS^T Q_i     (A = dS^T in swizzled smem)
+//   dQ_i^T = K^T dS^T   (M = d padded to 128, A = K read MN-major, B = dS^T MN-major) -> TMEM
+// 448 threads: warp 0 TMA (K, V once; Q_i, dO_i, lse_i, delta_i per half-block through a stage ring),
+// warp 1 TMEM owner + MMA issuer (scores of i+1 issued before the gradient MMAs of i, so the element-wise
+// work of one half-block overlaps the tensor core), warps 2-9 element-wise (two warpgroups ping-pong on
+// alternate half-blocks; thread = key row), warps 10-13 drain dQ_i^T (thread = d index).
+//
+// dQ is deterministic (bit-identity rule ii, no atomics): every half-block i of a (sample, head) receives
+// its contributions in a FIXED order, key tile floor(i/2) first down to key tile 0, through an fp32
+// accumulator in global memory (L2-resident).  A per-(sample, head, i) counter orders them: the first
+// contributor stores its partial with a 1-D bulk copy, the later ones bulk-reduce-add (cp.reduce.async.bulk,
+// performed in L2), each releasing the counter once its operation has completed.  A small kernel then
+// scales, rounds once to bf16 into dqkv and zeroes the counters.  The grid runs the key tiles of a (sample,
+// head) lightest-first (largest kt first), so a CTA only ever waits for CTAs dispatched before it (no
+// deadlock), which are moreover ahead of it in their own half-block sequence.
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "kernels.h"
 #include "ptx.cuh"
@@ -20,10 +35,38 @@ namespace mk {
 
 namespace {
 
-constexpr int TR = 128;  // rows per CTA (TMEM lanes)
-constexpr int TH = 64;   // half tile
-constexpr int NTHR = 320;  // 2 + 8 warps
-constexpr int NEW = 8;     // element-wise warps (two warpgroups)
+constexpr int TKEY = 128;  // keys per CTA (TMEM lanes)
+constexpr int TQH = 64;    // queries per half-block (N of the score products)
+constexpr int NTHR = 448;  // 14 warps
+
+template <int D>
+struct BwdCfg {
+  static constexpr int NA = (D + 63) / 64;      // 64-wide swizzle atoms along d
+  static constexpr int NB = (D <= 96) ? 2 : 1;  // S^T / dP^T TMEM buffers
+  static constexpr int F_ATOM = TKEY * 128;     // [128 rows][64] bf16
+  static constexpr int H_ATOM = TQH * 128;      // [64 rows][64] bf16
+  // K then V, each NA atoms; with NA = 1 the dQ^T MMA (M = 128 > d) reads its second M chunk from V
+  static constexpr int KV_BYTES = NA * F_ATOM;
+  static constexpr int QH_BYTES = NA * H_ATOM;
+  static constexpr int STAGE_BYTES = 2 * QH_BYTES;               // Q, dO (lse, delta in their own region)
+  static constexpr int DS_BYTES = TKEY * 128;                     // dS^T [128 keys][64 q] bf16
+  // Q / dO / lse / delta stages: as many as fit (a stage lives from its TMA load to the completion of the
+  // half-block's gradient MMAs, so the ring depth hides the load latency)
+  static constexpr int STG_BYTES = TQH * D * 4;                   // dQ staging [64 q][d] fp32 (one buffer)
+  static constexpr int FIXED = 2 * KV_BYTES + 2 * DS_BYTES + STG_BYTES + 1024 + 256;
+  static constexpr int ST_FIT = (227 * 1024 - FIXED) / (STAGE_BYTES + 2 * TQH * 4);
+  static constexpr int ST = ST_FIT > 6 ? 6 : ST_FIT;
+  static constexpr int SMEM = FIXED + ST * (STAGE_BYTES + 2 * TQH * 4);
+  // TMEM columns (32-aligned regions)
+  static constexpr uint32_t DPAD = (D + 31) / 32 * 32;
+  static constexpr uint32_t SP0 = 0;              // S^T (then P^T) of buffer b: SP0 + 64 b
+  static constexpr uint32_t DP0 = 64 * NB;        // dP^T of buffer b:           DP0 + 64 b
+  static constexpr uint32_t DV = 128 * NB;
+  static constexpr uint32_t DK = DV + DPAD;
+  static constexpr uint32_t DQT = DK + DPAD;      // dQ_i^T [128 lanes = d][64 q]
+  static_assert(DQT + 64 <= 512, "TMEM budget");
+  static_assert(SMEM <= 227 * 1024, "smem budget");
+};
 
 MK_DEV void tmem_ld16b(uint32_t taddr, uint32_t *r) {
   asm volatile(
@@ -32,444 +75,257 @@ MK_DEV void tmem_ld16b(uint32_t taddr, uint32_t *r) {
         "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
-
-template <int D>
-struct BwdCfg {
-  static constexpr int NA = (D + 63) / 64;
-  static constexpr int F_ATOM = TR * 128;  // [128 rows][64] bf16
-  static constexpr int H_ATOM = TH * 128;  // [64 rows][64] bf16
-  static constexpr int FULL = NA * F_ATOM;
-  static constexpr int HALF = NA * H_ATOM;
-  static constexpr int X_BYTES = TR * 128;  // [128 rows][64] bf16 element-wise result (one atom)
-  // dQ kernel: Q, dO (full) + KST stages of K, V (half) + one dS buffer
-  static constexpr int KST = (D <= 64) ? 3 : 2;
-  static constexpr int DQ_SMEM = 2 * FULL + KST * 2 * HALF + X_BYTES + 1024 + 256;
-  // dK/dV kernel: K, V (full) + 2 stages of Q, dO (half) + lse/delta + P^T, dS^T
-  static constexpr int DKV_SMEM = 2 * FULL + 2 * (2 * HALF + 512) + 2 * X_BYTES + 1024 + 256;
-  static constexpr int DQ_TMEM = (128 + D <= 256) ? 256 : 512;
-  static constexpr int DKV_TMEM = (128 + 2 * D <= 256) ? 256 : 512;
-  static constexpr int DQ_MIN = (2 * (DQ_SMEM + 1024) <= 228 * 1024 && DQ_TMEM == 256) ? 2 : 1;
-  static constexpr int DKV_MIN = (2 * (DKV_SMEM + 1024) <= 228 * 1024 && DKV_TMEM == 256) ? 2 : 1;
-};
-
-// Diagnostics (AttnArgs::dbg): one recording thread per CTA stores SM-clock stamps --
-// [0] entry, [1] prologue done, [2 + j] iteration j's scores ready (j < 54), [60] epilogue start,
-// [61] exit, [56]/[57] globaltimer at entry / exit, [62] SM id, [63] iteration count.
-MK_DEV unsigned long long *dbg_slot(unsigned long long *base) {
-  if (!base) return nullptr;
-  const size_t cta = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
-  return base + cta * 64;
+// D[tmem] (+)= A[tmem] * B[smem desc]^T (A: lane = row, bf16 pairs along K in consecutive columns)
+MK_DEV void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
 }
-MK_DEV unsigned long long clk64() {
-  unsigned long long c;
-  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
-  return c;
+MK_DEV uint32_t ld_acquire_gpu(const int *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
-MK_DEV unsigned int smid() {
-  unsigned int r;
-  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-  return r;
+MK_DEV void st_release_gpu(int *p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-
-// 32 scores of this thread's row -> 32 bf16 values packed in 16 words
-MK_DEV void put_row_chunk(uint8_t *row, int r, int c32, const uint32_t (&w)[16]) {
-  // columns c32*32 .. +31 = 16-B chunks 4*c32 .. 4*c32+3 of the 128-B row (128-B swizzle)
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int ch = c32 * 4 + u;
-    *reinterpret_cast<uint4 *>(row + ((ch ^ (r & 7)) << 4)) = make_uint4(w[4 * u], w[4 * u + 1], w[4 * u + 2], w[4 * u + 3]);
-  }
+MK_DEV void tmem_st8(uint32_t taddr, const uint32_t *r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
 }
+MK_DEV void drain_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // the 4 dQ drain warps
+// 1-D bulk smem -> global copy / fp32 add-reduction (bulk async-group of the issuing thread)
+MK_DEV void bulk_store(void *dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+MK_DEV void bulk_reduce_add_f32(void *dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+MK_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
 }  // namespace
 
-// ------------------------------------------------------------------------------------------ dQ
 template <int D>
-__device__ __forceinline__ void dq_body(const CUtensorMap *tmq_p, const CUtensorMap *tmo_p, const CUtensorMap *tmkv_p,
-                                        const AttnArgs &a, const int tile) {
-  const CUtensorMap &tmq = *tmq_p, &tmo = *tmo_p, &tmkv = *tmkv_p;
+__global__ void __launch_bounds__(NTHR, 1)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                       const __grid_constant__ CUtensorMap tm_o, AttnArgs a) {
   using C = BwdCfg<D>;
-  constexpr int NA = C::NA;
+  constexpr int NA = C::NA, NB = C::NB, ST = C::ST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sQ = smem, *sO = sQ + C::FULL;
-  constexpr int KST = C::KST;
-  uint8_t *sK = sO + C::FULL;            // [KST][HALF]
-  uint8_t *sV = sK + KST * C::HALF;      // [KST][HALF]
-  uint8_t *sX = sV + KST * C::HALF;      // [X_BYTES] dS
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sX + C::X_BYTES);
-  uint64_t *qd_full = bar, *kv_full = bar + 1, *kv_empty = bar + 1 + KST, *sp_full = bar + 1 + 2 * KST;
-  uint64_t *sp_free = sp_full + 1, *x_full = sp_full + 2, *x_free = sp_full + 3;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(sp_full + 4);
-  constexpr uint32_t S_COL = 0, DP_COL = 64, DQ_COL = 128;
+  uint8_t *sK = smem, *sV = sK + C::KV_BYTES;
+  uint8_t *sStage = sV + C::KV_BYTES;                        // [ST] {Q, dO}   (1024-B aligned atoms)
+  uint8_t *sDS = sStage + ST * C::STAGE_BYTES;               // [2] dS^T (one per warpgroup)
+  float *sStg = reinterpret_cast<float *>(sDS + 2 * C::DS_BYTES);  // [64][D] dQ staging
+  float *sLD = sStg + TQH * D;                               // [ST] {lse[64], delta[64]}
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sLD + ST * 2 * TQH);
+  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = q_full + ST;
+  // s_full / p_full / ds_free are per element-wise warpgroup w = ii & 1 (phase (ii >> 1) & 1), so each
+  // barrier's completions are consumed in order by one waiter; the TMEM buffer is ii % NB
+  uint64_t *s_full = q_empty + ST, *p_full = s_full + 2, *ds_free = p_full + 2;
+  uint64_t *dq_full = ds_free + 2, *dq_free = dq_full + 1, *kv_done = dq_free + 1;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(kv_done + 1);
+  auto stQ = [&](int st) { return sStage + st * C::STAGE_BYTES; };
+  auto stO = [&](int st) { return sStage + st * C::STAGE_BYTES + C::QH_BYTES; };
+  auto stL = [&](int st) { return sLD + st * 2 * TQH; };
+  auto stD = [&](int st) { return stL(st) + TQH; };
 
   const int s = a.s, H = a.heads, hr = H * D;
-  const int nqt = (s + TR - 1) / TR;
-  const int qt = nqt - 1 - tile;  // heaviest (most key tiles) first
-  const int head = blockIdx.x, bi = blockIdx.y, tok0 = bi * s;
-  const int J = min(2 * (qt + 1), (s + TH - 1) / TH);
-  const int warp = warp_id(), lane = lane_id();
-  unsigned long long *dbg = (warp == 2 && lane == 0) ? dbg_slot(a.dbg) : nullptr;
-  if (dbg) {
-    dbg[0] = clk64();
-    dbg[56] = globaltimer();
-    dbg[62] = smid();
-    dbg[63] = J;
-  }
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmq);
-    tma_prefetch(&tmo);
-    tma_prefetch(&tmkv);
-    mbar_init(qd_full, 1);
-    for (int i = 0; i < KST; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-    }
-    mbar_init(x_full, NEW);
-    mbar_init(x_free, 1);
-    mbar_init(sp_full, 1);
-    mbar_init(sp_free, NEW);
-    fence_mbar_init();
-    fence_proxy_async();
-  }
-  if (warp == 1) tmem_alloc<C::DQ_TMEM>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(qd_full, 2 * C::FULL);
-      for (int c = 0; c < NA; ++c) {
-        tma_load_2d(sQ + c * C::F_ATOM, &tmq, qd_full, head * D + c * 64, tok0 + qt * TR);
-        tma_load_2d(sO + c * C::F_ATOM, &tmo, qd_full, head * D + c * 64, tok0 + qt * TR);
-      }
-    }
-    for (int j = 0; j < J; ++j) {
-      const int st = j % KST;
-      mbar_wait(&kv_empty[st], ((j / KST) & 1) ^ 1);
-      if (lane == 0) {
-        mbar_expect_tx(&kv_full[st], 2 * C::HALF);
-        for (int c = 0; c < NA; ++c) {
-          tma_load_2d(sK + st * C::HALF + c * C::H_ATOM, &tmkv, &kv_full[st], hr + head * D + c * 64, tok0 + j * TH);
-          tma_load_2d(sV + st * C::HALF + c * C::H_ATOM, &tmkv, &kv_full[st], 2 * hr + head * D + c * 64,
-                      tok0 + j * TH);
-        }
-      }
-      __syncwarp();
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc_s = idesc_bf16(TR, TH, false, false);
-    constexpr uint32_t idesc_q = idesc_bf16(TR, D, false, true);  // dS (K-major) x K (MN-major)
-    mbar_wait(qd_full, 0);
-    for (int j = 0; j <= J; ++j) {
-      if (j < J) {
-        const int st = j % KST;
-        mbar_wait(&kv_full[st], (j / KST) & 1);
-        mbar_wait(sp_free, (j & 1) ^ 1);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t q0 = smem_u32(sQ), o0 = smem_u32(sO);
-          const uint32_t k0 = smem_u32(sK + st * C::HALF), v0 = smem_u32(sV + st * C::HALF);
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t fo = (kk >> 2) * C::F_ATOM + (kk & 3) * 32, ho = (kk >> 2) * C::H_ATOM + (kk & 3) * 32;
-            tc_mma_f16(tmem + S_COL, sdesc_sw128(q0 + fo, 16, 1024), sdesc_sw128(k0 + ho, 16, 1024), idesc_s,
-                       kk > 0 ? 1u : 0u);
-            tc_mma_f16(tmem + DP_COL, sdesc_sw128(o0 + fo, 16, 1024), sdesc_sw128(v0 + ho, 16, 1024), idesc_s,
-                       kk > 0 ? 1u : 0u);
-          }
-          tc_commit(sp_full);
-        }
-        __syncwarp();
-      }
-      if (j >= 1) {
-        const int i = j - 1, st = i % KST;
-        mbar_wait(x_full, i & 1);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t x0 = smem_u32(sX), k0 = smem_u32(sK + st * C::HALF);
-#pragma unroll
-          for (int kk = 0; kk < TH / 16; ++kk)
-            tc_mma_f16(tmem + DQ_COL, sdesc_sw128(x0 + kk * 32, 16, 1024), sdesc_sw128(k0 + kk * 2048, C::H_ATOM, 1024),
-                       idesc_q, (i > 0 || kk > 0) ? 1u : 0u);
-          tc_commit(x_free);
-          tc_commit(&kv_empty[st]);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    const int q = warp & 3, r = q * 32 + lane, qi = qt * TR + r, cw = (warp - 2) >> 2;
-    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
-    const float scale = 1.f / sqrtf((float)D), sl2 = 1.4426950408889634f * scale;
-    const size_t srow = ((size_t)bi * H + head) * s;
-    // delta = rowsum(dO * O) comes from attn_delta_kernel (launched first)
-    const float lse = qi < s ? a.lse[srow + qi] : INFINITY, del = qi < s ? a.delta[srow + qi] : 0.f;
-    const float ls = lse;
-    if (dbg) dbg[1] = clk64();
-    for (int j = 0; j < J; ++j) {
-      mbar_wait(sp_full, j & 1);
-      tc_fence_after();
-      if (dbg && j < 54) dbg[2 + j] = clk64();
-      const int kj0 = j * TH;
-      const bool mask = (kj0 + TH - 1 > qt * TR) || (kj0 + TH > s);
-      uint32_t w[16];  // this warpgroup's 32 columns, bf16-packed
-#pragma unroll
-      for (int hc = 0; hc < 2; ++hc) {
-        const int col0 = cw * 32 + hc * 16;
-        uint32_t sv[16], dv[16];
-        tmem_ld16b(lb + S_COL + col0, sv);
-        tmem_ld16b(lb + DP_COL + col0, dv);
-        tmem_ld_wait();
-#pragma unroll
-        for (int k = 0; k < 16; k += 2) {
-          const int kj = kj0 + col0 + k;
-          float p0 = fast_exp2(fmaf(__uint_as_float(sv[k]), sl2, -ls));
-          float p1 = fast_exp2(fmaf(__uint_as_float(sv[k + 1]), sl2, -ls));
-          float g0 = p0 * (__uint_as_float(dv[k]) - del), g1 = p1 * (__uint_as_float(dv[k + 1]) - del);
-          if (mask) {
-            if (!(kj <= qi && kj < s)) g0 = 0.f;
-            if (!(kj + 1 <= qi && kj + 1 < s)) g1 = 0.f;
-          }
-          w[hc * 8 + (k >> 1)] = pack_bf16(g0, g1);
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(sp_free);
-      mbar_wait(x_free, (j & 1) ^ 1);  // the dS buffer was read by the MMA of j-1
-      put_row_chunk(sX + r * 128, r, cw, w);
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(x_full);
-    }
-    const int last = J - 1;
-    if (dbg) dbg[60] = clk64();
-    mbar_wait(x_free, last & 1);
-    tc_fence_after();
-    __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.dqkv) + (size_t)(tok0 + qi) * 3 * hr + head * D;
-#pragma unroll
-    for (int c = 0; c < D / 16; ++c) {
-      if ((c & 1) != cw) continue;  // warp-uniform: the warpgroups take alternate 16-column chunks
-      uint32_t o[16];
-      tmem_ld16b(lb + DQ_COL + c * 16, o);
-      tmem_ld_wait();
-      if (qi < s) {
-        uint4 u0, u1;
-        u0.x = pack_bf16(__uint_as_float(o[0]) * scale, __uint_as_float(o[1]) * scale);
-        u0.y = pack_bf16(__uint_as_float(o[2]) * scale, __uint_as_float(o[3]) * scale);
-        u0.z = pack_bf16(__uint_as_float(o[4]) * scale, __uint_as_float(o[5]) * scale);
-        u0.w = pack_bf16(__uint_as_float(o[6]) * scale, __uint_as_float(o[7]) * scale);
-        u1.x = pack_bf16(__uint_as_float(o[8]) * scale, __uint_as_float(o[9]) * scale);
-        u1.y = pack_bf16(__uint_as_float(o[10]) * scale, __uint_as_float(o[11]) * scale);
-        u1.z = pack_bf16(__uint_as_float(o[12]) * scale, __uint_as_float(o[13]) * scale);
-        u1.w = pack_bf16(__uint_as_float(o[14]) * scale, __uint_as_float(o[15]) * scale);
-        *reinterpret_cast<uint4 *>(dst + c * 16) = u0;
-        *reinterpret_cast<uint4 *>(dst + c * 16 + 8) = u1;
-      }
-    }
-  }
-  if (dbg) {
-    dbg[61] = clk64();
-    dbg[57] = globaltimer();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc<C::DQ_TMEM>(tmem);
-  }
-}
-
-// ------------------------------------------------------------------------------------------ dK / dV
-template <int D>
-__device__ __forceinline__ void dkdv_body(const CUtensorMap *tmf_p, const CUtensorMap *tmh_p,
-                                          const CUtensorMap *tmoh_p, const AttnArgs &a, const int tile) {
-  const CUtensorMap &tmf = *tmf_p, &tmh = *tmh_p, &tmoh = *tmoh_p;
-  using C = BwdCfg<D>;
-  constexpr int NA = C::NA;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sK = smem, *sV = sK + C::FULL;
-  uint8_t *sQ = sV + C::FULL;            // [2][HALF]
-  uint8_t *sO = sQ + 2 * C::HALF;        // [2][HALF] dO
-  uint8_t *sP = sO + 2 * C::HALF;        // P^T  [128 keys][64 q]
-  uint8_t *sS = sP + C::X_BYTES;         // dS^T [128 keys][64 q]
-  float *sL = reinterpret_cast<float *>(sS + C::X_BYTES);  // [2][64] lse, then [2][64] delta
-  float *sD = sL + 2 * TH;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sD + 2 * TH);
-  uint64_t *kv_full = bar, *q_full = bar + 1, *q_empty = bar + 3, *sp_full = bar + 5, *sp_free = bar + 6;
-  uint64_t *x_full = bar + 7, *x_free = bar + 8;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 9);
-  constexpr uint32_t ST_COL = 0, DPT_COL = 64, DV_COL = 128, DK_COL = 128 + D;
-
-  const int s = a.s, H = a.heads, hr = H * D;
-  const int kt = tile;  // kt = 0 has the most query tiles: heaviest first
-  const int head = blockIdx.x, bi = blockIdx.y, tok0 = bi * s;
-  const int i0 = 2 * kt, NI = (s + TH - 1) / TH - i0;
+  const int nkt = (s + TKEY - 1) / TKEY, NQ = (s + TQH - 1) / TQH;
+  // 1-D grid in groups of G (sample, head) pairs: inside a group, key tiles descending (lightest first), the
+  // pairs of the group fastest.  A key tile's predecessor in the dQ order (kt + 1 of the same pair) is then
+  // dispatched G CTAs earlier -- early enough to be ahead of it -- while a group's Q / dO / K / V / dQ
+  // accumulator stay L2-resident.
+  const int npairs = a.b * H, G = a.attn_group;
+  const int grp = (int)blockIdx.x / (G * nkt), r0 = (int)blockIdx.x - grp * G * nkt;
+  const int Gg = min(G, npairs - grp * G);  // the last group may be smaller
+  const int kt = nkt - 1 - r0 / Gg;
+  const int pair = grp * G + r0 % Gg;
+  const int head = pair % H, bi = pair / H, tok0 = bi * s;
+  const int i0 = 2 * kt, NI = NQ - i0;
   const size_t srow = ((size_t)bi * H + head) * s;
   const int warp = warp_id(), lane = lane_id();
-  unsigned long long *dbg = (warp == 2 && lane == 0) ? dbg_slot(a.dbg) : nullptr;
-  if (dbg) {
-    dbg[0] = clk64();
-    dbg[56] = globaltimer();
-    dbg[62] = smid();
-    dbg[63] = NI;
-  }
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmf);
-    tma_prefetch(&tmh);
-    tma_prefetch(&tmoh);
+    tma_prefetch(&tm_kv);
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_o);
     mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < ST; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
     }
-    mbar_init(sp_full, 1);
-    mbar_init(sp_free, NEW);
-    mbar_init(x_full, NEW);
-    mbar_init(x_free, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&ds_free[i], 1);
+    }
+    mbar_init(dq_full, 1);
+    mbar_init(dq_free, 4);
+    mbar_init(kv_done, 1);
     fence_mbar_init();
     fence_proxy_async();
   }
-  if (warp == 1) tmem_alloc<C::DKV_TMEM>(tmem_slot);
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // all 512 columns belong to this CTA, so the allocation starts at lane 0, column 0: a compile-time base
+  // keeps every TMEM address warp-uniform (single-instruction MMA issue, no per-lane broadcast loop)
+  if (*tmem_slot != 0u) __trap();
+  constexpr uint32_t tmem = 0u;
 
   if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      mbar_expect_tx(kv_full, 2 * C::FULL);
+      mbar_expect_tx(kv_full, 2 * C::KV_BYTES);
       for (int c = 0; c < NA; ++c) {
-        tma_load_2d(sK + c * C::F_ATOM, &tmf, kv_full, hr + head * D + c * 64, tok0 + kt * TR);
-        tma_load_2d(sV + c * C::F_ATOM, &tmf, kv_full, 2 * hr + head * D + c * 64, tok0 + kt * TR);
+        tma_load_2d(sK + c * C::F_ATOM, &tm_kv, kv_full, hr + head * D + c * 64, tok0 + kt * TKEY);
+        tma_load_2d(sV + c * C::F_ATOM, &tm_kv, kv_full, 2 * hr + head * D + c * 64, tok0 + kt * TKEY);
       }
     }
     for (int ii = 0; ii < NI; ++ii) {
-      const int i = i0 + ii, st = ii & 1;
-      mbar_wait(&q_empty[st], ((ii >> 1) & 1) ^ 1);
+      const int i = i0 + ii, st = ii % ST;
+      mbar_wait(&q_empty[st], ((ii / ST) & 1) ^ 1);
       if (lane == 0) {
-        const int nrow = min(TH, s - i * TH);
-        const uint32_t lbytes = (uint32_t)nrow * 4;
-        mbar_expect_tx(&q_full[st], 2 * C::HALF + 2 * lbytes);
+        const uint32_t lbytes = (uint32_t)min(TQH, s - i * TQH) * 4;
+        mbar_expect_tx(&q_full[st], 2 * C::QH_BYTES + 2 * lbytes);
         for (int c = 0; c < NA; ++c) {
-          tma_load_2d(sQ + st * C::HALF + c * C::H_ATOM, &tmh, &q_full[st], head * D + c * 64, tok0 + i * TH);
-          tma_load_2d(sO + st * C::HALF + c * C::H_ATOM, &tmoh, &q_full[st], head * D + c * 64, tok0 + i * TH);
+          tma_load_2d(stQ(st) + c * C::H_ATOM, &tm_q, &q_full[st], head * D + c * 64, tok0 + i * TQH);
+          tma_load_2d(stO(st) + c * C::H_ATOM, &tm_o, &q_full[st], head * D + c * 64, tok0 + i * TQH);
         }
-        bulk_load_1d(sL + st * TH, a.lse + srow + i * TH, lbytes, &q_full[st]);
-        bulk_load_1d(sD + st * TH, a.delta + srow + i * TH, lbytes, &q_full[st]);
+        bulk_load_1d(stL(st), a.lse + srow + i * TQH, lbytes, &q_full[st]);
+        bulk_load_1d(stD(st), a.delta + srow + i * TQH, lbytes, &q_full[st]);
       }
       __syncwarp();
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc_s = idesc_bf16(TR, TH, false, false);
-    constexpr uint32_t idesc_g = idesc_bf16(TR, D, false, true);
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc_s = idesc_bf16(TKEY, TQH, false, false);  // K Q^T, V dO^T
+    constexpr uint32_t idesc_g = idesc_bf16(TKEY, D, false, true);     // P^T dO, dS^T Q
+    constexpr uint32_t idesc_q = idesc_bf16(128, TQH, true, true);     // K^T dS^T (M = d padded)
+    unsigned long long *dbg = (a.dbg && lane == 0) ? a.dbg + (size_t)blockIdx.x * 80 : nullptr;
+    if (dbg) { dbg[0] = clock64(); dbg[76] = globaltimer(); dbg[77] = NI; unsigned sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); dbg[79] = sm; }
     mbar_wait(kv_full, 0);
-    for (int ii = 0; ii <= NI; ++ii) {
-      if (ii < NI) {
-        const int st = ii & 1;
-        mbar_wait(&q_full[st], (ii >> 1) & 1);
-        mbar_wait(sp_free, (ii & 1) ^ 1);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t k0 = smem_u32(sK), v0 = smem_u32(sV);
-          const uint32_t q0 = smem_u32(sQ + st * C::HALF), o0 = smem_u32(sO + st * C::HALF);
+    if (dbg) dbg[1] = clock64();
+    const uint32_t k0 = smem_u32(sK), v0 = smem_u32(sV);
+    // whole-warp issue (tc_*_w elect one lane inside the asm); descriptors are base + constant offsets
+    const uint64_t dK0 = sdesc_sw128(k0, 16, 1024), dV0 = sdesc_sw128(v0, 16, 1024);
+    const uint64_t dKmn = sdesc_sw128(k0, C::F_ATOM, 1024);
+    auto scores = [&](int ii) {
+      const int st = ii % ST, b = ii % NB, w = ii & 1;
+      mbar_wait(&q_full[st], (ii / ST) & 1);
+      if (dbg && ii < 36) dbg[2 + ii] = clock64();
+      tc_fence_after();
+      const uint64_t dQ0 = sdesc_sw128(smem_u32(stQ(st)), 16, 1024), dO0 = sdesc_sw128(smem_u32(stO(st)), 16, 1024);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t fo = (kk >> 2) * C::F_ATOM + (kk & 3) * 32, ho = (kk >> 2) * C::H_ATOM + (kk & 3) * 32;
-            tc_mma_f16(tmem + ST_COL, sdesc_sw128(k0 + fo, 16, 1024), sdesc_sw128(q0 + ho, 16, 1024), idesc_s,
-                       kk > 0 ? 1u : 0u);
-            tc_mma_f16(tmem + DPT_COL, sdesc_sw128(v0 + fo, 16, 1024), sdesc_sw128(o0 + ho, 16, 1024), idesc_s,
-                       kk > 0 ? 1u : 0u);
-          }
-          tc_commit(sp_full);
-        }
-        __syncwarp();
+      for (int kk = 0; kk < D / 16; ++kk) {
+        const uint32_t fo = ((kk >> 2) * C::F_ATOM + (kk & 3) * 32) >> 4, ho = ((kk >> 2) * C::H_ATOM + (kk & 3) * 32) >> 4;
+        tc_mma_f16_w(tmem + C::SP0 + 64 * b, dK0 + fo, dQ0 + ho, idesc_s, kk > 0 ? 1u : 0u);
+        tc_mma_f16_w(tmem + C::DP0 + 64 * b, dV0 + fo, dO0 + ho, idesc_s, kk > 0 ? 1u : 0u);
       }
-      if (ii >= 1) {
-        const int p = ii - 1, st = p & 1;
-        mbar_wait(x_full, p & 1);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t pp = smem_u32(sP), ps = smem_u32(sS);
-          const uint32_t q0 = smem_u32(sQ + st * C::HALF), o0 = smem_u32(sO + st * C::HALF);
+      tc_commit_w(&s_full[w]);
+    };
+    auto grads = [&](int p) {
+      const int st = p % ST, b = p % NB, w = p & 1;
+      mbar_wait(&p_full[w], (p >> 1) & 1);  // P^T in TMEM, dS^T in smem
+      if (dbg && p < 36) dbg[38 + p] = clock64();
+      tc_fence_after();
+      const uint64_t qmn = sdesc_sw128(smem_u32(stQ(st)), C::H_ATOM, 1024);
+      const uint64_t omn = sdesc_sw128(smem_u32(stO(st)), C::H_ATOM, 1024);
+      const uint64_t dsk = sdesc_sw128(smem_u32(sDS + w * C::DS_BYTES), 16, 1024);
+      const uint64_t dsmn = sdesc_sw128(smem_u32(sDS + w * C::DS_BYTES), C::F_ATOM, 1024);
 #pragma unroll
-          for (int kk = 0; kk < TH / 16; ++kk) {
-            const uint32_t acc = (p > 0 || kk > 0) ? 1u : 0u;
-            tc_mma_f16(tmem + DV_COL, sdesc_sw128(pp + kk * 32, 16, 1024), sdesc_sw128(o0 + kk * 2048, C::H_ATOM, 1024),
-                       idesc_g, acc);
-            tc_mma_f16(tmem + DK_COL, sdesc_sw128(ps + kk * 32, 16, 1024), sdesc_sw128(q0 + kk * 2048, C::H_ATOM, 1024),
-                       idesc_g, acc);
-          }
-          tc_commit(x_free);
-          tc_commit(&q_empty[st]);
-        }
-        __syncwarp();
+      for (int kk = 0; kk < TQH / 16; ++kk) {
+        const uint32_t acc = (p > 0 || kk > 0) ? 1u : 0u;
+        tc_mma_f16_ts_w(tmem + C::DV, tmem + C::SP0 + 64 * b + kk * 8, omn + (kk * 2048 >> 4), idesc_g, acc);
+        tc_mma_f16_w(tmem + C::DK, dsk + (kk * 32 >> 4), qmn + (kk * 2048 >> 4), idesc_g, acc);
+      }
+      if (p >= 1) mbar_wait(dq_free, (p - 1) & 1);  // the drain warps have read dQ^T of p - 1
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < TKEY / 16; ++kk)
+        tc_mma_f16_w(tmem + C::DQT, dKmn + (kk * 2048 >> 4), dsmn + (kk * 2048 >> 4), idesc_q, kk > 0 ? 1u : 0u);
+      tc_commit_w(dq_full);
+      tc_commit_w(&ds_free[w]);
+      tc_commit_w(&q_empty[st]);
+    };
+    for (int ii = 0; ii <= NI; ++ii) {
+      if (NB == 1) {  // one buffer: P^T of ii - 1 must be consumed before S^T of ii overwrites it
+        if (ii >= 1) grads(ii - 1);
+        if (ii < NI) scores(ii);
+      } else {
+        if (ii < NI) scores(ii);
+        if (ii >= 1) grads(ii - 1);
       }
     }
-  } else {
-    const int q = warp & 3, r = q * 32 + lane, kj = kt * TR + r, cw = (warp - 2) >> 2;
-    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16);
+    tc_commit_w(kv_done);
+    if (dbg) { dbg[74] = clock64(); }
+  } else if (warp < 10) {
+    // ------------------------------------------------------------ element-wise (thread = key row)
+    const int g = (warp - 2) >> 2, q4 = warp & 3, r = q4 * 32 + lane, kj = kt * TKEY + r;
+    const uint32_t lb = tmem + ((uint32_t)(q4 * 32) << 16);
     const float scale = 1.f / sqrtf((float)D), sl2 = 1.4426950408889634f * scale;
-    if (dbg) dbg[1] = clk64();
-    for (int ii = 0; ii < NI; ++ii) {
-      const int i = i0 + ii, st = ii & 1;
-      const int qi0 = i * TH;
-      mbar_wait(&q_full[st], (ii >> 1) & 1);  // lse / delta of this half tile are in smem
-      mbar_wait(sp_full, ii & 1);
+    for (int ii = g; ii < NI; ii += 2) {
+      const int st = ii % ST, b = ii % NB, qi0 = (i0 + ii) * TQH;  // warpgroup g == ii & 1
+      mbar_wait(&q_full[st], (ii / ST) & 1);  // lse / delta of this half-block
+      mbar_wait(&s_full[g], (ii >> 1) & 1);
       tc_fence_after();
-      if (dbg && ii < 54) dbg[2 + ii] = clk64();
-      const bool mask = (qi0 < kt * TR + TR - 1) || (qi0 + TH > s);
-      const float *L = sL + st * TH, *Dl = sD + st * TH;
-      uint32_t wp[16], ws[16];  // this warpgroup's 32 columns of P^T and dS^T, bf16-packed
+      const bool mask = (qi0 < kt * TKEY + TKEY - 1) || (qi0 + TQH > s);
+      const float *L = stL(st), *Dl = stD(st);
+      mbar_wait(&ds_free[g], ((ii >> 1) & 1) ^ 1);  // dS^T buffer g read by the MMAs of ii - 2
+      uint8_t *row = sDS + g * C::DS_BYTES + r * 128;
 #pragma unroll
-      for (int hc = 0; hc < 2; ++hc) {
-        const int col0 = cw * 32 + hc * 16;
-        uint32_t sv[16], dv[16];
-        tmem_ld16b(lb + ST_COL + col0, sv);
-        tmem_ld16b(lb + DPT_COL + col0, dv);
+      for (int c = 0; c < TQH / 16; ++c) {  // 16 query columns per step
+        uint32_t sv[16], dv[16], pw[8], dw[8];
+        tmem_ld16b(lb + C::SP0 + 64 * b + 16 * c, sv);
+        tmem_ld16b(lb + C::DP0 + 64 * b + 16 * c, dv);
         tmem_ld_wait();
 #pragma unroll
         for (int k = 0; k < 16; k += 2) {
-          const int c = col0 + k, qi = qi0 + c;
-          float p0 = fast_exp2(fmaf(__uint_as_float(sv[k]), sl2, -L[c]));
-          float p1 = fast_exp2(fmaf(__uint_as_float(sv[k + 1]), sl2, -L[c + 1]));
+          const int col = 16 * c + k, qi = qi0 + col;
+          const float2 l2 = *reinterpret_cast<const float2 *>(L + col);
+          const float2 d2 = *reinterpret_cast<const float2 *>(Dl + col);
+          float p0 = fast_exp2(fmaf(__uint_as_float(sv[k]), sl2, -l2.x));
+          float p1 = fast_exp2(fmaf(__uint_as_float(sv[k + 1]), sl2, -l2.y));
           if (mask) {
             if (!(kj <= qi && qi < s)) p0 = 0.f;
             if (!(kj <= qi + 1 && qi + 1 < s)) p1 = 0.f;
           }
-          const float g0 = p0 * (__uint_as_float(dv[k]) - Dl[c]), g1 = p1 * (__uint_as_float(dv[k + 1]) - Dl[c + 1]);
-          wp[hc * 8 + (k >> 1)] = pack_bf16(p0, p1);
-          ws[hc * 8 + (k >> 1)] = pack_bf16(g0, g1);
+          pw[k >> 1] = pack_bf16(p0, p1);
+          dw[k >> 1] = pack_bf16(p0 * (__uint_as_float(dv[k]) - d2.x), p1 * (__uint_as_float(dv[k + 1]) - d2.y));
         }
+        // P^T (bf16 pairs) over columns 8c..8c+7 of this buffer's S^T (already read): the A operand of dV
+        tmem_st8(lb + C::SP0 + 64 * b + 8 * c, pw);
+        // dS^T: 16-B chunks 2c, 2c+1 of this key row (128-B swizzle)
+        *reinterpret_cast<uint4 *>(row + (((2 * c) ^ (r & 7)) << 4)) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
+        *reinterpret_cast<uint4 *>(row + (((2 * c + 1) ^ (r & 7)) << 4)) = make_uint4(dw[4], dw[5], dw[6], dw[7]);
       }
+      tmem_st_wait();
+      fence_proxy_async();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(sp_free);
-      mbar_wait(x_free, (ii & 1) ^ 1);  // P^T / dS^T were read by the MMAs of ii-1
-      put_row_chunk(sP + r * 128, r, cw, wp);
-      put_row_chunk(sS + r * 128, r, cw, ws);
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(x_full);
+      if (lane == 0) mbar_arrive(&p_full[g]);
     }
-    const int last = NI - 1;
-    if (dbg) dbg[60] = clk64();
-    mbar_wait(x_free, last & 1);
+    // dK, dV epilogue
+    mbar_wait(kv_done, 0);
     tc_fence_after();
     __nv_bfloat16 *dk = reinterpret_cast<__nv_bfloat16 *>(a.dqkv) + (size_t)(tok0 + kj) * 3 * hr + hr + head * D;
     __nv_bfloat16 *dvp = dk + hr;
 #pragma unroll
     for (int c = 0; c < D / 16; ++c) {
-      if ((c & 1) != cw) continue;  // warp-uniform: alternate 16-column chunks per warpgroup
+      if ((c & 1) != g) continue;  // warp-uniform: alternate 16-column chunks per warpgroup
       uint32_t ov[16], ok[16];
-      tmem_ld16b(lb + DV_COL + c * 16, ov);
-      tmem_ld16b(lb + DK_COL + c * 16, ok);
+      tmem_ld16b(lb + C::DV + c * 16, ov);
+      tmem_ld16b(lb + C::DK + c * 16, ok);
       tmem_ld_wait();
       if (kj < s) {
         uint4 u;
@@ -488,20 +344,97 @@ __device__ __forceinline__ void dkdv_body(const CUtensorMap *tmf_p, const CUtens
         }
       }
     }
-  }
-  if (dbg) {
-    dbg[61] = clk64();
-    dbg[57] = globaltimer();
+  } else {
+    // ------------------------------------------------------------ dQ drain (thread = d index)
+    // Per half-block: TMEM -> fp32 staging smem -> one elected thread waits for its turn on the block's
+    // counter, bulk-stores (first contributor) or bulk-reduce-adds (cp.reduce.async.bulk, performed in L2) it
+    // into dq_acc, and releases the counter one iteration later, once the operation has completed, so the
+    // completion latency overlaps the next half-block instead of stalling the tensor core.
+    const int q4 = warp & 3, dd = q4 * 32 + lane;
+    const bool active = q4 * 32 < D;  // warp-uniform
+    const bool elected = (warp == 10 && lane == 0);
+    const uint32_t lb = tmem + ((uint32_t)(q4 * 32) << 16);
+    float *dqa = a.dq_acc + srow * D;
+    int *sem = a.dq_sem + ((size_t)bi * H + head) * NQ;
+    auto release = [&](int i) {  // the bulk operation of block i has completed (wait_group before)
+      fence_proxy_async_global();
+      st_release_gpu(&sem[i], (uint32_t)(i / 2 - kt + 1));
+    };
+    for (int ii = 0; ii < NI; ++ii) {
+      const int i = i0 + ii, nrow = min(TQH, s - i * TQH);
+      const int rank = i / 2 - kt;  // contributions before this one (key tiles floor(i/2) .. kt+1)
+      mbar_wait(dq_full, ii & 1);
+      tc_fence_after();
+      if (active) {
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          uint32_t v[32];
+          tmem_ld32(lb + C::DQT + 32 * h2, v);
+          tmem_ld_wait();
+          if (h2 == 1) {  // dQ^T read: the next dQ^T MMA may overwrite it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dq_free);
+          } else {
+            drain_bar();  // the staging buffer is free: the previous bulk operation has read it
+          }
+          if (dd < D) {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) sStg[(32 * h2 + q) * D + dd] = __uint_as_float(v[q]);
+          }
+        }
+      } else {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dq_free);
+        drain_bar();
+      }
+      fence_proxy_async();  // generic smem writes -> visible to the bulk copy (async proxy)
+      drain_bar();
+      if (elected) {
+        if (rank > 0) {
+          const uint64_t t0 = globaltimer();
+          int seen;
+          while ((seen = (int)ld_acquire_gpu(&sem[i])) != rank) {
+            __nanosleep(20);
+            if (globaltimer() - t0 > 4000000000ull) {  // 4 s: a broken ordering invariant, not a slow peer
+              printf("attn_bwd dQ order watchdog: b %d head %d kt %d block %d rank %d counter %d\n", bi, head, kt, i,
+                     rank, seen);
+              __trap();
+            }
+          }
+          fence_proxy_async_global();
+        }
+        float *qa = dqa + (size_t)i * TQH * D;
+        const uint32_t bytes = (uint32_t)nrow * D * 4;
+        if (rank == 0)
+          bulk_store(qa, sStg, bytes);
+        else
+          bulk_reduce_add_f32(qa, sStg, bytes);
+        tma_store_commit();
+        if (ii >= 1) {
+          tma_store_wait<1>();  // the previous block's operation has completed
+          release(i - 1);
+        }
+        tma_store_wait_read<0>();  // the staging buffer has been read (rewritten after the next barrier)
+      }
+      __syncwarp();  // reconverge warp 10 before the next warp-collective tcgen05.ld
+    }
+    if (elected && NI > 0) {
+      tma_store_wait<0>();
+      release(i0 + NI - 1);
+    }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<C::DKV_TMEM>(tmem);
+    tmem_dealloc<512>(tmem);
+    if (a.dbg && lane == 0) { a.dbg[(size_t)blockIdx.x * 80 + 75] = clock64(); a.dbg[(size_t)blockIdx.x * 80 + 78] = globaltimer(); }
   }
 }
 
-// ------------------------------------------------------------------------------------------ kernels
+// ------------------------------------------------------------------------------------------ delta
 // delta = rowsum(dO * O) per (sample, head, query): one thread per (token, head), head fastest, so a
 // warp reads contiguous 128-B rows of O and dO.
 template <int D>
@@ -527,19 +460,28 @@ __global__ void __launch_bounds__(256) attn_delta_kernel(AttnArgs a) {
   a.delta[((size_t)bi * H + e) * a.s + i] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
-// One launch for both halves of the backward (independent once delta exists): grid (heads, b, 2 x
-// tiles) with the tile slot slowest, so dispatch is globally heaviest-first; even slots compute dQ
-// tiles, odd slots dK/dV tiles, and the causal imbalance of one fills the other.
+// dQ = bf16(scale * dq_acc) into the q block of dqkv (one thread per 8 consecutive d), and every dQ ordering
+// counter back to 0 for the next launch.
 template <int D>
-__global__ void __launch_bounds__(NTHR, BwdCfg<D>::DQ_MIN < BwdCfg<D>::DKV_MIN ? BwdCfg<D>::DQ_MIN : BwdCfg<D>::DKV_MIN)
-    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmq_full, const __grid_constant__ CUtensorMap tmq_half,
-                       const __grid_constant__ CUtensorMap tmo_full, const __grid_constant__ CUtensorMap tmo_half,
-                       AttnArgs a) {
-  const int tile = blockIdx.z >> 1;
-  if (blockIdx.z & 1)
-    dkdv_body<D>(&tmq_full, &tmq_half, &tmo_half, a, tile);
-  else
-    dq_body<D>(&tmq_full, &tmo_full, &tmq_half, a, tile);
+__global__ void __launch_bounds__(256) attn_dq_out_kernel(AttnArgs a) {
+  const int H = a.heads, hr = H * D, s = a.s;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long nsem = (long)a.b * H * ((s + TQH - 1) / TQH);
+  if (idx < nsem) a.dq_sem[idx] = 0;
+  if (idx >= (long)a.b * H * s * (D / 8)) return;
+  const int c8 = (int)(idx % (D / 8));
+  const long row = idx / (D / 8);  // (bi * H + head) * s + q
+  const int q = (int)(row % s), bh = (int)(row / s), head = bh % H, bi = bh / H;
+  const float scale = 1.f / sqrtf((float)D);
+  const float4 *src = reinterpret_cast<const float4 *>(a.dq_acc + row * D + c8 * 8);
+  const float4 x0 = __ldcs(src), x1 = __ldcs(src + 1);
+  uint4 o;
+  o.x = pack_bf16(x0.x * scale, x0.y * scale);
+  o.y = pack_bf16(x0.z * scale, x0.w * scale);
+  o.z = pack_bf16(x1.x * scale, x1.y * scale);
+  o.w = pack_bf16(x1.z * scale, x1.w * scale);
+  *reinterpret_cast<uint4 *>(reinterpret_cast<__nv_bfloat16 *>(a.dqkv) + ((size_t)bi * s + q) * 3 * hr + head * D +
+                             c8 * 8) = o;
 }
 
 // ------------------------------------------------------------------------------------------ host
@@ -566,29 +508,46 @@ static bool make_rows_map(CUtensorMap *m, const void *base, int rows, int cols, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+size_t attn_bwd_ws_floats(int b, int s, int heads, int d) {
+  const size_t nq = (size_t)(s + TQH - 1) / TQH;
+  return (size_t)b * heads * s * (1 + (size_t)d) + (size_t)b * heads * nq;
+}
+
 template <int D>
 static cudaError_t bwd_tc_d(const AttnArgs &a, cudaStream_t st) {
   using C = BwdCfg<D>;
-  constexpr int SMEM = C::DQ_SMEM > C::DKV_SMEM ? C::DQ_SMEM : C::DKV_SMEM;
   static bool attr[MAX_DEV] = {};
   const int dev = cur_device();
   if (!attr[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr[dev] = true;
   }
+  if (!a.dq_acc || !a.dq_sem || !a.delta) return cudaErrorInvalidValue;
   const int tokens = a.b * a.s, hr = a.heads * D;
-  CUtensorMap mq_full, mq_half, mo_full, mo_half;
-  if (!make_rows_map(&mq_full, a.qkv, tokens, 3 * hr, 3 * hr, TR) ||
-      !make_rows_map(&mq_half, a.qkv, tokens, 3 * hr, 3 * hr, TH) ||
-      !make_rows_map(&mo_full, a.dctx, tokens, hr, hr, TR) || !make_rows_map(&mo_half, a.dctx, tokens, hr, hr, TH))
+  CUtensorMap m_kv, m_q, m_o;
+  if (!make_rows_map(&m_kv, a.qkv, tokens, 3 * hr, 3 * hr, TKEY) ||
+      !make_rows_map(&m_q, a.qkv, tokens, 3 * hr, 3 * hr, TQH) || !make_rows_map(&m_o, a.dctx, tokens, hr, hr, TQH))
     return cudaErrorInvalidValue;
   const long nd = (long)tokens * a.heads;
   attn_delta_kernel<D><<<(unsigned)((nd + 255) / 256), 256, 0, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  dim3 grid(a.heads, a.b, 2 * ((a.s + TR - 1) / TR));
-  attn_bwd_tc_kernel<D><<<grid, NTHR, SMEM, st>>>(mq_full, mq_half, mo_full, mo_half, a);
+  AttnArgs ag = a;
+  if (ag.attn_group <= 0) {
+    static int g_env = -1;
+    if (g_env < 0) {
+      const char *e = getenv("MERAK_ATTN_BWD_GROUP");
+      g_env = e ? atoi(e) : 0;
+    }
+    ag.attn_group = g_env > 0 ? g_env : 32;
+  }
+  if (ag.attn_group > a.b * a.heads) ag.attn_group = a.b * a.heads;
+  const int grid = a.b * a.heads * ((a.s + TKEY - 1) / TKEY);
+  attn_bwd_tc_kernel<D><<<grid, NTHR, C::SMEM, st>>>(m_kv, m_q, m_o, ag);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const long nq = (long)a.b * a.heads * a.s * (D / 8);
+  attn_dq_out_kernel<D><<<(unsigned)((nq + 255) / 256), 256, 0, st>>>(ag);
   return cudaGetLastError();
 }
 
@@ -606,6 +565,7 @@ cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st) {
 template <int D>
 static cudaError_t bwd_preload() {
   cudaError_t e = touch_kernel((const void *)attn_delta_kernel<D>);
+  if (e == cudaSuccess) e = touch_kernel((const void *)attn_dq_out_kernel<D>);
   return e != cudaSuccess ? e : touch_kernel((const void *)attn_bwd_tc_kernel<D>);
 }
 

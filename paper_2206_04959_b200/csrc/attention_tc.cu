@@ -138,7 +138,10 @@ __global__ void __launch_bounds__(320, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // all 512 columns belong to this CTA, so the allocation starts at lane 0, column 0: a compile-time base
+  // keeps every TMEM address warp-uniform (single-instruction MMA issue, no per-lane broadcast loop)
+  if (*tmem_slot != 0u) __trap();
+  constexpr uint32_t tmem = 0u;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer

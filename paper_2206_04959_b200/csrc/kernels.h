@@ -88,12 +88,18 @@ struct AttnArgs {
   const void *dctx;  // bf16 [b*s, hr]          (bwd in)
   void *dqkv;        // bf16 [b*s, 3*hr]        (bwd out)
   float *delta;      // [b, H_r, s] rowsum(dO*O) workspace (bwd)
+  float *dq_acc;     // [b, H_r, s, d] fp32 dQ accumulator workspace (bwd; no initialisation needed)
+  int *dq_sem;       // [b, H_r, ceil(s/64)] dQ ordering counters (bwd; zero before the first launch,
+                     // left zero by every launch)
   int b, s, heads, d;
   int ld_ctx;        // row stride of ctx (elements; >= heads*d)
-  unsigned long long *dbg;  // diagnostics only (nullptr): per-CTA clock stamps of the backward
+  int attn_group;    // bwd: (sample, head) pairs per dispatch group (0 = default)
+  unsigned long long *dbg;  // bwd diagnostics only (nullptr): per-CTA clock stamps, 80 per CTA
 };
+// workspace of attn_bwd in floats: delta, dq_acc, dq_sem (in that order)
+size_t attn_bwd_ws_floats(int b, int s, int heads, int d);
 cudaError_t attn_fwd(const AttnArgs &a, cudaStream_t st);  // attention_tc.cu
-cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st);  // attention_bwd_tc.cu: delta kernel, then dQ + dK/dV tiles
+cudaError_t attn_bwd(const AttnArgs &a, cudaStream_t st);  // attention_bwd_tc.cu: delta kernel, then the key-tile kernel
 
 // ---------------------------------------------------------------- fp32 check mode (check_f32.cu)
 struct F32GemmArgs {  // C[M,N] (epi) sum_k A(m,k) B(n,k); A(m,k) = a_mn ? A[k*lda+m] : A[m*lda+k], same for B

@@ -181,13 +181,18 @@ def test_attention_fwd_bwd(b, s, H, d):
     dctx = torch.randn(b * s, hr, device="cuda", generator=g).bfloat16()
     ref.backward(dctx.float())
     dqkv = torch.zeros_like(qkv)
-    delta = torch.zeros(b, H, s, device="cuda")
-    assert lib().merak_test_attn_bwd(P(qkv), P(ctx), P(lse), P(dctx), P(dqkv), P(delta), b, s, H, d, S()) == 0
+    ws = torch.zeros(lib().merak_test_attn_bwd_ws_bytes(b, s, H, d), device="cuda", dtype=torch.uint8)
+    assert lib().merak_test_attn_bwd(P(qkv), P(ctx), P(lse), P(dctx), P(dqkv), P(ws), b, s, H, d, S()) == 0
     torch.cuda.synchronize()
     gq = q.grad.view(b * s, 3, hr)
     dq = dqkv.view(b * s, 3, hr)
     for i in range(3):
         assert rel(dq[:, i], gq[:, i]) < 2e-2, i
+    # deterministic (ordered dQ accumulation, counters left at zero): a second call is bit-identical
+    dqkv2 = torch.zeros_like(qkv)
+    assert lib().merak_test_attn_bwd(P(qkv), P(ctx), P(lse), P(dctx), P(dqkv2), P(ws), b, s, H, d, S()) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(dqkv, dqkv2)
 
 
 # ------------------------------------------------------------------------------------------- LN / AR

@@ -1,69 +1,47 @@
-"""Where a tcgen05 attention-backward CTA spends its time (per-CTA clock stamps, see
-attention_bwd_tc.cu dbg layout).  Prints one JSON summary."""
-import ctypes
-import json
-import os
-import sys
-
-import numpy as np
+"""Per-CTA clock stamps of the attention backward (AttnArgs::dbg, 80 x u64 per CTA): time per half-block
+of the MMA issuer (q_full / p_full acquisition), prologue, epilogue, CTA spans (diagnostics only)."""
+import ctypes, json, os, sys
 import torch
-
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2206_04959_b200.binding import lib  # noqa: E402
 
+b, s, H, d = (int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "2,2048,64,96").split(","))
+L = lib()
+L.merak_test_attn_bwd_dbg.argtypes = [ctypes.c_void_p] * 6 + [ctypes.c_int] * 4 + [ctypes.c_void_p, ctypes.c_void_p]
 P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
-
-
-def main():
-    b, s, H, d = (int(v) for v in (sys.argv[1:5] if len(sys.argv) > 4 else (4, 1024, 25, 64)))
-    hr = H * d
-    L = lib()
-    L.merak_test_attn_bwd_dbg.argtypes = [ctypes.c_void_p] * 6 + [ctypes.c_int] * 4 + [ctypes.c_void_p, ctypes.c_void_p]
-    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    qkv = torch.randn(b * s, 3 * hr, device="cuda").bfloat16()
-    ctx = torch.empty(b * s, hr, device="cuda").bfloat16()
-    lse = torch.empty(b, H, s, device="cuda")
-    dctx = torch.randn(b * s, hr, device="cuda").bfloat16()
-    dqkv = torch.empty_like(qkv)
-    delta = torch.empty(b, H, s, device="cuda")
-    assert L.merak_test_attn_fwd(P(qkv), P(ctx), P(lse), b, s, H, d, st) == 0
-    nq = (s + 127) // 128
-    ncta = nq * H * b
-    dbg = torch.zeros(2 * ncta * 64, dtype=torch.int64, device="cuda")
-    for _ in range(3):
-        assert L.merak_test_attn_bwd_dbg(P(qkv), P(ctx), P(lse), P(dctx), P(dqkv), P(delta), b, s, H, d, P(dbg), st) == 0
-    torch.cuda.synchronize()
-    # one merged launch, grid (H, b, 2 x tiles): role = z & 1 (even: dQ, odd: dK/dV)
-    A = dbg.cpu().numpy().astype(np.int64).reshape(2 * nq, H * b, 64)
-    D = [A[0::2].reshape(-1, 64), A[1::2].reshape(-1, 64)]
-    out = {}
-    for k, name in enumerate(("dq", "dkdv")):
-        X = D[k]
-        ns = (X[:, 57] - X[:, 56]).astype(np.float64)
-        cyc = (X[:, 61] - X[:, 0]).astype(np.float64)
-        ghz = float(np.median(cyc / np.maximum(ns, 1)))
-        n_it = X[:, 63]
-        pro = (X[:, 1] - X[:, 0]) / ghz / 1e3
-        first = (X[:, 2] - X[:, 1]) / ghz / 1e3
-        its = []
-        for c in range(ncta):
-            n = int(min(n_it[c], 54))
-            if n > 1:
-                its.extend(list(np.diff(X[c, 2:2 + n]) / ghz / 1e3))
-        epi = (X[:, 61] - X[:, 60]) / ghz / 1e3
-        tot = cyc / ghz / 1e3
-        t0 = min(D[0][:, 56].min(), D[1][:, 56].min())
-        span = (X[:, 57].max() - t0) / 1e3
-        out[name] = {"ctas": ncta, "kernel_span_us": round(span, 1), "clock_ghz": round(ghz, 3),
-                     "cta_total_us": {"mean": round(float(tot.mean()), 2), "max": round(float(tot.max()), 2)},
-                     "prologue_us_mean": round(float(pro.mean()), 2), "first_scores_us_mean": round(float(first.mean()), 2),
-                     "iter_us": {"mean": round(float(np.mean(its)), 3), "p50": round(float(np.median(its)), 3),
-                                 "p90": round(float(np.percentile(its, 90)), 3)},
-                     "epilogue_us_mean": round(float(epi.mean()), 2),
-                     "iters_mean": round(float(n_it.mean()), 2),
-                     "sum_cta_us_per_sm": round(float(tot.sum()) / 148, 1)}
-    print(json.dumps(out))
-
-
-if __name__ == "__main__":
-    main()
+st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+hr = H * d
+qkv = torch.randn(b * s, 3 * hr, device="cuda").bfloat16()
+ctx = torch.empty(b * s, hr, device="cuda", dtype=torch.bfloat16)
+lse = torch.empty(b, H, s, device="cuda")
+dctx = torch.randn(b * s, hr, device="cuda").bfloat16()
+dqkv = torch.empty_like(qkv)
+ws = torch.zeros(L.merak_test_attn_bwd_ws_bytes(b, s, H, d), device="cuda", dtype=torch.uint8)
+nkt = (s + 127) // 128
+ncta = b * H * nkt
+dbg = torch.zeros(ncta * 80, dtype=torch.int64, device="cuda")
+assert L.merak_test_attn_fwd(P(qkv), P(ctx), P(lse), b, s, H, d, st) == 0
+for _ in range(3):
+    assert L.merak_test_attn_bwd_dbg(P(qkv), P(ctx), P(lse), P(dctx), P(dqkv), P(ws), b, s, H, d, P(dbg), st) == 0
+torch.cuda.synchronize()
+D = dbg.view(ncta, 80).cpu().tolist()
+t0 = min(r[76] for r in D)
+t1 = max(r[78] for r in D)
+per_it, gaps_q, gaps_p, prol, epi = [], [], [], [], []
+for r in D:
+    ni = r[77]
+    prol.append(r[1] - r[0])
+    if ni >= 4:
+        q = [r[2 + i] for i in range(min(ni, 36))]
+        pp = [r[38 + i] for i in range(min(ni, 36))]
+        per_it.append((q[-1] - q[1]) / (len(q) - 2))
+        gaps_q += [pp[i] - q[i] for i in range(len(q))]
+        gaps_p += [q[i + 1] - pp[i] for i in range(len(q) - 1)]
+    epi.append(r[75] - r[74])
+med = lambda v: sorted(v)[len(v) // 2]  # noqa: E731
+print(json.dumps({"shape": [b, s, H, d], "kernel_span_us": (t1 - t0) / 1e3, "ctas": ncta,
+                  "cta_span_us_median": med([(r[78] - r[76]) / 1e3 for r in D]),
+                  "clk_per_halfblock_median": med(per_it), "prologue_clk_median": med(prol),
+                  "q_to_p_clk_median": med(gaps_q), "p_to_nextq_clk_median": med(gaps_p),
+                  "epilogue_clk_median": med(epi),
+                  "sum_cta_span_over_148_us": sum((r[78] - r[76]) for r in D) / 148 / 1e3}))

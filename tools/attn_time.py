@@ -15,20 +15,23 @@ SHAPES = [(2, 2048, 64, 96), (4, 1024, 25, 64), (4, 1024, 32, 80), (4, 1024, 32,
 
 
 def main():
+    shapes = SHAPES
+    if len(sys.argv) > 1:  # b,s,H,d[:b,s,H,d...]
+        shapes = [tuple(int(v) for v in x.split(",")) for x in sys.argv[1].split(":")]
     L = lib()
     P = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    for (b, s, H, d) in SHAPES:
+    for (b, s, H, d) in shapes:
         hr = H * d
         qkv = torch.randn(b * s, 3 * hr, device="cuda").bfloat16()
         ctx = torch.empty(b * s, hr, device="cuda", dtype=torch.bfloat16)
         lse = torch.empty(b, H, s, device="cuda")
         dctx = torch.randn(b * s, hr, device="cuda").bfloat16()
         dqkv = torch.empty_like(qkv)
-        delta = torch.empty(b, H, s, device="cuda")
+        ws = torch.zeros(L.merak_test_attn_bwd_ws_bytes(b, s, H, d), device="cuda", dtype=torch.uint8)
         res = {"b": b, "s": s, "H": H, "d": d}
         for name, fn in (("fwd", lambda: L.merak_test_attn_fwd(P(qkv), P(ctx), P(lse), b, s, H, d, st)),
-                         ("bwd", lambda: L.merak_test_attn_bwd(P(qkv), P(ctx), P(lse), P(dctx), P(dqkv), P(delta),
+                         ("bwd", lambda: L.merak_test_attn_bwd(P(qkv), P(ctx), P(lse), P(dctx), P(dqkv), P(ws),
                                                                b, s, H, d, st))):
             for _ in range(3):
                 assert fn() == 0
