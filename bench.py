@@ -224,20 +224,26 @@ class Stack:
                 del os.environ["MERAK_STREAMS"]
         self.saved = [self.layer.new_saved() for _ in range(L)]
 
-    def step(self, flags=0, X=None, DY=None):
+    def step(self, flags=0, X=None, DY=None, recompute=None):
         """L layers forward, then backward in reverse (overlap across layers): every call but the last
         backward passes MERAK_FLAG_CHAIN, so layer k+1's sub-batch 0 starts while layer k's last all-reduce is
-        in flight; the last backward joins the caller stream."""
-        from paper_2206_04959_b200 import FLAG_CHAIN
+        in flight; the last backward joins the caller stream.  recompute: per-layer bools -- those layers keep
+        no activations (their forward writes a shared scratch buffer) and regenerate them inside the backward
+        (MERAK_FLAG_RECOMPUTE)."""
+        from paper_2206_04959_b200 import FLAG_CHAIN, FLAG_RECOMPUTE
         X = self.X if X is None else X
         DY = self.DY if DY is None else DY
         L, lay = self.L, self.layer
+        rc = list(recompute) if recompute is not None else [False] * L
+        if any(rc) and getattr(self, "scratch", None) is None:
+            self.scratch = lay.new_saved()
+        sv = [self.scratch if rc[k] else self.saved[k] for k in range(L)]
         for k in range(L):
-            lay.forward(self.ws[k], X if k == 0 else self.Ys[k - 1], self.Ys[k], self.saved[k], flags=flags | FLAG_CHAIN)
+            lay.forward(self.ws[k], X if k == 0 else self.Ys[k - 1], self.Ys[k], sv[k], flags=flags | FLAG_CHAIN)
         for k in reversed(range(L)):
-            lay.backward(self.ws[k], X if k == 0 else self.Ys[k - 1], self.saved[k],
+            lay.backward(self.ws[k], X if k == 0 else self.Ys[k - 1], sv[k],
                          DY if k == L - 1 else self.DXs[k + 1], self.DXs[k], self.grads[k],
-                         flags=flags | (FLAG_CHAIN if k > 0 else 0))
+                         flags=flags | (FLAG_CHAIN if k > 0 else 0) | (FLAG_RECOMPUTE if rc[k] else 0))
 
     def close(self):
         self.layer.close()
@@ -291,7 +297,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
-    def timed(st, nsteps, flags=0, prof=False):
+    def timed(st, nsteps, flags=0, prof=False, recompute=None):
         """nsteps back-to-back steps between one pair of CUDA events on the caller stream, bracketed by
         synchronize + barrier; returns (max-over-ranks ms per step, kernel launches, profile)."""
         if prof:
@@ -301,7 +307,7 @@ def main():
         barrier()
         e0.record(stream)
         for _ in range(nsteps):
-            st.step(flags)
+            st.step(flags, recompute=recompute)
         e1.record(stream)
         barrier()
         launches = st.layer.launch_count() - l0
@@ -364,6 +370,8 @@ def main():
         extras["roofline"], extras["serialized_ms_per_step"] = roofline_pass(cfg, L, T, rank, dev, group, n_sub, args,
                                                                              timed, value)
         stage("profiling pass done")
+        extras["recompute"] = recompute_pass(cfg, L, stack, timed, ms_step, nx)
+        stage("recompute pass done")
         extras["side_workloads"] = side_workloads(args, T, rank, dev, group, timed, stack)
         stage("side workloads done")
 
@@ -468,6 +476,45 @@ def e2e_pass(stack, ne, world, rank, dev, fl, dist, barrier, max_over_ranks):
                     "(one event pair around back-to-back steps); the extra join after the last forward (y must be "
                     "complete before its download) is the only schedule difference; at T > 1 each rank moves its "
                     "1/T row slice over PCIe and the inputs are all-gathered over NVLink (NCCL); bytes are per GPU"}
+
+
+def recompute_pass(cfg, L, stack, timed, ms_step, nx):
+    """the same stack with every layer recomputing its activations in
+    the backward (MERAK_FLAG_RECOMPUTE), and the stage-aware plan (merak_tune_alpha1 / merak_stage_alpha) for a
+    pipeline of s stages of these L layers on this GPU's memory, timed with stage 1's recompute count."""
+    import torch
+
+    from paper_2206_04959_b200.planner import recompute_plan
+    all_rc = [True] * L
+    stack.step(recompute=all_rc)
+    ms_rc, _, _ = timed(stack, nx, recompute=all_rc)
+    lay = stack.layer
+    sb = lay.saved_bytes()
+    wbytes = sum(t.numel() * t.element_size() for t in stack.ws[0].values())
+    gbytes = sum(t.numel() * t.element_size() for t in stack.grads[0].values())
+    cap = float(torch.cuda.get_device_properties(stack.dev).total_memory)
+    # runtime memory of a stage of L layers: weights + fp32 grads + one microbatch's activations (the one being
+    # computed) + the boundary activations / workspace (x, y, dy, dx per layer), M_a = one microbatch's
+    # activations of the stage
+    act_io = 4 * stack.X.numel() * stack.X.element_size()
+    m_r = L * (wbytes + gbytes + act_io) + L * sb
+    out = {"all_layers_recompute_ms_per_step": ms_rc, "no_recompute_ms_per_step": ms_step,
+           "recompute_overhead_frac": ms_rc / ms_step - 1.0, "saved_bytes_per_layer": sb,
+           "note": "recompute regenerates LN1, QKV, attention, proj + AR#1 + LN2, fc1 + GeLU (fc2 / AR#2 skipped); "
+                   "bit-identical results (tests/test_gpu_recompute.py)", "plans": {}}
+    for s in (4, 8):
+        try:
+            plan = recompute_plan(s, L, cap, m_r, sb)
+        except Exception as e:  # noqa: BLE001  (runtime memory alone exceeds capacity)
+            out["plans"][f"s{s}"] = {"error": str(e)}
+            continue
+        keep0 = plan["layers_kept"][0]
+        rc = [k >= keep0 for k in range(L)]  # stage 1 keeps the activations of its first layers_kept[0] layers
+        ms_plan = timed(stack, nx, recompute=rc)[0] if keep0 < L else ms_step
+        plan.update({"stage1_recomputed_layers": L - keep0, "stage1_ms_per_step": ms_plan,
+                     "capacity_bytes": cap, "m_r_bytes": m_r, "m_a_bytes": L * sb})
+        out["plans"][f"s{s}"] = plan
+    return out
 
 
 def roofline_pass(cfg, L, T, rank, dev, group, n_sub, args, timed, value):

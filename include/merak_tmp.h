@@ -105,8 +105,20 @@ enum {
   MERAK_FLAG_CHAIN = 1u,   /* do not join the caller stream at the end; the next merak call
                               on this handle (or merak_tmp_join) joins.  Lets layer k+1's first
                               sub-batch start while layer k's last all-reduce is in flight.        */
-  MERAK_FLAG_NO_COMM = 2u  /* measurement only: every all-reduce reads the local partial alone
+  MERAK_FLAG_NO_COMM = 2u, /* measurement only: every all-reduce reads the local partial alone
                               (wrong result for T > 1); used to measure exposed communication.   */
+  MERAK_FLAG_RECOMPUTE = 4u /* activation recomputation ("the recomputation ... could be
+                              estimated as T_m").  layer_bwd: `saved` is a
+                              SCRATCH buffer of merak_tmp_saved_bytes() bytes whose contents on entry
+                              are ignored; the backward first regenerates every activation it reads
+                              from x (the attention block incl. AR#1 / LN2, and fc1 + GeLU; fc2 and
+                              AR#2 are not needed), then runs as usual.  layer_fwd: that
+                              regeneration alone (a separately schedulable recompute pass, e.g. the
+                              early recomputation of P:461); y is not written and may be NULL.
+                              Results are bit-identical to a backward on the forward's own `saved`,
+                              so a forward whose activations are recomputed may write its `saved`
+                              into the same scratch buffer that every recomputed layer shares.
+                              Collective (it contains AR#1).  EUNSUPPORTED in fp32 check mode.     */
 };
 
 typedef struct {
@@ -174,7 +186,8 @@ merak_status merak_tmp_layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, con
                                  void *saved, uint32_t flags, void *st);
 
 /* Backward: reads x, `saved` (from the matching layer_fwd), dy; writes dx
- * ([B*s, h] bf16) and ACCUMULATES fp32 gradients into *g.  Collective over the TMP group. */
+ * ([B*s, h] bf16) and ACCUMULATES fp32 gradients into *g.  Collective over the TMP group.
+ * With MERAK_FLAG_RECOMPUTE, `saved` is written (regenerated from x) before it is read. */
 merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const void *x,
                                  const void *saved, const void *dy, void *dx, const merak_tmp_grads *g,
                                  uint32_t flags, void *st);

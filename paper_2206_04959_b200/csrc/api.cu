@@ -399,8 +399,12 @@ static merak_status leave(merak_tmp_t *h, cudaStream_t st, uint32_t flags, int l
 }
 
 // ------------------------------------------------------------------------------ forward
+// recompute = true: the activation-recomputation pass of a MERAK_FLAG_RECOMPUTE backward (SURVEY §8(f) NEXT-3,
+// P:459): everything the backward reads is regenerated into `saved` -- the attention block with AR#1 / LN2 and
+// fc1 + GeLU -- while fc2 and AR#2 (whose output y the backward never reads) are skipped.  It leaves the chain
+// open with each sub-batch's stream event after its fc1, so the backward's first kernels follow directly.
 static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const bf16 *x, bf16 *y, char *saved,
-                              uint32_t flags, cudaStream_t st) {
+                              uint32_t flags, cudaStream_t st, bool recompute = false) {
   const SavedLayout L = saved_layout(h);
   const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr;
   const bool comm = !(flags & MERAK_FLAG_NO_COMM) && !h->local;
@@ -475,6 +479,10 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     GemmArgs g = gargs(u2, w->w_1, m, fr, hh, L.ld_u2, hh, false, false, EPI_BIAS_GELU);
     g.out = z; g.ldo = fr; g.out2 = gg; g.ldo2 = L.ld_g; g.bias = w->b_1;
     TRY(run_gemm(h, g, cst));
+    if (recompute) {
+      CK(h, cudaEventRecord(h->ev_p[j], cst));
+      continue;
+    }
     if (h->ev_ar_valid[1][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[1][j], 0));
     g = gargs(gg, w->w_2, m, hh, fr, L.ld_g, fr, false, false, EPI_STORE_BF16);
     g.out = slot_ptr(h, h->r, 1) + r0 * hh; g.ldo = hh;
@@ -497,6 +505,11 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     }
     CK(h, cudaEventRecord(h->ev_ar[1][j], h->ms));
     h->ev_ar_valid[1][j] = true;
+  }
+  if (recompute) {
+    TRY(leave(h, st, flags, 0));
+    for (int j = 0; j < n; ++j) h->prev_out[j] = h->ev_p[j];  // fc1(j) done (after AR#1(j) on its stream)
+    return MERAK_OK;
   }
   return leave(h, st, flags, 1);
 }
@@ -1178,14 +1191,16 @@ static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 merak_status merak_tmp_layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const void *x, void *y, void *saved,
                                  uint32_t flags, void *st) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
-  if (!w || !x || !y || !saved) return fail(h, MERAK_EINVAL, "NULL argument");
-  const void *ps[] = {w->ln1_g, w->ln1_b, w->w_qkv, w->b_qkv, w->w_o, w->b_o, w->ln2_g, w->ln2_b, w->w_1, w->b_1, w->w_2, w->b_2, x, y, saved};
+  const bool rc = (flags & MERAK_FLAG_RECOMPUTE) != 0;  // regenerate `saved` only: y is not written
+  if (rc && h->f32) return fail(h, MERAK_EUNSUPPORTED, "MERAK_FLAG_RECOMPUTE is not available in the fp32 check mode");
+  if (!w || !x || (!y && !rc) || !saved) return fail(h, MERAK_EINVAL, "NULL argument");
+  const void *ps[] = {w->ln1_g, w->ln1_b, w->w_qkv, w->b_qkv, w->w_o, w->b_o, w->ln2_g, w->ln2_b, w->w_1, w->b_1, w->w_2, w->b_2, x, rc ? x : y, saved};
   for (const void *p : ps)
     if (!p || !aligned16(p)) return fail(h, MERAK_EINVAL, "NULL or non-16B-aligned pointer");
   if (h->broken) return fail(h, MERAK_ESTATE, "handle unusable after an earlier failure: %s", h->err.c_str());
   const uint32_t e0 = h->epoch;
   const merak_status s = h->f32 ? layer_fwd_f32(h, w, (const float *)x, (float *)y, (char *)saved, flags, (cudaStream_t)st)
-                                : layer_fwd(h, w, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st);
+                                : layer_fwd(h, w, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st, rc);
   if (s != MERAK_OK && (h->epoch != e0 || s == MERAK_ETIMEOUT)) h->broken = true;
   return s;
 }
@@ -1200,7 +1215,18 @@ merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, con
   for (const void *p : ps)
     if (!p || !aligned16(p)) return fail(h, MERAK_EINVAL, "NULL or non-16B-aligned pointer");
   if (h->broken) return fail(h, MERAK_ESTATE, "handle unusable after an earlier failure: %s", h->err.c_str());
+  if ((flags & MERAK_FLAG_RECOMPUTE) && h->f32)
+    return fail(h, MERAK_EUNSUPPORTED, "MERAK_FLAG_RECOMPUTE is not available in the fp32 check mode");
   const uint32_t e0 = h->epoch;
+  if (flags & MERAK_FLAG_RECOMPUTE) {  // regenerate `saved` (scratch) from x, then the backward proper
+    const merak_status r = layer_fwd(h, w, (const bf16 *)x, nullptr, (char *)const_cast<void *>(saved),
+                                     MERAK_FLAG_CHAIN | (flags & MERAK_FLAG_NO_COMM), (cudaStream_t)st, true);
+    // (the backward below continues the open chain: its sub-batch streams follow each fc1 directly)
+    if (r != MERAK_OK) {
+      if (h->epoch != e0 || r == MERAK_ETIMEOUT) h->broken = true;
+      return r;
+    }
+  }
   const merak_status s =
       h->f32 ? layer_bwd_f32(h, w, (const float *)x, (const char *)saved, (const float *)dy, (float *)dx, g, flags,
                              (cudaStream_t)st)

@@ -61,12 +61,16 @@ def compare_to_oracle(out, y_ref, dx_ref, grads_ref_rank, cfg, tol=TOL_BF16):
     return errs, bad
 
 
-def run_gpu_chain(cfg, params_list, x, dy, T=1, rank=0, group=None, chain=True, n_sub=None):
+def run_gpu_chain(cfg, params_list, x, dy, T=1, rank=0, group=None, chain=True, n_sub=None, recompute=None,
+                  early=False):
     """K stacked layers through the C ABI: forward 0..K-1, backward K-1..0.  chain=True passes
     MERAK_FLAG_CHAIN on every call but the last backward (cross-layer overlap, the bench's mode), so
     the library's cross-layer event hazards (workspace reuse between layers) are exercised.
+    recompute: per-layer bools -- those layers write their forward activations into ONE shared scratch
+    buffer and regenerate them in the backward (MERAK_FLAG_RECOMPUTE); early=True runs the regeneration as
+    a separate forward call (MERAK_FLAG_RECOMPUTE on layer_fwd) just before the layer's backward.
     Returns dict: y (last layer), dx (first layer), grads[k]."""
-    from paper_2206_04959_b200 import FLAG_CHAIN
+    from paper_2206_04959_b200 import FLAG_CHAIN, FLAG_RECOMPUTE
     dev = torch.device("cuda", torch.cuda.current_device())
     K = len(params_list)
     n = cfg.n_sub if n_sub is None else n_sub
@@ -79,13 +83,23 @@ def run_gpu_chain(cfg, params_list, x, dy, T=1, rank=0, group=None, chain=True, 
     Ys = [torch.empty_like(X) for _ in range(K)]
     DXs = [torch.empty_like(X) for _ in range(K)]
     grads = [zero_grads_like(w) for w in ws]
-    saved = [layer.new_saved() for _ in range(K)]
+    rc = list(recompute) if recompute is not None else [False] * K
+    scratch = layer.new_saved() if any(rc) else None
+    saved = [scratch if rc[k] else layer.new_saved() for k in range(K)]
     f = FLAG_CHAIN if chain else 0
     for k in range(K):
         layer.forward(ws[k], X if k == 0 else Ys[k - 1], Ys[k], saved[k], flags=f)
+    if scratch is not None:  # nothing may depend on what the forwards left in the scratch buffer
+        torch.cuda.synchronize()
+        scratch.fill_(0xFF)
     for k in reversed(range(K)):
-        layer.backward(ws[k], X if k == 0 else Ys[k - 1], saved[k], DY if k == K - 1 else DXs[k + 1], DXs[k],
-                       grads[k], flags=f if k > 0 else 0)
+        xin = X if k == 0 else Ys[k - 1]
+        bf = f if k > 0 else 0
+        if rc[k] and early:
+            layer.forward(ws[k], xin, None, saved[k], flags=f | FLAG_RECOMPUTE)
+        elif rc[k]:
+            bf |= FLAG_RECOMPUTE
+        layer.backward(ws[k], xin, saved[k], DY if k == K - 1 else DXs[k + 1], DXs[k], grads[k], flags=bf)
     torch.cuda.synchronize()
     out = {"y": Ys[K - 1].clone(), "dx": DXs[0].clone(), "grads": [{k: g[k].clone() for k in PARAM_NAMES}
                                                                   for g in grads]}
