@@ -374,6 +374,9 @@ def main():
         stage("recompute pass done")
         extras["side_workloads"] = side_workloads(args, T, rank, dev, group, timed, stack)
         stage("side workloads done")
+        if world > 1:
+            extras["pipeline"] = pipeline_pass(args, rank, world, dev, barrier, max_over_ranks)
+            stage("pipeline pass done")
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -514,6 +517,67 @@ def recompute_pass(cfg, L, stack, timed, ms_step, nx):
         plan.update({"stage1_recomputed_layers": L - keep0, "stage1_ms_per_step": ms_plan,
                      "capacity_bytes": cap, "m_r_bytes": m_r, "m_a_bytes": L * sb})
         out["plans"][f"s{s}"] = plan
+    return out
+
+
+def pipeline_pass(args, rank, world, dev, barrier, max_over_ranks, K=2, layer_cfg="gpt1.5b"):
+    """a pipeline of P = N stages (one per GPU, T = 1 each), K layers of the
+    gpt1.5b shape per stage, m = 2P microbatches, driven by each schedule of merak_pipeline_schedule over NCCL
+    point-to-point.  Per policy: iteration time (max over ranks) and the measured bubble ratio against the
+    stage's own busy time -- the same actions run back to back on each GPU with no inputs to wait for (max
+    over ranks) -- next to the paper's ratio (P:460 (s-1)/m, P:461 3(s-1)/(4m), P:470 3(s-2)/(4m))."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2206_04959_b200 import TmpLayer, shard_weights, zero_grads_like
+    from paper_2206_04959_b200.pipeline import PipelineStage, run_distributed, schedule
+    from synth import CONFIGS, make_activations_torch, make_params_torch
+    cfg = CONFIGS[layer_cfg].with_(tmp_degree=1)
+    s, m = world, 2 * world
+    fwd_g, bwd_g = dist.new_group(list(range(world))), dist.new_group(list(range(world)))
+    lay = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, n_sub=cfg.n_sub, device=dev.index)
+    ws = [shard_weights(make_params_torch(cfg, dev, layer=rank * K + k), cfg.heads, 1, 0, dev) for k in range(K)]
+    grads = [zero_grads_like(w) for w in ws]
+    X, DY = make_activations_torch(cfg, dev)
+    xs, dys = [X] * m, [DY] * m
+    shape, dt = (cfg.tokens, cfg.hidden), torch.bfloat16
+    paper = {"1f1b": (s - 1) / m, "early": 3 * (s - 1) / (4 * m), "scp": 3 * (s - 2) / (4 * m),
+             "none": (s - 1) / m}
+    out = {"stages": s, "microbatches": m, "layers_per_stage": K, "layer_config": layer_cfg, "tmp_degree": 1,
+           "policies": {}}
+    stream = torch.cuda.current_stream()
+
+    def run(actions, solo):
+        acts = actions
+        # stages whose schedule recomputes nothing (SCP's last stage, "none") keep every layer's activations
+        kept = 0 if any(k in ("R", "BR") for k, _ in acts) else K
+        st = PipelineStage(lay, ws, grads, rank, s, kept=kept)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        if solo:  # the stage's own work back to back: no waiting for neighbours (pure busy time)
+            for kind, mb in acts:
+                if kind == "F":
+                    st.forward(mb, X)
+                elif kind == "R":
+                    st.recompute(mb)
+                else:
+                    st.backward(mb, DY, fused_recompute=kind == "BR")
+        else:
+            run_distributed(st, acts, xs, dys, fwd_g, bwd_g, shape, dt, dev)
+        e1.record(stream)
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1))
+
+    for pol in ("1f1b", "early", "scp", "none"):
+        acts = schedule(pol, s, m)[rank]
+        for _ in range(2):
+            run(acts, False)
+        it = min(run(acts, False) for _ in range(3))
+        busy = min(run(acts, True) for _ in range(2))
+        out["policies"][pol] = {"iteration_ms": it, "stage_busy_ms": busy, "measured_bubble_ratio": it / busy - 1.0,
+                                "paper_bubble_ratio": paper[pol]}
+    lay.close()
     return out
 
 

@@ -36,6 +36,44 @@ int merak_tune_alpha1(int32_t stages, double step, double capacity, double m_r, 
 /* Layers of a K-layer stage that keep activations under alpha (rounded down to whole layers). */
 int32_t merak_layers_kept(double alpha, int32_t layers);
 
+/* ---- pipeline schedules of a K-layer TMP stage (§6.1) ---------------
+ * One action per int32: (kind << 24) | microbatch.  Kinds:
+ *   MERAK_ACT_F   forward of microbatch mb through the stage (keeps each layer's input; the layers that keep
+ *                 their activations keep them, the others write a scratch buffer);
+ *   MERAK_ACT_R   recomputation of mb's activations (layer_fwd with MERAK_FLAG_RECOMPUTE for every recomputed
+ *                 layer); "the activation recomputation operation does not depend on the output of previous
+ *                 stages", so it runs as soon as the stage reaches it;
+ *   MERAK_ACT_B   backward of mb on activations that exist (kept or recomputed by an earlier R);
+ *   MERAK_ACT_BR  backward of mb with the recomputation fused in front of it (layer_bwd with
+ *                 MERAK_FLAG_RECOMPUTE): it starts only once mb's gradient has arrived (Fig. 5a's 1F1B).
+ * A forward on stage j > 0 receives mb's activation from stage j-1; a backward on stage j < s-1 receives mb's
+ * gradient from stage j+1 (sends are implied by the producer's F / B / BR).
+ * Policies:
+ *   MERAK_PIPE_1F1B            Fig. 5a: stage j runs min(s-1-j, m) warm-up forwards, then one forward / one
+ *                              backward alternately, then drains the backwards; every backward is BR.
+ *                              Bubble (s-1)(T_m + T_m + 2T_m), ratio (s-1)/m.
+ *   MERAK_PIPE_EARLY_RECOMPUTE Fig. 5b: the same order with each backward split into R then B, so the
+ *                              recomputation no longer waits for the gradient.  Bubble (s-1)(T_m + 2T_m),
+ *                              ratio 3(s-1)/(4m).
+ *   MERAK_PIPE_SCP             Fig. 5c, shifted critical path: EARLY_RECOMPUTE with (a) no
+ *                              recomputation on the last stage ("the last stage only stores one activation":
+ *                              its backwards are B), (b) on stage s-2, one forward brought ahead into the
+ *                              warm-up bubble (the first forward after its first R / B moves in front of
+ *                              them), (c) its first backwards' recomputations following that order.  Bubble
+ *                              3(s-2)T_m, ratio 3(s-2)/(4m) for m >= max(s, 3).  Needs s >= 2 (EINVAL).
+ *   MERAK_PIPE_1F1B_NO_RECOMPUTE  1F1B with every activation kept (F and B only).
+ * actions: host array of stages x capacity int32; row j receives stage j's ordered actions and count[j]
+ * their number (3 m at most).  EINVAL: bad policy / sizes; ENOMEM: capacity < 3 m. */
+enum {
+  MERAK_PIPE_1F1B = 0,
+  MERAK_PIPE_EARLY_RECOMPUTE = 1,
+  MERAK_PIPE_SCP = 2,
+  MERAK_PIPE_1F1B_NO_RECOMPUTE = 3
+};
+enum { MERAK_ACT_F = 0, MERAK_ACT_R = 1, MERAK_ACT_B = 2, MERAK_ACT_BR = 3 };
+int merak_pipeline_schedule(int32_t policy, int32_t stages, int32_t microbatches, int32_t *actions,
+                            int32_t capacity, int32_t *count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,9 +1,12 @@
 // schedule.cu -- host-side planners of the C ABI in include/merak_sched.h (no device code).
 //
-// Stage-aware recomputation.  Read each function against the passage
-// it cites; the fp64 oracle (oracle/stage.py) restates the same passages independently for the tests.
+// Stage-aware recomputation and the pipeline schedules of a K-layer TMP
+// stage (NEXT-4).  Read each function against the passage it cites; the oracle (oracle/stage.py,
+// oracle/pipeline.py) restates the passages independently and simulates the schedules for the tests.
 #include <math.h>
 #include <stddef.h>
+
+#include <vector>
 
 #include "merak_sched.h"
 #include "merak_tmp.h"
@@ -67,4 +70,69 @@ extern "C" int32_t merak_layers_kept(double alpha, int32_t layers) {
   if (layers <= 0 || !(alpha > 0.0)) return 0;
   if (alpha >= 1.0) return layers;
   return (int32_t)floor(alpha * (double)layers + 1e-9);
+}
+
+// ------------------------------------------------------------------------------------ pipeline schedules
+namespace {
+
+inline int32_t act(int kind, int mb) { return (kind << 24) | mb; }
+inline int kind_of(int32_t a) { return a >> 24; }
+
+// P:460 / Fig. 5a order on stage j of s with m microbatches: min(s-1-j, m) warm-up forwards, then one
+// forward / one backward, then the remaining backwards.  `bwd` lists the action kinds of one backward.
+std::vector<int32_t> one_f_one_b(int s, int m, int j, const std::vector<int> &bwd) {
+  std::vector<int32_t> a;
+  const int w = (s - 1 - j) < m ? (s - 1 - j) : m;
+  int f = 0, b = 0;
+  for (; f < w; ++f) a.push_back(act(MERAK_ACT_F, f));
+  auto backward = [&]() {
+    for (int k : bwd) a.push_back(act(k, b));
+    ++b;
+  };
+  while (f < m) {
+    a.push_back(act(MERAK_ACT_F, f++));
+    backward();
+  }
+  while (b < m) backward();
+  return a;
+}
+
+}  // namespace
+
+extern "C" int merak_pipeline_schedule(int32_t policy, int32_t stages, int32_t microbatches, int32_t *actions,
+                                       int32_t capacity, int32_t *count) {
+  const int s = stages, m = microbatches;
+  if (s < 1 || m < 1 || m >= (1 << 24) || !actions || !count) return MERAK_EINVAL;
+  if (policy < MERAK_PIPE_1F1B || policy > MERAK_PIPE_1F1B_NO_RECOMPUTE) return MERAK_EINVAL;
+  if (policy == MERAK_PIPE_SCP && s < 2) return MERAK_EINVAL;
+  if (capacity < 3 * m) return MERAK_ENOMEM;
+  for (int j = 0; j < s; ++j) {
+    std::vector<int32_t> a;
+    switch (policy) {
+      case MERAK_PIPE_1F1B: a = one_f_one_b(s, m, j, {MERAK_ACT_BR}); break;
+      case MERAK_PIPE_1F1B_NO_RECOMPUTE: a = one_f_one_b(s, m, j, {MERAK_ACT_B}); break;
+      case MERAK_PIPE_EARLY_RECOMPUTE: a = one_f_one_b(s, m, j, {MERAK_ACT_R, MERAK_ACT_B}); break;
+      case MERAK_PIPE_SCP:
+        if (j == s - 1) {  // (a) "drop the recomputation of the last stage"
+          a = one_f_one_b(s, m, j, {MERAK_ACT_B});
+        } else {
+          a = one_f_one_b(s, m, j, {MERAK_ACT_R, MERAK_ACT_B});
+          if (j == s - 2) {  // (b) "bring one forward pass computation of the second to last stage ahead"
+            size_t first_rb = 0;
+            while (first_rb < a.size() && kind_of(a[first_rb]) == MERAK_ACT_F) ++first_rb;
+            size_t nf = first_rb;
+            while (nf < a.size() && kind_of(a[nf]) != MERAK_ACT_F) ++nf;
+            if (nf < a.size()) {  // (c) the first backwards' recomputations then follow that forward
+              const int32_t f = a[nf];
+              a.erase(a.begin() + (long)nf);
+              a.insert(a.begin() + (long)first_rb, f);
+            }
+          }
+        }
+        break;
+    }
+    count[j] = (int32_t)a.size();
+    for (size_t k = 0; k < a.size(); ++k) actions[(size_t)j * capacity + k] = a[k];
+  }
+  return MERAK_OK;
 }
