@@ -375,6 +375,8 @@ def main():
         extras["side_workloads"] = side_workloads(args, T, rank, dev, group, timed, stack)
         stage("side workloads done")
         if world > 1:
+            extras["nvls"] = nvls_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step)
+            stage("nvls pass done")
             extras["pipeline"] = pipeline_pass(args, rank, world, dev, barrier, max_over_ranks)
             stage("pipeline pass done")
 
@@ -518,6 +520,33 @@ def recompute_pass(cfg, L, stack, timed, ms_step, nx):
                      "capacity_bytes": cap, "m_r_bytes": m_r, "m_a_bytes": L * sb})
         out["plans"][f"s{s}"] = plan
     return out
+
+
+def nvls_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step):
+    """the same stack with MERAK_COMM_NVLS (reduce-scatter phase in the NVSwitch with
+    multimem.ld_reduce / multimem.st): per-GPU TFLOP/s, exposed all-reduce, and the all-reduce alone."""
+    from paper_2206_04959_b200 import FLAG_NO_COMM, MERAK_COMM_NVLS, MerakError
+    nx = max(3, args.steps // 2)
+    try:
+        st = Stack(cfg, L, T, rank, dev, group, n_sub, comm=MERAK_COMM_NVLS, comm_ctas=args.comm_ctas)
+    except MerakError as e:
+        return {"unavailable": str(e)}
+    for _ in range(3):
+        st.step()
+    ms, _, _ = timed(st, nx)
+    ms_nc, _, _ = timed(st, nx, flags=FLAG_NO_COMM)
+    rows = cfg.tokens // n_sub
+    t_f = st.layer.bench_allreduce(0, rows, 20)
+    t_b = st.layer.bench_allreduce(1, rows, 20)
+    st.close()
+    fl = L * layer_flops(cfg)
+    msg = rows * cfg.hidden * 2
+    return {"tflops_per_gpu": fl / T / (ms * 1e-3) / 1e12, "ms_per_step": ms, "vs_peer_two_shot": ms_step / ms,
+            "exposed_allreduce_ms_per_layer": (ms - ms_nc) / L, "exposed_allreduce_frac": (ms - ms_nc) / ms,
+            "allreduce": {"rows": rows, "msg_bytes": msg, "fwd_ar_us": t_f * 1e3, "bwd_ar_us": t_b * 1e3,
+                          "algbw_GBps": msg / (t_f * 1e-3) / 1e9,
+                          "note": "algorithmic bandwidth = message bytes / time (the all-reduce of one [m, h] bf16 "
+                                  "partial incl. handshakes); NVLS moves ~(1 + 1/T) x msg per GPU and direction"}}
 
 
 def pipeline_pass(args, rank, world, dev, barrier, max_over_ranks, K=2, layer_cfg="gpt1.5b"):

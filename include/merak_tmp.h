@@ -98,7 +98,15 @@ enum { MERAK_BF16 = 0, MERAK_FP32_CHECK = 1 };      /* merak_tmp_config.precisio
  * slots (same context, no CUDA IPC), with the same handshake, kernels and arithmetic as MERAK_COMM_PEER.
  * It exists so that T > 1 runs of the method (P:107 partial sums over T ranks, P:571 sub-batch overlap)
  * can be checked against the oracle on a single GPU.  Not for throughput (the ranks share one GPU). */
-enum { MERAK_COMM_PEER = 0, MERAK_COMM_NCCL = 1, MERAK_COMM_LOCAL = 2, MERAK_COMM_INPROC = 3 };
+/* MERAK_COMM_NVLS: as MERAK_COMM_PEER, but the all-reduce slots of the T ranks are bound to one CUDA
+ * multicast object (NVLink SHARP) and the reduce-scatter phase runs in the NVSwitch:
+ * rank r reads the rows it owns with multimem.ld_reduce (the switch sums the T bf16 partials with fp32
+ * accumulation and returns them rounded once to bf16 -- reading R10n) and broadcasts the result
+ * (plus bias and residual in the forward, rounded again) with multimem.st into every rank's slot; the fused
+ * epilogue then reads every row locally.  Init exchanges the multicast handle as a POSIX descriptor
+ * (pidfd_getfd: the ranks must run as the same user).  EUNSUPPORTED when a device lacks multicast support
+ * or in the fp32 check mode.  Same call sequence and results (up to the switch's rounding) as PEER. */
+enum { MERAK_COMM_PEER = 0, MERAK_COMM_NCCL = 1, MERAK_COMM_LOCAL = 2, MERAK_COMM_INPROC = 3, MERAK_COMM_NVLS = 4 };
 
 /* flags for layer_fwd / layer_bwd */
 enum {

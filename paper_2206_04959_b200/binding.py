@@ -19,7 +19,7 @@ MERAK_ECUDA, MERAK_EPEER, MERAK_ENOMEM, MERAK_ETIMEOUT, MERAK_ESTATE = -4, -5, -
 STATUS_NAMES = {0: "OK", -1: "EINVAL", -2: "EINDIVISIBLE", -3: "EUNSUPPORTED", -4: "ECUDA", -5: "EPEER",
                 -6: "ENOMEM", -7: "ETIMEOUT", -8: "ESTATE"}
 MERAK_BF16, MERAK_FP32_CHECK = 0, 1
-MERAK_COMM_PEER, MERAK_COMM_NCCL, MERAK_COMM_LOCAL, MERAK_COMM_INPROC = 0, 1, 2, 3
+MERAK_COMM_PEER, MERAK_COMM_NCCL, MERAK_COMM_LOCAL, MERAK_COMM_INPROC, MERAK_COMM_NVLS = 0, 1, 2, 3, 4
 FLAG_CHAIN, FLAG_NO_COMM, FLAG_RECOMPUTE = 1, 2, 4
 KERNEL_CLASSES = ("gemm", "attn_fwd", "attn_bwd", "layernorm", "allreduce", "reduce")
 PARAM_NAMES = ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_o", "b_o", "ln2_g", "ln2_b", "w_1", "b_1", "w_2", "b_2")

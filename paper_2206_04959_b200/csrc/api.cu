@@ -117,6 +117,8 @@ struct merak_tmp {
   std::string err;
   ncclComm_t nccl = nullptr;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // watchdog (env MERAK_AR_TIMEOUT_MS)
+  bool use_nvls = false;  // MERAK_COMM_NVLS: slots bound to a multicast object, phase 1 reduced in the switch
+  Nvls nvls = {};
   bool two_shot = false;  // T >= 4: reduce-scatter + all-gather instead of one-shot (env MERAK_AR_TWO_SHOT)
   bool pdl = false;       // programmatic dependent launch along the all-reduce kernel chain (env MERAK_AR_PDL)
   int gemm_smem_kb = 192;  // GEMM TMA ring: 160 KB at T > 1 leaves smem for co-resident all-reduce kernels
@@ -254,6 +256,8 @@ static PeerSync make_sync(merak_tmp_t *h, bool comm) {
 }
 
 static bf16 *slot_ptr(merak_tmp_t *h, int rank, int slot) {
+  if (h->use_nvls)  // own slots only (multicast-bound memory, unicast mapping); peers' are reached by the switch
+    return reinterpret_cast<bf16 *>(reinterpret_cast<char *>(h->nvls.uc_va) + (size_t)slot * h->slot_bytes);
   return reinterpret_cast<bf16 *>(h->peer_pv[rank] + (size_t)slot * h->slot_bytes);
 }
 
@@ -299,7 +303,8 @@ static int ar_partials(merak_tmp_t *h, bool comm, int slot, size_t r0, const bf1
     out[0] = slot_ptr(h, h->r, slot) + r0 * h->h;
     return 1;
   }
-  for (int q = 0; q < h->T; ++q) out[q] = slot_ptr(h, q, slot) + r0 * h->h;
+  // NVLS: after the in-switch reduction every row is in this rank's own slot ("gathered" mode reads locally)
+  for (int q = 0; q < h->T; ++q) out[q] = slot_ptr(h, h->use_nvls ? h->r : q, slot) + r0 * h->h;
   return h->T;
 }
 
@@ -320,6 +325,27 @@ static bool two_shot_on(merak_tmp_t *h, bool comm) { return comm && h->T > 1 && 
 static merak_status two_shot_rs(merak_tmp_t *h, int slot, size_t r0, int m, const bf16 *resid, const bf16 *bias,
                                 int *chunk) {
   const int c = (m + h->T - 1) / h->T;
+  if (h->use_nvls) {  // phase 1 in the switch: multimem.ld_reduce of the owned rows, multimem.st to all ranks
+    NvlsRsArgs a;
+    memset(&a, 0, sizeof(a));
+    a.mc = reinterpret_cast<bf16 *>(reinterpret_cast<char *>(h->nvls.mc_va) + (size_t)slot * h->slot_bytes) + r0 * h->h;
+    a.h = h->h;
+    a.row0 = h->r * c < m ? h->r * c : m;
+    a.row1 = (h->r + 1) * c < m ? (h->r + 1) * c : m;
+    a.resid = resid;
+    a.bias = bias;
+    a.ctas = h->cfg.comm_ctas;
+    a.pdl = h->pdl && !h->prof;
+    {
+      Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+      CK(h, nvls_rs(a, h->ms));
+    }
+    PeerSync ps = make_sync(h, true);
+    ps.pdl = h->pdl && !h->prof;
+    TRY(sync_peers(h, ps));
+    *chunk = c;
+    return MERAK_OK;
+  }
   ArRsArgs a;
   memset(&a, 0, sizeof(a));
   for (int q = 0; q < h->T; ++q) a.partial[q] = slot_ptr(h, q, slot) + r0 * h->h;
@@ -871,8 +897,10 @@ static merak_status validate(const merak_tmp_config *c) {
   if (c->precision != MERAK_BF16 && c->precision != MERAK_FP32_CHECK)
     return fail(nullptr, MERAK_EINVAL, "bad precision");
   if (c->comm != MERAK_COMM_PEER && c->comm != MERAK_COMM_NCCL && c->comm != MERAK_COMM_LOCAL &&
-      c->comm != MERAK_COMM_INPROC)
+      c->comm != MERAK_COMM_INPROC && c->comm != MERAK_COMM_NVLS)
     return fail(nullptr, MERAK_EINVAL, "bad comm");
+  if (c->comm == MERAK_COMM_NVLS && c->precision == MERAK_FP32_CHECK)
+    return fail(nullptr, MERAK_EUNSUPPORTED, "MERAK_COMM_NVLS needs bf16 (the switch reduces bf16 partials)");
   const int T = c->tmp_degree, f = c->ffn_hidden ? c->ffn_hidden : 4 * c->hidden;
   if (c->hidden % c->heads) return fail(nullptr, MERAK_EINDIVISIBLE, "hidden %% heads != 0");
   if (c->heads < T) return fail(nullptr, MERAK_EINDIVISIBLE, "heads < tmp_degree");
@@ -897,6 +925,7 @@ static void release(merak_tmp_t *h) {
   for (int q = 0; q < MAX_T; ++q)
     if (!h->inproc && h->peer_pv[q] && h->peer_pv[q] != h->pv) cudaIpcCloseMemHandle(h->peer_pv[q]);
   if (h->nccl) g_nccl.CommDestroy(h->nccl);
+  if (h->use_nvls) nvls_release(&h->nvls);
   if (h->pv) cudaFree(h->pv);
   if (h->ws) cudaFree(h->ws);
   if (h->ws32) cudaFree(h->ws32);
@@ -1011,7 +1040,10 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
   }
   // peer-visible slots + flags
   h->slot_bytes = align256((size_t)h->M * h->h * (h->f32 ? 4 : 2));
-  h->flags_off = NSLOT * h->slot_bytes;
+  // MERAK_COMM_NVLS (T > 1): the slots live in multicast-bound memory set up by merak_tmp_init; the IPC-shared
+  // block holds the handshake flags only
+  const bool nvls = cfg->comm == MERAK_COMM_NVLS && h->T > 1;
+  h->flags_off = nvls ? 0 : NSLOT * h->slot_bytes;
   h->pv_bytes = h->flags_off + align256(2 * MAX_AR_CTAS * MAX_T * sizeof(uint32_t));
   CKI(cudaMalloc(&h->pv, h->pv_bytes));
   CKI(cudaMemset(h->pv + h->flags_off, 0, h->pv_bytes - h->flags_off));
@@ -1057,6 +1089,7 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
   CKI(h->f32 ? f32_preload() : gemm_preload());
   if (!h->f32) CKI(attn_preload(h->d));
   CKI(ln_ar_preload());
+  CKI(nvls_preload());
   CKI(cudaDeviceSynchronize());
   for (int q = 0; q < MAX_T; ++q) h->peer_pv[q] = nullptr;
   h->peer_pv[h->r] = h->pv;
@@ -1112,6 +1145,16 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
       fail(h, MERAK_EPEER, "allgather barrier failed");
       return bail(MERAK_EPEER);
     }
+  }
+  if (cfg->comm == MERAK_COMM_NVLS && h->T > 1) {
+    std::string why;
+    const int rc = nvls_setup(&h->nvls, h->dev, h->T, h->r, (size_t)NSLOT * h->slot_bytes, ag, ag_ctx, &why);
+    if (rc != 0) {
+      fail(h, rc == -2 ? MERAK_EUNSUPPORTED : MERAK_EPEER, "NVLS multicast setup: %s", why.c_str());
+      return bail(rc == -2 ? MERAK_EUNSUPPORTED : MERAK_EPEER);
+    }
+    h->use_nvls = true;
+    h->two_shot = true;  // phase 1 in the switch, phase 2 = the gathered epilogue reading the own slot
   }
   if (cfg->comm == MERAK_COMM_NCCL && h->T > 1) {
     if (!g_nccl.load()) {
@@ -1386,7 +1429,7 @@ merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t ro
     }
     if (cudaMemsetAsync(tmp, 0, 3 * nb + 4 * hh * 4, h->ms) != cudaSuccess ||
         cudaMemsetAsync(stats, 0, 2 * (size_t)rows * 4, h->ms) != cudaSuccess ||
-        cudaMemsetAsync(h->pv + h->slot_bytes, 0, nb, h->ms) != cudaSuccess) {
+        cudaMemsetAsync(slot_ptr(h, h->r, 1), 0, nb, h->ms) != cudaSuccess) {
       st = fail(h, MERAK_ECUDA, "memset");
       break;
     }

@@ -5,6 +5,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <string>
+
 namespace mk {
 
 // ---------------------------------------------------------------- GEMM (gemm.cu)
@@ -238,5 +240,30 @@ cudaError_t colsum_sample(const __nv_bfloat16 *X, int ld, int s, int b, int n, f
 // for t = 0 and (if p1) t = 1; q0/q1: fp32 workspace [b * n] each.  Two launches.
 cudaError_t sample_reduce2(const float *p0, const float *p1, int gps, int b, int n, float *q0, float *q1, float *g0,
                            float *g1, cudaStream_t st);
+
+// ---------------------------------------------------------------- NVLS in-switch reduction (nvls.cu)
+// The all-reduce slots of this rank bound to a CUDA multicast object shared by the T ranks.
+struct Nvls {
+  void *uc_va, *mc_va;  // this rank's slots: unicast mapping / multicast mapping (same offsets)
+  size_t size;
+  unsigned long long mem_handle, mc_handle;  // CUmemGenericAllocationHandle
+  int dev, fd;
+  bool bound;
+};
+typedef int (*nvls_allgather_fn)(void *ctx, const void *send, void *recv, size_t bytes_per_rank);
+bool nvls_supported(int dev);
+// collective over the T ranks; 0 = OK, -2 = multicast unsupported on some rank, -1 = other failure (*err)
+int nvls_setup(Nvls *n, int dev, int T, int r, size_t bytes, nvls_allgather_fn ag, void *ctx, std::string *err);
+void nvls_release(Nvls *n);
+struct NvlsRsArgs {
+  __nv_bfloat16 *mc;            // multicast address of row 0 of the sub-batch in the slot
+  int h, row0, row1;            // rows owned by this rank
+  const __nv_bfloat16 *resid;   // nullptr: plain sum (backward); else + bias + resid (forward epilogue terms)
+  const __nv_bfloat16 *bias;
+  int ctas;
+  bool pdl;
+};
+cudaError_t nvls_rs(const NvlsRsArgs &a, cudaStream_t st);
+cudaError_t nvls_preload();
 
 }  // namespace mk

@@ -95,6 +95,34 @@ def main():
         print(f"[rank {rank}] {name} T={T} nccl", {k: f"{v:.2e}" for k, v in errs.items()}, flush=True)
         if bad:
             failures.append((name + "/nccl", bad))
+        # NVLS in-switch reduction (MERAK_COMM_NVLS) where every device supports multicast:
+        # oracle parity, replicated outputs equal on every rank, run-to-run determinism of the switch's sum,
+        # and n = 1 vs n = 2 bit-identity
+        from paper_2206_04959_b200 import MERAK_COMM_NVLS, MerakError
+        try:
+            outv = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group, comm=MERAK_COMM_NVLS)
+        except MerakError as e:
+            if e.status != -3:
+                raise
+            print(f"[rank {rank}] {name} T={T} nvls: unsupported here ({e})", flush=True)
+            continue
+        errs, bad = compare_to_oracle(outv, y, dx, oracle_rank_slices(g, cfg, T, rank), cfg)
+        print(f"[rank {rank}] {name} T={T} nvls", {k: f"{v:.2e}" for k, v in errs.items()}, flush=True)
+        if bad:
+            failures.append((name + "/nvls", bad))
+        for k in ("y", "dx", "ln1_g", "ln1_b", "ln2_g", "ln2_b", "b_o", "b_2"):
+            t = outv[k].contiguous()
+            gathered = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(gathered, t)
+            if not all(torch.equal(gathered[0], q) for q in gathered):
+                failures.append((name, f"nvls: {k} differs across ranks"))
+        outv2 = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group, comm=MERAK_COMM_NVLS, reps=2)
+        outv1 = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group, comm=MERAK_COMM_NVLS, n_sub=1)
+        for k in outv:
+            if not torch.equal(outv[k], outv2[k]):
+                failures.append((name, f"nvls: {k} not run-to-run deterministic"))
+            if not torch.equal(outv[k], outv1[k]):
+                failures.append((name, f"nvls: {k}: n={cfg.n_sub} vs n=1 not bit-identical"))
     # chained stack (cross-layer overlap + workspace hazards across ranks): chained == unchained bitwise
     from gpu_layer_util import run_gpu_chain
     from synth import make_activations, make_params
