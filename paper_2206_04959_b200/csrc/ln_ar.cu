@@ -145,68 +145,121 @@ MK_DEV void row_sources(const __nv_bfloat16 *const *partial, int chunk, int row,
 }
 __host__ __device__ constexpr int ar_ch(int nt) { return nt >= 8 ? 1 : nt >= 4 ? 2 : 4; }
 
+// ------------------------------------------------------------------------------ row engine
+// The replicated epilogues are HBM-bound row kernels.  A sub-block of `tpr` threads (32..256) owns a row;
+// thread t holds chunks c = t + k*tpr (k < CPT, 8 bf16 each) in registers, so every row is read from HBM
+// once and all passes over it (sums, LayerNorm statistics, outputs) run from registers.  Row statistics are
+// fixed-order sub-block reductions (warp butterfly, then the warps in order) through a ping-pong smem slot
+// and one named barrier per sub-block (ids 1..8), so sub-blocks never wait for each other.
+__host__ int row_tpr(int nc) {
+  for (int t = 32; t < 256; t *= 2)
+    if (nc <= 3 * t) return t;
+  return 256;
+}
+MK_DEV void sub_sync(int sub, int tpr) { asm volatile("bar.sync %0, %1;" ::"r"(1 + sub), "r"(tpr) : "memory"); }
+template <int NV>
+MK_DEV void sub_reduce(float (&v)[NV], int tpr, int sub, int t, float *red, int &par) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  if (tpr == 32) return;
+  const int nw = tpr >> 5, w = t >> 5;
+  float *slot = red + (size_t)((sub * 2 + par) * 8) * NV;
+  if ((t & 31) == 0)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) slot[w * NV + i] = v[i];
+  sub_sync(sub, tpr);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float acc = 0.f;
+    for (int k = 0; k < nw; ++k) acc += slot[k * NV + i];
+    v[i] = acc;
+  }
+  par ^= 1;  // the next reduction writes the other slot: one barrier per reduction suffices
+}
+MK_DEV uint4 ldg16(const __nv_bfloat16 *p) { return *reinterpret_cast<const uint4 *>(p); }
+
 // ------------------------------------------------------------------------------ forward all-reduce
-template <int NT>
-__global__ void __launch_bounds__(256) ar_fwd_kernel(ArFwdArgs a, PeerSync ps) {
-  constexpr int CH = ar_ch(NT);
+template <int NT, int CPT>
+__global__ void __launch_bounds__(256, 2) ar_fwd_kernel(ArFwdArgs a, PeerSync ps, int tpr) {
   griddep_wait();  // PDL: the handshake before this kernel has completed (peers' data is ready)
   griddep_launch();
-  extern __shared__ uint4 row_s[];  // do_ln: per warp, the stored bf16 row (LN2 reads it, reading R12)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = blockDim.x >> 5;
+  __shared__ float red[8 * 2 * 8 * 1];
+  const int nsub = blockDim.x / tpr, sub = threadIdx.x / tpr, t = threadIdx.x % tpr;
   const int h = a.h, nc = h >> 3;
   const bool gathered = a.chunk > 0;
-  uint4 *rb = row_s + (size_t)warp * nc;
-  for (int row = blockIdx.x * nw + warp; row < a.m; row += gridDim.x * nw) {
+  int par = 0;
+  for (int row = blockIdx.x * nsub + sub; row < a.m; row += gridDim.x * nsub) {
     const size_t ro = (size_t)row * h;
-    float sum = 0.f;
     const __nv_bfloat16 *src[NT];
     row_sources<NT>(a.partial, a.chunk, row, src);
-    for (int c0 = lane; c0 < nc; c0 += 32 * CH) {
-      float v[CH][8];
-      rank_sum<NT, CH>(src, ro, c0, nc, v);
+    uint4 raw[CPT][NT], rr[CPT], bb[CPT];
 #pragma unroll
-      for (int i = 0; i < CH; ++i) {
-        const int c = c0 + 32 * i;
-        if (c >= nc) continue;
-        if (!gathered) {
-          add8(a.bias + c * 8, v[i]);
-          add8(a.resid + ro + c * 8, v[i]);
-        }
-        uint4 pk;
-        pk.x = pack_bf16(v[i][0], v[i][1]); pk.y = pack_bf16(v[i][2], v[i][3]);
-        pk.z = pack_bf16(v[i][4], v[i][5]); pk.w = pack_bf16(v[i][6], v[i][7]);
+    for (int k = 0; k < CPT; ++k) {  // every load of the row is in flight before any arithmetic
+      const int c = t + k * tpr;
+      const bool ok = c < nc;
+#pragma unroll
+      for (int r = 0; r < NT; ++r) raw[k][r] = ok ? ldg16(src[r] + ro + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
+      if (!gathered) {
+        rr[k] = ok ? ldg16(a.resid + ro + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
+        bb[k] = ok ? ldg16(a.bias + c * 8) : make_uint4(0, 0, 0, 0);
+      }
+    }
+    float q[CPT][8];
+    float sum[1] = {0.f};
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      float v[8];
+      unpack8(raw[k][0], v);  // fp32 sum in rank order 0..T-1, + bias, + residual, one rounding (R10)
+#pragma unroll
+      for (int r = 1; r < NT; ++r) {
+        float u[8];
+        unpack8(raw[k][r], u);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] += u[e];
+      }
+      if (!gathered) {
+        float u[8];
+        unpack8(bb[k], u);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] += u[e];
+        unpack8(rr[k], u);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] += u[e];
+      }
+      uint4 pk;
+      pk.x = pack_bf16(v[0], v[1]); pk.y = pack_bf16(v[2], v[3]);
+      pk.z = pack_bf16(v[4], v[5]); pk.w = pack_bf16(v[6], v[7]);
+      const int c = t + k * tpr;
+      if (c < nc) {
         *reinterpret_cast<uint4 *>(a.out + ro + c * 8) = pk;
-        if (a.do_ln) {
-          rb[c] = pk;
-          float q[8];
-          unpack8(pk, q);
+        unpack8(pk, q[k]);  // LN2 reads the stored bf16 x1 (R12)
 #pragma unroll
-          for (int k = 0; k < 8; ++k) sum += q[k];  // LN2 of the stored bf16 x1 (R12)
-        }
+        for (int e = 0; e < 8; ++e) sum[0] += q[k][e];
       }
     }
     if (!a.do_ln) continue;
-    __syncwarp();
-    const float mean = warp_sum(sum) / h;
-    float var = 0.f;
-    for (int c = lane; c < nc; c += 32) {
-      float q[8];
-      unpack8(rb[c], q);
+    sub_reduce<1>(sum, tpr, sub, t, red, par);
+    const float mean = sum[0] / h;
+    float var[1] = {0.f};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) var += (q[i] - mean) * (q[i] - mean);
-    }
-    const float rstd = rsqrtf(warp_sum(var) / h + a.eps);
-    for (int c = lane; c < nc; c += 32) {
-      float q[8], gm[8], bt[8];
-      unpack8(rb[c], q);
+    for (int k = 0; k < CPT; ++k)
+      if (t + k * tpr < nc)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) var[0] += (q[k][e] - mean) * (q[k][e] - mean);
+    sub_reduce<1>(var, tpr, sub, t, red, par);
+    const float rstd = rsqrtf(var[0] / h + a.eps);
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      const int c = t + k * tpr;
+      if (c >= nc) continue;
+      float gm[8], bt[8], o[8];
       load8(a.gamma + c * 8, gm);
       load8(a.beta + c * 8, bt);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) q[i] = (q[i] - mean) * rstd * gm[i] + bt[i];
-      store8(a.ln_out + (size_t)row * a.ld_ln + c * 8, q);
+      for (int e = 0; e < 8; ++e) o[e] = (q[k][e] - mean) * rstd * gm[e] + bt[e];
+      store8(a.ln_out + (size_t)row * a.ld_ln + c * 8, o);
     }
-    if (lane == 0) {
+    if (t == 0) {
       a.mean[row] = mean;
       a.rstd[row] = rstd;
     }
@@ -245,172 +298,177 @@ __global__ void __launch_bounds__(256) ar_rs_kernel(ArRsArgs a) {
 }
 
 // ------------------------------------------------------------------------------ backward all-reduce
-template <int G, int NT, bool STASH>
-__global__ void __launch_bounds__(256) ar_bwd_kernel(ArBwdArgs a, PeerSync ps) {
-  constexpr int CH = ar_ch(NT);
+// Groups of G = 8 rows per sub-block (row engine above): for each row the all-reduced gradient du (rounded
+// once to bf16, R10), the LayerNorm backward dx = dres + rstd (g du - mean(g du) - xhat mean(g du xhat)), and
+// the group's fixed-order column partials of dgamma = sum du xhat, dbeta = sum du accumulated in registers.
+template <int NT, int CPT>
+__global__ void __launch_bounds__(256, 2) ar_bwd_kernel(ArBwdArgs a, PeerSync ps, int tpr) {
+  constexpr int G = 8;
   griddep_wait();
   griddep_launch();
-  extern __shared__ __align__(16) float du_s[];  // [G][h] the all-reduced gradient (bf16-rounded),
-                                                 // then [G][h/8] uint4 x_ln rows, [G][h/8] uint4 dres rows
-  __shared__ float s_mean[G], s_rstd[G];
-  uint4 *xs = reinterpret_cast<uint4 *>(du_s + (size_t)G * a.h), *ds_res = xs + (size_t)G * (a.h >> 3);
-  {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int h = a.h, nc = h >> 3;
-    const float inv_h = 1.f / h;
-    const int ngroups = a.m / G;
-    const bool gathered = a.chunk > 0;
-    for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-      // phase 1: warp per row -- all-reduce, LN backward, residual
-      for (int ri = warp; ri < G; ri += 8) {
-        const int row = grp * G + ri;
-        const size_t ro = (size_t)row * h;
-        const float mean = a.mean[row], rstd = a.rstd[row];
-        float acc1 = 0.f, acc2 = 0.f;
-        const __nv_bfloat16 *src[NT];
-        row_sources<NT>(a.partial, a.chunk, row, src);
-        for (int c0 = lane; c0 < nc; c0 += 32 * CH) {
-          float dv[CH][8];
-          rank_sum<NT, CH>(src, ro, c0, nc, dv);
+  __shared__ float red[8 * 2 * 8 * 2];
+  const int nsub = blockDim.x / tpr, sub = threadIdx.x / tpr, t = threadIdx.x % tpr;
+  const int h = a.h, nc = h >> 3;
+  const float inv_h = 1.f / h;
+  const int ngroups = a.m / G;
+  const bool gathered = a.chunk > 0;
+  int par = 0;
+  for (int grp = blockIdx.x * nsub + sub; grp < ngroups; grp += gridDim.x * nsub) {
+    float sg[CPT][8], sb[CPT][8];
 #pragma unroll
-          for (int i = 0; i < CH; ++i) {
-            const int c = c0 + 32 * i;
-            if (c >= nc) continue;
-            float x[8], gm[8];
-            if (!gathered) {
+    for (int k = 0; k < CPT; ++k)
 #pragma unroll
-              for (int k = 0; k < 8; ++k) dv[i][k] = bf16_round(dv[i][k]);  // AR result rounded once (R10)
-            }
-            float4 *ds = reinterpret_cast<float4 *>(du_s + ri * h + c * 8);
-            ds[0] = make_float4(dv[i][0], dv[i][1], dv[i][2], dv[i][3]);
-            ds[1] = make_float4(dv[i][4], dv[i][5], dv[i][6], dv[i][7]);
-            const uint4 xr = *reinterpret_cast<const uint4 *>(a.x_ln + ro + c * 8);
-            if constexpr (STASH) {
-              xs[ri * nc + c] = xr;
-              ds_res[ri * nc + c] = *reinterpret_cast<const uint4 *>(a.dres + ro + c * 8);
-            }
-            unpack8(xr, x);
-            load8(a.gamma + c * 8, gm);
+      for (int e = 0; e < 8; ++e) sg[k][e] = sb[k][e] = 0.f;
+#pragma unroll 1
+    for (int ri = 0; ri < G; ++ri) {
+      const int row = grp * G + ri;
+      const size_t ro = (size_t)row * h;
+      const float mean = a.mean[row], rstd = a.rstd[row];
+      const __nv_bfloat16 *src[NT];
+      row_sources<NT>(a.partial, a.chunk, row, src);
+      // registers hold the row as packed bf16: du (exactly bf16 after its one rounding), x, dres
+      uint4 dup[CPT], xr[CPT], dr[CPT];
+      {
+        uint4 raw[CPT][NT];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const float xh = (x[k] - mean) * rstd, dxh = dv[i][k] * gm[k];
-              acc1 += dxh;
-              acc2 += dxh * xh;
-            }
-          }
+        for (int k = 0; k < CPT; ++k) {
+          const int c = t + k * tpr;
+          const bool ok = c < nc;
+#pragma unroll
+          for (int r = 0; r < NT; ++r) raw[k][r] = ok ? ldg16(src[r] + ro + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
+          xr[k] = ok ? ldg16(a.x_ln + ro + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
+          dr[k] = ok ? ldg16(a.dres + ro + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
         }
-        __syncwarp();
-        const float m1 = warp_sum(acc1) * inv_h, m2 = warp_sum(acc2) * inv_h;
-        for (int c = lane; c < nc; c += 32) {
-          float x[8], gm[8], dr[8], o[8];
-          const float4 *ds = reinterpret_cast<const float4 *>(du_s + ri * h + c * 8);
-          const float4 d0 = ds[0], d1 = ds[1];
-          const float du[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-          if constexpr (STASH) {
-            unpack8(xs[ri * nc + c], x);
-            unpack8(ds_res[ri * nc + c], dr);
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+          if (NT == 1) {
+            dup[k] = raw[k][0];  // one source: a bf16 value already (the slot, or two-shot's rounded sum)
           } else {
-            load8(a.x_ln + ro + c * 8, x);
-            load8(a.dres + ro + c * 8, dr);
-          }
-          load8(a.gamma + c * 8, gm);
+            float v[8];
+            unpack8(raw[k][0], v);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float xh = (x[i] - mean) * rstd, dxh = du[i] * gm[i];
-            o[i] = dr[i] + rstd * (dxh - m1 - xh * m2);
+            for (int r = 1; r < NT; ++r) {
+              float u[8];
+              unpack8(raw[k][r], u);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[e] += u[e];
+            }
+            // AR result rounded once (R10)
+            dup[k].x = pack_bf16(v[0], v[1]); dup[k].y = pack_bf16(v[2], v[3]);
+            dup[k].z = pack_bf16(v[4], v[5]); dup[k].w = pack_bf16(v[6], v[7]);
           }
-          store8(a.dx + ro + c * 8, o);
-        }
-        if (lane == 0) {
-          s_mean[ri] = mean;
-          s_rstd[ri] = rstd;
         }
       }
-      __syncthreads();
-      // phase 2: fixed-order column partials over the G rows (dbeta = sum du, dgamma = sum du*xhat)
-      for (int cc = threadIdx.x; cc < nc; cc += blockDim.x) {
-        float sg[8], sb[8];
+      float acc[2] = {0.f, 0.f};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) sg[i] = sb[i] = 0.f;
-        for (int i = 0; i < G; ++i) {
-          float x[8];
-          if constexpr (STASH)
-            unpack8(xs[i * nc + cc], x);
-          else
-            load8(a.x_ln + (size_t)(grp * G + i) * h + cc * 8, x);
-          const float4 *ds = reinterpret_cast<const float4 *>(du_s + i * h + cc * 8);
-          const float4 d0 = ds[0], d1 = ds[1];
-          const float du[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+      for (int k = 0; k < CPT; ++k) {
+        const int c = t + k * tpr;
+        if (c >= nc) continue;
+        float du[8], x[8], gm[8];
+        unpack8(dup[k], du);
+        unpack8(xr[k], x);
+        load8(a.gamma + c * 8, gm);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            sb[k] += du[k];
-            sg[k] += du[k] * ((x[k] - s_mean[i]) * s_rstd[i]);
-          }
+        for (int e = 0; e < 8; ++e) {
+          const float xh = (x[e] - mean) * rstd, dxh = du[e] * gm[e];
+          acc[0] += dxh;
+          acc[1] += dxh * xh;
         }
-        float4 *pg = reinterpret_cast<float4 *>(a.part_dg + (size_t)grp * h + cc * 8);
-        float4 *pb = reinterpret_cast<float4 *>(a.part_db + (size_t)grp * h + cc * 8);
-        pg[0] = make_float4(sg[0], sg[1], sg[2], sg[3]);
-        pg[1] = make_float4(sg[4], sg[5], sg[6], sg[7]);
-        pb[0] = make_float4(sb[0], sb[1], sb[2], sb[3]);
-        pb[1] = make_float4(sb[4], sb[5], sb[6], sb[7]);
       }
-      __syncthreads();
+      sub_reduce<2>(acc, tpr, sub, t, red, par);
+      const float m1 = acc[0] * inv_h, m2 = acc[1] * inv_h;
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        const int c = t + k * tpr;
+        if (c >= nc) continue;
+        float du[8], x[8], gm[8], d[8], o[8];
+        unpack8(dup[k], du);
+        unpack8(xr[k], x);
+        unpack8(dr[k], d);
+        load8(a.gamma + c * 8, gm);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float xh = (x[e] - mean) * rstd, dxh = du[e] * gm[e];
+          o[e] = d[e] + rstd * (dxh - m1 - xh * m2);
+          sb[k][e] += du[e];
+          sg[k][e] += du[e] * xh;
+        }
+        store8(a.dx + ro + c * 8, o);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      const int c = t + k * tpr;
+      if (c >= nc) continue;
+      float4 *pg = reinterpret_cast<float4 *>(a.part_dg + (size_t)grp * h + c * 8);
+      float4 *pb = reinterpret_cast<float4 *>(a.part_db + (size_t)grp * h + c * 8);
+      pg[0] = make_float4(sg[k][0], sg[k][1], sg[k][2], sg[k][3]);
+      pg[1] = make_float4(sg[k][4], sg[k][5], sg[k][6], sg[k][7]);
+      pb[0] = make_float4(sb[k][0], sb[k][1], sb[k][2], sb[k][3]);
+      pb[1] = make_float4(sb[k][4], sb[k][5], sb[k][6], sb[k][7]);
     }
   }
 }
 
 // ------------------------------------------------------------------------------ LayerNorm forward
+template <int CPT>
 __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16 *x, const __nv_bfloat16 *gamma,
                                                      const __nv_bfloat16 *beta, __nv_bfloat16 *u, int ld_u,
                                                      float *mean_out, float *rstd_out, int m, int h, float eps,
-                                                     OnesPad pad) {
-  extern __shared__ uint4 row_s[];  // per warp: the x row (one global read; passes 2-3 from smem)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int row = blockIdx.x * nw + warp;
-  if (row >= m) return;
+                                                     OnesPad pad, int tpr) {
+  __shared__ float red[8 * 2 * 8 * 1];
+  const int nsub = blockDim.x / tpr, sub = threadIdx.x / tpr, t = threadIdx.x % tpr;
   const int nc = h >> 3;
-  const size_t ro = (size_t)row * h;
-  uint4 *rb = row_s + (size_t)warp * nc;
-  float sum = 0.f;
-#pragma unroll 4
-  for (int c = lane; c < nc; c += 32) {
-    const uint4 u4 = *reinterpret_cast<const uint4 *>(x + ro + c * 8);
-    rb[c] = u4;
-    float q[8];
-    unpack8(u4, q);
+  int par = 0;
+  for (int row = blockIdx.x * nsub + sub; row < m; row += gridDim.x * nsub) {
+    const size_t ro = (size_t)row * h;
+    uint4 raw[CPT];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) sum += q[i];
-  }
-  __syncwarp();
-  const float mean = warp_sum(sum) / h;
-  float var = 0.f;
-  for (int c = lane; c < nc; c += 32) {
-    float q[8];
-    unpack8(rb[c], q);
+    for (int k = 0; k < CPT; ++k) {
+      const int c = t + k * tpr;
+      raw[k] = c < nc ? ldg16(x + ro + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
+    }
+    float q[CPT][8];
+    float sum[1] = {0.f};
 #pragma unroll
-    for (int i = 0; i < 8; ++i) var += (q[i] - mean) * (q[i] - mean);
-  }
-  const float rstd = rsqrtf(warp_sum(var) / h + eps);
-  for (int c = lane; c < nc; c += 32) {
-    float q[8], gm[8], bt[8];
-    unpack8(rb[c], q);
-    load8(gamma + c * 8, gm);
-    load8(beta + c * 8, bt);
+    for (int k = 0; k < CPT; ++k) {
+      unpack8(raw[k], q[k]);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) q[i] = (q[i] - mean) * rstd * gm[i] + bt[i];
-    store8(u + (size_t)row * ld_u + c * 8, q);
-  }
-  if (lane < pad.n) {
-    uint4 one;
-    one.x = pack_bf16(1.f, 0.f);
-    one.y = one.z = one.w = 0u;
+      for (int e = 0; e < 8; ++e) sum[0] += q[k][e];  // zero-filled beyond the row
+    }
+    sub_reduce<1>(sum, tpr, sub, t, red, par);
+    const float mean = sum[0] / h;
+    float var[1] = {0.f};
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
-      if (k == lane) *reinterpret_cast<uint4 *>(pad.ptr[k] + (size_t)row * pad.ld[k] + pad.col[k]) = one;
-  }
-  if (lane == 0) {
-    mean_out[row] = mean;
-    rstd_out[row] = rstd;
+    for (int k = 0; k < CPT; ++k)
+      if (t + k * tpr < nc)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) var[0] += (q[k][e] - mean) * (q[k][e] - mean);
+    sub_reduce<1>(var, tpr, sub, t, red, par);
+    const float rstd = rsqrtf(var[0] / h + eps);
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      const int c = t + k * tpr;
+      if (c >= nc) continue;
+      float gm[8], bt[8], o[8];
+      load8(gamma + c * 8, gm);
+      load8(beta + c * 8, bt);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o[e] = (q[k][e] - mean) * rstd * gm[e] + bt[e];
+      store8(u + (size_t)row * ld_u + c * 8, o);
+    }
+    if (t < pad.n) {  // the ones-column pads of u, ctx, u2, g
+      uint4 one;
+      one.x = pack_bf16(1.f, 0.f);
+      one.y = one.z = one.w = 0u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k == t) *reinterpret_cast<uint4 *>(pad.ptr[k] + (size_t)row * pad.ld[k] + pad.col[k]) = one;
+    }
+    if (t == 0) {
+      mean_out[row] = mean;
+      rstd_out[row] = rstd;
+    }
   }
 }
 
@@ -519,32 +577,31 @@ static int clamp_ctas(int want, int work, int resident) {
   return want < 1 ? 1 : want;
 }
 
-template <int NT>
-static cudaError_t ar_fwd_t(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
-  const size_t smem = a.do_ln ? (size_t)8 * a.h * 2 : 0;  // 8 warps x one bf16 row
+template <int NT, int CPT>
+static cudaError_t ar_fwd_t(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st, int tpr) {
   static int resident[MAX_DEV] = {};
-  static size_t res_smem[MAX_DEV], attr[MAX_DEV] = {};
-  static bool init[MAX_DEV] = {};
   const int dev = cur_device();
-  if (smem > attr[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(ar_fwd_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr[dev] = smem;
+  if (!resident[dev]) resident[dev] = resident_ctas((const void *)ar_fwd_kernel<NT, CPT>, 256, 0);
+  const int grid = clamp_ctas(a.ctas, (a.m + 256 / tpr - 1) / (256 / tpr), resident[dev]);
+  return launch_k(ar_fwd_kernel<NT, CPT>, dim3(grid), dim3(256), 0, st, a.pdl, a, ps, tpr);
+}
+template <int NT>
+static cudaError_t ar_fwd_n(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
+  const int nc = a.h / 8, tpr = row_tpr(nc), cpt = (nc + tpr - 1) / tpr;
+  switch (cpt) {
+    case 1: return ar_fwd_t<NT, 1>(a, ps, st, tpr);
+    case 2: return ar_fwd_t<NT, 2>(a, ps, st, tpr);
+    case 3: return ar_fwd_t<NT, 3>(a, ps, st, tpr);
+    case 4: return ar_fwd_t<NT, 4>(a, ps, st, tpr);
   }
-  if (!init[dev] || res_smem[dev] != smem) {
-    resident[dev] = resident_ctas((const void *)ar_fwd_kernel<NT>, 256, smem);
-    res_smem[dev] = smem;
-    init[dev] = true;
-  }
-  const int grid = clamp_ctas(a.ctas, (a.m + 7) / 8, resident[dev]);
-  return launch_k(ar_fwd_kernel<NT>, dim3(grid), dim3(256), smem, st, a.pdl, a, ps);
+  return cudaErrorInvalidValue;  // h > 8192
 }
 cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st) {
   switch (a.chunk > 0 ? 1 : a.T) {
-    case 1: return ar_fwd_t<1>(a, ps, st);
-    case 2: return ar_fwd_t<2>(a, ps, st);
-    case 4: return ar_fwd_t<4>(a, ps, st);
-    case 8: return ar_fwd_t<8>(a, ps, st);
+    case 1: return ar_fwd_n<1>(a, ps, st);
+    case 2: return ar_fwd_n<2>(a, ps, st);
+    case 4: return ar_fwd_n<4>(a, ps, st);
+    case 8: return ar_fwd_n<8>(a, ps, st);
   }
   return cudaErrorInvalidValue;
 }
@@ -570,55 +627,60 @@ cudaError_t ar_rs(const ArRsArgs &a, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
-template <int NT, bool STASH>
-static cudaError_t ar_bwd_t(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
-  constexpr int G = 8;
-  // du fp32 rows, plus (STASH) the x_ln and dres bf16 rows so the later passes read smem, not HBM
-  const size_t smem = (size_t)G * a.h * (sizeof(float) + (STASH ? 4 : 0));
-  static size_t attr[MAX_DEV] = {};
-  const int dev = cur_device();
-  if (smem > attr[dev]) {
-    cudaError_t e =
-        cudaFuncSetAttribute(ar_bwd_kernel<G, NT, STASH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr[dev] = smem;
-  }
+template <int NT, int CPT>
+static cudaError_t ar_bwd_t(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st, int tpr) {
   static int resident[MAX_DEV] = {};
-  static size_t res_smem[MAX_DEV] = {};
-  if (!resident[dev] || res_smem[dev] != smem) {
-    resident[dev] = resident_ctas((const void *)ar_bwd_kernel<G, NT, STASH>, 256, smem);
-    res_smem[dev] = smem;
+  const int dev = cur_device();
+  if (!resident[dev]) resident[dev] = resident_ctas((const void *)ar_bwd_kernel<NT, CPT>, 256, 0);
+  const int groups = a.m / 8, nsub = 256 / tpr;
+  const int grid = clamp_ctas(a.ctas, (groups + nsub - 1) / nsub, resident[dev]);
+  return launch_k(ar_bwd_kernel<NT, CPT>, dim3(grid), dim3(256), 0, st, a.pdl, a, ps, tpr);
+}
+template <int NT>
+static cudaError_t ar_bwd_n(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
+  const int nc = a.h / 8, tpr = row_tpr(nc), cpt = (nc + tpr - 1) / tpr;
+  switch (cpt) {
+    case 1: return ar_bwd_t<NT, 1>(a, ps, st, tpr);
+    case 2: return ar_bwd_t<NT, 2>(a, ps, st, tpr);
+    case 3: return ar_bwd_t<NT, 3>(a, ps, st, tpr);
+    case 4: return ar_bwd_t<NT, 4>(a, ps, st, tpr);
   }
-  const int grid = clamp_ctas(a.ctas, a.m / G, resident[dev]);
-  return launch_k(ar_bwd_kernel<G, NT, STASH>, dim3(grid), dim3(256), smem, st, a.pdl, a, ps);
+  return cudaErrorInvalidValue;
 }
 cudaError_t ar_bwd(const ArBwdArgs &a, const PeerSync &ps, cudaStream_t st) {
   if (a.G != 8 || a.m % 8) return cudaErrorInvalidValue;
-  // Stashing x_ln / dres rows in smem (STASH) measured slower (25.7 vs 20.8 us per launch at h = 1600):
-  // 102 KB of smem per CTA halves the resident CTAs of this latency-bound kernel.  Kept selectable.
-  const char *e = getenv("MERAK_ARBWD_STASH");
-  const bool stash = e && atoi(e) == 1 && (size_t)8 * a.h * 8 <= 160 * 1024;
   switch (a.chunk > 0 ? 1 : a.T) {
-    case 1: return stash ? ar_bwd_t<1, true>(a, ps, st) : ar_bwd_t<1, false>(a, ps, st);
-    case 2: return stash ? ar_bwd_t<2, true>(a, ps, st) : ar_bwd_t<2, false>(a, ps, st);
-    case 4: return stash ? ar_bwd_t<4, true>(a, ps, st) : ar_bwd_t<4, false>(a, ps, st);
-    case 8: return stash ? ar_bwd_t<8, true>(a, ps, st) : ar_bwd_t<8, false>(a, ps, st);
+    case 1: return ar_bwd_n<1>(a, ps, st);
+    case 2: return ar_bwd_n<2>(a, ps, st);
+    case 4: return ar_bwd_n<4>(a, ps, st);
+    case 8: return ar_bwd_n<8>(a, ps, st);
   }
   return cudaErrorInvalidValue;
 }
 
+template <int CPT>
+static cudaError_t ln_fwd_t(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bfloat16 *b, __nv_bfloat16 *u,
+                            int ld_u, float *mean, float *rstd, int m, int h, float eps, const OnesPad &pad,
+                            cudaStream_t st, int tpr) {
+  static int resident[MAX_DEV] = {};
+  const int dev = cur_device();
+  if (!resident[dev]) resident[dev] = resident_ctas((const void *)ln_fwd_kernel<CPT>, 256, 0);
+  const int nsub = 256 / tpr;
+  const int grid = clamp_ctas(0, (m + nsub - 1) / nsub, resident[dev]);
+  ln_fwd_kernel<CPT><<<grid, 256, 0, st>>>(x, g, b, u, ld_u, mean, rstd, m, h, eps, pad, tpr);
+  return cudaGetLastError();
+}
+
 cudaError_t ln_fwd(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bfloat16 *b, __nv_bfloat16 *u,
                    int ld_u, float *mean, float *rstd, int m, int h, float eps, const OnesPad &pad, cudaStream_t st) {
-  const size_t smem = (size_t)8 * h * 2;
-  static size_t attr[MAX_DEV] = {};
-  const int dev = cur_device();
-  if (smem > attr[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(ln_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr[dev] = smem;
+  const int nc = h / 8, tpr = row_tpr(nc), cpt = (nc + tpr - 1) / tpr;
+  switch (cpt) {
+    case 1: return ln_fwd_t<1>(x, g, b, u, ld_u, mean, rstd, m, h, eps, pad, st, tpr);
+    case 2: return ln_fwd_t<2>(x, g, b, u, ld_u, mean, rstd, m, h, eps, pad, st, tpr);
+    case 3: return ln_fwd_t<3>(x, g, b, u, ld_u, mean, rstd, m, h, eps, pad, st, tpr);
+    case 4: return ln_fwd_t<4>(x, g, b, u, ld_u, mean, rstd, m, h, eps, pad, st, tpr);
   }
-  ln_fwd_kernel<<<(m + 7) / 8, 256, smem, st>>>(x, g, b, u, ld_u, mean, rstd, m, h, eps, pad);
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t colsum_sample(const __nv_bfloat16 *X, int ld, int s, int b, int n, float *Q, cudaStream_t st) {
@@ -638,19 +700,28 @@ cudaError_t sample_reduce2(const float *p0, const float *p1, int gps, int b, int
   return cudaGetLastError();
 }
 
-template <int NT>
-static cudaError_t ar_preload_t() {
-  const void *ks[] = {(const void *)ar_fwd_kernel<NT>, (const void *)ar_rs_kernel<NT>,
-                      (const void *)ar_bwd_kernel<8, NT, false>, (const void *)ar_bwd_kernel<8, NT, true>};
+template <int NT, int CPT>
+static cudaError_t ar_preload_c() {
+  const void *ks[] = {(const void *)ar_fwd_kernel<NT, CPT>, (const void *)ar_bwd_kernel<NT, CPT>};
   for (const void *k : ks) {
     cudaError_t e = touch_kernel(k);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
+template <int NT>
+static cudaError_t ar_preload_t() {
+  cudaError_t e = touch_kernel((const void *)ar_rs_kernel<NT>);
+  if (e == cudaSuccess) e = ar_preload_c<NT, 1>();
+  if (e == cudaSuccess) e = ar_preload_c<NT, 2>();
+  if (e == cudaSuccess) e = ar_preload_c<NT, 3>();
+  if (e == cudaSuccess) e = ar_preload_c<NT, 4>();
+  return e;
+}
 
 cudaError_t ln_ar_preload() {
-  const void *ks[] = {(const void *)peer_ready_kernel, (const void *)ln_fwd_kernel, (const void *)colsum_sample_kernel,
+  const void *ks[] = {(const void *)peer_ready_kernel, (const void *)ln_fwd_kernel<1>, (const void *)ln_fwd_kernel<2>,
+                      (const void *)ln_fwd_kernel<3>, (const void *)ln_fwd_kernel<4>, (const void *)colsum_sample_kernel,
                       (const void *)sample_sum_kernel, (const void *)sample_chain_kernel};
   for (const void *k : ks) {
     cudaError_t e = touch_kernel(k);
