@@ -79,7 +79,7 @@ typedef enum {
   MERAK_OK = 0,
   MERAK_EINVAL = -1,       /* NULL/misaligned pointer, non-positive size, bad enum value      */
   MERAK_EINDIVISIBLE = -2, /* B % n_sub, h % H or f % T non-zero, or H < T                    */
-  MERAK_EUNSUPPORTED = -3, /* head dim not in {32,64,80,96,128}, T not in {1,2,4,8}, no P2P   */
+  MERAK_EUNSUPPORTED = -3, /* head dim not in {32,64,80,96,128}, T not in {1,2,4,8}, h > 8192, no P2P */
   MERAK_ECUDA = -4,        /* a CUDA runtime/driver call failed (message has the CUDA error)  */
   MERAK_EPEER = -5,        /* IPC handle exchange / peer mapping failed                       */
   MERAK_ENOMEM = -6,       /* device allocation failed                                        */

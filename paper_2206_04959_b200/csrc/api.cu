@@ -914,6 +914,7 @@ static merak_status validate(const merak_tmp_config *c) {
   if (c->seq_len % 16) return fail(nullptr, MERAK_EUNSUPPORTED, "seq_len must be a multiple of 16");
   if (c->microbatch > 48) return fail(nullptr, MERAK_EUNSUPPORTED, "microbatch > 48");
   if (c->hidden % 8 || (f / T) % 8) return fail(nullptr, MERAK_EUNSUPPORTED, "h and f/T must be multiples of 8");
+  if (c->hidden > 8192) return fail(nullptr, MERAK_EUNSUPPORTED, "hidden > 8192 (row-engine register budget)");
   return MERAK_OK;
 }
 
