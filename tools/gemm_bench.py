@@ -25,9 +25,9 @@ def shapes(h, f, hr, m):
 
 
 def main():
-    h, T, m = 1600, int(os.environ.get("T", 1)), int(os.environ.get("M_TOK", 4096))
+    h, T, m = int(os.environ.get("H", 1600)), int(os.environ.get("T", 1)), int(os.environ.get("M_TOK", 4096))
     f = 4 * h // T
-    hr = 832 if T == 2 else h // T
+    hr = 832 if (T == 2 and h == 1600) else h // T
     flush = torch.empty(256 * 1024 * 1024 // 4, device="cuda")
     out = {}
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
@@ -59,9 +59,27 @@ def main():
         ts.sort()
         t = ts[len(ts) // 2]
         out[name] = {"M": M, "N": N, "K": K, "us": round(t * 1e3, 2), "tflops": round(2 * M * N * K / (t * 1e-3) / 1e12, 1)}
+        if os.environ.get("CUBLAS") and not amn and not bmn:
+            Bt = B[:N, :K]
+            def cb():
+                torch.matmul(A, Bt.T, out=o)
+            for _ in range(3):
+                cb()
+            ts = []
+            for _ in range(10):
+                flush.zero_()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                cb()
+                b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            ts.sort()
+            out[name]["cublas_tflops"] = round(2 * M * N * K / (ts[len(ts) // 2] * 1e-3) / 1e12, 1)
     tot_f = sum(2 * v["M"] * v["N"] * v["K"] for v in out.values())
     tot_t = sum(v["us"] for v in out.values()) * 1e-6
-    print(json.dumps({"cg": os.environ.get("MERAK_GEMM_CG", "2"), "T": T, "m": m, "total_tflops": tot_f / tot_t / 1e12,
+    print(json.dumps({"cg": os.environ.get("MERAK_GEMM_CG", "2"), "bn": os.environ.get("MERAK_GEMM_BN", "auto"),
+                      "h": h, "T": T, "m": m, "total_tflops": tot_f / tot_t / 1e12,
                       "total_us": tot_t * 1e6, "gemms": out}))
 
 
