@@ -57,16 +57,6 @@ MK_DEV void tmem_st16(uint32_t taddr, const uint32_t *r) {
       "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
-// D[tmem] (+)= A[tmem] * B[smem desc]^T, kind::f16; A (M x K, K-major) read from TMEM: lane = row,
-// bf16 pairs packed along K in consecutive 32-bit columns
-MK_DEV void tc_mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 
 // packed fp32 pairs (FFMA2 / FADD2 on sm_100): lo = first element
 MK_DEV uint64_t pack_u64(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
@@ -180,32 +170,28 @@ __global__ void __launch_bounds__(320, 1)
           const int i = j - 1, st = i % ST;
           mbar_wait(&p_full[t], i & 1);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t v0 = smem_u32(sV + st * C::V_BYTES);
+          // whole-warp issue (tc_*_w elect one lane inside the asm: no per-lane broadcast loop per MMA)
+          const uint64_t vd = sdesc_sw128(smem_u32(sV + st * C::V_BYTES), C::ATOM, 1024);
 #pragma unroll
-            for (int kk = 0; kk < TK / 16; ++kk)
-              tc_mma_f16_ts(tmem + C::O_COL + 128 * t, tmem + C::S_COL + 128 * t + kk * 8,
-                            sdesc_sw128(v0 + kk * 2048, C::ATOM, 1024), idesc_o, (i > 0 || kk > 0) ? 1u : 0u);
-            tc_commit(&o_done[t]);
-          }
-          __syncwarp();
+          for (int kk = 0; kk < TK / 16; ++kk)
+            tc_mma_f16_ts_w(tmem + C::O_COL + 128 * t, tmem + C::S_COL + 128 * t + kk * 8, vd + (kk * 2048 >> 4),
+                            idesc_o, (i > 0 || kk > 0) ? 1u : 0u);
+          tc_commit_w(&o_done[t]);
         }
         // S_t(j) = Q_t K_j^T into S_t's columns (issued after the P V that reads them: in-order execution)
         if (j < (t ? J1 : J0)) {
-          if (lane == 0) {
-            const uint32_t q0 = smem_u32(sQ + t * C::Q_BYTES), k0 = smem_u32(sK + (j % ST) * C::K_BYTES);
+          const uint64_t qd = sdesc_sw128(smem_u32(sQ + t * C::Q_BYTES), 16, 1024);
+          const uint64_t kd = sdesc_sw128(smem_u32(sK + (j % ST) * C::K_BYTES), 16, 1024);
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)
-              tc_mma_f16(tmem + C::S_COL + 128 * t, sdesc_sw128(q0 + (kk >> 2) * C::ATOM + (kk & 3) * 32, 16, 1024),
-                         sdesc_sw128(k0 + (kk >> 2) * C::ATOM + (kk & 3) * 32, 16, 1024), idesc_s, kk > 0 ? 1u : 0u);
-            tc_commit(&s_full[t]);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = ((kk >> 2) * C::ATOM + (kk & 3) * 32) >> 4;
+            tc_mma_f16_w(tmem + C::S_COL + 128 * t, qd + off, kd + off, idesc_s, kk > 0 ? 1u : 0u);
           }
-          __syncwarp();
+          tc_commit_w(&s_full[t]);
         }
       }
       // K/V stage of j-1 is free once both tiles' P V of j-1 have completed
-      if (j >= 1 && lane == 0) tc_commit(&kv_empty[(j - 1) % ST]);
-      __syncwarp();
+      if (j >= 1) tc_commit_w(&kv_empty[(j - 1) % ST]);
     }
   } else {
     // ------------------------------------------------------------ softmax (thread = query row)

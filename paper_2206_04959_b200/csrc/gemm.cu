@@ -316,28 +316,24 @@ __global__ void __launch_bounds__(256, 1)
         const int s = it % S;
         mbar_wait(&full[s], (it / S) & 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a0 = smem_u32(smA + s * C::A_BYTES);
-          const uint32_t b0 = smem_u32(smB + s * C::B_BYTES);
+        // whole-warp issue: elect.sync inside the asm (one instruction per MMA, no per-lane broadcast loop)
+        const uint64_t ad0 = sdesc_sw128(smem_u32(smA + s * C::A_BYTES), a_lbo, a_sbo);
+        const uint64_t bd0 = sdesc_sw128(smem_u32(smB + s * C::B_BYTES), b_lbo, b_sbo);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk) {
-            const uint64_t ad = sdesc_sw128(a0 + kk * a_kstep, a_lbo, a_sbo);
-            const uint64_t bd = sdesc_sw128(b0 + kk * b_kstep, b_lbo, b_sbo);
-            const uint32_t acc = (EPI == EPI_ACC_F32 || kb > 0 || kk > 0) ? 1u : 0u;
-            if constexpr (CG == 2)
-              tc_mma_f16_cg2(d_tmem, ad, bd, idesc, acc);
-            else
-              tc_mma_f16(d_tmem, ad, bd, idesc, acc);
-          }
-          if constexpr (CG == 2) {
-            tc_commit_cg2_mc(&empty[s], 0x3);
-            if (kb == nk - 1) tc_commit_cg2_mc(&tfull[buf], 0x3);
-          } else {
-            tc_commit(&empty[s]);
-            if (kb == nk - 1) tc_commit(&tfull[buf]);
-          }
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          const uint32_t acc = (EPI == EPI_ACC_F32 || kb > 0 || kk > 0) ? 1u : 0u;
+          if constexpr (CG == 2)
+            tc_mma_f16_cg2_w(d_tmem, ad0 + ((kk * a_kstep) >> 4), bd0 + ((kk * b_kstep) >> 4), idesc, acc);
+          else
+            tc_mma_f16_w(d_tmem, ad0 + ((kk * a_kstep) >> 4), bd0 + ((kk * b_kstep) >> 4), idesc, acc);
         }
-        __syncwarp();
+        if constexpr (CG == 2) {
+          tc_commit_cg2_mc_w(&empty[s], 0x3);
+          if (kb == nk - 1) tc_commit_cg2_mc_w(&tfull[buf], 0x3);
+        } else {
+          tc_commit_w(&empty[s]);
+          if (kb == nk - 1) tc_commit_w(&tfull[buf]);
+        }
       }
     }
   } else if (warp >= 4) {
