@@ -12,7 +12,8 @@ import os
 
 import torch
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmerak_tmp.so")
+# MERAK_LIB: an alternative in-tree build of the same library (A/B measurements only)
+LIB_PATH = os.environ.get("MERAK_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmerak_tmp.so")
 
 MERAK_OK, MERAK_EINVAL, MERAK_EINDIVISIBLE, MERAK_EUNSUPPORTED = 0, -1, -2, -3
 MERAK_ECUDA, MERAK_EPEER, MERAK_ENOMEM, MERAK_ETIMEOUT, MERAK_ESTATE = -4, -5, -6, -7, -8
