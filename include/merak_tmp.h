@@ -143,7 +143,20 @@ typedef struct {
   int32_t comm;        /* MERAK_COMM_PEER | MERAK_COMM_NCCL | MERAK_COMM_LOCAL        */
   int32_t comm_ctas;   /* CTAs used by each all-reduce kernel; 0 => auto              */
   int32_t device;      /* CUDA device ordinal this handle lives on                    */
+  int32_t seq_parallel; /* 1 = sequence-parallel layout, see below   */
 } merak_tmp_config;
+
+/* Sequence-parallel layout (seq_parallel = 1, T > 1, comm PEER or INPROC, bf16): the row-parallel
+ * all-reduces become reduce-scatters and the replicated LN / residual work is sharded by T.  x, y, dx, dy
+ * are then the rank's TOKEN SHARD, [B*s/T, h]: for every sub-batch j (m = B*s/n tokens) rank r holds tokens
+ * [j*m + r*m/T, j*m + (r+1)*m/T) as its local rows [j*m/T, (j+1)*m/T) -- the shard depends on n (the caller
+ * reshards after merak_tmp_set_subbatches).  Forward per sub-batch: LN1 on the own rows; all-gather of u;
+ * QKV, attention, proj (partial); reduce-scatter + b_o + residual + LN2 on the own rows; all-gather of u2; fc1,
+ * fc2 (partial); reduce-scatter + b_2 + residual = the own rows of y.  Backward mirrors it with all-gathers of
+ * dy and dx1 and reduce-scatters of the fc1 / QKV dgrad partials; the LN gradients are summed over the own
+ * rows, then over the ranks in rank order.  Requires (B*s/n) % (8 T) == 0 (EINDIVISIBLE).  Numerics: every
+ * row is computed by the same kernels as without sequence parallelism, so y, dx and the weight / bias
+ * gradients are bit-identical to the replicated layout; the LN-parameter gradients differ in summation order. */
 
 /* Collective used ONLY during init to exchange CUDA IPC handles (and the NCCL unique id):
  * gathers `bytes_per_rank` bytes from every rank of the TMP group into `recv` in rank order

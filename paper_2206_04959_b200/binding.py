@@ -37,7 +37,7 @@ class Config(ctypes.Structure):
                 ("microbatch", ctypes.c_int32), ("tmp_degree", ctypes.c_int32), ("tmp_rank", ctypes.c_int32),
                 ("n_sub", ctypes.c_int32), ("ffn_hidden", ctypes.c_int32), ("ln_eps", ctypes.c_float),
                 ("precision", ctypes.c_int32), ("comm", ctypes.c_int32), ("comm_ctas", ctypes.c_int32),
-                ("device", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("seq_parallel", ctypes.c_int32)]
 
 
 class Weights(ctypes.Structure):
@@ -178,6 +178,14 @@ def _make_allgather(group):
     return cb
 
 
+def sp_rows(tokens: int, n_sub: int, T: int, r: int):
+    """Global token indices of rank r's shard in the sequence-parallel layout (merak_tmp.h): for every
+    sub-batch j of m = tokens / n_sub tokens, tokens [j*m + r*m/T, j*m + (r+1)*m/T), in that order."""
+    m = tokens // n_sub
+    mr = m // T
+    return torch.cat([torch.arange(j * m + r * mr, j * m + (r + 1) * mr) for j in range(n_sub)])
+
+
 class TmpLayer:
     """One rank's handle of the sub-pipelined TMP transformer layer (merak_tmp_t).
 
@@ -185,13 +193,13 @@ class TmpLayer:
 
     def __init__(self, hidden, heads, seq_len, microbatch, tmp_degree=1, tmp_rank=0, n_sub=2, ffn_hidden=0,
                  ln_eps=1e-5, comm=MERAK_COMM_PEER, comm_ctas=0, device=None, group=None,
-                 precision=MERAK_BF16):
+                 precision=MERAK_BF16, seq_parallel=False):
         L = lib()
         if device is None:
             device = torch.cuda.current_device()
         self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
         self.cfg = Config(hidden, heads, seq_len, microbatch, tmp_degree, tmp_rank, n_sub, ffn_hidden, ln_eps,
-                          precision, comm, comm_ctas, self.device.index or 0)
+                          precision, comm, comm_ctas, self.device.index or 0, int(bool(seq_parallel)))
         self._cb = ALLGATHER_FN(_make_allgather(group)) if tmp_degree > 1 and comm != MERAK_COMM_LOCAL else ALLGATHER_FN(0)
         h = ctypes.c_void_p()
         st = L.merak_tmp_init(ctypes.byref(self.cfg), self._cb, None, ctypes.byref(h))
@@ -201,7 +209,7 @@ class TmpLayer:
 
     @classmethod
     def group(cls, hidden, heads, seq_len, microbatch, tmp_degree, n_sub=2, ffn_hidden=0, ln_eps=1e-5, comm_ctas=0,
-              device=None, precision=MERAK_BF16):
+              device=None, precision=MERAK_BF16, seq_parallel=False):
         """All T ranks of a TMP group as handles of this process on ONE device (merak_tmp_init_group,
         MERAK_COMM_INPROC): rank r's all-reduces read the other ranks' partials straight from their slots.
         Returns [rank 0, ..., rank T-1].  Issue every collective call on every rank (in any order from
@@ -217,7 +225,7 @@ class TmpLayer:
             device = torch.cuda.current_device()
         dev = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
         cfg = Config(hidden, heads, seq_len, microbatch, tmp_degree, 0, n_sub, ffn_hidden, ln_eps, precision,
-                     MERAK_COMM_INPROC, comm_ctas, dev.index or 0)
+                     MERAK_COMM_INPROC, comm_ctas, dev.index or 0, int(bool(seq_parallel)))
         hs = (ctypes.c_void_p * tmp_degree)()
         st = L.merak_tmp_init_group(ctypes.byref(cfg), hs)
         if st != MERAK_OK:
@@ -227,7 +235,7 @@ class TmpLayer:
             o = cls.__new__(cls)
             o.device = dev
             o.cfg = Config(hidden, heads, seq_len, microbatch, tmp_degree, r, n_sub, ffn_hidden, ln_eps, precision,
-                           MERAK_COMM_INPROC, comm_ctas, dev.index or 0)
+                           MERAK_COMM_INPROC, comm_ctas, dev.index or 0, int(bool(seq_parallel)))
             o._cb = ALLGATHER_FN(0)
             o.h = ctypes.c_void_p(hs[r])
             out.append(o)

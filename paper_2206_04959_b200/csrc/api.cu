@@ -31,7 +31,8 @@ typedef __nv_bfloat16 bf16;
 namespace {
 
 constexpr int MAXN = 64;  // max sub-batches
-constexpr int NSLOT = 4;  // AR#1..AR#4 partial slots
+constexpr int NSLOT = 5;  // AR#1..AR#4 partial slots (+ the sequence-parallel all-gather slot, index 4)
+constexpr int AG_SLOT = 4;
 
 struct ProfRec {
   int cls;
@@ -117,6 +118,9 @@ struct merak_tmp {
   std::string err;
   ncclComm_t nccl = nullptr;
   uint64_t timeout_ns = 20ull * 1000 * 1000 * 1000;  // watchdog (env MERAK_AR_TIMEOUT_MS)
+  bool sp = false;        // seq_parallel (T > 1): token-sharded x / y / dx / dy, reduce-scatter + all-gather
+  size_t lnx_off = 0;     // sp: peer-visible LN-gradient exchange area [MAXN][4][h] fp32 after the flags
+  bf16 *dyf = nullptr;    // sp: the all-gathered dy [M, h] (fc2 dgrad and the W2 wgrad read every token)
   bool use_nvls = false;  // MERAK_COMM_NVLS: slots bound to a multicast object, phase 1 reduced in the switch
   Nvls nvls = {};
   bool two_shot = false;  // T >= 4: reduce-scatter + all-gather instead of one-shot (env MERAK_AR_TWO_SHOT)
@@ -637,7 +641,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.dctx = dctx; a.dqkv = dqkv; a.delta = h->delta + so; a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
       a.dq_acc = h->dq_acc + so * h->d;
       a.dq_sem = h->dq_sem + (size_t)j * b * h->Hr * ((h->s + 63) / 64);
-      Launch Lk(h, MERAK_K_ATTN_BWD, cst, 4.0 * b * hr * (double)h->s * (h->s + 1), 2);
+      Launch Lk(h, MERAK_K_ATTN_BWD, cst, 4.0 * b * hr * (double)h->s * (h->s + 1), 3);
       CK(h, attn_bwd(a, cst));
     }
     CK(h, cudaEventRecord(h->ev_dq[j], cst));
@@ -683,6 +687,300 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
   TRY(run_wgrad(h, h->dqkv, 3 * hr, 3 * hr, (const bf16 *)S(L.u), L.ld_u, hh, h->M, gr->w_qkv, gr->b_qkv));
   CK(h, cudaEventRecord(h->ev_wqkv, h->cw));
   CK(h, cudaEventRecord(h->ev_red, h->cr));  // the next backward's AR#3/#4 rewrite the LN partials
+  h->have_wg = true;
+  return leave(h, st, flags, 3);
+}
+
+// ------------------------------------------------------------------------------ sequence parallelism
+// seq_parallel (merak_tmp.h): x / y / dx / dy are token shards; rank r owns the rows
+// [j*m + r*m/T, j*m + (r+1)*m/T) of sub-batch j (local rows [j*m/T, (j+1)*m/T)).  The row-parallel all-reduces
+// become reduce-scatters (the fused epilogue kernels run on the own rows only) and the column-parallel GEMMs'
+// inputs come from all-gathers through the peer-visible slot AG_SLOT.  Every writer of AG_SLOT is ordered
+// after a handshake that follows the previous all-gather of the same rows (module comment in ln_ar.cu).
+static float *lnx_ptr(merak_tmp_t *h, int q, int j, int k) {
+  return reinterpret_cast<float *>(h->peer_pv[q] + h->lnx_off) + ((size_t)j * 4 + k) * h->h;
+}
+static merak_status sp_handshake(merak_tmp_t *h, PeerSync *out = nullptr) {
+  PeerSync ps = make_sync(h, true);
+  TRY(sync_peers(h, ps));
+  if (out) *out = ps;
+  return MERAK_OK;
+}
+// all-gather of the m rows of sub-batch region r0 from every rank's AG_SLOT into dst (row stride ld)
+static merak_status sp_gather(merak_tmp_t *h, size_t r0, int m, bf16 *dst, int ld, const OnesPad &pad) {
+  AgArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int q = 0; q < h->T; ++q) a.src[q] = slot_ptr(h, q, AG_SLOT) + r0 * h->h;
+  a.T = h->T; a.m = m; a.h = h->h; a.rows_per = m / h->T; a.dst = dst; a.ld_dst = ld;
+  Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+  CK(h, ag_rows(a, pad, h->ms));
+  return MERAK_OK;
+}
+
+static merak_status layer_fwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, const bf16 *x, bf16 *y, char *saved,
+                                 uint32_t flags, cudaStream_t st) {
+  const SavedLayout L = saved_layout(h);
+  const int n = h->n, m = h->M / n, mr = m / h->T, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr, r = h->r;
+  TRY(enter(h, st, true));
+  auto S = [&](size_t off) { return saved + off; };
+  // ---- attention block, sub-batch j: LN1 (own rows) -> all-gather u -> QKV -> attention -> proj (partial)
+  //      -> reduce-scatter + b_o + residual + LN2 (own rows) -> all-gather u2
+  for (int j = 0; j < n; ++j) {
+    cudaStream_t cst = sub_stream(h, j);
+    if (h->chain_open) CK(h, cudaStreamWaitEvent(cst, h->prev_out[j], 0));
+    const size_t r0 = (size_t)j * m, l0 = (size_t)j * mr, own = r0 + (size_t)r * mr;
+    const bf16 *xj = x + l0 * hh;
+    bf16 *ag_own = slot_ptr(h, r, AG_SLOT) + own * hh;
+    bf16 *u = (bf16 *)S(L.u) + r0 * L.ld_u;
+    bf16 *qkv = (bf16 *)S(L.qkv) + r0 * 3 * hr;
+    bf16 *ctx = (bf16 *)S(L.ctx) + r0 * L.ld_ctx;
+    float *lse = (float *)S(L.lse) + (size_t)j * b * h->Hr * h->s;
+    {
+      OnesPad nopad;
+      memset(&nopad, 0, sizeof(nopad));
+      Launch Lk(h, MERAK_K_LN, cst, 0.0);
+      CK(h, ln_fwd(xj, (const bf16 *)w->ln1_g, (const bf16 *)w->ln1_b, ag_own, hh, (float *)S(L.mean1) + l0,
+                   (float *)S(L.rstd1) + l0, mr, hh, h->eps, nopad, cst));
+    }
+    CK(h, cudaEventRecord(h->ev_p[j], cst));
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
+    TRY(sp_handshake(h));
+    {
+      OnesPad pad;  // the ones columns of u and ctx for all m rows (wgrad bias columns)
+      memset(&pad, 0, sizeof(pad));
+      pad.n = 2;
+      pad.ptr[0] = u; pad.ld[0] = L.ld_u; pad.col[0] = hh;
+      pad.ptr[1] = ctx; pad.ld[1] = L.ld_ctx; pad.col[1] = hr;
+      TRY(sp_gather(h, r0, m, u, L.ld_u, pad));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[AG_SLOT][j], h->ms));
+    CK(h, cudaStreamWaitEvent(cst, h->ev_ar[AG_SLOT][j], 0));
+    GemmArgs g = gargs(u, w->w_qkv, m, 3 * hr, hh, L.ld_u, hh, false, false, EPI_BIAS_BF16);
+    g.out = qkv; g.ldo = 3 * hr; g.bias = w->b_qkv;
+    TRY(run_gemm(h, g, cst));
+    {
+      AttnArgs a;
+      memset(&a, 0, sizeof(a));
+      a.qkv = qkv; a.ctx = ctx; a.ld_ctx = L.ld_ctx; a.lse = lse; a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
+      Launch Lk(h, MERAK_K_ATTN_FWD, cst, 2.0 * b * hr * (double)h->s * (h->s + 1));
+      CK(h, attn_fwd(a, cst));
+    }
+    if (h->ev_ar_valid[0][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[0][j], 0));
+    g = gargs(ctx, w->w_o, m, hh, hr, L.ld_ctx, hr, false, false, EPI_STORE_BF16);
+    g.out = slot_ptr(h, r, 0) + r0 * hh; g.ldo = hh;
+    TRY(run_gemm(h, g, cst));
+    CK(h, cudaEventRecord(h->ev_p[j], cst));
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
+    {
+      PeerSync ps;
+      TRY(sp_handshake(h, &ps));
+      ArFwdArgs a;
+      memset(&a, 0, sizeof(a));
+      for (int q = 0; q < h->T; ++q) a.partial[q] = slot_ptr(h, q, 0) + own * hh;
+      a.T = h->T; a.m = mr; a.h = hh; a.resid = xj; a.bias = (const bf16 *)w->b_o;
+      a.out = (bf16 *)S(L.x1) + l0 * hh;
+      a.do_ln = true; a.gamma = (const bf16 *)w->ln2_g; a.beta = (const bf16 *)w->ln2_b;
+      a.ln_out = ag_own; a.ld_ln = hh;  // u2 rows for the all-gather
+      a.mean = (float *)S(L.mean2) + l0; a.rstd = (float *)S(L.rstd2) + l0;
+      a.eps = h->eps; a.ctas = h->cfg.comm_ctas;
+      Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+      CK(h, ar_fwd(a, ps, h->ms));
+    }
+    TRY(sp_handshake(h));
+    {
+      OnesPad pad;  // the ones columns of u2 and g
+      memset(&pad, 0, sizeof(pad));
+      pad.n = 2;
+      pad.ptr[0] = (bf16 *)S(L.u2) + r0 * L.ld_u2; pad.ld[0] = L.ld_u2; pad.col[0] = hh;
+      pad.ptr[1] = (bf16 *)S(L.g) + r0 * L.ld_g; pad.ld[1] = L.ld_g; pad.col[1] = fr;
+      TRY(sp_gather(h, r0, m, (bf16 *)S(L.u2) + r0 * L.ld_u2, L.ld_u2, pad));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[0][j], h->ms));
+    h->ev_ar_valid[0][j] = true;
+  }
+  // ---- FFN block, sub-batch j: fc1 (+bias+GeLU) -> fc2 (partial) -> reduce-scatter + b_2 + residual (own rows)
+  for (int j = 0; j < n; ++j) {
+    cudaStream_t cst = sub_stream(h, j);
+    const size_t r0 = (size_t)j * m, l0 = (size_t)j * mr, own = r0 + (size_t)r * mr;
+    CK(h, cudaStreamWaitEvent(cst, h->ev_ar[0][j], 0));
+    bf16 *u2 = (bf16 *)S(L.u2) + r0 * L.ld_u2;
+    bf16 *z = (bf16 *)S(L.z) + r0 * fr, *gg = (bf16 *)S(L.g) + r0 * L.ld_g;
+    GemmArgs g = gargs(u2, w->w_1, m, fr, hh, L.ld_u2, hh, false, false, EPI_BIAS_GELU);
+    g.out = z; g.ldo = fr; g.out2 = gg; g.ldo2 = L.ld_g; g.bias = w->b_1;
+    TRY(run_gemm(h, g, cst));
+    if (h->ev_ar_valid[1][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[1][j], 0));
+    g = gargs(gg, w->w_2, m, hh, fr, L.ld_g, fr, false, false, EPI_STORE_BF16);
+    g.out = slot_ptr(h, r, 1) + r0 * hh; g.ldo = hh;
+    TRY(run_gemm(h, g, cst));
+    CK(h, cudaEventRecord(h->ev_p[j], cst));
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
+    {
+      PeerSync ps;
+      TRY(sp_handshake(h, &ps));
+      ArFwdArgs a;
+      memset(&a, 0, sizeof(a));
+      for (int q = 0; q < h->T; ++q) a.partial[q] = slot_ptr(h, q, 1) + own * hh;
+      a.T = h->T; a.m = mr; a.h = hh; a.resid = (const bf16 *)S(L.x1) + l0 * hh; a.bias = (const bf16 *)w->b_2;
+      a.out = y + l0 * hh; a.do_ln = false; a.ctas = h->cfg.comm_ctas;
+      Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+      CK(h, ar_fwd(a, ps, h->ms));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[1][j], h->ms));
+    h->ev_ar_valid[1][j] = true;
+  }
+  return leave(h, st, flags, 1);
+}
+
+static merak_status layer_bwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, const bf16 *x, const char *saved_c,
+                                 const bf16 *dy, bf16 *dx, const merak_tmp_grads *gr, uint32_t flags, cudaStream_t st) {
+  char *saved = const_cast<char *>(saved_c);
+  const SavedLayout L = saved_layout(h);
+  const int n = h->n, m = h->M / n, mr = m / h->T, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr, r = h->r;
+  TRY(enter(h, st, false));
+  auto S = [&](size_t off) { return saved + off; };
+  // ---- FFN block: all-gather dy -> fc2 dgrad (x GeLU') -> fc1 dgrad (partial) -> reduce-scatter + LN2 backward
+  //      (own rows) -> all-gather dx1; LN2 gradients: own rows, then ranks in order
+  for (int j = 0; j < n; ++j) {
+    cudaStream_t cst = sub_stream(h, j);
+    if (h->chain_open) CK(h, cudaStreamWaitEvent(cst, h->prev_out[j], 0));
+    if (h->have_wg) CK(h, cudaStreamWaitEvent(cst, h->ev_w1, 0));  // previous W1 wgrad read dz
+    const size_t r0 = (size_t)j * m, l0 = (size_t)j * mr, own = r0 + (size_t)r * mr;
+    bf16 *ag_own = slot_ptr(h, r, AG_SLOT) + own * hh;
+    {
+      Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+      CK(h, copy_rows(dy + l0 * hh, hh, ag_own, hh, mr, hh, h->ms));
+    }
+    TRY(sp_handshake(h));
+    {
+      OnesPad nopad;
+      memset(&nopad, 0, sizeof(nopad));
+      TRY(sp_gather(h, r0, m, h->dyf + r0 * hh, hh, nopad));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[AG_SLOT][j], h->ms));
+    CK(h, cudaStreamWaitEvent(cst, h->ev_ar[AG_SLOT][j], 0));
+    bf16 *dz = h->dz + r0 * fr;
+    GemmArgs g = gargs(h->dyf + r0 * hh, w->w_2, m, fr, hh, hh, fr, false, true, EPI_GELU_BWD);
+    g.out = dz; g.ldo = fr; g.aux = (const bf16 *)S(L.z) + r0 * fr; g.ld_aux = fr;
+    TRY(run_gemm(h, g, cst));
+    CK(h, cudaEventRecord(h->ev_dz[j], cst));
+    if (h->ev_ar_valid[2][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[2][j], 0));
+    g = gargs(dz, w->w_1, m, hh, fr, fr, hh, false, true, EPI_STORE_BF16);
+    g.out = slot_ptr(h, r, 2) + r0 * hh; g.ldo = hh;
+    TRY(run_gemm(h, g, cst));
+    CK(h, cudaEventRecord(h->ev_p[j], cst));
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
+    {
+      PeerSync ps;
+      TRY(sp_handshake(h, &ps));
+      ArBwdArgs a;
+      memset(&a, 0, sizeof(a));
+      for (int q = 0; q < h->T; ++q) a.partial[q] = slot_ptr(h, q, 2) + own * hh;
+      a.T = h->T; a.m = mr; a.h = hh; a.x_ln = (const bf16 *)S(L.x1) + l0 * hh;
+      a.mean = (const float *)S(L.mean2) + l0; a.rstd = (const float *)S(L.rstd2) + l0;
+      a.gamma = (const bf16 *)w->ln2_g; a.dres = dy + l0 * hh; a.dx = ag_own;  // dx1 rows for the all-gather
+      a.part_dg = h->part_lng + (l0 / h->G) * hh; a.part_db = h->part_lnb + (l0 / h->G) * hh;
+      a.G = h->G; a.ctas = h->cfg.comm_ctas;
+      Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+      CK(h, ar_bwd(a, ps, h->ms));
+    }
+    {
+      Launch Lk(h, MERAK_K_REDUCE, h->ms, 0.0);
+      CK(h, group_chain2(h->part_lng + (l0 / h->G) * hh, h->part_lnb + (l0 / h->G) * hh, mr / h->G, hh,
+                         lnx_ptr(h, r, j, 0), lnx_ptr(h, r, j, 1), h->ms));
+    }
+    TRY(sp_handshake(h));  // every rank's dx1 rows and LN2 partials are written
+    {
+      OnesPad nopad;
+      memset(&nopad, 0, sizeof(nopad));
+      TRY(sp_gather(h, r0, m, h->dx1 + r0 * hh, hh, nopad));
+    }
+    {
+      const float *s0[MAX_T], *s1[MAX_T];
+      for (int q = 0; q < h->T; ++q) {
+        s0[q] = lnx_ptr(h, q, j, 0);
+        s1[q] = lnx_ptr(h, q, j, 1);
+      }
+      Launch Lk(h, MERAK_K_REDUCE, h->ms, 0.0);
+      CK(h, rank_sum_add2(s0, s1, h->T, hh, gr->ln2_g, gr->ln2_b, h->ms));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[2][j], h->ms));
+    h->ev_ar_valid[2][j] = true;
+  }
+  // weight + bias gradients of the FFN block over ALL tokens (one accumulation chain, as without sp)
+  for (int j = 0; j < n; ++j) CK(h, cudaStreamWaitEvent(h->cw, h->ev_ar[AG_SLOT][j], 0));
+  TRY(run_wgrad(h, h->dyf, hh, hh, (const bf16 *)S(L.g), L.ld_g, fr, h->M, gr->w_2, gr->b_2));
+  for (int j = 0; j < n; ++j) CK(h, cudaStreamWaitEvent(h->cw, h->ev_dz[j], 0));
+  TRY(run_wgrad(h, h->dz, fr, fr, (const bf16 *)S(L.u2), L.ld_u2, hh, h->M, gr->w_1, gr->b_1));
+  CK(h, cudaEventRecord(h->ev_w1, h->cw));
+  // ---- attention block: proj dgrad -> attention bwd -> QKV dgrad (partial) -> reduce-scatter + LN1 backward
+  for (int j = 0; j < n; ++j) {
+    cudaStream_t cst = sub_stream(h, j);
+    const size_t r0 = (size_t)j * m, l0 = (size_t)j * mr, own = r0 + (size_t)r * mr;
+    CK(h, cudaStreamWaitEvent(cst, h->ev_ar[2][j], 0));
+    const bf16 *dx1 = h->dx1 + r0 * hh;
+    bf16 *dctx = h->dctx + r0 * hr, *dqkv = h->dqkv + r0 * 3 * hr;
+    const bf16 *qkv = (const bf16 *)S(L.qkv) + r0 * 3 * hr, *ctx = (const bf16 *)S(L.ctx) + r0 * L.ld_ctx;
+    GemmArgs g = gargs(dx1, w->w_o, m, hr, hh, hh, hr, false, true, EPI_STORE_BF16);
+    g.out = dctx; g.ldo = hr;
+    TRY(run_gemm(h, g, cst));
+    if (h->have_wg) CK(h, cudaStreamWaitEvent(cst, h->ev_wqkv, 0));  // previous W_qkv wgrad read dqkv
+    {
+      AttnArgs a;
+      memset(&a, 0, sizeof(a));
+      const size_t so = (size_t)j * b * h->Hr * h->s;
+      a.qkv = qkv; a.ctx = (void *)ctx; a.ld_ctx = L.ld_ctx; a.lse = (float *)S(L.lse) + so;
+      a.dctx = dctx; a.dqkv = dqkv; a.delta = h->delta + so; a.b = b; a.s = h->s; a.heads = h->Hr; a.d = h->d;
+      a.dq_acc = h->dq_acc + so * h->d;
+      a.dq_sem = h->dq_sem + (size_t)j * b * h->Hr * ((h->s + 63) / 64);
+      Launch Lk(h, MERAK_K_ATTN_BWD, cst, 4.0 * b * hr * (double)h->s * (h->s + 1), 3);
+      CK(h, attn_bwd(a, cst));
+    }
+    CK(h, cudaEventRecord(h->ev_dq[j], cst));
+    if (h->ev_ar_valid[3][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[3][j], 0));
+    g = gargs(dqkv, w->w_qkv, m, hh, 3 * hr, 3 * hr, hh, false, true, EPI_STORE_BF16);
+    g.out = slot_ptr(h, r, 3) + r0 * hh; g.ldo = hh;
+    TRY(run_gemm(h, g, cst));
+    CK(h, cudaEventRecord(h->ev_p[j], cst));
+    CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
+    {
+      PeerSync ps;
+      TRY(sp_handshake(h, &ps));
+      ArBwdArgs a;
+      memset(&a, 0, sizeof(a));
+      for (int q = 0; q < h->T; ++q) a.partial[q] = slot_ptr(h, q, 3) + own * hh;
+      a.T = h->T; a.m = mr; a.h = hh; a.x_ln = x + l0 * hh;
+      a.mean = (const float *)S(L.mean1) + l0; a.rstd = (const float *)S(L.rstd1) + l0;
+      a.gamma = (const bf16 *)w->ln1_g; a.dres = h->dx1 + own * hh; a.dx = dx + l0 * hh;
+      a.part_dg = h->part_lng1 + (l0 / h->G) * hh; a.part_db = h->part_lnb1 + (l0 / h->G) * hh;
+      a.G = h->G; a.ctas = h->cfg.comm_ctas;
+      Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+      CK(h, ar_bwd(a, ps, h->ms));
+    }
+    {
+      Launch Lk(h, MERAK_K_REDUCE, h->ms, 0.0);
+      CK(h, group_chain2(h->part_lng1 + (l0 / h->G) * hh, h->part_lnb1 + (l0 / h->G) * hh, mr / h->G, hh,
+                         lnx_ptr(h, r, j, 2), lnx_ptr(h, r, j, 3), h->ms));
+    }
+    TRY(sp_handshake(h));  // every rank's LN1 partials are written
+    {
+      const float *s0[MAX_T], *s1[MAX_T];
+      for (int q = 0; q < h->T; ++q) {
+        s0[q] = lnx_ptr(h, q, j, 2);
+        s1[q] = lnx_ptr(h, q, j, 3);
+      }
+      Launch Lk(h, MERAK_K_REDUCE, h->ms, 0.0);
+      CK(h, rank_sum_add2(s0, s1, h->T, hh, gr->ln1_g, gr->ln1_b, h->ms));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[3][j], h->ms));
+    h->ev_ar_valid[3][j] = true;
+  }
+  CK(h, cudaStreamWaitEvent(h->cw, h->ev_ar[2][n - 1], 0));  // every dx1 row (the all-gathers run in order on ms)
+  TRY(run_wgrad(h, h->dx1, hh, hh, (const bf16 *)S(L.ctx), L.ld_ctx, hr, h->M, gr->w_o, gr->b_o));
+  CK(h, cudaEventRecord(h->ev_wo, h->cw));
+  for (int j = 0; j < n; ++j) CK(h, cudaStreamWaitEvent(h->cw, h->ev_dq[j], 0));
+  TRY(run_wgrad(h, h->dqkv, 3 * hr, 3 * hr, (const bf16 *)S(L.u), L.ld_u, hh, h->M, gr->w_qkv, gr->b_qkv));
+  CK(h, cudaEventRecord(h->ev_wqkv, h->cw));
+  CK(h, cudaEventRecord(h->ev_red, h->ms));  // the next backward rewrites the LN partials (on ms as well)
   h->have_wg = true;
   return leave(h, st, flags, 3);
 }
@@ -915,6 +1213,13 @@ static merak_status validate(const merak_tmp_config *c) {
   if (c->microbatch > 48) return fail(nullptr, MERAK_EUNSUPPORTED, "microbatch > 48");
   if (c->hidden % 8 || (f / T) % 8) return fail(nullptr, MERAK_EUNSUPPORTED, "h and f/T must be multiples of 8");
   if (c->hidden > 8192) return fail(nullptr, MERAK_EUNSUPPORTED, "hidden > 8192 (row-engine register budget)");
+  if (c->seq_parallel && T > 1) {
+    if (c->comm != MERAK_COMM_PEER && c->comm != MERAK_COMM_INPROC)
+      return fail(nullptr, MERAK_EUNSUPPORTED, "seq_parallel needs comm PEER or INPROC");
+    if (c->precision != MERAK_BF16) return fail(nullptr, MERAK_EUNSUPPORTED, "seq_parallel needs bf16");
+    if (((long)c->microbatch * c->seq_len / c->n_sub) % (8 * T))
+      return fail(nullptr, MERAK_EINDIVISIBLE, "seq_parallel: tokens per sub-batch %% (8 T) != 0");
+  }
   return MERAK_OK;
 }
 
@@ -1044,8 +1349,14 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
   // MERAK_COMM_NVLS (T > 1): the slots live in multicast-bound memory set up by merak_tmp_init; the IPC-shared
   // block holds the handshake flags only
   const bool nvls = cfg->comm == MERAK_COMM_NVLS && h->T > 1;
-  h->flags_off = nvls ? 0 : NSLOT * h->slot_bytes;
+  h->sp = cfg->seq_parallel && h->T > 1;
+  const int nslot_pv = h->sp ? NSLOT : NSLOT - 1;  // the all-gather slot exists only in the sp layout
+  h->flags_off = nvls ? 0 : nslot_pv * h->slot_bytes;
   h->pv_bytes = h->flags_off + align256(2 * MAX_AR_CTAS * MAX_T * sizeof(uint32_t));
+  if (h->sp) {  // LN-gradient partial exchange: [MAXN sub-batches][dγ2, dβ2, dγ1, dβ1][h] fp32
+    h->lnx_off = h->pv_bytes;
+    h->pv_bytes += align256((size_t)MAXN * 4 * h->h * sizeof(float));
+  }
   CKI(cudaMalloc(&h->pv, h->pv_bytes));
   CKI(cudaMemset(h->pv + h->flags_off, 0, h->pv_bytes - h->flags_off));
   CKI(cudaHostAlloc(&h->err_host, 8 * sizeof(int), cudaHostAllocMapped));
@@ -1063,7 +1374,9 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
     const size_t o_pg = take((M / h->G) * (size_t)h->h * 4), o_pb = take((M / h->G) * (size_t)h->h * 4);
     const size_t o_pg1 = take((M / h->G) * (size_t)h->h * 4), o_pb1 = take((M / h->G) * (size_t)h->h * 4);
     const size_t o_ctr = take(64);
+    const size_t o_dyf = h->sp ? take(M * h->h * 2) : 0;
     CKI(cudaMalloc(&h->ws, o));
+    if (h->sp) h->dyf = (bf16 *)(h->ws + o_dyf);
     CKI(cudaMemset(h->ws + o_ctr, 0, 64));
     CKI(cudaMemset(h->ws + o_delta, 0, attn_bwd_ws_floats(h->B, h->s, h->Hr, h->d) * 4));  // dQ counters start at 0
     // dynamic GEMM tile schedule: opt-in (measured no gain over the static schedule at gpt1.5b, T=1)
@@ -1149,7 +1462,7 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
   }
   if (cfg->comm == MERAK_COMM_NVLS && h->T > 1) {
     std::string why;
-    const int rc = nvls_setup(&h->nvls, h->dev, h->T, h->r, (size_t)NSLOT * h->slot_bytes, ag, ag_ctx, &why);
+    const int rc = nvls_setup(&h->nvls, h->dev, h->T, h->r, (size_t)(NSLOT - 1) * h->slot_bytes, ag, ag_ctx, &why);
     if (rc != 0) {
       fail(h, rc == -2 ? MERAK_EUNSUPPORTED : MERAK_EPEER, "NVLS multicast setup: %s", why.c_str());
       return bail(rc == -2 ? MERAK_EUNSUPPORTED : MERAK_EPEER);
@@ -1216,6 +1529,8 @@ merak_status merak_tmp_set_subbatches(merak_tmp_t *h, int32_t n_sub) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
   if (h->chain_open) return fail(h, MERAK_ESTATE, "set_subbatches while a MERAK_FLAG_CHAIN sequence is open");
   if (n_sub <= 0 || n_sub > MAXN) return fail(h, MERAK_EINVAL, "n_sub out of range");
+  if (h->sp && ((long)h->M / n_sub) % (8 * h->T))
+    return fail(h, MERAK_EINDIVISIBLE, "seq_parallel: tokens per sub-batch %% (8 T) != 0");
   if (h->B % n_sub) return fail(h, MERAK_EINDIVISIBLE, "microbatch %% n_sub != 0");
   // all outstanding work of the old split must finish before slot/event indices are reinterpreted
   TRY(sync_all(h));
@@ -1243,8 +1558,12 @@ merak_status merak_tmp_layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, con
     if (!p || !aligned16(p)) return fail(h, MERAK_EINVAL, "NULL or non-16B-aligned pointer");
   if (h->broken) return fail(h, MERAK_ESTATE, "handle unusable after an earlier failure: %s", h->err.c_str());
   const uint32_t e0 = h->epoch;
-  const merak_status s = h->f32 ? layer_fwd_f32(h, w, (const float *)x, (float *)y, (char *)saved, flags, (cudaStream_t)st)
-                                : layer_fwd(h, w, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st, rc);
+  if (h->sp && (flags & (MERAK_FLAG_RECOMPUTE | MERAK_FLAG_NO_COMM)))
+    return fail(h, MERAK_EUNSUPPORTED, "seq_parallel: MERAK_FLAG_RECOMPUTE / MERAK_FLAG_NO_COMM are not available");
+  const merak_status s =
+      h->f32  ? layer_fwd_f32(h, w, (const float *)x, (float *)y, (char *)saved, flags, (cudaStream_t)st)
+      : h->sp ? layer_fwd_sp(h, w, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st)
+              : layer_fwd(h, w, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st, rc);
   if (s != MERAK_OK && (h->epoch != e0 || s == MERAK_ETIMEOUT)) h->broken = true;
   return s;
 }
@@ -1259,6 +1578,8 @@ merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, con
   for (const void *p : ps)
     if (!p || !aligned16(p)) return fail(h, MERAK_EINVAL, "NULL or non-16B-aligned pointer");
   if (h->broken) return fail(h, MERAK_ESTATE, "handle unusable after an earlier failure: %s", h->err.c_str());
+  if (h->sp && (flags & (MERAK_FLAG_RECOMPUTE | MERAK_FLAG_NO_COMM)))
+    return fail(h, MERAK_EUNSUPPORTED, "seq_parallel: MERAK_FLAG_RECOMPUTE / MERAK_FLAG_NO_COMM are not available");
   if ((flags & MERAK_FLAG_RECOMPUTE) && h->f32)
     return fail(h, MERAK_EUNSUPPORTED, "MERAK_FLAG_RECOMPUTE is not available in the fp32 check mode");
   const uint32_t e0 = h->epoch;
@@ -1272,10 +1593,12 @@ merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, con
     }
   }
   const merak_status s =
-      h->f32 ? layer_bwd_f32(h, w, (const float *)x, (const char *)saved, (const float *)dy, (float *)dx, g, flags,
+      h->f32  ? layer_bwd_f32(h, w, (const float *)x, (const char *)saved, (const float *)dy, (float *)dx, g, flags,
+                              (cudaStream_t)st)
+      : h->sp ? layer_bwd_sp(h, w, (const bf16 *)x, (const char *)saved, (const bf16 *)dy, (bf16 *)dx, g, flags,
                              (cudaStream_t)st)
-             : layer_bwd(h, w, (const bf16 *)x, (const char *)saved, (const bf16 *)dy, (bf16 *)dx, g, flags,
-                         (cudaStream_t)st);
+              : layer_bwd(h, w, (const bf16 *)x, (const char *)saved, (const bf16 *)dy, (bf16 *)dx, g, flags,
+                          (cudaStream_t)st);
   if (s != MERAK_OK && (h->epoch != e0 || s == MERAK_ETIMEOUT)) h->broken = true;
   return s;
 }

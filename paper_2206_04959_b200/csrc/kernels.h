@@ -241,6 +241,28 @@ cudaError_t colsum_sample(const __nv_bfloat16 *X, int ld, int s, int b, int n, f
 cudaError_t sample_reduce2(const float *p0, const float *p1, int gps, int b, int n, float *q0, float *q1, float *g0,
                            float *g1, cudaStream_t st);
 
+// ---------------------------------------------------------------- sequence-parallel helpers (ln_ar.cu)
+// All-gather of row shards: dst row i (row stride ld_dst) = row i of src[i / rows_per]
+// (row stride h; src[q] = rank q's peer-visible buffer), i < m; plus the ones-column pads of `pad` for every
+// row (written here because the row shards' producer only saw its own rows).
+struct AgArgs {
+  const __nv_bfloat16 *src[MAX_T];
+  int T, m, h, rows_per;
+  __nv_bfloat16 *dst;
+  int ld_dst;
+  bool pdl;
+};
+cudaError_t ag_rows(const AgArgs &a, const OnesPad &pad, cudaStream_t st);
+// out[c] = fixed-order chain over the g-row-group partials p[k][c], k < ngroups (t = 0 and, if p1, t = 1)
+cudaError_t group_chain2(const float *p0, const float *p1, int ngroups, int n, float *out0, float *out1,
+                         cudaStream_t st);
+// g_t[c] += sum over ranks q = 0..T-1 (in order) of src_t[q][c]  (t = 0, 1)
+cudaError_t rank_sum_add2(const float *const *src0, const float *const *src1, int T, int n, float *g0, float *g1,
+                          cudaStream_t st);
+// plain 16-byte-vector copy of rows (dst row stride ld_dst, src row stride ld_src, h multiple of 8)
+cudaError_t copy_rows(const __nv_bfloat16 *src, int ld_src, __nv_bfloat16 *dst, int ld_dst, int m, int h,
+                      cudaStream_t st);
+
 // ---------------------------------------------------------------- NVLS in-switch reduction (nvls.cu)
 // The all-reduce slots of this rank bound to a CUDA multicast object shared by the T ranks.
 struct Nvls {

@@ -700,6 +700,115 @@ cudaError_t sample_reduce2(const float *p0, const float *p1, int gps, int b, int
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------ sequence-parallel helpers
+// All-gather of row shards: each thread moves CHG 16-byte chunks (loads of all of them first: a peer load
+// over NVLink costs ~1-2 us), grid-stride over the m * h/8 chunks.
+constexpr int CHG = 4;
+__global__ void __launch_bounds__(256) ag_rows_kernel(AgArgs a, OnesPad pad) {
+  griddep_wait();
+  griddep_launch();
+  const int nc = a.h >> 3;
+  const long total = (long)a.m * nc;
+  const long stride = (long)gridDim.x * blockDim.x * CHG;
+  for (long base = ((long)blockIdx.x * blockDim.x + threadIdx.x) * CHG; base < total; base += stride) {
+    uint4 v[CHG];
+#pragma unroll
+    for (int k = 0; k < CHG; ++k) {
+      const long i = base + k;
+      if (i < total) {
+        const int row = (int)(i / nc), c = (int)(i % nc);
+        v[k] = ldg16(a.src[row / a.rows_per] + (size_t)row * a.h + (size_t)c * 8);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < CHG; ++k) {
+      const long i = base + k;
+      if (i < total) {
+        const int row = (int)(i / nc), c = (int)(i % nc);
+        *reinterpret_cast<uint4 *>(a.dst + (size_t)row * a.ld_dst + (size_t)c * 8) = v[k];
+        if (c < pad.n) {  // one thread per (row, pad): the ones column of pad c
+          uint4 one;
+          one.x = pack_bf16(1.f, 0.f);
+          one.y = one.z = one.w = 0u;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (q == c) *reinterpret_cast<uint4 *>(pad.ptr[q] + (size_t)row * pad.ld[q] + pad.col[q]) = one;
+        }
+      }
+    }
+  }
+}
+
+// out_t[c] = p_t[0][c] + p_t[1][c] + ... (sequential in k: a fixed order)
+__global__ void __launch_bounds__(256) group_chain_kernel(const float *p0, const float *p1, int ngroups, int n,
+                                                          float *out0, float *out1) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const float *p = blockIdx.y ? p1 : p0;
+  float acc = 0.f;
+  for (int k = 0; k < ngroups; ++k) acc += p[(size_t)k * n + c];
+  (blockIdx.y ? out1 : out0)[c] = acc;
+}
+
+struct RankSrc {
+  const float *q[2][MAX_T];
+};
+__global__ void __launch_bounds__(256) rank_sum_add_kernel(RankSrc s, int T, int n, float *g0, float *g1) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int t = blockIdx.y;
+  float acc = 0.f;
+  for (int q = 0; q < T; ++q) acc += s.q[t][q][c];  // rank order 0..T-1
+  float *g = t ? g1 : g0;
+  g[c] += acc;
+}
+
+__global__ void __launch_bounds__(256) copy_rows_kernel(const __nv_bfloat16 *src, int ld_src, __nv_bfloat16 *dst,
+                                                        int ld_dst, int m, int nc) {
+  const long total = (long)m * nc;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const int row = (int)(i / nc), c = (int)(i % nc);
+    *reinterpret_cast<uint4 *>(dst + (size_t)row * ld_dst + (size_t)c * 8) =
+        ldg16(src + (size_t)row * ld_src + (size_t)c * 8);
+  }
+}
+
+cudaError_t ag_rows(const AgArgs &a, const OnesPad &pad, cudaStream_t st) {
+  if (a.h % 8 || a.rows_per <= 0 || pad.n > 4 || (pad.n > a.h / 8)) return cudaErrorInvalidValue;
+  static int resident[MAX_DEV] = {};
+  const int dev = cur_device();
+  if (!resident[dev]) resident[dev] = resident_ctas((const void *)ag_rows_kernel, 256, 0);
+  const long work = ((long)a.m * (a.h / 8) + 256 * CHG - 1) / (256 * CHG);
+  const int grid = clamp_ctas(0, (int)(work < (1 << 30) ? work : (1 << 30)), resident[dev]);
+  return launch_k(ag_rows_kernel, dim3(grid), dim3(256), 0, st, a.pdl, a, pad);
+}
+
+cudaError_t group_chain2(const float *p0, const float *p1, int ngroups, int n, float *out0, float *out1,
+                         cudaStream_t st) {
+  group_chain_kernel<<<dim3((n + 255) / 256, p1 ? 2 : 1), 256, 0, st>>>(p0, p1, ngroups, n, out0, out1);
+  return cudaGetLastError();
+}
+
+cudaError_t rank_sum_add2(const float *const *src0, const float *const *src1, int T, int n, float *g0, float *g1,
+                          cudaStream_t st) {
+  RankSrc s;
+  for (int q = 0; q < T; ++q) {
+    s.q[0][q] = src0[q];
+    s.q[1][q] = src1 ? src1[q] : nullptr;
+  }
+  rank_sum_add_kernel<<<dim3((n + 255) / 256, src1 ? 2 : 1), 256, 0, st>>>(s, T, n, g0, g1);
+  return cudaGetLastError();
+}
+
+cudaError_t copy_rows(const __nv_bfloat16 *src, int ld_src, __nv_bfloat16 *dst, int ld_dst, int m, int h,
+                      cudaStream_t st) {
+  if (h % 8) return cudaErrorInvalidValue;
+  const long total = (long)m * (h / 8);
+  const int grid = (int)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
+  copy_rows_kernel<<<grid > 0 ? grid : 1, 256, 0, st>>>(src, ld_src, dst, ld_dst, m, h / 8);
+  return cudaGetLastError();
+}
+
 template <int NT, int CPT>
 static cudaError_t ar_preload_c() {
   const void *ks[] = {(const void *)ar_fwd_kernel<NT, CPT>, (const void *)ar_bwd_kernel<NT, CPT>};
@@ -722,6 +831,8 @@ static cudaError_t ar_preload_t() {
 cudaError_t ln_ar_preload() {
   const void *ks[] = {(const void *)peer_ready_kernel, (const void *)ln_fwd_kernel<1>, (const void *)ln_fwd_kernel<2>,
                       (const void *)ln_fwd_kernel<3>, (const void *)ln_fwd_kernel<4>, (const void *)colsum_sample_kernel,
+                      (const void *)ag_rows_kernel, (const void *)group_chain_kernel, (const void *)rank_sum_add_kernel,
+                      (const void *)copy_rows_kernel,
                       (const void *)sample_sum_kernel, (const void *)sample_chain_kernel};
   for (const void *k : ks) {
     cudaError_t e = touch_kernel(k);
