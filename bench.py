@@ -203,13 +203,16 @@ def run_reference(args, cfg, rank, world):
 class Stack:
     """L chained layers of one rank (weights, grads, saved activations, outputs) on one TmpLayer handle."""
 
-    def __init__(self, cfg, L, T, rank, dev, group, n_sub, comm=0, comm_ctas=0, streams1=False):
+    def __init__(self, cfg, L, T, rank, dev, group, n_sub, comm=0, comm_ctas=0, streams1=False, seq_parallel=False):
         import torch
 
-        from paper_2206_04959_b200 import TmpLayer, shard_weights, zero_grads_like
+        from paper_2206_04959_b200 import TmpLayer, shard_weights, sp_rows, zero_grads_like
         from synth import make_activations_torch, make_params_torch
         self.cfg, self.L, self.T, self.dev = cfg, L, T, dev
         self.X, self.DY = make_activations_torch(cfg, dev)
+        if seq_parallel:  # this rank's token shard (merak_tmp.h, sequence-parallel layout)
+            rows = sp_rows(cfg.tokens, n_sub, T, rank).to(dev)
+            self.X, self.DY = self.X[rows].contiguous(), self.DY[rows].contiguous()
         self.ws = [shard_weights(make_params_torch(cfg, dev, layer=k), cfg.heads, T, rank, dev) for k in range(L)]
         self.Ys = [torch.empty_like(self.X) for _ in range(L)]
         self.DXs = [torch.empty_like(self.X) for _ in range(L)]
@@ -218,7 +221,8 @@ class Stack:
             os.environ["MERAK_STREAMS"] = "1"
         try:
             self.layer = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, tmp_degree=T, tmp_rank=rank,
-                                  n_sub=n_sub, comm=comm, comm_ctas=comm_ctas, device=dev.index, group=group)
+                                  n_sub=n_sub, comm=comm, comm_ctas=comm_ctas, device=dev.index, group=group,
+                                  seq_parallel=seq_parallel)
         finally:
             if streams1:
                 del os.environ["MERAK_STREAMS"]
@@ -377,6 +381,8 @@ def main():
         if world > 1:
             extras["nvls"] = nvls_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step)
             stage("nvls pass done")
+            extras["seq_parallel"] = seqpar_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step)
+            stage("seq-parallel pass done")
             extras["pipeline"] = pipeline_pass(args, rank, world, dev, barrier, max_over_ranks)
             stage("pipeline pass done")
 
@@ -547,6 +553,24 @@ def nvls_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step):
                           "algbw_GBps": msg / (t_f * 1e-3) / 1e9,
                           "note": "algorithmic bandwidth = message bytes / time (the all-reduce of one [m, h] bf16 "
                                   "partial incl. handshakes); NVLS moves ~(1 + 1/T) x msg per GPU and direction"}}
+
+
+def seqpar_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step):
+    """the same stack in the sequence-parallel layout (token-sharded x / y, reduce-scatter
+    epilogues on the own rows, all-gathers of u, u2, dy, dx1): per-GPU TFLOP/s next to the replicated layout."""
+    from paper_2206_04959_b200 import MerakError
+    nx = max(3, args.steps // 2)
+    try:
+        st = Stack(cfg, L, T, rank, dev, group, n_sub, comm_ctas=args.comm_ctas, seq_parallel=True)
+    except MerakError as e:
+        return {"unavailable": str(e)}
+    for _ in range(3):
+        st.step()
+    ms, _, _ = timed(st, nx)
+    st.close()
+    return {"tflops_per_gpu": L * layer_flops(cfg) / T / (ms * 1e-3) / 1e12, "ms_per_step": ms,
+            "vs_replicated": ms_step / ms,
+            "note": "x / y / dx / dy token-sharded by T; the LN / residual epilogues run on the own rows"}
 
 
 def pipeline_pass(args, rank, world, dev, barrier, max_over_ranks, K=2, layer_cfg="gpt1.5b"):

@@ -123,6 +123,34 @@ def main():
                 failures.append((name, f"nvls: {k} not run-to-run deterministic"))
             if not torch.equal(outv[k], outv1[k]):
                 failures.append((name, f"nvls: {k}: n={cfg.n_sub} vs n=1 not bit-identical"))
+    # sequence-parallel layout across processes (NEXT-2): y / dx / weight gradients bit-identical to the replicated
+    # layout (each rank's token shard), LN gradients within 1e-5
+    from paper_2206_04959_b200 import FLAG_CHAIN as _FC, PARAM_NAMES, TmpLayer, shard_weights, sp_rows, zero_grads_like
+    scfg = tiny.with_(hidden=256, heads=8, seq_len=128, microbatch=4, n_sub=2, tmp_degree=T)
+    sparams, sx, sdy = make_all(scfg, seed=77)
+    ref = run_gpu_layer(scfg, sparams, sx, sdy, T=T, rank=rank, group=group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    lay = TmpLayer(scfg.hidden, scfg.heads, scfg.seq_len, scfg.microbatch, tmp_degree=T, tmp_rank=rank, n_sub=2,
+                   device=dev.index, group=group, seq_parallel=True)
+    rows = sp_rows(scfg.tokens, 2, T, rank).to(dev)
+    X = torch.as_tensor(np.asarray(sx).reshape(scfg.tokens, scfg.hidden)).to(dev, torch.bfloat16)[rows].contiguous()
+    DY = torch.as_tensor(np.asarray(sdy).reshape(scfg.tokens, scfg.hidden)).to(dev, torch.bfloat16)[rows].contiguous()
+    w = shard_weights(sparams, scfg.heads, T, rank, dev)
+    G = zero_grads_like(w)
+    Y, DX, SV = torch.empty_like(X), torch.empty_like(X), lay.new_saved()
+    lay.forward(w, X, Y, SV)
+    lay.backward(w, X, SV, DY, DX, G)
+    torch.cuda.synchronize()
+    lay.close()
+    if not (torch.equal(Y, ref["y"][rows]) and torch.equal(DX, ref["dx"][rows])):
+        failures.append(("seqpar", "y / dx differ from the replicated layout"))
+    for k in PARAM_NAMES:
+        if k.startswith("ln"):
+            if (G[k] - ref[k]).norm() > 1e-5 * ref[k].norm() + 1e-6:
+                failures.append(("seqpar", f"{k} off"))
+        elif not torch.equal(G[k], ref[k]):
+            failures.append(("seqpar", f"{k} not bit-identical to the replicated layout"))
+    print(f"[rank {rank}] seqpar T={T} done", flush=True)
     # chained stack (cross-layer overlap + workspace hazards across ranks): chained == unchained bitwise
     from gpu_layer_util import run_gpu_chain
     from synth import make_activations, make_params
