@@ -95,9 +95,16 @@ enum { MERAK_BF16 = 0, MERAK_FP32_CHECK = 1 };      /* merak_tmp_config.precisio
  * on one GPU (SURVEY §8(d) "TMP=8" projection).  Results are NOT the layer's. */
 /* MERAK_COMM_INPROC: the T ranks of the group are T handles of ONE process on ONE device, created
  * together by merak_tmp_init_group; every all-reduce reads the peers' partials straight from their
- * slots (same context, no CUDA IPC), with the same handshake, kernels and arithmetic as MERAK_COMM_PEER.
- * It exists so that T > 1 runs of the method (P:107 partial sums over T ranks, P:571 sub-batch overlap)
- * can be checked against the oracle on a single GPU.  Not for throughput (the ranks share one GPU). */
+ * slots (same context, no CUDA IPC), with the same kernels and arithmetic as MERAK_COMM_PEER.  The
+ * cross-rank handshake is an event exchange instead of the spinning handshake kernel: a rank's
+ * merak_tmp_layer_fwd / _bwd call is DEFERRED (returns MERAK_OK at once, nothing issued) until every rank
+ * of the group has made its matching call; the call that completes the set issues all T calls from the
+ * calling thread, switching between the ranks at each handshake point, and returns the first failure of
+ * the set.  Pointers passed to a deferred call must stay valid until the set completes.  A second layer
+ * call on a rank before the set completes, or merak_tmp_join / set_subbatches / profiling calls on a rank
+ * with a deferred call, fail with MERAK_ESTATE.  It exists so that T > 1 runs of the method (P:107
+ * partial sums over T ranks, P:571 sub-batch overlap) can be checked against the oracle on a single GPU.
+ * Not for throughput (the ranks share one GPU). */
 /* MERAK_COMM_NVLS: as MERAK_COMM_PEER, but the all-reduce slots of the T ranks are bound to one CUDA
  * multicast object (NVLink SHARP) and the reduce-scatter phase runs in the NVSwitch:
  * rank r reads the rows it owns with multimem.ld_reduce (the switch sums the T bf16 partials with fp32

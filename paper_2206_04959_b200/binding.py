@@ -212,14 +212,9 @@ class TmpLayer:
               device=None, precision=MERAK_BF16, seq_parallel=False):
         """All T ranks of a TMP group as handles of this process on ONE device (merak_tmp_init_group,
         MERAK_COMM_INPROC): rank r's all-reduces read the other ranks' partials straight from their slots.
-        Returns [rank 0, ..., rank T-1].  Issue every collective call on every rank (in any order from
-        one thread: the layer calls never block the host)."""
-        # T ranks' internal streams share one context: with fewer hardware queues than streams, one rank's
-        # compute can queue behind another rank's spinning handshake (merak_tmp.h, MERAK_COMM_INPROC)
-        conn = int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8"))
-        if conn < 32:
-            raise RuntimeError("in-process TMP groups need CUDA_DEVICE_MAX_CONNECTIONS=32 in the environment "
-                               "before CUDA initialises (tests/conftest.py sets it)")
+        Returns [rank 0, ..., rank T-1].  Issue every layer call on every rank, from one thread, in any rank
+        order: the library defers each rank's call until all T ranks made it, then issues them together
+        (merak_tmp.h, MERAK_COMM_INPROC); the layer calls never block the host."""
         L = lib()
         if device is None:
             device = torch.cuda.current_device()

@@ -17,7 +17,10 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <ucontext.h>
+
 #include <algorithm>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -123,6 +126,7 @@ struct merak_tmp {
   bf16 *dyf = nullptr;    // sp: the all-gathered dy [M, h] (fc2 dgrad and the W2 wgrad read every token)
   bool use_nvls = false;  // MERAK_COMM_NVLS: slots bound to a multicast object, phase 1 reduced in the switch
   Nvls nvls = {};
+  bool fused_wait = false;  // two-shot: phase-1 kernel publishes, phase-2 kernel waits in kernel (env MERAK_AR_FUSED_WAIT)
   bool two_shot = false;  // T >= 4: reduce-scatter + all-gather instead of one-shot (env MERAK_AR_TWO_SHOT)
   bool pdl = false;       // programmatic dependent launch along the all-reduce kernel chain (env MERAK_AR_PDL)
   int gemm_smem_kb = 192;  // GEMM TMA ring: 160 KB at T > 1 leaves smem for co-resident all-reduce kernels
@@ -141,7 +145,52 @@ struct merak_tmp {
   int *tile_ctr = nullptr;  // dynamic GEMM tile counters, one per compute stream (cs, cs1); MERAK_GEMM_DYN=1
   char *ws32 = nullptr;
   float *dz32 = nullptr, *dx1_32 = nullptr, *dctx32 = nullptr, *dqkv32 = nullptr, *delta32 = nullptr, *du32 = nullptr;
+  struct InprocGroup *grp = nullptr;  // MERAK_COMM_INPROC: the group this rank belongs to
+  cudaEvent_t ev_hs[2] = {};          // INPROC: this rank's handshake points (alternating generations)
 };
+
+// ------------------------------------------------------------------------------ in-process groups
+// MERAK_COMM_INPROC runs the T ranks of a group as handles of one process on one device.  A spinning handshake
+// kernel cannot be used there: the ranks are issued one after another from one host thread, so rank 0's
+// handshake of epoch e sits on the GPU before rank 1's work up to epoch e is even issued, and when the two
+// ranks' streams share a hardware queue (the device has at most 32; torch's stream pools alone create more)
+// rank 1's work queues behind the spinning kernel for good.  Instead a group DEFERS its ranks' layer calls
+// until every rank has made the matching call, then issues them together, each rank's call running as a
+// coroutine on this thread: at every handshake point a rank records an event on the stream the handshake
+// would run on and yields; once all ranks have arrived, each waits on every peer's event and continues.  The
+// issue order is then topological (every stream command waits only on commands issued before it), which makes
+// the group deadlock-free whatever the stream-to-queue mapping, with the same ordering the handshake kernel
+// gives (peer q's partial written and q's earlier readers of my slot done before I proceed).
+struct InprocGroup {
+  int T = 0;
+  merak_tmp_t *hs[MAX_T] = {};
+  int alive = 0;                                   // handles not yet destroyed
+  std::function<merak_status()> pending[MAX_T];    // deferred layer call of each rank (empty: none)
+  int npending = 0;
+  bool running = false;                            // the coroutines are issuing
+  ucontext_t main_ctx;
+  ucontext_t ctx[MAX_T];
+  char *stack[MAX_T] = {};
+  bool done[MAX_T] = {};
+  merak_status status[MAX_T] = {};
+  int cur = -1, live = 0, arrive = 0;
+  uint64_t gen = 0;
+  uint64_t rec_gen[MAX_T] = {};  // generation of each rank's latest handshake event (+1; 0 = none)
+};
+static constexpr size_t kCoStack = 8u << 20;  // per-rank coroutine stack (the CUDA runtime's launch path is deep)
+static InprocGroup *g_co_group = nullptr;     // the group whose coroutines this thread is running
+
+static void co_entry() {
+  InprocGroup *g = g_co_group;
+  const int r = g->cur;
+  g->status[r] = g->pending[r]();
+  g->done[r] = true;
+  // a rank that finished (or failed) no longer takes part in the barriers
+  if (--g->live > 0 && g->arrive == g->live) {
+    g->arrive = 0;
+    ++g->gen;
+  }
+}  // returns to main_ctx through uc_link
 
 static std::string g_init_err;
 
@@ -313,10 +362,31 @@ static int ar_partials(merak_tmp_t *h, bool comm, int slot, size_t r0, const bf1
 }
 
 // 1-warp cross-rank barrier on the communication stream before an all-reduce (see ln_ar.cu)
-static merak_status sync_peers(merak_tmp_t *h, const PeerSync &ps) {
+// In-process groups: the same ordering through events between coroutines (InprocGroup above).
+static merak_status group_barrier(merak_tmp_t *h, cudaStream_t st) {
+  InprocGroup *g = h->grp;
+  if (!g || !g->running) return fail(h, MERAK_ESTATE, "in-process handshake outside a group issue");
+  cudaEvent_t mine = h->ev_hs[g->gen & 1];
+  CK(h, cudaEventRecord(mine, st));
+  const uint64_t gen = g->gen;
+  g->rec_gen[h->r] = gen + 1;
+  if (++g->arrive == g->live) {
+    g->arrive = 0;
+    ++g->gen;
+  }
+  while (g->gen == gen) swapcontext(&g->ctx[h->r], &g->main_ctx);
+  // every rank recorded its generation-`gen` event; none can re-record it before all of us passed this point
+  for (int q = 0; q < g->T; ++q)
+    if (q != h->r && g->rec_gen[q] >= gen + 1) CK(h, cudaStreamWaitEvent(st, g->hs[q]->ev_hs[gen & 1], 0));
+  return MERAK_OK;
+}
+
+static merak_status sync_peers(merak_tmp_t *h, const PeerSync &ps, cudaStream_t st = nullptr) {
   if (!ps.enabled) return MERAK_OK;
-  Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
-  CK(h, peer_ready(ps, h->ms));
+  if (!st) st = h->ms;
+  if (h->inproc) return group_barrier(h, st);
+  Launch Lk(h, MERAK_K_ALLREDUCE, st, 0.0);
+  CK(h, peer_ready(ps, st));
   return MERAK_OK;
 }
 
@@ -326,9 +396,17 @@ static merak_status sync_peers(merak_tmp_t *h, const PeerSync &ps) {
 // from its owner's slot ("gathered" mode).  NVLink bytes per rank: 2(T-1)/T of a slot instead of
 // (T-1) for one-shot.  Returns the chunk (rows per owner) for the epilogue kernel.
 static bool two_shot_on(merak_tmp_t *h, bool comm) { return comm && h->T > 1 && !h->nccl && h->two_shot; }
+// With h->fused_wait the second handshake kernel disappears: the phase-1 kernel's last CTA publishes the epoch
+// and the phase-2 epilogue kernel waits for the peers' epochs in kernel (*wait_ps, PeerSync::wait).  Safe from
+// the deadlock of DESIGN.md §7: the waiting kernel depends only on the peers' phase-1 kernels, which precede
+// their own phase-2 kernels on their communication streams and never wait themselves.
 static merak_status two_shot_rs(merak_tmp_t *h, int slot, size_t r0, int m, const bf16 *resid, const bf16 *bias,
-                                int *chunk) {
+                                int *chunk, PeerSync *wait_ps) {
   const int c = (m + h->T - 1) / h->T;
+  PeerSync pub = make_sync(h, true);
+  pub.publish = h->fused_wait;
+  pub.ctr = reinterpret_cast<uint32_t *>(h->pv + h->flags_off) + 64;
+  pub.pdl = false;
   if (h->use_nvls) {  // phase 1 in the switch: multimem.ld_reduce of the owned rows, multimem.st to all ranks
     NvlsRsArgs a;
     memset(&a, 0, sizeof(a));
@@ -340,13 +418,18 @@ static merak_status two_shot_rs(merak_tmp_t *h, int slot, size_t r0, int m, cons
     a.bias = bias;
     a.ctas = h->cfg.comm_ctas;
     a.pdl = h->pdl && !h->prof;
+    a.ps = pub;
     {
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
       CK(h, nvls_rs(a, h->ms));
     }
-    PeerSync ps = make_sync(h, true);
-    ps.pdl = h->pdl && !h->prof;
-    TRY(sync_peers(h, ps));
+    if (!h->fused_wait) {
+      pub.pdl = h->pdl && !h->prof;
+      TRY(sync_peers(h, pub));
+    }
+    pub.wait = h->fused_wait;
+    pub.publish = false;
+    *wait_ps = pub;
     *chunk = c;
     return MERAK_OK;
   }
@@ -360,13 +443,18 @@ static merak_status two_shot_rs(merak_tmp_t *h, int slot, size_t r0, int m, cons
   a.out = slot_ptr(h, h->r, slot) + r0 * h->h;
   a.ctas = h->cfg.comm_ctas;
   a.pdl = h->pdl && !h->prof;  // (profiling events between launches would break the PDL pairing)
+  a.ps = pub;
   {
     Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
     CK(h, ar_rs(a, h->ms));
   }
-  PeerSync ps = make_sync(h, true);
-  ps.pdl = h->pdl && !h->prof;
-  TRY(sync_peers(h, ps));
+  if (!h->fused_wait) {
+    pub.pdl = h->pdl && !h->prof;
+    TRY(sync_peers(h, pub));
+  }
+  pub.wait = h->fused_wait;
+  pub.publish = false;
+  *wait_ps = pub;
   *chunk = c;
   return MERAK_OK;
 }
@@ -491,7 +579,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.eps = h->eps; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
-      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 0, r0, m, xj, (const bf16 *)w->b_o, &a.chunk));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 0, r0, m, xj, (const bf16 *)w->b_o, &a.chunk, &ps));
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
       a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
       CK(h, ar_fwd(a, ps, h->ms));
@@ -528,7 +616,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.out = y + r0 * hh; a.do_ln = false; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
-      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 1, r0, m, a.resid, a.bias, &a.chunk));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 1, r0, m, a.resid, a.bias, &a.chunk, &ps));
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
       a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
       CK(h, ar_fwd(a, ps, h->ms));
@@ -598,7 +686,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.G = h->G; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
-      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 2, r0, m, nullptr, nullptr, &a.chunk));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 2, r0, m, nullptr, nullptr, &a.chunk, &ps));
       {
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         a.pdl = h->pdl && !h->prof && ps.enabled;
@@ -663,7 +751,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.G = h->G; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
-      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 3, r0, m, nullptr, nullptr, &a.chunk));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 3, r0, m, nullptr, nullptr, &a.chunk, &ps));
       {
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         a.pdl = h->pdl && !h->prof && ps.enabled;
@@ -1032,8 +1120,7 @@ static merak_status ar32_prologue(merak_tmp_t *h, bool comm, int slot, size_t r0
     a.T = h->T;
     for (int q = 0; q < h->T; ++q) a.partial[q] = slot32(h, q, slot) + r0 * h->h;
     PeerSync ps = make_sync(h, comm);
-    Launch Lk(h, MERAK_K_ALLREDUCE, h->cs, 0.0);
-    CK(h, peer_ready(ps, h->cs));
+    TRY(sync_peers(h, ps, h->cs));
   }
   a.m = m; a.h = h->h; a.eps = h->eps;
   return MERAK_OK;
@@ -1238,8 +1325,16 @@ static void release(merak_tmp_t *h) {
   if (h->err_host) cudaFreeHost(h->err_host);
   for (auto e : h->evpool) cudaEventDestroy(e);
   for (cudaEvent_t e : {h->ev_entry, h->ev_cs_end, h->ev_cs1_end, h->ev_cw_end, h->ev_cr_end, h->ev_w1, h->ev_wo,
-                        h->ev_wqkv, h->ev_red})
+                        h->ev_wqkv, h->ev_red, h->ev_hs[0], h->ev_hs[1]})
     if (e) cudaEventDestroy(e);
+  if (InprocGroup *g = h->grp) {
+    g->hs[h->r] = nullptr;
+    g->pending[h->r] = nullptr;
+    if (--g->alive == 0) {
+      for (int r = 0; r < MAX_T; ++r) free(g->stack[r]);
+      delete g;
+    }
+  }
   for (int i = 0; i < 5; ++i)
     for (int k = 0; k < 64; ++k)
       if (h->tr_ev[i][k]) cudaEventDestroy(h->tr_ev[i][k]);
@@ -1260,6 +1355,64 @@ static void release(merak_tmp_t *h) {
 
 static merak_status sync_all(merak_tmp_t *h) {
   for (cudaStream_t c : {h->cs, h->cs1, h->cw, h->cr, h->ms}) CK(h, cudaStreamSynchronize(c));
+  return MERAK_OK;
+}
+
+// In-process group: keep rank h->r's call until every rank has made its matching call, then issue all of
+// them as coroutines of this thread (InprocGroup).  The call that completes the set returns the first
+// failure of the set (named by rank); the earlier callers got MERAK_OK.
+static merak_status group_issue(merak_tmp_t *h, std::function<merak_status()> fn) {
+  InprocGroup *g = h->grp;
+  if (g->running) return fail(h, MERAK_ESTATE, "layer call re-entered during an in-process group issue");
+  if (g->alive != g->T) return fail(h, MERAK_ESTATE, "a rank of this in-process group was destroyed");
+  if (g->pending[h->r])
+    return fail(h, MERAK_ESTATE, "rank %d made a second layer call before every rank of its in-process group "
+                "made the first", h->r);
+  g->pending[h->r] = std::move(fn);
+  if (++g->npending < g->T) return MERAK_OK;
+  for (int r = 0; r < g->T; ++r) {
+    if (!g->stack[r]) g->stack[r] = (char *)malloc(kCoStack);
+    if (!g->stack[r]) return fail(h, MERAK_ENOMEM, "coroutine stack");
+    getcontext(&g->ctx[r]);
+    g->ctx[r].uc_stack.ss_sp = g->stack[r];
+    g->ctx[r].uc_stack.ss_size = kCoStack;
+    g->ctx[r].uc_link = &g->main_ctx;
+    makecontext(&g->ctx[r], co_entry, 0);
+    g->done[r] = false;
+    g->status[r] = MERAK_OK;
+    g->rec_gen[r] = 0;
+  }
+  g->running = true;
+  g->live = g->T;
+  g->arrive = 0;
+  InprocGroup *outer = g_co_group;
+  g_co_group = g;
+  for (int left = g->T; left > 0;)
+    for (int r = 0; r < g->T; ++r) {
+      if (g->done[r]) continue;
+      g->cur = r;
+      swapcontext(&g->main_ctx, &g->ctx[r]);  // runs rank r until its next handshake point or its end
+      if (g->done[r]) --left;
+    }
+  g_co_group = outer;
+  g->running = false;
+  g->npending = 0;
+  merak_status st = MERAK_OK;
+  for (int r = 0; r < g->T; ++r) {
+    g->pending[r] = nullptr;
+    if (g->status[r] != MERAK_OK && st == MERAK_OK) {
+      st = g->status[r];
+      if (g->hs[r] != h) fail(h, st, "rank %d: %s", r, g->hs[r]->err.c_str());
+    }
+  }
+  return st;
+}
+
+// Calls that act on a handle's streams at once must not overtake its deferred layer call.
+static merak_status group_idle(merak_tmp_t *h) {
+  if (h->grp && h->grp->pending[h->r])
+    return fail(h, MERAK_ESTATE, "rank %d has a layer call waiting for the other ranks of its in-process group",
+                h->r);
   return MERAK_OK;
 }
 
@@ -1292,6 +1445,11 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
   if (const char *t = getenv("MERAK_GEMM_SMEM_KB")) h->gemm_smem_kb = atoi(t) == 160 ? 160 : 192;
   if (const char *t = getenv("MERAK_DEBUG_TRACE")) h->trace = atoi(t) == 1;
   if (const char *t = getenv("MERAK_AR_TWO_SHOT")) h->two_shot = h->T > 1 && !h->f32 && atoi(t) == 1;
+  if (const char *t = getenv("MERAK_AR_FUSED_WAIT")) h->fused_wait = atoi(t) != 0;
+  // in-process groups share ONE GPU: a waiting epilogue kernel of one rank can fill the SMs that another rank's
+  // phase-1 kernel (the one it waits for) needs, so they keep the 1-warp handshake kernel
+  if (h->inproc) h->fused_wait = false;
+  if (h->inproc) h->pdl = false;  // no handshake kernel to pair with (group_barrier)
   auto bail = [&](merak_status st) {
     g_init_err = h->err;
     release(h);
@@ -1522,6 +1680,21 @@ merak_status merak_tmp_init_group(const merak_tmp_config *cfg, merak_tmp_t **out
   // every rank maps every peer's peer-visible buffer directly: same process, same device, same context
   for (int q = 0; q < T; ++q)
     for (int p = 0; p < T; ++p) out[q]->peer_pv[p] = out[p]->pv;
+  InprocGroup *g = new InprocGroup();
+  g->T = g->alive = T;
+  for (int q = 0; q < T; ++q) {
+    g->hs[q] = out[q];
+    out[q]->grp = g;
+  }
+  for (int q = 0; q < T; ++q)
+    for (int k = 0; k < 2; ++k)
+      if (cudaEventCreateWithFlags(&out[q]->ev_hs[k], cudaEventDisableTiming) != cudaSuccess) {
+        for (int p = 0; p < T; ++p) {
+          release(out[p]);
+          out[p] = nullptr;
+        }
+        return fail(nullptr, MERAK_ECUDA, "init_group: cudaEventCreate");
+      }
   return MERAK_OK;
 }
 
@@ -1529,6 +1702,7 @@ merak_status merak_tmp_set_subbatches(merak_tmp_t *h, int32_t n_sub) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
   if (h->chain_open) return fail(h, MERAK_ESTATE, "set_subbatches while a MERAK_FLAG_CHAIN sequence is open");
   if (n_sub <= 0 || n_sub > MAXN) return fail(h, MERAK_EINVAL, "n_sub out of range");
+  TRY(group_idle(h));
   if (h->sp && ((long)h->M / n_sub) % (8 * h->T))
     return fail(h, MERAK_EINDIVISIBLE, "seq_parallel: tokens per sub-batch %% (8 T) != 0");
   if (h->B % n_sub) return fail(h, MERAK_EINDIVISIBLE, "microbatch %% n_sub != 0");
@@ -1547,6 +1721,7 @@ size_t merak_tmp_saved_bytes(const merak_tmp_t *h) {
 
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
+
 merak_status merak_tmp_layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const void *x, void *y, void *saved,
                                  uint32_t flags, void *st) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
@@ -1557,15 +1732,19 @@ merak_status merak_tmp_layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, con
   for (const void *p : ps)
     if (!p || !aligned16(p)) return fail(h, MERAK_EINVAL, "NULL or non-16B-aligned pointer");
   if (h->broken) return fail(h, MERAK_ESTATE, "handle unusable after an earlier failure: %s", h->err.c_str());
-  const uint32_t e0 = h->epoch;
   if (h->sp && (flags & (MERAK_FLAG_RECOMPUTE | MERAK_FLAG_NO_COMM)))
     return fail(h, MERAK_EUNSUPPORTED, "seq_parallel: MERAK_FLAG_RECOMPUTE / MERAK_FLAG_NO_COMM are not available");
-  const merak_status s =
-      h->f32  ? layer_fwd_f32(h, w, (const float *)x, (float *)y, (char *)saved, flags, (cudaStream_t)st)
-      : h->sp ? layer_fwd_sp(h, w, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st)
-              : layer_fwd(h, w, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st, rc);
-  if (s != MERAK_OK && (h->epoch != e0 || s == MERAK_ETIMEOUT)) h->broken = true;
-  return s;
+  const merak_tmp_weights wv = *w;  // by value: an in-process group may issue the call later
+  auto body = [h, wv, x, y, saved, flags, st, rc]() -> merak_status {
+    const uint32_t e0 = h->epoch;
+    const merak_status s =
+        h->f32  ? layer_fwd_f32(h, &wv, (const float *)x, (float *)y, (char *)saved, flags, (cudaStream_t)st)
+        : h->sp ? layer_fwd_sp(h, &wv, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st)
+                : layer_fwd(h, &wv, (const bf16 *)x, (bf16 *)y, (char *)saved, flags, (cudaStream_t)st, rc);
+    if (s != MERAK_OK && (h->epoch != e0 || s == MERAK_ETIMEOUT)) h->broken = true;
+    return s;
+  };
+  return h->grp ? group_issue(h, body) : body();
 }
 
 merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const void *x, const void *saved,
@@ -1582,29 +1761,37 @@ merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, con
     return fail(h, MERAK_EUNSUPPORTED, "seq_parallel: MERAK_FLAG_RECOMPUTE / MERAK_FLAG_NO_COMM are not available");
   if ((flags & MERAK_FLAG_RECOMPUTE) && h->f32)
     return fail(h, MERAK_EUNSUPPORTED, "MERAK_FLAG_RECOMPUTE is not available in the fp32 check mode");
-  const uint32_t e0 = h->epoch;
-  if (flags & MERAK_FLAG_RECOMPUTE) {  // regenerate `saved` (scratch) from x, then the backward proper
-    const merak_status r = layer_fwd(h, w, (const bf16 *)x, nullptr, (char *)const_cast<void *>(saved),
-                                     MERAK_FLAG_CHAIN | (flags & MERAK_FLAG_NO_COMM), (cudaStream_t)st, true);
-    // (the backward below continues the open chain: its sub-batch streams follow each fc1 directly)
-    if (r != MERAK_OK) {
-      if (h->epoch != e0 || r == MERAK_ETIMEOUT) h->broken = true;
-      return r;
+  const merak_tmp_weights wv = *w;  // by value: an in-process group may issue the call later
+  const merak_tmp_grads gv = *g;
+  auto body = [h, wv, gv, x, saved, dy, dx, flags, st]() -> merak_status {
+    const merak_tmp_weights *w = &wv;
+    const merak_tmp_grads *g = &gv;
+    const uint32_t e0 = h->epoch;
+    if (flags & MERAK_FLAG_RECOMPUTE) {  // regenerate `saved` (scratch) from x, then the backward proper
+      const merak_status r = layer_fwd(h, w, (const bf16 *)x, nullptr, (char *)const_cast<void *>(saved),
+                                       MERAK_FLAG_CHAIN | (flags & MERAK_FLAG_NO_COMM), (cudaStream_t)st, true);
+      // (the backward below continues the open chain: its sub-batch streams follow each fc1 directly)
+      if (r != MERAK_OK) {
+        if (h->epoch != e0 || r == MERAK_ETIMEOUT) h->broken = true;
+        return r;
+      }
     }
-  }
-  const merak_status s =
-      h->f32  ? layer_bwd_f32(h, w, (const float *)x, (const char *)saved, (const float *)dy, (float *)dx, g, flags,
-                              (cudaStream_t)st)
-      : h->sp ? layer_bwd_sp(h, w, (const bf16 *)x, (const char *)saved, (const bf16 *)dy, (bf16 *)dx, g, flags,
-                             (cudaStream_t)st)
-              : layer_bwd(h, w, (const bf16 *)x, (const char *)saved, (const bf16 *)dy, (bf16 *)dx, g, flags,
-                          (cudaStream_t)st);
-  if (s != MERAK_OK && (h->epoch != e0 || s == MERAK_ETIMEOUT)) h->broken = true;
-  return s;
+    const merak_status s =
+        h->f32  ? layer_bwd_f32(h, w, (const float *)x, (const char *)saved, (const float *)dy, (float *)dx, g, flags,
+                                (cudaStream_t)st)
+        : h->sp ? layer_bwd_sp(h, w, (const bf16 *)x, (const char *)saved, (const bf16 *)dy, (bf16 *)dx, g, flags,
+                               (cudaStream_t)st)
+                : layer_bwd(h, w, (const bf16 *)x, (const char *)saved, (const bf16 *)dy, (bf16 *)dx, g, flags,
+                            (cudaStream_t)st);
+    if (s != MERAK_OK && (h->epoch != e0 || s == MERAK_ETIMEOUT)) h->broken = true;
+    return s;
+  };
+  return h->grp ? group_issue(h, body) : body();
 }
 
 merak_status merak_tmp_join(merak_tmp_t *h, void *st) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
+  TRY(group_idle(h));
   if (!h->have_prev) return MERAK_OK;
   TRY(wait_all(h, (cudaStream_t)st));
   for (int j = 0; j < h->n; ++j) CK(h, cudaStreamWaitEvent((cudaStream_t)st, h->prev_out[j], 0));
@@ -1640,6 +1827,7 @@ const char *merak_tmp_last_error(const merak_tmp_t *h) { return h ? h->err.c_str
 
 merak_status merak_tmp_set_profiling(merak_tmp_t *h, int32_t on) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
+  TRY(group_idle(h));
   TRY(sync_all(h));
   h->prof = on != 0;
   h->recs.clear();
@@ -1654,6 +1842,7 @@ merak_status merak_tmp_set_profiling(merak_tmp_t *h, int32_t on) {
 
 merak_status merak_tmp_get_profile(merak_tmp_t *h, double *ms, int64_t *launches, double *flops) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
+  TRY(group_idle(h));
   TRY(sync_all(h));
   for (auto &r : h->recs) {
     float t = 0;
@@ -1674,6 +1863,7 @@ merak_status merak_tmp_get_profile(merak_tmp_t *h, double *ms, int64_t *launches
 merak_status merak_tmp_get_timeline(merak_tmp_t *h, int32_t cap, int32_t *count, int32_t *cls, int32_t *stream,
                                     float *t0, float *t1) {
   if (!h || !count) return fail(h, MERAK_EINVAL, "NULL argument");
+  TRY(group_idle(h));
   TRY(sync_all(h));
   int32_t n = 0;
   if (!h->recs.empty()) {
@@ -1730,7 +1920,8 @@ merak_status merak_tmp_debug_state(const merak_tmp_t *h, int32_t *out) {
 
 merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t rows, int32_t iters, float *ms) {
   if (!h || !ms) return fail(h, MERAK_EINVAL, "NULL argument");
-  if (h->T < 2 || h->nccl || h->f32 || h->local) return fail(h, MERAK_EUNSUPPORTED, "needs T > 1, peer comm, bf16");
+  if (h->T < 2 || h->nccl || h->f32 || h->local || h->inproc)
+    return fail(h, MERAK_EUNSUPPORTED, "needs T > 1, peer comm across processes, bf16");
   if (rows <= 0 || rows > h->M || iters <= 0 || which < 0 || which > 2 || rows % h->G)
     return fail(h, MERAK_EINVAL, "bad rows / iters / which");
   TRY(sync_all(h));
@@ -1768,7 +1959,7 @@ merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t ro
         memset(&a, 0, sizeof(a));
         a.T = ar_partials(h, true, 1, 0, a.partial);
         a.m = rows; a.h = (int)hh; a.resid = resid; a.bias = gam; a.out = out; a.ctas = h->cfg.comm_ctas;
-        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, resid, gam, &a.chunk));
+        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, resid, gam, &a.chunk, &ps));
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
       CK(h, ar_fwd(a, ps, h->ms));
@@ -1778,7 +1969,7 @@ merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t ro
         a.T = ar_partials(h, true, 1, 0, a.partial);
         a.m = rows; a.h = (int)hh; a.x_ln = resid; a.mean = mean; a.rstd = rstd; a.gamma = gam; a.dres = resid;
         a.dx = out; a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
-        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, nullptr, nullptr, &a.chunk));
+        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, nullptr, nullptr, &a.chunk, &ps));
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         a.pdl = h->pdl && !h->prof && ps.enabled;
         CK(h, ar_bwd(a, ps, h->ms));

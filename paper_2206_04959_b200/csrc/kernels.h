@@ -163,6 +163,11 @@ struct PeerSync {
   int *err_word;              // device word set to 1 on watchdog timeout
   uint64_t timeout_ns;
   bool pdl;                   // host: launch as a programmatic dependent of the previous kernel
+  // two-shot without the second handshake kernel: the phase-1 kernel's last CTA publishes `epoch` to the peers
+  // (ctr: a zeroed device counter of this rank), and the phase-2 epilogue kernel waits for the peers' epoch in
+  // kernel (thread 0 of every CTA) before it reads their rows
+  bool publish, wait;
+  uint32_t *ctr;
 };
 
 struct ArFwdArgs {
@@ -191,6 +196,7 @@ cudaError_t ar_fwd(const ArFwdArgs &a, const PeerSync &ps, cudaStream_t st);
 // rank: v = sum_r partial[r] (rank order) [+ bias + resid], rounded once to bf16 and written IN
 // PLACE into this rank's own slot (out = partial[rank]).  Peers read those rows in phase 2.
 struct ArRsArgs {
+  PeerSync ps;  // ps.publish: publish the completion of this phase to the peers (see PeerSync)
   const __nv_bfloat16 *partial[MAX_T];
   int T, h, row0, row1;
   const __nv_bfloat16 *resid;  // nullptr: plain sum (backward); else forward AR epilogue terms
@@ -278,6 +284,7 @@ bool nvls_supported(int dev);
 int nvls_setup(Nvls *n, int dev, int T, int r, size_t bytes, nvls_allgather_fn ag, void *ctx, std::string *err);
 void nvls_release(Nvls *n);
 struct NvlsRsArgs {
+  PeerSync ps;                  // ps.publish: as ArRsArgs
   __nv_bfloat16 *mc;            // multicast address of row 0 of the sub-batch in the slot
   int h, row0, row1;            // rows owned by this rank
   const __nv_bfloat16 *resid;   // nullptr: plain sum (backward); else + bias + resid (forward epilogue terms)

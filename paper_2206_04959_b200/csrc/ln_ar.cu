@@ -183,6 +183,7 @@ template <int NT, int CPT>
 __global__ void __launch_bounds__(256, 2) ar_fwd_kernel(ArFwdArgs a, PeerSync ps, int tpr) {
   griddep_wait();  // PDL: the handshake before this kernel has completed (peers' data is ready)
   griddep_launch();
+  if (ps.wait) wait_peers(ps);  // two-shot: every owner's reduced rows are written
   __shared__ float red[8 * 2 * 8 * 1];
   const int nsub = blockDim.x / tpr, sub = threadIdx.x / tpr, t = threadIdx.x % tpr;
   const int h = a.h, nc = h >> 3;
@@ -295,6 +296,7 @@ __global__ void __launch_bounds__(256) ar_rs_kernel(ArRsArgs a) {
       }
     }
   }
+  if (a.ps.publish) publish_when_done(a.ps);
 }
 
 // ------------------------------------------------------------------------------ backward all-reduce
@@ -306,6 +308,7 @@ __global__ void __launch_bounds__(256, 2) ar_bwd_kernel(ArBwdArgs a, PeerSync ps
   constexpr int G = 8;
   griddep_wait();
   griddep_launch();
+  if (ps.wait) wait_peers(ps);  // two-shot: every owner's reduced rows are written
   __shared__ float red[8 * 2 * 8 * 2];
   const int nsub = blockDim.x / tpr, sub = threadIdx.x / tpr, t = threadIdx.x % tpr;
   const int h = a.h, nc = h >> 3;

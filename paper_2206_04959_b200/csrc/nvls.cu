@@ -257,6 +257,7 @@ __global__ void __launch_bounds__(256) nvls_rs_kernel(NvlsRsArgs a) {
     mm_st_bf16x8(p, v);
   }
   asm volatile("fence.acq_rel.sys;" ::: "memory");  // the multicast stores precede the handshake's release
+  if (a.ps.publish) publish_when_done(a.ps);
 }
 
 cudaError_t nvls_rs(const NvlsRsArgs &a, cudaStream_t st) {

@@ -339,10 +339,56 @@ MK_DEV uint32_t ld_acquire_sys(const uint32_t *p) {
 MK_DEV void st_release_sys(uint32_t *p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Two-shot fused handshake (kernels.h PeerSync::publish / wait).  publish_when_done: call at the very end of a
+// kernel by every thread; the last CTA to finish releases `epoch` into every peer's flag array.  wait_peers:
+// call at the start of a kernel by every thread; thread 0 spins (watchdog -> err_word) until every peer
+// published `epoch`, then the CTA proceeds.
+template <class PS>
+MK_DEV void publish_when_done(const PS &ps);
+template <class PS>
+MK_DEV void wait_peers(const PS &ps);
 MK_DEV uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+template <class PS>
+MK_DEV void publish_when_done(const PS &ps) {
+  __threadfence_system();  // this thread's writes precede the release stores of the last CTA
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(ps.ctr, 1u);
+    if (prev == gridDim.x - 1) {
+      *ps.ctr = 0u;  // the next launch on this (stream-ordered) counter starts from zero
+      __threadfence_system();
+      for (int q = 0; q < ps.T; ++q)
+        if (q != ps.rank) st_release_sys(ps.flags_peer[q] + ps.rank, ps.epoch);
+    }
+  }
+}
+template <class PS>
+MK_DEV void wait_peers(const PS &ps) {
+  if (threadIdx.x == 0) {
+    volatile int *err = ps.err_word;
+    const uint64_t t0 = globaltimer();
+    for (int q = 0; q < ps.T; ++q) {
+      if (q == ps.rank) continue;
+      uint32_t v;
+      for (uint32_t it = 1; (int)((v = ld_acquire_sys(ps.flags_local + q)) - ps.epoch) < 0; ++it) {
+        if ((it & 255) == 0 && (*err || globaltimer() - t0 > ps.timeout_ns)) {
+          if (atomicExch(ps.err_word, 1) == 0) {
+            err[1] = (int)ps.epoch;
+            err[2] = (int)blockIdx.x;
+            err[3] = 16 + q;
+            err[4] = (int)v;
+          }
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
 }
 
 }  // namespace mk

@@ -4,8 +4,9 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-# In-process TMP groups (tests/test_gpu_group.py) run T ranks' streams in one CUDA context: give every
-# stream its own hardware queue (read when the context is created, i.e. before any CUDA call).
+# In-process TMP groups (tests/test_gpu_group.py) run T ranks' streams in one CUDA context: more hardware
+# queues keep the ranks from serialising behind each other (read when the context is created).  Correctness
+# does not depend on it: the group issues its ranks' calls in a topological order (api.cu, InprocGroup).
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -125,9 +125,8 @@ def oracle_chain(params_list, x, dy, heads):
 def run_gpu_group(cfg, params, x, dy, T, n_sub=None, precision=0, flags=0, chain_params=None, chain=True):
     """The T ranks of a TMP group as handles of this process on one GPU (merak_tmp_init_group,
     MERAK_COMM_INPROC): each rank holds its own weight shard and outputs, every all-reduce sums the T
-    ranks' partials through the peer kernels.  Each rank issues its calls on its own caller stream (a
-    shared caller stream would serialise rank r+1 behind rank r's join, while rank r's all-reduce waits
-    for rank r+1).  chain_params: list of per-layer params -> K chained layers (MERAK_FLAG_CHAIN on every
+    ranks' partials through the peer kernels.  Each rank issues its calls on its own caller stream (the
+    library defers each call until every rank made it, then issues the set together).  chain_params: list of per-layer params -> K chained layers (MERAK_FLAG_CHAIN on every
     call but the last backward; chain=False: no chaining), else one layer with `params`.
     Returns [per-rank dict]: y, dx and the rank's gradient shards (grads[k] per layer when chained)."""
     from paper_2206_04959_b200 import FLAG_CHAIN

@@ -1,7 +1,7 @@
 """T > 1 parity on ONE GPU (driver-verifiable): the T ranks of a TMP group as handles of one process
 (merak_tmp_init_group, MERAK_COMM_INPROC), each holding its weight shard, every all-reduce summing the
 T ranks' bf16 partials in rank order through the same peer kernels (one-shot at T = 2, two-shot at
-T >= 4) -- the method itself: row-parallel partial sums over T ranks with sub-microbatches
+T >= 4; the cross-rank handshake is the group's event exchange, see merak_tmp.h) -- the method itself: row-parallel partial sums over T ranks with sub-microbatches
 overlapping.  Checked per rank against the fp64 oracle's slices (rel. Frobenius <= 2e-2; fp32
 check mode <= 1e-5), replicated outputs bit-equal across ranks, n = 1 vs n > 1 bit-identical per rank,
 one-shot vs two-shot bit-identical, chained stacks equal to unchained ones."""
