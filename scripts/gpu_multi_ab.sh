@@ -4,8 +4,9 @@ cd "${GRAFT_REPO_ROOT:-.}"
 N=${1:-4}; VAR=${2:-MERAK_AR_FUSED_WAIT}
 mkdir -p gpurun_out
 python -c 'import __graft_entry__ as g; g.build()' > gpurun_out/build.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_multi.py -x -q -m gpu -p no:cacheprovider -rs > gpurun_out/multi_tests_N$N.log 2>&1
-echo "exit $?" >> gpurun_out/multi_tests_N$N.log
+# the multi-process tests with the switch ON (its default is off)
+env $VAR=1 timeout 900 python -m pytest tests/test_gpu_multi.py -x -q -m gpu -p no:cacheprovider -rs > gpurun_out/multi_tests_N${N}_$VAR.log 2>&1
+echo "exit $?" >> gpurun_out/multi_tests_N${N}_$VAR.log
 for i in 1 2; do
   for v in 0 1; do
     for CFG in gpt1.5b gpt20b; do
