@@ -15,12 +15,14 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libmerak_tmp.so")
+# MERAK_LIB_OUT / MERAK_EXTRA_NVCC: experiment builds (an alternative library with extra -D flags, loaded through
+# MERAK_LIB for same-box A/B runs); the product build uses neither
+LIB = os.environ.get("MERAK_LIB_OUT") or os.path.join(PKG, "libmerak_tmp.so")
 BUILD = os.path.join(ROOT, "build", "objs")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
-         "-diag-suppress", "177", "--expt-relaxed-constexpr"]
+         "-diag-suppress", "177", "--expt-relaxed-constexpr"] + os.environ.get("MERAK_EXTRA_NVCC", "").split()
 
 
 def _deps_hash(src):

@@ -11,10 +11,12 @@
 //   dV  += P^T dO_i     (A = P^T read from TMEM: bf16 written over S^T by the element-wise warps)
 //   dK  += dS^T Q_i     (A = dS^T in swizzled smem)
 //   dQ_i^T = K^T dS^T   (M = d padded to 128, A = K read MN-major, B = dS^T MN-major) -> TMEM
-// 448 threads: warp 0 TMA (K, V once; Q_i, dO_i, lse_i, delta_i per half-block through a stage ring),
+// 512 threads: warp 0 TMA (K, V once; Q_i, dO_i, lse_i, delta_i per half-block through a stage ring),
 // warp 1 TMEM owner + MMA issuer (scores of i+1 issued before the gradient MMAs of i, so the element-wise
 // work of one half-block overlaps the tensor core), warps 2-9 element-wise (two warpgroups ping-pong on
-// alternate half-blocks; thread = key row), warps 10-13 drain dQ_i^T (thread = d index).
+// alternate half-blocks; thread = key row), warps 10-13 drain dQ_i^T (thread = d index) into a staging buffer,
+// warps 14-15 (one thread each, alternate half-blocks) move the staged blocks into the dQ accumulator in their
+// fixed order.
 //
 // dQ is deterministic (bit-identity rule ii, no atomics): every half-block i of a (sample, head) receives
 // its contributions in a FIXED order, key tile floor(i/2) first down to key tile 0, through an fp32
@@ -37,7 +39,7 @@ namespace {
 
 constexpr int TKEY = 128;  // keys per CTA (TMEM lanes)
 constexpr int TQH = 64;    // queries per half-block (N of the score products)
-constexpr int NTHR = 448;  // 14 warps
+constexpr int NTHR = 512;  // 16 warps
 
 template <int D>
 struct BwdCfg {
@@ -88,7 +90,6 @@ MK_DEV void tmem_st8(uint32_t taddr, const uint32_t *r) {
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
 }
-MK_DEV void drain_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }  // the 4 dQ drain warps
 // 1-D bulk smem -> global copy / fp32 add-reduction (bulk async-group of the issuing thread)
 MK_DEV void bulk_store(void *dst, const void *src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
@@ -123,7 +124,9 @@ __global__ void __launch_bounds__(NTHR, 1)
   // barrier's completions are consumed in order by one waiter; the TMEM buffer is ii % NB
   uint64_t *s_full = q_empty + ST, *p_full = s_full + 2, *ds_free = p_full + 2;
   uint64_t *dq_full = ds_free + 2, *dq_free = dq_full + 1, *kv_done = dq_free + 1;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(kv_done + 1);
+  // dQ staging buffer: drain warps <-> bulk thread k = ii & 1 (one barrier pair per bulk thread)
+  uint64_t *stg_full = kv_done + 1, *stg_free = stg_full + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(stg_free + 2);
   auto stQ = [&](int st) { return sStage + st * C::STAGE_BYTES; };
   auto stO = [&](int st) { return sStage + st * C::STAGE_BYTES + C::QH_BYTES; };
   auto stL = [&](int st) { return sLD + st * 2 * TQH; };
@@ -162,6 +165,10 @@ __global__ void __launch_bounds__(NTHR, 1)
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 4);
     mbar_init(kv_done, 1);
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&stg_full[k], 4);
+      mbar_init(&stg_free[k], 1);
+    }
     fence_mbar_init();
     fence_proxy_async();
   }
@@ -335,85 +342,73 @@ __global__ void __launch_bounds__(NTHR, 1)
         }
       }
     }
-  } else {
+  } else if (warp < 14) {
     // ------------------------------------------------------------ dQ drain (thread = d index)
-    // Per half-block: TMEM -> fp32 staging smem -> one elected thread waits for its turn on the block's
-    // counter, bulk-stores (first contributor) or bulk-reduce-adds (cp.reduce.async.bulk, performed in L2) it
-    // into dq_acc, and releases the counter one iteration later, once the operation has completed, so the
-    // completion latency overlaps the next half-block instead of stalling the tensor core.
+    // Per half-block: dQ_i^T TMEM -> registers (64 columns), release the TMEM buffer to the MMA warp at once,
+    // then the registers -> fp32 staging smem once the bulk warp has finished reading the previous block.
+    // The MMA warp therefore waits only for the TMEM read, never for the dQ ordering or the L2 operations.
     const int q4 = warp & 3, dd = q4 * 32 + lane;
     const bool active = q4 * 32 < D;  // warp-uniform
-    const bool elected = (warp == 10 && lane == 0);
     const uint32_t lb = tmem + ((uint32_t)(q4 * 32) << 16);
-    float *dqa = a.dq_acc + srow * D;
-    int *sem = a.dq_sem + ((size_t)bi * H + head) * NQ;
-    auto release = [&](int i) {  // the bulk operation of block i has completed (wait_group before)
-      fence_proxy_async_global();
-      st_release_gpu(&sem[i], (uint32_t)(i / 2 - kt + 1));
-    };
     for (int ii = 0; ii < NI; ++ii) {
-      const int i = i0 + ii, nrow = min(TQH, s - i * TQH);
-      const int rank = i / 2 - kt;  // contributions before this one (key tiles floor(i/2) .. kt+1)
       mbar_wait(dq_full, ii & 1);
       tc_fence_after();
+      uint32_t v[2][32];
       if (active) {
+        tmem_ld32(lb + C::DQT, v[0]);
+        tmem_ld32(lb + C::DQT + 32, v[1]);
+        tmem_ld_wait();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_free);  // dQ^T read: the next dQ^T MMA may overwrite it
+      if (ii >= 1) mbar_wait(&stg_free[(ii - 1) & 1], ((ii - 1) >> 1) & 1);  // block ii - 1's op has read it
+      if (active && dd < D) {
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2) {
-          uint32_t v[32];
-          tmem_ld32(lb + C::DQT + 32 * h2, v);
-          tmem_ld_wait();
-          if (h2 == 1) {  // dQ^T read: the next dQ^T MMA may overwrite it
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(dq_free);
-          } else {
-            drain_bar();  // the staging buffer is free: the previous bulk operation has read it
-          }
-          if (dd < D) {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) sStg[(32 * h2 + q) * D + dd] = __uint_as_float(v[q]);
-          }
-        }
-      } else {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(dq_free);
-        drain_bar();
+        for (int q = 0; q < 64; ++q) sStg[q * D + dd] = __uint_as_float(v[q >> 5][q & 31]);
       }
       fence_proxy_async();  // generic smem writes -> visible to the bulk copy (async proxy)
-      drain_bar();
-      if (elected) {
-        if (rank > 0) {
-          const uint64_t t0 = globaltimer();
-          int seen;
-          while ((seen = (int)ld_acquire_gpu(&sem[i])) != rank) {
-            __nanosleep(20);
-            if (globaltimer() - t0 > 4000000000ull) {  // 4 s: a broken ordering invariant, not a slow peer
-              printf("attn_bwd dQ order watchdog: b %d head %d kt %d block %d rank %d counter %d\n", bi, head, kt, i,
-                     rank, seen);
-              __trap();
-            }
-          }
-          fence_proxy_async_global();
-        }
-        float *qa = dqa + (size_t)i * TQH * D;
-        const uint32_t bytes = (uint32_t)nrow * D * 4;
-        if (rank == 0)
-          bulk_store(qa, sStg, bytes);
-        else
-          bulk_reduce_add_f32(qa, sStg, bytes);
-        tma_store_commit();
-        if (ii >= 1) {
-          tma_store_wait<1>();  // the previous block's operation has completed
-          release(i - 1);
-        }
-        tma_store_wait_read<0>();  // the staging buffer has been read (rewritten after the next barrier)
-      }
-      __syncwarp();  // reconverge warp 10 before the next warp-collective tcgen05.ld
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&stg_full[ii & 1]);
     }
-    if (elected && NI > 0) {
-      tma_store_wait<0>();
-      release(i0 + NI - 1);
+  } else if (lane == 0) {
+    // ------------------------------------------------------------ dQ bulk threads (warps 14, 15: lane 0)
+    // Thread k takes the blocks ii = k mod 2: waits for its turn on the block's counter, bulk-stores (first
+    // contributor) or bulk-reduce-adds (cp.reduce.async.bulk, performed in L2) the staged block into dq_acc,
+    // frees the staging buffer once the operation has read it, and releases the counter as soon as the
+    // operation has completed -- the completion latency of one block overlaps the other thread's next block.
+    const int k = warp - 14;
+    float *dqa = a.dq_acc + srow * D;
+    int *sem = a.dq_sem + ((size_t)bi * H + head) * NQ;
+    for (int ii = k; ii < NI; ii += 2) {
+      const int i = i0 + ii, nrow = min(TQH, s - i * TQH);
+      const int rank = i / 2 - kt;  // contributions before this one (key tiles floor(i/2) .. kt+1)
+      mbar_wait(&stg_full[k], (ii >> 1) & 1);
+      if (rank > 0) {
+        const uint64_t t0 = globaltimer();
+        int seen;
+        while ((seen = (int)ld_acquire_gpu(&sem[i])) != rank) {
+          __nanosleep(20);
+          if (globaltimer() - t0 > 4000000000ull) {  // 4 s: a broken ordering invariant, not a slow peer
+            printf("attn_bwd dQ order watchdog: b %d head %d kt %d block %d rank %d counter %d\n", bi, head, kt, i,
+                   rank, seen);
+            __trap();
+          }
+        }
+        fence_proxy_async_global();
+      }
+      float *qa = dqa + (size_t)i * TQH * D;
+      const uint32_t bytes = (uint32_t)nrow * D * 4;
+      if (rank == 0)
+        bulk_store(qa, sStg, bytes);
+      else
+        bulk_reduce_add_f32(qa, sStg, bytes);
+      tma_store_commit();
+      tma_store_wait_read<0>();  // the staging buffer has been read: the drain warps may refill it
+      mbar_arrive(&stg_free[k]);
+      tma_store_wait<0>();       // the operation has completed: the next contributor may go
+      fence_proxy_async_global();
+      st_release_gpu(&sem[i], (uint32_t)(rank + 1));
     }
   }
   tc_fence_before();
@@ -531,7 +526,7 @@ static cudaError_t bwd_tc_d(const AttnArgs &a, cudaStream_t st) {
       const char *e = getenv("MERAK_ATTN_BWD_GROUP");
       g_env = e ? atoi(e) : 0;
     }
-    ag.attn_group = g_env > 0 ? g_env : 32;
+    ag.attn_group = g_env > 0 ? g_env : 64;  // measured: 64 >= 32 > 16 > 8 at the gpt shapes
   }
   if (ag.attn_group > a.b * a.heads) ag.attn_group = a.b * a.heads;
   const int grid = a.b * a.heads * ((a.s + TKEY - 1) / TKEY);
