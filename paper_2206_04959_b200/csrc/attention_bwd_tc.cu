@@ -40,6 +40,7 @@ namespace {
 constexpr int TKEY = 128;  // keys per CTA (TMEM lanes)
 constexpr int TQH = 64;    // queries per half-block (N of the score products)
 constexpr int NTHR = 512;  // 16 warps
+constexpr int DBG_STRIDE = 96;  // u64 clock stamps per CTA (AttnArgs::dbg, diagnostics only)
 
 template <int D>
 struct BwdCfg {
@@ -124,9 +125,9 @@ __global__ void __launch_bounds__(NTHR, 1)
   // barrier's completions are consumed in order by one waiter; the TMEM buffer is ii % NB
   uint64_t *s_full = q_empty + ST, *p_full = s_full + 2, *ds_free = p_full + 2;
   uint64_t *dq_full = ds_free + 2, *dq_free = dq_full + 1, *kv_done = dq_free + 1;
-  // dQ staging buffer: drain warps <-> bulk thread k = ii & 1 (one barrier pair per bulk thread)
-  uint64_t *stg_full = kv_done + 1, *stg_free = stg_full + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(stg_free + 2);
+  // dQ staging buffer, two 32-row halves h: drain warps <-> bulk thread k = ii & 1; barrier [h * 2 + k]
+  uint64_t *stg_full = kv_done + 1, *stg_free = stg_full + 4;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(stg_free + 4);
   auto stQ = [&](int st) { return sStage + st * C::STAGE_BYTES; };
   auto stO = [&](int st) { return sStage + st * C::STAGE_BYTES + C::QH_BYTES; };
   auto stL = [&](int st) { return sLD + st * 2 * TQH; };
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     mbar_init(dq_full, 1);
     mbar_init(dq_free, 4);
     mbar_init(kv_done, 1);
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < 4; ++k) {
       mbar_init(&stg_full[k], 4);
       mbar_init(&stg_free[k], 1);
     }
@@ -210,7 +211,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     constexpr uint32_t idesc_s = idesc_bf16(TKEY, TQH, false, false);  // K Q^T, V dO^T
     constexpr uint32_t idesc_g = idesc_bf16(TKEY, D, false, true);     // P^T dO, dS^T Q
     constexpr uint32_t idesc_q = idesc_bf16(128, TQH, true, true);     // K^T dS^T (M = d padded)
-    unsigned long long *dbg = (a.dbg && lane == 0) ? a.dbg + (size_t)blockIdx.x * 80 : nullptr;
+    unsigned long long *dbg = (a.dbg && lane == 0) ? a.dbg + (size_t)blockIdx.x * DBG_STRIDE : nullptr;
     if (dbg) { dbg[0] = clock64(); dbg[76] = globaltimer(); dbg[77] = NI; unsigned sm; asm volatile("mov.u32 %0, %%smid;" : "=r"(sm)); dbg[79] = sm; }
     mbar_wait(kv_full, 0);
     if (dbg) dbg[1] = clock64();
@@ -281,31 +282,39 @@ __global__ void __launch_bounds__(NTHR, 1)
       const float *L = stL(st), *Dl = stD(st);
       mbar_wait(&ds_free[g], ((ii >> 1) & 1) ^ 1);  // dS^T buffer g read by the MMAs of ii - 2
       uint8_t *row = sDS + g * C::DS_BYTES + r * 128;
+      // 16 query columns per step; the TMEM loads of step c + 1 are in flight while step c computes
+      uint32_t sv[2][16], dv[2][16];
+      tmem_ld16b(lb + C::SP0 + 64 * b, sv[0]);
+      tmem_ld16b(lb + C::DP0 + 64 * b, dv[0]);
+      tmem_ld_wait();
 #pragma unroll
-      for (int c = 0; c < TQH / 16; ++c) {  // 16 query columns per step
-        uint32_t sv[16], dv[16], pw[8], dw[8];
-        tmem_ld16b(lb + C::SP0 + 64 * b + 16 * c, sv);
-        tmem_ld16b(lb + C::DP0 + 64 * b + 16 * c, dv);
-        tmem_ld_wait();
+      for (int c = 0; c < TQH / 16; ++c) {
+        const int cb = c & 1;
+        if (c + 1 < TQH / 16) {
+          tmem_ld16b(lb + C::SP0 + 64 * b + 16 * (c + 1), sv[cb ^ 1]);
+          tmem_ld16b(lb + C::DP0 + 64 * b + 16 * (c + 1), dv[cb ^ 1]);
+        }
+        uint32_t pw[8], dw[8];
 #pragma unroll
         for (int k = 0; k < 16; k += 2) {
           const int col = 16 * c + k, qi = qi0 + col;
           const float2 l2 = *reinterpret_cast<const float2 *>(L + col);
           const float2 d2 = *reinterpret_cast<const float2 *>(Dl + col);
-          float p0 = fast_exp2(fmaf(__uint_as_float(sv[k]), sl2, -l2.x));
-          float p1 = fast_exp2(fmaf(__uint_as_float(sv[k + 1]), sl2, -l2.y));
+          float p0 = fast_exp2(fmaf(__uint_as_float(sv[cb][k]), sl2, -l2.x));
+          float p1 = fast_exp2(fmaf(__uint_as_float(sv[cb][k + 1]), sl2, -l2.y));
           if (mask) {
             if (!(kj <= qi && qi < s)) p0 = 0.f;
             if (!(kj <= qi + 1 && qi + 1 < s)) p1 = 0.f;
           }
           pw[k >> 1] = pack_bf16(p0, p1);
-          dw[k >> 1] = pack_bf16(p0 * (__uint_as_float(dv[k]) - d2.x), p1 * (__uint_as_float(dv[k + 1]) - d2.y));
+          dw[k >> 1] = pack_bf16(p0 * (__uint_as_float(dv[cb][k]) - d2.x), p1 * (__uint_as_float(dv[cb][k + 1]) - d2.y));
         }
         // P^T (bf16 pairs) over columns 8c..8c+7 of this buffer's S^T (already read): the A operand of dV
         tmem_st8(lb + C::SP0 + 64 * b + 8 * c, pw);
         // dS^T: 16-B chunks 2c, 2c+1 of this key row (128-B swizzle)
         *reinterpret_cast<uint4 *>(row + (((2 * c) ^ (r & 7)) << 4)) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
         *reinterpret_cast<uint4 *>(row + (((2 * c + 1) ^ (r & 7)) << 4)) = make_uint4(dw[4], dw[5], dw[6], dw[7]);
+        if (c + 1 < TQH / 16) tmem_ld_wait();
       }
       tmem_st_wait();
       fence_proxy_async();
@@ -316,8 +325,13 @@ __global__ void __launch_bounds__(NTHR, 1)
     // dK, dV epilogue
     mbar_wait(kv_done, 0);
     tc_fence_after();
-    __nv_bfloat16 *dk = reinterpret_cast<__nv_bfloat16 *>(a.dqkv) + (size_t)(tok0 + kj) * 3 * hr + hr + head * D;
-    __nv_bfloat16 *dvp = dk + hr;
+    unsigned long long *dbg = (a.dbg && warp == 2 && lane == 0 && NI <= 32) ? a.dbg + (size_t)blockIdx.x * DBG_STRIDE : nullptr;
+    if (dbg) dbg[70] = clock64();
+    // TMEM -> bf16 rows in smem (K / V / stage-ring space, free once every MMA completed; padded rows: the
+    // row-per-thread 16-B writes are bank-conflict free), then coalesced 16-B global stores of whole rows.
+    constexpr int SROW = 2 * D + 16, CPR = D / 8;  // staging row bytes, 16-B chunks per row
+    static_assert(2 * TKEY * SROW <= 2 * C::KV_BYTES + ST * C::STAGE_BYTES, "dK/dV staging");
+    uint8_t *stgK = sK, *stgV = sK + TKEY * SROW;
 #pragma unroll
     for (int c = 0; c < D / 16; ++c) {
       if ((c & 1) != g) continue;  // warp-uniform: alternate 16-column chunks per warpgroup
@@ -325,23 +339,32 @@ __global__ void __launch_bounds__(NTHR, 1)
       tmem_ld16b(lb + C::DV + c * 16, ov);
       tmem_ld16b(lb + C::DK + c * 16, ok);
       tmem_ld_wait();
-      if (kj < s) {
-        uint4 u;
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          u.x = pack_bf16(__uint_as_float(ov[8 * hh + 0]), __uint_as_float(ov[8 * hh + 1]));
-          u.y = pack_bf16(__uint_as_float(ov[8 * hh + 2]), __uint_as_float(ov[8 * hh + 3]));
-          u.z = pack_bf16(__uint_as_float(ov[8 * hh + 4]), __uint_as_float(ov[8 * hh + 5]));
-          u.w = pack_bf16(__uint_as_float(ov[8 * hh + 6]), __uint_as_float(ov[8 * hh + 7]));
-          *reinterpret_cast<uint4 *>(dvp + c * 16 + 8 * hh) = u;
-          u.x = pack_bf16(__uint_as_float(ok[8 * hh + 0]) * scale, __uint_as_float(ok[8 * hh + 1]) * scale);
-          u.y = pack_bf16(__uint_as_float(ok[8 * hh + 2]) * scale, __uint_as_float(ok[8 * hh + 3]) * scale);
-          u.z = pack_bf16(__uint_as_float(ok[8 * hh + 4]) * scale, __uint_as_float(ok[8 * hh + 5]) * scale);
-          u.w = pack_bf16(__uint_as_float(ok[8 * hh + 6]) * scale, __uint_as_float(ok[8 * hh + 7]) * scale);
-          *reinterpret_cast<uint4 *>(dk + c * 16 + 8 * hh) = u;
-        }
+      for (int hh = 0; hh < 2; ++hh) {
+        uint4 u;
+        u.x = pack_bf16(__uint_as_float(ov[8 * hh + 0]), __uint_as_float(ov[8 * hh + 1]));
+        u.y = pack_bf16(__uint_as_float(ov[8 * hh + 2]), __uint_as_float(ov[8 * hh + 3]));
+        u.z = pack_bf16(__uint_as_float(ov[8 * hh + 4]), __uint_as_float(ov[8 * hh + 5]));
+        u.w = pack_bf16(__uint_as_float(ov[8 * hh + 6]), __uint_as_float(ov[8 * hh + 7]));
+        *reinterpret_cast<uint4 *>(stgV + r * SROW + c * 32 + 16 * hh) = u;
+        u.x = pack_bf16(__uint_as_float(ok[8 * hh + 0]) * scale, __uint_as_float(ok[8 * hh + 1]) * scale);
+        u.y = pack_bf16(__uint_as_float(ok[8 * hh + 2]) * scale, __uint_as_float(ok[8 * hh + 3]) * scale);
+        u.z = pack_bf16(__uint_as_float(ok[8 * hh + 4]) * scale, __uint_as_float(ok[8 * hh + 5]) * scale);
+        u.w = pack_bf16(__uint_as_float(ok[8 * hh + 6]) * scale, __uint_as_float(ok[8 * hh + 7]) * scale);
+        *reinterpret_cast<uint4 *>(stgK + r * SROW + c * 32 + 16 * hh) = u;
       }
     }
+    asm volatile("bar.sync 3, 256;" ::: "memory");  // the 8 element-wise warps
+    const int et = (warp - 2) * 32 + lane;
+    __nv_bfloat16 *dk0 = reinterpret_cast<__nv_bfloat16 *>(a.dqkv) + (size_t)(tok0 + kt * TKEY) * 3 * hr + hr + head * D;
+    const int nrows = min(TKEY, s - kt * TKEY);
+    for (int idx = et; idx < 2 * TKEY * CPR; idx += 256) {
+      const int t = idx / (TKEY * CPR), rem = idx - t * TKEY * CPR, rr = rem / CPR, ch = rem - rr * CPR;
+      if (rr < nrows)
+        *reinterpret_cast<uint4 *>(dk0 + (size_t)rr * 3 * hr + t * hr + ch * 8) =
+            *reinterpret_cast<const uint4 *>((t ? stgV : stgK) + rr * SROW + ch * 16);
+    }
+    if (dbg) dbg[71] = clock64();
   } else if (warp < 14) {
     // ------------------------------------------------------------ dQ drain (thread = d index)
     // Per half-block: dQ_i^T TMEM -> registers (64 columns), release the TMEM buffer to the MMA warp at once,
@@ -352,6 +375,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     const uint32_t lb = tmem + ((uint32_t)(q4 * 32) << 16);
     for (int ii = 0; ii < NI; ++ii) {
       mbar_wait(dq_full, ii & 1);
+      if (a.dbg && warp == 10 && lane == 0 && ii + 1 == NI) a.dbg[(size_t)blockIdx.x * DBG_STRIDE + 88] = clock64();
       tc_fence_after();
       uint32_t v[2][32];
       if (active) {
@@ -362,14 +386,17 @@ __global__ void __launch_bounds__(NTHR, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_free);  // dQ^T read: the next dQ^T MMA may overwrite it
-      if (ii >= 1) mbar_wait(&stg_free[(ii - 1) & 1], ((ii - 1) >> 1) & 1);  // block ii - 1's op has read it
-      if (active && dd < D) {
 #pragma unroll
-        for (int q = 0; q < 64; ++q) sStg[q * D + dd] = __uint_as_float(v[q >> 5][q & 31]);
+      for (int h = 0; h < 2; ++h) {  // rows 32h .. 32h + 31 of the staging buffer, each half handed over alone
+        if (ii >= 1) mbar_wait(&stg_free[h * 2 + ((ii - 1) & 1)], ((ii - 1) >> 1) & 1);  // block ii - 1 read it
+        if (active && dd < D) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) sStg[(32 * h + q) * D + dd] = __uint_as_float(v[h][q]);
+        }
+        fence_proxy_async();  // generic smem writes -> visible to the bulk copy (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&stg_full[h * 2 + (ii & 1)]);
       }
-      fence_proxy_async();  // generic smem writes -> visible to the bulk copy (async proxy)
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&stg_full[ii & 1]);
     }
   } else if (lane == 0) {
     // ------------------------------------------------------------ dQ bulk threads (warps 14, 15: lane 0)
@@ -383,8 +410,9 @@ __global__ void __launch_bounds__(NTHR, 1)
     for (int ii = k; ii < NI; ii += 2) {
       const int i = i0 + ii, nrow = min(TQH, s - i * TQH);
       const int rank = i / 2 - kt;  // contributions before this one (key tiles floor(i/2) .. kt+1)
-      mbar_wait(&stg_full[k], (ii >> 1) & 1);
-      if (rank > 0) {
+      unsigned long long *dbl = (a.dbg && ii + 2 >= NI) ? a.dbg + (size_t)blockIdx.x * DBG_STRIDE + 80 + 4 * k : nullptr;
+      if (dbl) dbl[0] = clock64();
+      if (rank > 0) {  // the turn does not depend on the staging: wait for it first
         const uint64_t t0 = globaltimer();
         int seen;
         while ((seen = (int)ld_acquire_gpu(&sem[i])) != rank) {
@@ -397,26 +425,37 @@ __global__ void __launch_bounds__(NTHR, 1)
         }
         fence_proxy_async_global();
       }
+      if (dbl) dbl[1] = clock64();
       float *qa = dqa + (size_t)i * TQH * D;
-      const uint32_t bytes = (uint32_t)nrow * D * 4;
-      if (rank == 0)
-        bulk_store(qa, sStg, bytes);
-      else
-        bulk_reduce_add_f32(qa, sStg, bytes);
-      tma_store_commit();
-      tma_store_wait_read<0>();  // the staging buffer has been read: the drain warps may refill it
-      mbar_arrive(&stg_free[k]);
-      tma_store_wait<0>();       // the operation has completed: the next contributor may go
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rows = min(32, nrow - 32 * h);
+        mbar_wait(&stg_full[h * 2 + k], (ii >> 1) & 1);
+        if (rows > 0) {
+          const uint32_t bytes = (uint32_t)rows * D * 4;
+          if (rank == 0)
+            bulk_store(qa + 32 * h * D, sStg + 32 * h * D, bytes);
+          else
+            bulk_reduce_add_f32(qa + 32 * h * D, sStg + 32 * h * D, bytes);
+          tma_store_commit();
+          tma_store_wait_read<0>();  // this half has been read: the drain warps may refill it
+        }
+        mbar_arrive(&stg_free[h * 2 + k]);
+      }
+      if (dbl) dbl[2] = clock64();
+      tma_store_wait<0>();  // both halves have completed: the next contributor may go
+      if (dbl) dbl[3] = clock64();
       fence_proxy_async_global();
       st_release_gpu(&sem[i], (uint32_t)(rank + 1));
     }
+    if (a.dbg && NI <= 32) a.dbg[(size_t)blockIdx.x * DBG_STRIDE + 72 + k] = clock64();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
-    if (a.dbg && lane == 0) { a.dbg[(size_t)blockIdx.x * 80 + 75] = clock64(); a.dbg[(size_t)blockIdx.x * 80 + 78] = globaltimer(); }
+    if (a.dbg && lane == 0) { a.dbg[(size_t)blockIdx.x * DBG_STRIDE + 75] = clock64(); a.dbg[(size_t)blockIdx.x * DBG_STRIDE + 78] = globaltimer(); }
   }
 }
 
