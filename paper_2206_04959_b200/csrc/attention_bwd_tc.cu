@@ -40,7 +40,7 @@ namespace {
 constexpr int TKEY = 128;  // keys per CTA (TMEM lanes)
 constexpr int TQH = 64;    // queries per half-block (N of the score products)
 constexpr int NTHR = 512;  // 16 warps
-constexpr int DBG_STRIDE = 96;  // u64 clock stamps per CTA (AttnArgs::dbg, diagnostics only)
+constexpr int DBG_STRIDE = 160;  // u64 clock stamps per CTA (AttnArgs::dbg, diagnostics only)
 
 template <int D>
 struct BwdCfg {
@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       tc_commit_w(dq_full);
       tc_commit_w(&ds_free[w]);
       tc_commit_w(&q_empty[st]);
+      if (dbg && !(p & 1) && p < 32) dbg[112 + (p >> 1)] = clock64();
     };
     for (int ii = 0; ii <= NI; ++ii) {
       if (NB == 1) {  // one buffer: P^T of ii - 1 must be consumed before S^T of ii overwrites it
@@ -277,6 +278,8 @@ __global__ void __launch_bounds__(NTHR, 1)
       const int st = ii % ST, b = ii % NB, qi0 = (i0 + ii) * TQH;  // warpgroup g == ii & 1
       mbar_wait(&q_full[st], (ii / ST) & 1);  // lse / delta of this half-block
       mbar_wait(&s_full[g], (ii >> 1) & 1);
+      unsigned long long *dbe = (a.dbg && warp == 2 && lane == 0 && ii < 32) ? a.dbg + (size_t)blockIdx.x * DBG_STRIDE : nullptr;
+      if (dbe) dbe[96 + (ii >> 1)] = clock64();
       tc_fence_after();
       const bool mask = (qi0 < kt * TKEY + TKEY - 1) || (qi0 + TQH > s);
       const float *L = stL(st), *Dl = stD(st);
@@ -320,6 +323,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       fence_proxy_async();
       tc_fence_before();
       __syncwarp();
+      if (dbe) dbe[128 + (ii >> 1)] = clock64();
       if (lane == 0) mbar_arrive(&p_full[g]);
     }
     // dK, dV epilogue
@@ -428,20 +432,25 @@ __global__ void __launch_bounds__(NTHR, 1)
       if (dbl) dbl[1] = clock64();
       float *qa = dqa + (size_t)i * TQH * D;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      // both halves in flight: half 1 is issued as soon as it is staged, before half 0 has been read
+      auto issue = [&](int h) {
         const int rows = min(32, nrow - 32 * h);
-        mbar_wait(&stg_full[h * 2 + k], (ii >> 1) & 1);
         if (rows > 0) {
-          const uint32_t bytes = (uint32_t)rows * D * 4;
           if (rank == 0)
-            bulk_store(qa + 32 * h * D, sStg + 32 * h * D, bytes);
+            bulk_store(qa + 32 * h * D, sStg + 32 * h * D, (uint32_t)rows * D * 4);
           else
-            bulk_reduce_add_f32(qa + 32 * h * D, sStg + 32 * h * D, bytes);
-          tma_store_commit();
-          tma_store_wait_read<0>();  // this half has been read: the drain warps may refill it
+            bulk_reduce_add_f32(qa + 32 * h * D, sStg + 32 * h * D, (uint32_t)rows * D * 4);
         }
-        mbar_arrive(&stg_free[h * 2 + k]);
-      }
+        tma_store_commit();  // (an empty group when the half has no rows)
+      };
+      mbar_wait(&stg_full[k], (ii >> 1) & 1);
+      issue(0);
+      mbar_wait(&stg_full[2 + k], (ii >> 1) & 1);
+      issue(1);
+      tma_store_wait_read<1>();  // half 0 read
+      mbar_arrive(&stg_free[k]);
+      tma_store_wait_read<0>();  // half 1 read
+      mbar_arrive(&stg_free[2 + k]);
       if (dbl) dbl[2] = clock64();
       tma_store_wait<0>();  // both halves have completed: the next contributor may go
       if (dbl) dbl[3] = clock64();
