@@ -9,8 +9,8 @@
 //   S^T  = K Q_i^T      (M 128 keys, N 64 queries, K d)        -> TMEM, double-buffered
 //   dP^T = V dO_i^T     (same shape)                            -> TMEM, double-buffered
 //   dV  += P^T dO_i     (A = P^T read from TMEM: bf16 written over S^T by the element-wise warps)
-//   dK  += dS^T Q_i     (A = dS^T in swizzled smem)
-//   dQ_i^T = K^T dS^T   (M = d padded to 128, A = K read MN-major, B = dS^T MN-major) -> TMEM
+//   dK  += dS^T Q_i     (A = dS^T read from TMEM: bf16 written over dP^T by the element-wise warps)
+//   dQ_i^T = K^T dS^T   (M = d padded to 128, A = K read MN-major, B = dS^T MN-major from smem) -> TMEM
 // 512 threads: warp 0 TMA (K, V once; Q_i, dO_i, lse_i, delta_i per half-block through a stage ring),
 // warp 1 TMEM owner + MMA issuer (scores of i+1 issued before the gradient MMAs of i, so the element-wise
 // work of one half-block overlaps the tensor core), warps 2-9 element-wise (two warpgroups ping-pong on
@@ -40,7 +40,7 @@ namespace {
 constexpr int TKEY = 128;  // keys per CTA (TMEM lanes)
 constexpr int TQH = 64;    // queries per half-block (N of the score products)
 constexpr int NTHR = 512;  // 16 warps
-constexpr int DBG_STRIDE = 160;  // u64 clock stamps per CTA (AttnArgs::dbg, diagnostics only)
+constexpr int DBG_STRIDE = 192;  // u64 clock stamps per CTA (AttnArgs::dbg, diagnostics only)
 
 template <int D>
 struct BwdCfg {
@@ -240,15 +240,16 @@ __global__ void __launch_bounds__(NTHR, 1)
       tc_fence_after();
       const uint64_t qmn = sdesc_sw128(smem_u32(stQ(st)), C::H_ATOM, 1024);
       const uint64_t omn = sdesc_sw128(smem_u32(stO(st)), C::H_ATOM, 1024);
-      const uint64_t dsk = sdesc_sw128(smem_u32(sDS + w * C::DS_BYTES), 16, 1024);
       const uint64_t dsmn = sdesc_sw128(smem_u32(sDS + w * C::DS_BYTES), C::F_ATOM, 1024);
 #pragma unroll
       for (int kk = 0; kk < TQH / 16; ++kk) {
         const uint32_t acc = (p > 0 || kk > 0) ? 1u : 0u;
         tc_mma_f16_ts_w(tmem + C::DV, tmem + C::SP0 + 64 * b + kk * 8, omn + (kk * 2048 >> 4), idesc_g, acc);
-        tc_mma_f16_w(tmem + C::DK, dsk + (kk * 32 >> 4), qmn + (kk * 2048 >> 4), idesc_g, acc);
+        tc_mma_f16_ts_w(tmem + C::DK, tmem + C::DP0 + 64 * b + kk * 8, qmn + (kk * 2048 >> 4), idesc_g, acc);
       }
+      if (dbg && !(p & 1) && p < 32) dbg[144 + (p >> 1)] = clock64();
       if (p >= 1) mbar_wait(dq_free, (p - 1) & 1);  // the drain warps have read dQ^T of p - 1
+      if (dbg && !(p & 1) && p < 32) dbg[160 + (p >> 1)] = clock64();
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < TKEY / 16; ++kk)
@@ -314,6 +315,8 @@ __global__ void __launch_bounds__(NTHR, 1)
         }
         // P^T (bf16 pairs) over columns 8c..8c+7 of this buffer's S^T (already read): the A operand of dV
         tmem_st8(lb + C::SP0 + 64 * b + 8 * c, pw);
+        // dS^T likewise over columns 8c..8c+7 of dP^T (already read): the A operand of dK
+        tmem_st8(lb + C::DP0 + 64 * b + 8 * c, dw);
         // dS^T: 16-B chunks 2c, 2c+1 of this key row (128-B swizzle)
         *reinterpret_cast<uint4 *>(row + (((2 * c) ^ (r & 7)) << 4)) = make_uint4(dw[0], dw[1], dw[2], dw[3]);
         *reinterpret_cast<uint4 *>(row + (((2 * c + 1) ^ (r & 7)) << 4)) = make_uint4(dw[4], dw[5], dw[6], dw[7]);

@@ -1,4 +1,4 @@
-"""Per-CTA clock stamps of the attention backward (AttnArgs::dbg, 160 x u64 per CTA): time per half-block
+"""Per-CTA clock stamps of the attention backward (AttnArgs::dbg, 192 x u64 per CTA): time per half-block
 of the MMA issuer (q_full / p_full acquisition), prologue, epilogue, CTA spans (diagnostics only)."""
 import ctypes, json, os, sys
 import torch
@@ -19,12 +19,12 @@ dqkv = torch.empty_like(qkv)
 ws = torch.zeros(L.merak_test_attn_bwd_ws_bytes(b, s, H, d), device="cuda", dtype=torch.uint8)
 nkt = (s + 127) // 128
 ncta = b * H * nkt
-dbg = torch.zeros(ncta * 160, dtype=torch.int64, device="cuda")
+dbg = torch.zeros(ncta * 192, dtype=torch.int64, device="cuda")
 assert L.merak_test_attn_fwd(P(qkv), P(ctx), P(lse), b, s, H, d, st) == 0
 for _ in range(3):
     assert L.merak_test_attn_bwd_dbg(P(qkv), P(ctx), P(lse), P(dctx), P(dqkv), P(ws), b, s, H, d, P(dbg), st) == 0
 torch.cuda.synchronize()
-D = dbg.view(ncta, 160).cpu().tolist()
+D = dbg.view(ncta, 192).cpu().tolist()
 t0 = min(r[76] for r in D)
 t1 = max(r[78] for r in D)
 per_it, gaps_q, gaps_p, prol, epi = [], [], [], [], []
@@ -50,6 +50,8 @@ print(json.dumps({"shape": [b, s, H, d], "kernel_span_us": (t1 - t0) / 1e3, "cta
                   "bulk1_end_after_lastissue_clk": med([r[73] - r[74] for r in D if r[77] <= 32 and r[77] > 1]),
                   "last_dqfull_after_lastissue_clk": med([r[88] - r[74] for r in D]),
                   "ew_busy_clk": med([r[128 + j] - r[96 + j] for r in D if r[77] >= 8 for j in range(1, (min(r[77], 32) + 1) // 2 - 1)]),
+                  "grads_to_dqfree_wait_clk": med([r[144 + j] - r[38 + 2 * j] for r in D if r[77] >= 8 for j in range(1, (min(r[77], 32) - 2) // 2)]),
+                  "dqfree_wait_clk": med([r[160 + j] - r[144 + j] for r in D if r[77] >= 8 for j in range(1, (min(r[77], 32) - 2) // 2)]),
                   "grads_issue_clk": med([r[112 + j] - r[38 + 2 * j] for r in D if r[77] >= 8 for j in range(1, (min(r[77], 32) - 2) // 2)]),
                   "sdone_after_grads_issue_clk": med([r[96 + j + 1] - r[38 + 2 * j] for r in D if r[77] >= 8 for j in range(1, (min(r[77], 32) - 2) // 2)]),
                   "next_scores_issue_after_grads_clk": med([r[2 + 2 * j + 2] - r[38 + 2 * j] for r in D if r[77] >= 8 for j in range(1, (min(r[77], 32) - 2) // 2)]),
