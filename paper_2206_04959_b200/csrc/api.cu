@@ -34,6 +34,7 @@ typedef __nv_bfloat16 bf16;
 namespace {
 
 constexpr int MAXN = 64;  // max sub-batches
+#define MAXN_ 64
 constexpr int NSLOT = 5;  // AR#1..AR#4 partial slots (+ the sequence-parallel all-gather slot, index 4)
 constexpr int AG_SLOT = 4;
 
@@ -146,6 +147,14 @@ struct merak_tmp {
   char *ws32 = nullptr;
   float *dz32 = nullptr, *dx1_32 = nullptr, *dctx32 = nullptr, *dqkv32 = nullptr, *delta32 = nullptr, *du32 = nullptr;
   struct InprocGroup *grp = nullptr;  // MERAK_COMM_INPROC: the group this rank belongs to
+  // LN1 fused into a chained AR#2: a forward with MERAK_FLAG_CHAIN leaves its AR#2 epilogue
+  // kernels unlaunched (handshakes done); the next call on the handle launches them first -- computing the next
+  // layer's LN1 as well when that call is a forward on y.  MERAK_FUSE_LN1=0 disables.
+  bool fuse_ln1 = true;
+  bool ar2_pending = false;
+  const bf16 *ar2_y = nullptr;
+  ArFwdArgs ar2_a[MAXN_];
+  PeerSync ar2_ps[MAXN_];
   cudaEvent_t ev_hs[2] = {};          // INPROC: this rank's handshake points (alternating generations)
 };
 
@@ -517,6 +526,48 @@ static merak_status leave(merak_tmp_t *h, cudaStream_t st, uint32_t flags, int l
 }
 
 // ------------------------------------------------------------------------------ forward
+// LN1's ones-column pads of u, ctx, u2, g for the rows from r0 of a saved buffer
+static OnesPad ln1_pads(const merak_tmp_t *h, const SavedLayout &L, char *saved, size_t r0) {
+  OnesPad pad;
+  pad.n = 4;
+  pad.ptr[0] = (bf16 *)(saved + L.u) + r0 * L.ld_u; pad.ld[0] = L.ld_u; pad.col[0] = h->h;
+  pad.ptr[1] = (bf16 *)(saved + L.ctx) + r0 * L.ld_ctx; pad.ld[1] = L.ld_ctx; pad.col[1] = h->hr;
+  pad.ptr[2] = (bf16 *)(saved + L.u2) + r0 * L.ld_u2; pad.ld[2] = L.ld_u2; pad.col[2] = h->h;
+  pad.ptr[3] = (bf16 *)(saved + L.g) + r0 * L.ld_g; pad.ld[3] = L.ld_g; pad.col[3] = h->fr;
+  return pad;
+}
+
+// Launch the deferred AR#2 epilogues of the previous chained forward (in sub-batch order, on the
+// communication stream, right behind their handshakes).  With w / saved: the layer being entered runs on
+// their output y, so each epilogue also computes that layer's LN1 (u, mean1, rstd1 and the ones-column pads
+// of its rows in `saved`) -- the same row-engine arithmetic as ln_fwd_kernel on the stored bf16 y, so the
+// result is bit-identical to the unfused LN1.
+static merak_status flush_ar2(merak_tmp_t *h, const merak_tmp_weights *w = nullptr, char *saved = nullptr) {
+  if (!h->ar2_pending) return MERAK_OK;
+  h->ar2_pending = false;
+  const SavedLayout L = saved_layout(h);
+  const int n = h->n, m = h->M / n;
+  for (int j = 0; j < n; ++j) {
+    ArFwdArgs a = h->ar2_a[j];
+    if (w) {
+      const size_t r0 = (size_t)j * m;
+      a.do_ln = true;
+      a.gamma = (const bf16 *)w->ln1_g; a.beta = (const bf16 *)w->ln1_b;
+      a.ln_out = (bf16 *)(saved + L.u) + r0 * L.ld_u; a.ld_ln = L.ld_u;
+      a.mean = (float *)(saved + L.mean1) + r0; a.rstd = (float *)(saved + L.rstd1) + r0;
+      a.eps = h->eps;
+      a.pad = ln1_pads(h, L, saved, r0);
+    }
+    {
+      Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+      CK(h, ar_fwd(a, h->ar2_ps[j], h->ms));
+    }
+    CK(h, cudaEventRecord(h->ev_ar[1][j], h->ms));
+    h->ev_ar_valid[1][j] = true;
+  }
+  return MERAK_OK;
+}
+
 // recompute = true: the activation-recomputation pass of a MERAK_FLAG_RECOMPUTE backward (SURVEY §8(f) NEXT-3,
 // P:459): everything the backward reads is regenerated into `saved` -- the attention block with AR#1 / LN2 and
 // fc1 + GeLU -- while fc2 and AR#2 (whose output y the backward never reads) are skipped.  It leaves the chain
@@ -527,6 +578,11 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
   const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr;
   const bool comm = !(flags & MERAK_FLAG_NO_COMM) && !h->local;
   TRY(enter(h, st, true));
+  // the previous chained layer's AR#2 epilogues, with this layer's LN1 when x is their output
+  const bool ln1_fused = h->ar2_pending && !recompute && x == h->ar2_y;
+  TRY(flush_ar2(h, ln1_fused ? w : nullptr, ln1_fused ? saved : nullptr));
+  // this layer's AR#2 epilogues are deferred to the next call when the chain stays open
+  const bool defer_ar2 = (flags & MERAK_FLAG_CHAIN) && !recompute && h->fuse_ln1;
   auto S = [&](size_t off) { return saved + off; };
   // ---- attention block, sub-batch j: LN1 -> QKV -> attention -> proj (partial into slot 0) -> AR#1
   for (int j = 0; j < n; ++j) {
@@ -539,14 +595,9 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     bf16 *qkv = (bf16 *)S(L.qkv) + r0 * 3 * hr;
     bf16 *ctx = (bf16 *)S(L.ctx) + r0 * L.ld_ctx;
     float *lse = (float *)S(L.lse) + (size_t)j * b * h->Hr * h->s;
-    {
+    if (!ln1_fused) {
       // LN1, which also writes the ones-column pads of u, ctx, u2, g for these rows
-      OnesPad pad;
-      pad.n = 4;
-      pad.ptr[0] = u; pad.ld[0] = L.ld_u; pad.col[0] = hh;
-      pad.ptr[1] = ctx; pad.ld[1] = L.ld_ctx; pad.col[1] = hr;
-      pad.ptr[2] = (bf16 *)S(L.u2) + r0 * L.ld_u2; pad.ld[2] = L.ld_u2; pad.col[2] = hh;
-      pad.ptr[3] = (bf16 *)S(L.g) + r0 * L.ld_g; pad.ld[3] = L.ld_g; pad.col[3] = fr;
+      const OnesPad pad = ln1_pads(h, L, saved, r0);
       Launch Lk(h, MERAK_K_LN, cst, 0.0);
       CK(h, ln_fwd(xj, (const bf16 *)w->ln1_g, (const bf16 *)w->ln1_b, u, L.ld_u, mean1, rstd1, m, hh, h->eps, pad,
                    cst));
@@ -617,12 +668,22 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
       if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 1, r0, m, a.resid, a.bias, &a.chunk, &ps));
+      if (defer_ar2) {  // launched by the next call (flush_ar2), possibly with the next layer's LN1
+        a.pdl = false;
+        h->ar2_a[j] = a;
+        h->ar2_ps[j] = ps;
+        continue;
+      }
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
       a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
       CK(h, ar_fwd(a, ps, h->ms));
     }
     CK(h, cudaEventRecord(h->ev_ar[1][j], h->ms));
     h->ev_ar_valid[1][j] = true;
+  }
+  if (defer_ar2) {
+    h->ar2_pending = true;
+    h->ar2_y = y;
   }
   if (recompute) {
     TRY(leave(h, st, flags, 0));
@@ -650,6 +711,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
   const int n = h->n, m = h->M / n, b = h->B / n, hh = h->h, hr = h->hr, fr = h->fr;
   const bool comm = !(flags & MERAK_FLAG_NO_COMM) && !h->local;
   TRY(enter(h, st, false));
+  TRY(flush_ar2(h));  // a chained forward's deferred AR#2 epilogues (plain: no LN1 follows)
   auto S = [&](size_t off) { return saved + off; };
   // W2 / b2 grads need only dy and the saved g: they can fill from the start of the backward
   if (h->chain_open)
@@ -1446,6 +1508,8 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
   if (const char *t = getenv("MERAK_DEBUG_TRACE")) h->trace = atoi(t) == 1;
   if (const char *t = getenv("MERAK_AR_TWO_SHOT")) h->two_shot = h->T > 1 && !h->f32 && atoi(t) == 1;
   if (const char *t = getenv("MERAK_AR_FUSED_WAIT")) h->fused_wait = atoi(t) != 0;
+  if (const char *t = getenv("MERAK_FUSE_LN1")) h->fuse_ln1 = atoi(t) != 0;
+  if (h->f32) h->fuse_ln1 = false;
   // in-process groups share ONE GPU: a waiting epilogue kernel of one rank can fill the SMs that another rank's
   // phase-1 kernel (the one it waits for) needs, so they keep the 1-warp handshake kernel
   if (h->inproc) h->fused_wait = false;
@@ -1792,6 +1856,7 @@ merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, con
 merak_status merak_tmp_join(merak_tmp_t *h, void *st) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
   TRY(group_idle(h));
+  TRY(flush_ar2(h));
   if (!h->have_prev) return MERAK_OK;
   TRY(wait_all(h, (cudaStream_t)st));
   for (int j = 0; j < h->n; ++j) CK(h, cudaStreamWaitEvent((cudaStream_t)st, h->prev_out[j], 0));
@@ -1800,6 +1865,15 @@ merak_status merak_tmp_join(merak_tmp_t *h, void *st) {
 }
 
 merak_status merak_tmp_destroy(merak_tmp_t *h) {
+  if (h) {  // an open chain's last AR#2 epilogues: y is an output the caller may still read
+    cudaSetDevice(h->dev);
+    if (h->grp) {  // in-process group: while every rank's slots still exist
+      for (int q = 0; q < h->grp->T; ++q)
+        if (h->grp->hs[q]) flush_ar2(h->grp->hs[q]);
+    } else {
+      flush_ar2(h);
+    }
+  }
   if (h && h->inproc) {
     // every rank of the group has enqueued its collective calls (they never block the host), so the
     // shared device drains: no rank frees its slots while a peer's all-reduce may still read them
@@ -1828,6 +1902,7 @@ const char *merak_tmp_last_error(const merak_tmp_t *h) { return h ? h->err.c_str
 merak_status merak_tmp_set_profiling(merak_tmp_t *h, int32_t on) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
   TRY(group_idle(h));
+  TRY(flush_ar2(h));
   TRY(sync_all(h));
   h->prof = on != 0;
   h->recs.clear();
@@ -1843,6 +1918,7 @@ merak_status merak_tmp_set_profiling(merak_tmp_t *h, int32_t on) {
 merak_status merak_tmp_get_profile(merak_tmp_t *h, double *ms, int64_t *launches, double *flops) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
   TRY(group_idle(h));
+  TRY(flush_ar2(h));
   TRY(sync_all(h));
   for (auto &r : h->recs) {
     float t = 0;
@@ -1864,6 +1940,7 @@ merak_status merak_tmp_get_timeline(merak_tmp_t *h, int32_t cap, int32_t *count,
                                     float *t0, float *t1) {
   if (!h || !count) return fail(h, MERAK_EINVAL, "NULL argument");
   TRY(group_idle(h));
+  TRY(flush_ar2(h));
   TRY(sync_all(h));
   int32_t n = 0;
   if (!h->recs.empty()) {
@@ -1922,6 +1999,7 @@ merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t ro
   if (!h || !ms) return fail(h, MERAK_EINVAL, "NULL argument");
   if (h->T < 2 || h->nccl || h->f32 || h->local || h->inproc)
     return fail(h, MERAK_EUNSUPPORTED, "needs T > 1, peer comm across processes, bf16");
+  TRY(flush_ar2(h));
   if (rows <= 0 || rows > h->M || iters <= 0 || which < 0 || which > 2 || rows % h->G)
     return fail(h, MERAK_EINVAL, "bad rows / iters / which");
   TRY(sync_all(h));

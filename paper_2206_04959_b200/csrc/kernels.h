@@ -170,6 +170,13 @@ struct PeerSync {
   uint32_t *ctr;
 };
 
+// ones-column pads written per row by the LayerNorm kernels: element col[k] of row r of
+// ptr[k] (row stride ld[k]) = 1, the next 7 = 0, for k < n
+struct OnesPad {
+  __nv_bfloat16 *ptr[4];
+  int ld[4], col[4];
+  int n;
+};
 struct ArFwdArgs {
   const __nv_bfloat16 *partial[MAX_T];  // rank-ordered partial sums, rows [0, m) of this sub-batch
   int T;                                // number of partials summed (1 with NO_COMM)
@@ -177,8 +184,10 @@ struct ArFwdArgs {
   const __nv_bfloat16 *resid;           // [m, h]
   const __nv_bfloat16 *bias;            // [h]
   __nv_bfloat16 *out;                   // [m, h]   x1 (AR#1) or y (AR#2)
-  // LayerNorm of the stored (bf16) out, AR#1 only (u2 = LN2(x1))
+  // LayerNorm of the stored (bf16) out: AR#1 (u2 = LN2(x1)), or AR#2 of a chained layer fused with the next
+  // layer's LN1 (u = LN1'(y), with that layer's ones-column pads)
   bool do_ln;
+  OnesPad pad;
   const __nv_bfloat16 *gamma, *beta;
   __nv_bfloat16 *ln_out;
   int ld_ln;                            // row stride of ln_out
@@ -231,11 +240,6 @@ int ar_bwd_group_rows(int h);
 // Optionally writes the 8-wide pad [1, 0, ..., 0] at column pad_col[k] of rows of pad_ptr[k] (row
 // stride pad_ld[k]) for k < npad: the "ones column" of saved activations that turns each wgrad
 // GEMM into dW | db (bias gradient = dY^T 1).
-struct OnesPad {
-  __nv_bfloat16 *ptr[4];
-  int ld[4], col[4];
-  int n;
-};
 cudaError_t ln_fwd(const __nv_bfloat16 *x, const __nv_bfloat16 *g, const __nv_bfloat16 *b, __nv_bfloat16 *u,
                    int ld_u, float *mean, float *rstd, int m, int h, float eps, const OnesPad &pad, cudaStream_t st);
 

@@ -260,6 +260,14 @@ __global__ void __launch_bounds__(256, 2) ar_fwd_kernel(ArFwdArgs a, PeerSync ps
       for (int e = 0; e < 8; ++e) o[e] = (q[k][e] - mean) * rstd * gm[e] + bt[e];
       store8(a.ln_out + (size_t)row * a.ld_ln + c * 8, o);
     }
+    if (t < a.pad.n) {  // LN1 fused into a chained AR#2: the next layer's ones-column pads (as ln_fwd_kernel)
+      uint4 one;
+      one.x = pack_bf16(1.f, 0.f);
+      one.y = one.z = one.w = 0u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k == t) *reinterpret_cast<uint4 *>(a.pad.ptr[k] + (size_t)row * a.pad.ld[k] + a.pad.col[k]) = one;
+    }
     if (t == 0) {
       a.mean[row] = mean;
       a.rstd[row] = rstd;

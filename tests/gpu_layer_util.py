@@ -90,6 +90,7 @@ def run_gpu_chain(cfg, params_list, x, dy, T=1, rank=0, group=None, chain=True, 
     for k in range(K):
         layer.forward(ws[k], X if k == 0 else Ys[k - 1], Ys[k], saved[k], flags=f)
     if scratch is not None:  # nothing may depend on what the forwards left in the scratch buffer
+        layer.join()  # a chained forward's AR#2 epilogue (reads its saved x1) is launched by the next call / join
         torch.cuda.synchronize()
         scratch.fill_(0xFF)
     for k in reversed(range(K)):

@@ -47,3 +47,43 @@ def test_chained_layers_vs_oracle_and_unchained(n_sub):
     print({k: f"{v:.1e}" for k, v in errs.items()})
     bad = {k: v for k, v in errs.items() if not v <= TOL_BF16}
     assert not bad, bad
+
+
+def test_chained_ln1_fused_into_ar2(monkeypatch):
+    """in a chain, layer k+1's LN1 is computed by layer k's AR#2 epilogue kernel (launched
+    by the next call).  The fused LN1 uses the row engine's arithmetic on the stored bf16 y, so the stack is
+    bit-identical to MERAK_FUSE_LN1=0 (separate LN1 kernels), and the LN kernel launches drop by (K-1) n."""
+    import numpy as np
+    from gpu_layer_util import run_gpu_chain
+    from paper_2206_04959_b200 import FLAG_CHAIN, TmpLayer, shard_weights
+    K, n = 3, 2
+    cfg = CFG.with_(n_sub=n)
+    params = [make_params(cfg, layer=k) for k in range(K)]
+    x, dy = make_activations(cfg)
+    fused = run_gpu_chain(cfg, params, x, dy, chain=True)
+    monkeypatch.setenv("MERAK_FUSE_LN1", "0")
+    plain = run_gpu_chain(cfg, params, x, dy, chain=True)
+    assert torch.equal(fused["y"], plain["y"]) and torch.equal(fused["dx"], plain["dx"])
+    for k in range(K):
+        for name in fused["grads"][k]:
+            assert torch.equal(fused["grads"][k][name], plain["grads"][k][name]), (k, name)
+    # LN launches of a chained forward stack, per setting (profiling counts launches per kernel class)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    M, h = cfg.tokens, cfg.hidden
+    X = torch.as_tensor(np.asarray(x).reshape(M, h)).to(dev, torch.bfloat16)
+    counts = {}
+    for env in ("1", "0"):
+        monkeypatch.setenv("MERAK_FUSE_LN1", env)
+        lay = TmpLayer(cfg.hidden, cfg.heads, cfg.seq_len, cfg.microbatch, n_sub=n, device=dev.index)
+        ws = [shard_weights(p, cfg.heads, 1, 0, dev) for p in params]
+        Ys = [torch.empty_like(X) for _ in range(K)]
+        sv = [lay.new_saved() for _ in range(K)]
+        lay.set_profiling(True)
+        for k in range(K):
+            lay.forward(ws[k], X if k == 0 else Ys[k - 1], Ys[k], sv[k], flags=FLAG_CHAIN)
+        lay.join()
+        counts[env] = lay.get_profile()["layernorm"]["launches"]
+        torch.cuda.synchronize()
+        assert torch.equal(Ys[K - 1], fused["y"])
+        lay.close()
+    assert counts["0"] - counts["1"] == (K - 1) * n, counts
