@@ -120,12 +120,14 @@ enum {
   MERAK_FLAG_CHAIN = 1u,   /* do not join the caller stream at the end; the next merak call
                               on this handle (or merak_tmp_join) joins.  Lets layer k+1's first
                               sub-batch start while layer k's last all-reduce is in flight.
-                              On layer_fwd: the layer's AR#2 epilogue kernels,
-                              which write y, are launched by the next call on the handle -- fused
-                              with that layer's LN1 when it is a layer_fwd whose x is this y -- or
-                              by merak_tmp_join / merak_tmp_destroy.  Until then y is not written
-                              and the layer's weights and `saved` buffer must stay unchanged; a
-                              device synchronize does not complete y, merak_tmp_join does.       */
+                              With MERAK_FUSE_LN1=1 in the environment at init (SURVEY §8(a)
+                              F1/F8), a chained layer_fwd's AR#2s (handshakes and the epilogue
+                              kernels, which write y) are issued by the next call on the handle --
+                              fused with that layer's LN1 when it is a layer_fwd whose x is this y
+                              -- or by merak_tmp_join / merak_tmp_destroy.  Until then y is not
+                              written and the layer's weights and `saved` buffer must stay
+                              unchanged; a device synchronize does not complete y, merak_tmp_join
+                              does (profiling calls fail with ESTATE before it).                 */
   MERAK_FLAG_NO_COMM = 2u, /* measurement only: every all-reduce reads the local partial alone
                               (wrong result for T > 1); used to measure exposed communication.   */
   MERAK_FLAG_RECOMPUTE = 4u /* activation recomputation ("the recomputation ... could be
@@ -226,8 +228,8 @@ merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, con
                                  const void *saved, const void *dy, void *dx, const merak_tmp_grads *g,
                                  uint32_t flags, void *st);
 
-/* Join a MERAK_FLAG_CHAIN sequence: launch a chained forward's deferred AR#2 epilogues (see
- * MERAK_FLAG_CHAIN) and make `st` wait for every outstanding all-reduce. */
+/* Join a MERAK_FLAG_CHAIN sequence: issue a chained forward's deferred AR#2s (MERAK_FUSE_LN1=1, see
+ * MERAK_FLAG_CHAIN; collective then: every rank joins) and make `st` wait for every outstanding all-reduce. */
 merak_status merak_tmp_join(merak_tmp_t *h, void *st);
 
 /* Release all resources (synchronises the internal streams first).  NULL is a no-op. */

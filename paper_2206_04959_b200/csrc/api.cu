@@ -147,14 +147,15 @@ struct merak_tmp {
   char *ws32 = nullptr;
   float *dz32 = nullptr, *dx1_32 = nullptr, *dctx32 = nullptr, *dqkv32 = nullptr, *delta32 = nullptr, *du32 = nullptr;
   struct InprocGroup *grp = nullptr;  // MERAK_COMM_INPROC: the group this rank belongs to
-  // LN1 fused into a chained AR#2: a forward with MERAK_FLAG_CHAIN leaves its AR#2 epilogue
-  // kernels unlaunched (handshakes done); the next call on the handle launches them first -- computing the next
-  // layer's LN1 as well when that call is a forward on y.  MERAK_FUSE_LN1=0 disables.
-  bool fuse_ln1 = true;
-  bool ar2_pending = false;
+  // LN1 fused into a chained AR#2: a forward with MERAK_FLAG_CHAIN leaves its AR#2s
+  // (handshakes and epilogue kernels) unissued; the next call on the handle issues them first -- computing the
+  // next layer's LN1 in the epilogues when that call is a forward on y.  Opt-in (MERAK_FUSE_LN1=1): measured
+  // 1-5 % slower than LN1 on the compute stream (profiles/r02/fuse_ln1_ab.txt), the LN work lands on the
+  // communication stream's critical path.
+  bool fuse_ln1 = false;
+  bool ar2_pending = false, ar2_comm = false;
   const bf16 *ar2_y = nullptr;
   ArFwdArgs ar2_a[MAXN_];
-  PeerSync ar2_ps[MAXN_];
   cudaEvent_t ev_hs[2] = {};          // INPROC: this rank's handshake points (alternating generations)
 };
 
@@ -537,11 +538,30 @@ static OnesPad ln1_pads(const merak_tmp_t *h, const SavedLayout &L, char *saved,
   return pad;
 }
 
-// Launch the deferred AR#2 epilogues of the previous chained forward (in sub-batch order, on the
-// communication stream, right behind their handshakes).  With w / saved: the layer being entered runs on
-// their output y, so each epilogue also computes that layer's LN1 (u, mean1, rstd1 and the ones-column pads
+// AR#2 of sub-batch j (F8): after fc2(j), the handshake (two-shot: phase 1 + second handshake), then the
+// epilogue kernel y = x1 + sum of partials + b_2 -- with do_ln set by the caller, also the next layer's LN1.
+static merak_status ar2_issue(merak_tmp_t *h, int j, ArFwdArgs a, bool comm) {
+  const size_t r0 = (size_t)j * (h->M / h->n);
+  CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
+  if (comm && h->nccl) TRY(nccl_allreduce(h, slot_ptr(h, h->r, 1) + r0 * h->h, (size_t)a.m * h->h));
+  PeerSync ps = make_sync(h, comm);
+  TRY(sync_peers(h, ps));
+  if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 1, r0, a.m, a.resid, a.bias, &a.chunk, &ps));
+  {
+    Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
+    a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
+    CK(h, ar_fwd(a, ps, h->ms));
+  }
+  CK(h, cudaEventRecord(h->ev_ar[1][j], h->ms));
+  h->ev_ar_valid[1][j] = true;
+  return MERAK_OK;
+}
+
+// Issue the deferred AR#2 of the previous chained forward (every sub-batch in order, each handshake right
+// before its epilogue, so AR#2(j) still waits only for fc2(j)).  With w / saved: the layer being entered runs
+// on their output y, so each epilogue also computes that layer's LN1 (u, mean1, rstd1 and the ones-column pads
 // of its rows in `saved`) -- the same row-engine arithmetic as ln_fwd_kernel on the stored bf16 y, so the
-// result is bit-identical to the unfused LN1.
+// result is bit-identical to the unfused LN1.  A collective step: every rank flushes at its matching call.
 static merak_status flush_ar2(merak_tmp_t *h, const merak_tmp_weights *w = nullptr, char *saved = nullptr) {
   if (!h->ar2_pending) return MERAK_OK;
   h->ar2_pending = false;
@@ -558,12 +578,7 @@ static merak_status flush_ar2(merak_tmp_t *h, const merak_tmp_weights *w = nullp
       a.eps = h->eps;
       a.pad = ln1_pads(h, L, saved, r0);
     }
-    {
-      Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
-      CK(h, ar_fwd(a, h->ar2_ps[j], h->ms));
-    }
-    CK(h, cudaEventRecord(h->ev_ar[1][j], h->ms));
-    h->ev_ar_valid[1][j] = true;
+    TRY(ar2_issue(h, j, a, h->ar2_comm));
   }
   return MERAK_OK;
 }
@@ -657,32 +672,20 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     g.out = slot_ptr(h, h->r, 1) + r0 * hh; g.ldo = hh;
     TRY(run_gemm(h, g, cst));
     CK(h, cudaEventRecord(h->ev_p[j], cst));
-    CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
-    {
-      ArFwdArgs a;
-      memset(&a, 0, sizeof(a));
-      if (comm && h->nccl) TRY(nccl_allreduce(h, slot_ptr(h, h->r, 1) + r0 * hh, (size_t)m * hh));
-      a.T = ar_partials(h, comm, 1, r0, a.partial);
-      a.m = m; a.h = hh; a.resid = (const bf16 *)S(L.x1) + r0 * hh; a.bias = (const bf16 *)w->b_2;
-      a.out = y + r0 * hh; a.do_ln = false; a.ctas = h->cfg.comm_ctas;
-      PeerSync ps = make_sync(h, comm);
-      TRY(sync_peers(h, ps));
-      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 1, r0, m, a.resid, a.bias, &a.chunk, &ps));
-      if (defer_ar2) {  // launched by the next call (flush_ar2), possibly with the next layer's LN1
-        a.pdl = false;
-        h->ar2_a[j] = a;
-        h->ar2_ps[j] = ps;
-        continue;
-      }
-      Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
-      a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
-      CK(h, ar_fwd(a, ps, h->ms));
+    ArFwdArgs a;
+    memset(&a, 0, sizeof(a));
+    a.T = ar_partials(h, comm, 1, r0, a.partial);
+    a.m = m; a.h = hh; a.resid = (const bf16 *)S(L.x1) + r0 * hh; a.bias = (const bf16 *)w->b_2;
+    a.out = y + r0 * hh; a.do_ln = false; a.ctas = h->cfg.comm_ctas;
+    if (defer_ar2) {  // issued by the next call (flush_ar2), possibly with the next layer's LN1
+      h->ar2_a[j] = a;
+      continue;
     }
-    CK(h, cudaEventRecord(h->ev_ar[1][j], h->ms));
-    h->ev_ar_valid[1][j] = true;
+    TRY(ar2_issue(h, j, a, comm));
   }
   if (defer_ar2) {
     h->ar2_pending = true;
+    h->ar2_comm = comm;
     h->ar2_y = y;
   }
   if (recompute) {
@@ -1423,6 +1426,7 @@ static merak_status sync_all(merak_tmp_t *h) {
 // In-process group: keep rank h->r's call until every rank has made its matching call, then issue all of
 // them as coroutines of this thread (InprocGroup).  The call that completes the set returns the first
 // failure of the set (named by rank); the earlier callers got MERAK_OK.
+static merak_status group_run(InprocGroup *g, merak_tmp_t *h);
 static merak_status group_issue(merak_tmp_t *h, std::function<merak_status()> fn) {
   InprocGroup *g = h->grp;
   if (g->running) return fail(h, MERAK_ESTATE, "layer call re-entered during an in-process group issue");
@@ -1432,6 +1436,12 @@ static merak_status group_issue(merak_tmp_t *h, std::function<merak_status()> fn
                 "made the first", h->r);
   g->pending[h->r] = std::move(fn);
   if (++g->npending < g->T) return MERAK_OK;
+  return group_run(g, h);
+}
+
+// Run every rank's pending call of the group as coroutines of this thread; the first failure is reported
+// on h (named by rank).
+static merak_status group_run(InprocGroup *g, merak_tmp_t *h) {
   for (int r = 0; r < g->T; ++r) {
     if (!g->stack[r]) g->stack[r] = (char *)malloc(kCoStack);
     if (!g->stack[r]) return fail(h, MERAK_ENOMEM, "coroutine stack");
@@ -1468,6 +1478,14 @@ static merak_status group_issue(merak_tmp_t *h, std::function<merak_status()> fn
     }
   }
   return st;
+}
+
+// Per-rank (non-collective) calls cannot issue a chained forward's deferred AR#2s (their handshakes are
+// collective): they need merak_tmp_join first.
+static merak_status chain_closed_ar2(merak_tmp_t *h) {
+  if (h->ar2_pending)
+    return fail(h, MERAK_ESTATE, "a MERAK_FLAG_CHAIN forward's all-reduce is still open: call merak_tmp_join first");
+  return MERAK_OK;
 }
 
 // Calls that act on a handle's streams at once must not overtake its deferred layer call.
@@ -1855,23 +1873,38 @@ merak_status merak_tmp_layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, con
 
 merak_status merak_tmp_join(merak_tmp_t *h, void *st) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
-  TRY(group_idle(h));
-  TRY(flush_ar2(h));
-  if (!h->have_prev) return MERAK_OK;
-  TRY(wait_all(h, (cudaStream_t)st));
-  for (int j = 0; j < h->n; ++j) CK(h, cudaStreamWaitEvent((cudaStream_t)st, h->prev_out[j], 0));
-  h->chain_open = false;
-  return check_async_error(h);  // a watchdog that already fired (the word is host-mapped; no sync here)
+  auto body = [h, st]() -> merak_status {
+    TRY(flush_ar2(h));  // a chained forward's deferred AR#2s (collective: every rank joins)
+    if (!h->have_prev) return MERAK_OK;
+    TRY(wait_all(h, (cudaStream_t)st));
+    for (int j = 0; j < h->n; ++j) CK(h, cudaStreamWaitEvent((cudaStream_t)st, h->prev_out[j], 0));
+    h->chain_open = false;
+    return check_async_error(h);  // a watchdog that already fired (the word is host-mapped; no sync here)
+  };
+  // in-process group with deferred AR#2s: their handshakes need every rank, so the join is a group call
+  return (h->grp && h->ar2_pending) ? group_issue(h, body) : body();
 }
 
 merak_status merak_tmp_destroy(merak_tmp_t *h) {
-  if (h) {  // an open chain's last AR#2 epilogues: y is an output the caller may still read
+  if (h && h->ar2_pending) {  // an open chain's last AR#2s: y is an output the caller may still read
     cudaSetDevice(h->dev);
-    if (h->grp) {  // in-process group: while every rank's slots still exist
-      for (int q = 0; q < h->grp->T; ++q)
-        if (h->grp->hs[q]) flush_ar2(h->grp->hs[q]);
-    } else {
-      flush_ar2(h);
+    InprocGroup *g = h->grp;
+    if (g && !g->running && g->alive == g->T) {  // every rank at once, while every rank's slots exist
+      bool any = false;
+      for (int q = 0; q < g->T; ++q) {
+        merak_tmp_t *hq = g->hs[q];
+        g->pending[q] = [hq]() { return flush_ar2(hq); };
+        any = any || hq->ar2_pending;
+      }
+      g->npending = g->T;
+      if (any) {
+        group_run(g, h);
+      } else {
+        for (int q = 0; q < g->T; ++q) g->pending[q] = nullptr;
+        g->npending = 0;
+      }
+    } else if (!g) {
+      flush_ar2(h);  // PEER / NCCL: each rank flushes in its own destroy, before the final barrier
     }
   }
   if (h && h->inproc) {
@@ -1902,7 +1935,7 @@ const char *merak_tmp_last_error(const merak_tmp_t *h) { return h ? h->err.c_str
 merak_status merak_tmp_set_profiling(merak_tmp_t *h, int32_t on) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
   TRY(group_idle(h));
-  TRY(flush_ar2(h));
+  TRY(chain_closed_ar2(h));
   TRY(sync_all(h));
   h->prof = on != 0;
   h->recs.clear();
@@ -1918,7 +1951,7 @@ merak_status merak_tmp_set_profiling(merak_tmp_t *h, int32_t on) {
 merak_status merak_tmp_get_profile(merak_tmp_t *h, double *ms, int64_t *launches, double *flops) {
   if (!h) return fail(nullptr, MERAK_EINVAL, "handle is NULL");
   TRY(group_idle(h));
-  TRY(flush_ar2(h));
+  TRY(chain_closed_ar2(h));
   TRY(sync_all(h));
   for (auto &r : h->recs) {
     float t = 0;
@@ -1940,7 +1973,7 @@ merak_status merak_tmp_get_timeline(merak_tmp_t *h, int32_t cap, int32_t *count,
                                     float *t0, float *t1) {
   if (!h || !count) return fail(h, MERAK_EINVAL, "NULL argument");
   TRY(group_idle(h));
-  TRY(flush_ar2(h));
+  TRY(chain_closed_ar2(h));
   TRY(sync_all(h));
   int32_t n = 0;
   if (!h->recs.empty()) {
@@ -1999,7 +2032,7 @@ merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t ro
   if (!h || !ms) return fail(h, MERAK_EINVAL, "NULL argument");
   if (h->T < 2 || h->nccl || h->f32 || h->local || h->inproc)
     return fail(h, MERAK_EUNSUPPORTED, "needs T > 1, peer comm across processes, bf16");
-  TRY(flush_ar2(h));
+  TRY(chain_closed_ar2(h));
   if (rows <= 0 || rows > h->M || iters <= 0 || which < 0 || which > 2 || rows % h->G)
     return fail(h, MERAK_EINVAL, "bad rows / iters / which");
   TRY(sync_all(h));

@@ -51,8 +51,9 @@ def test_chained_layers_vs_oracle_and_unchained(n_sub):
 
 def test_chained_ln1_fused_into_ar2(monkeypatch):
     """in a chain, layer k+1's LN1 is computed by layer k's AR#2 epilogue kernel (launched
-    by the next call).  The fused LN1 uses the row engine's arithmetic on the stored bf16 y, so the stack is
-    bit-identical to MERAK_FUSE_LN1=0 (separate LN1 kernels), and the LN kernel launches drop by (K-1) n."""
+    by the next call; opt-in MERAK_FUSE_LN1=1).  The fused LN1 uses the row engine's arithmetic on the stored
+    bf16 y, so the stack is bit-identical to MERAK_FUSE_LN1=0 (separate LN1 kernels), and the LN kernel
+    launches drop by (K-1) n."""
     import numpy as np
     from gpu_layer_util import run_gpu_chain
     from paper_2206_04959_b200 import FLAG_CHAIN, TmpLayer, shard_weights
@@ -60,6 +61,7 @@ def test_chained_ln1_fused_into_ar2(monkeypatch):
     cfg = CFG.with_(n_sub=n)
     params = [make_params(cfg, layer=k) for k in range(K)]
     x, dy = make_activations(cfg)
+    monkeypatch.setenv("MERAK_FUSE_LN1", "1")
     fused = run_gpu_chain(cfg, params, x, dy, chain=True)
     monkeypatch.setenv("MERAK_FUSE_LN1", "0")
     plain = run_gpu_chain(cfg, params, x, dy, chain=True)
