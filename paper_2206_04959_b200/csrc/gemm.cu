@@ -56,10 +56,12 @@ struct EpiParams {
   float *db32;  // EPI_ACC_F32: column n_main (the ones column of B) accumulates into db32[m]
   int n_main;
   int *tile_ctr;  // dynamic tile scheduler counter (zero between launches), nullptr = static schedule
+  int group_m;    // m-tiles per raster band (tile_coords): 1 = n fastest over all of N, tiles_m = m fastest
+  int hint_a, hint_b, hint_c;  // L2 eviction priority of the A / B TMA loads and the fp32 C accesses (l2_policy)
 };
 
 template <int EPI>
-MK_DEV void epi_store_chunk(const EpiParams &p, int gm, int gn0, const uint32_t (&r)[32]) {
+MK_DEV void epi_store_chunk(const EpiParams &p, int gm, int gn0, const uint32_t (&r)[32], uint64_t pol_c = 0) {
   if constexpr (EPI == 5) {  // microbenchmark variant: drain TMEM, store nothing
     if (r[0] == 0x7fc00001u && gm < 0) p.out[0] = __float2bfloat16_rn(0.f);
     return;
@@ -72,7 +74,12 @@ MK_DEV void epi_store_chunk(const EpiParams &p, int gm, int gn0, const uint32_t 
     float *dst = p.out32 + (size_t)gm * p.ld32 + gn0;
     if (gn0 + 32 <= p.n_main && (p.ld32 % 4 == 0)) {
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      for (int i = 0; i < 32; i += 4) {
+        if (p.hint_c)
+          stg_f4_hint(dst + i, make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]), pol_c);
+        else
+          *reinterpret_cast<float4 *>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
     } else {
       for (int i = 0; i < 32; ++i) {
         if (gn0 + i < p.n_main) dst[i] = v[i];
@@ -143,16 +150,16 @@ MK_DEV void epi_store_chunk(const EpiParams &p, int gm, int gn0, const uint32_t 
   }
 }
 
-// Tile raster: bands of GROUP_M m-tiles, n-major inside a band (m fastest within a group column), so the
-// ~74 tiles a persistent wave runs at once cover a compact block of about 8 x 9 tiles and share their A and B
-// k-slabs in L2 (m-fastest order over all of M made every wave of the wgrad GEMMs -- M' = 24576 rows -- stream
-// 74 distinct A panels: 4x the algorithmic DRAM bytes).  The order never changes a tile's K reduction.
-constexpr int GROUP_M = 8;
-MK_DEV void tile_coords(int tile, int tiles_m, int tiles_n, int &tm, int &tn) {
-  const int band = tile / (GROUP_M * tiles_n);
-  const int m0 = band * GROUP_M;
-  const int gm = min(GROUP_M, tiles_m - m0);  // last band may be narrower
-  const int r = tile - band * GROUP_M * tiles_n;
+// Tile raster: bands of group_m m-tiles, n-major inside a band (m fastest within a group column).  The host
+// picks group_m per GEMM (pick_group_m): when one operand fits in L2 the band makes it the one every wave
+// shares -- group_m = tiles_m keeps all of A resident while B streams through once, group_m = 1 keeps all of B
+// resident while A streams once -- otherwise bands of 8 make each ~74-tile wave a compact ~8 x 9 block sharing
+// its A and B k-slabs.  The order never changes a tile's K reduction.
+MK_DEV void tile_coords(int tile, int tiles_m, int tiles_n, int group_m, int &tm, int &tn) {
+  const int band = tile / (group_m * tiles_n);
+  const int m0 = band * group_m;
+  const int gm = min(group_m, tiles_m - m0);  // last band may be narrower
+  const int r = tile - band * group_m * tiles_n;
   tm = m0 + r % gm;
   tn = r / gm;
 }
@@ -261,12 +268,13 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer (both CTAs of a pair load their own halves)
+    const uint64_t pol_a = l2_policy(p.hint_a), pol_b = l2_policy(p.hint_b);
     int it = 0;
     for (int lt = 0;; ++lt) {
       const int tile = (rank == 0) ? fetch(lt) : consume(lt);
       if (tile >= ntiles) break;
       int tm, tn;
-      tile_coords(tile, tiles_m, tiles_n, tm, tn);
+      tile_coords(tile, tiles_m, tiles_n, p.group_m, tm, tn);
       const int row0 = tm * BMT + rank * BM;
       const int n0 = tn * BN + rank * C::BNC;
       for (int kb = 0; kb < nk; ++kb, ++it) {
@@ -277,23 +285,26 @@ __global__ void __launch_bounds__(256, 1)
           if (rank == 0) mbar_expect_tx(&full[s], C::STAGE_BYTES * CG);
           uint8_t *a = smA + s * C::A_BYTES;
           uint8_t *b = smB + s * C::B_BYTES;
-          auto load = [&](void *dst, const CUtensorMap *m, int c0, int c1) {
-            if constexpr (CG == 2)
-              tma_load_2d_cg2(dst, m, &full[s], c0, c1);
-            else
-              tma_load_2d(dst, m, &full[s], c0, c1);
+          auto load = [&](void *dst, const CUtensorMap *m, int c0, int c1, int hint, uint64_t pol) {
+            if constexpr (CG == 2) {
+              if (hint) tma_load_2d_cg2_hint(dst, m, &full[s], c0, c1, pol);
+              else tma_load_2d_cg2(dst, m, &full[s], c0, c1);
+            } else {
+              if (hint) tma_load_2d_hint(dst, m, &full[s], c0, c1, pol);
+              else tma_load_2d(dst, m, &full[s], c0, c1);
+            }
           };
           if constexpr (!A_MN) {
-            load(a, &tmA, kb * BK, row0);
+            load(a, &tmA, kb * BK, row0, p.hint_a, pol_a);
           } else {
 #pragma unroll
-            for (int c = 0; c < BM / 64; ++c) load(a + c * 8192, &tmA, row0 + c * 64, kb * BK);
+            for (int c = 0; c < BM / 64; ++c) load(a + c * 8192, &tmA, row0 + c * 64, kb * BK, p.hint_a, pol_a);
           }
           if constexpr (!B_MN) {
-            load(b, &tmB, kb * BK, n0);
+            load(b, &tmB, kb * BK, n0, p.hint_b, pol_b);
           } else {
 #pragma unroll
-            for (int c = 0; c < C::BNC / 64; ++c) load(b + c * 8192, &tmB, n0 + c * 64, kb * BK);
+            for (int c = 0; c < C::BNC / 64; ++c) load(b + c * 8192, &tmB, n0 + c * 64, kb * BK, p.hint_b, pol_b);
           }
         }
         __syncwarp();
@@ -340,6 +351,7 @@ __global__ void __launch_bounds__(256, 1)
     // ---------------- epilogue (each CTA drains its own 128 TMEM lanes = its 128 rows of the tile)
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const uint32_t row_base = tmem_base + ((uint32_t)(q * 32) << 16);
+    const uint64_t pol_c = l2_policy(p.hint_c);
     const uint32_t tfree_leader[2] = {CG == 2 ? mapa_shared(&tfree[0], 0) : 0u,
                                       CG == 2 ? mapa_shared(&tfree[1], 0) : 0u};
     auto release = [&](int buf) {
@@ -354,7 +366,7 @@ __global__ void __launch_bounds__(256, 1)
     };
     auto preload = [&](int tile, int buf) {
       int tm, tn;
-      tile_coords(tile, tiles_m, tiles_n, tm, tn);
+      tile_coords(tile, tiles_m, tiles_n, p.group_m, tm, tn);
       const int gm = tm * BMT + rank * BM + q * 32 + lane;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
@@ -364,7 +376,7 @@ __global__ void __launch_bounds__(256, 1)
         if (gm < p.M && gn0 + 32 <= p.n_main && (p.ld32 % 4 == 0)) {
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
-            float4 f = *reinterpret_cast<const float4 *>(src + i);
+            const float4 f = p.hint_c ? ldg_f4_hint(src + i, pol_c) : *reinterpret_cast<const float4 *>(src + i);
             r[i] = __float_as_uint(f.x); r[i + 1] = __float_as_uint(f.y);
             r[i + 2] = __float_as_uint(f.z); r[i + 3] = __float_as_uint(f.w);
           }
@@ -418,7 +430,7 @@ __global__ void __launch_bounds__(256, 1)
       mbar_wait(&tfull[buf], (lt >> 1) & 1);
       tc_fence_after();
       int tm, tn;
-      tile_coords(tile, tiles_m, tiles_n, tm, tn);
+      tile_coords(tile, tiles_m, tiles_n, p.group_m, tm, tn);
       const int gm = tm * BMT + rank * BM + q * 32 + lane;
       if constexpr (EPI == EPI_ACC_F32 || EPI == 5) {
 #pragma unroll 1
@@ -428,7 +440,7 @@ __global__ void __launch_bounds__(256, 1)
           uint32_t r[32];
           tmem_ld32(row_base + buf * BN + c * 32, r);
           tmem_ld_wait();
-          if (gm < p.M) epi_store_chunk<EPI>(p, gm, gn0, r);
+          if (gm < p.M) epi_store_chunk<EPI>(p, gm, gn0, r, pol_c);
         }
       } else {
         const int grow0 = tm * BMT + rank * BM + q * 32;
@@ -633,6 +645,20 @@ static int pick_bn(const GemmArgs &a, int cg) {
   return best;
 }
 
+// Raster band height (tile_coords): 8 m-tiles.  Measured (profiles/r02/gemm_raster.txt): bands spanning all of
+// M or N to keep the smaller operand L2-resident moved MORE DRAM bytes (the ~100 MB operand does not survive
+// the streamed one and the fp32 accumulator tiles) and lowered the power-capped clock.
+static int pick_group_m(const GemmArgs &a, int cg) {
+  const int tiles_m = (a.M + BM * cg - 1) / (BM * cg);
+  static int env = -2;
+  if (env == -2) {
+    const char *e = getenv("MERAK_GEMM_GROUP_M");  // measurement override: 0 = auto
+    env = e ? atoi(e) : 0;
+  }
+  if (env > 0) return env < tiles_m ? env : tiles_m;
+  return tiles_m < 8 ? tiles_m : 8;
+}
+
 static int gemm_cg() {
   static int cg = 0;
   if (!cg) {
@@ -701,6 +727,16 @@ cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
   p.out32 = a.out32; p.ld32 = a.ld32;
   p.db32 = a.db32;
   p.tile_ctr = a.tile_ctr;
+  p.group_m = pick_group_m(a, cg);
+  {  // L2 eviction priorities (measurement switch MERAK_GEMM_HINT="abc", digits 0 none / 1 first / 2 last)
+    static int hint = -1;
+    if (hint < 0) {
+      const char *e = getenv("MERAK_GEMM_HINT");
+      hint = (e && strlen(e) == 3) ? (e[0] - '0') * 100 + (e[1] - '0') * 10 + (e[2] - '0') : 0;
+    }
+    p.hint_a = hint / 100 % 10; p.hint_b = hint / 10 % 10; p.hint_c = hint % 10;
+    if (a.epi != EPI_ACC_F32) p.hint_c = 0;
+  }
   if (!p.tile_ctr) {  // test entry points: MERAK_GEMM_DYN=1 selects the dynamic schedule on a global counter
     const char *e = getenv("MERAK_GEMM_DYN");
     if (e && atoi(e) == 1) {
