@@ -9,7 +9,7 @@ for H in $HS; do
   MERAK_GEMM_HINT=$H timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none --csv --log-file gpurun_out/launches_h$H.csv $CMD > gpurun_out/ncu_h$H.log 2>&1
 done
-for i in 1 2; do
+for i in $(seq 1 ${R:-2}); do
   for H in $HS; do
     MERAK_GEMM_HINT=$H timeout 600 python bench.py --no-extras --no-cpu-baseline --steps 10 --warmup 3 > gpurun_out/hab_${H}_$i.json 2>> gpurun_out/hab.err
   done
