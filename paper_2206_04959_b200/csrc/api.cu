@@ -188,7 +188,7 @@ struct InprocGroup {
   uint64_t rec_gen[MAX_T] = {};  // generation of each rank's latest handshake event (+1; 0 = none)
 };
 static constexpr size_t kCoStack = 8u << 20;  // per-rank coroutine stack (the CUDA runtime's launch path is deep)
-static InprocGroup *g_co_group = nullptr;     // the group whose coroutines this thread is running
+static thread_local InprocGroup *g_co_group = nullptr;  // the group whose coroutines this thread is running
 
 static void co_entry() {
   InprocGroup *g = g_co_group;
