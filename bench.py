@@ -383,6 +383,8 @@ def main():
             stage("nvls pass done")
             extras["seq_parallel"] = seqpar_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step)
             stage("seq-parallel pass done")
+            extras["push"] = push_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step)
+            stage("push pass done")
             extras["pipeline"] = pipeline_pass(args, rank, world, dev, barrier, max_over_ranks)
             stage("pipeline pass done")
 
@@ -571,6 +573,45 @@ def seqpar_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step):
     return {"tflops_per_gpu": L * layer_flops(cfg) / T / (ms * 1e-3) / 1e12, "ms_per_step": ms,
             "vs_replicated": ms_step / ms,
             "note": "x / y / dx / dy token-sharded by T; the LN / residual epilogues run on the own rows"}
+
+
+def push_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step):
+    """SURVEY §8(f) NEXT-2, tile-granular fusion (MERAK_AR_PUSH=1): the row-parallel GEMMs (proj, fc2, fc1 / QKV
+    dgrad) store each 32-row output box straight into the owner rank's slot over NVLink, so the reduce-scatter
+    phase (two-shot phase 1, or the sequence-parallel reduce-scatter) reads only local HBM.  Per-GPU TFLOP/s of
+    the replicated two-shot and the sequence-parallel layouts next to the main line."""
+    from paper_2206_04959_b200 import FLAG_NO_COMM, MerakError
+    nx = max(3, args.steps // 2)
+    keep = {k: os.environ.get(k) for k in ("MERAK_AR_PUSH", "MERAK_AR_TWO_SHOT")}
+    os.environ["MERAK_AR_PUSH"] = "1"
+    os.environ["MERAK_AR_TWO_SHOT"] = "1"
+    out = {}
+    try:
+        for name, sp in (("two_shot", False), ("seq_parallel", True)):
+            try:
+                st = Stack(cfg, L, T, rank, dev, group, n_sub, comm_ctas=args.comm_ctas, seq_parallel=sp)
+            except MerakError as e:
+                out[name] = {"unavailable": str(e)}
+                continue
+            for _ in range(3):
+                st.step()
+            ms, _, _ = timed(st, nx)
+            r = {"tflops_per_gpu": L * layer_flops(cfg) / T / (ms * 1e-3) / 1e12, "ms_per_step": ms,
+                 "vs_main": ms_step / ms, "push_active": st.layer.debug_host()["push"]}
+            if not sp:
+                ms_nc, _, _ = timed(st, nx, flags=FLAG_NO_COMM)
+                r["exposed_allreduce_ms_per_layer"] = (ms - ms_nc) / L
+                r["exposed_allreduce_frac"] = (ms - ms_nc) / ms
+            st.close()
+            out[name] = r
+    finally:
+        for k, v in keep.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    out["note"] = "row-parallel GEMM epilogues push 32-row boxes to the owner's slot (TMA store via peer tensor maps)"
+    return out
 
 
 def pipeline_pass(args, rank, world, dev, barrier, max_over_ranks, K=2, layer_cfg="gpt1.5b"):

@@ -281,7 +281,10 @@ merak_status merak_tmp_debug_state(const merak_tmp_t *h, int32_t *out);
 
 /* Host-memory-only part of the diagnostics (no CUDA call, so it cannot block behind a launch):
  * out[0..4] = watchdog error word, out[5] = handshake epoch, out[6] = launches enqueued so far,
- * out[7..11] = traced launches enqueued per stream (cs, cs1, cw, cr, ms; MERAK_DEBUG_TRACE=1). */
+ * out[7..11] = traced launches enqueued per stream (cs, cs1, cw, cr, ms; MERAK_DEBUG_TRACE=1), out[12] = 1 when
+ * the fused GEMM -> reduce-scatter push is set up (env MERAK_AR_PUSH=1 at init, PEER / INPROC, T > 1, bf16; it
+ * applies to calls whose owner row blocks B*s/(n T) are whole 32-row boxes, in the sequence-parallel layout or
+ * with the two-shot all-reduce), out[13] = 1 when the two-shot all-reduce is selected.  out has 14 entries. */
 merak_status merak_tmp_debug_host(const merak_tmp_t *h, int32_t *out);
 
 #ifdef __cplusplus

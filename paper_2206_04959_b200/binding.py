@@ -313,10 +313,11 @@ class TmpLayer:
 
     def debug_host(self) -> dict:
         """Host-memory-only diagnostics (never blocks)."""
-        o = (ctypes.c_int32 * 12)()
+        o = (ctypes.c_int32 * 14)()
         lib().merak_tmp_debug_host(self.h, o)
         return {"err": list(o[0:5]), "epoch": o[5], "launches": o[6],
-                "traced": dict(zip(("cs", "cs1", "cw", "cr", "ms"), list(o[7:12])))}
+                "traced": dict(zip(("cs", "cs1", "cw", "cr", "ms"), list(o[7:12]))),
+                "push": bool(o[12]), "two_shot": bool(o[13])}
 
     def launch_count(self) -> int:
         return lib().merak_tmp_launch_count(self.h)

@@ -129,6 +129,11 @@ struct merak_tmp {
   Nvls nvls = {};
   bool fused_wait = false;  // two-shot: phase-1 kernel publishes, phase-2 kernel waits in kernel (env MERAK_AR_FUSED_WAIT)
   bool two_shot = false;  // T >= 4: reduce-scatter + all-gather instead of one-shot (env MERAK_AR_TWO_SHOT)
+  // Fused GEMM -> reduce-scatter push (env MERAK_AR_PUSH): the row-parallel GEMMs (proj,
+  // fc2, fc1 dgrad, QKV dgrad) store each 32-row output box straight into the slot of the rank that owns the
+  // rows (TMA store through a peer tensor map), so the reduce-scatter phase reads only local HBM.
+  bool push_req = false, push = false;
+  void *push_maps = nullptr;  // device: [4 row-parallel slots][T owners] CUtensorMap (128 B each)
   bool pdl = false;       // programmatic dependent launch along the all-reduce kernel chain (env MERAK_AR_PDL)
   int gemm_smem_kb = 192;  // GEMM TMA ring: 160 KB at T > 1 leaves smem for co-resident all-reduce kernels
   // MERAK_DEBUG_TRACE=1: an event after every launch, per stream (cs, cs1, cw, cr, ms), in a 64-deep ring, so
@@ -406,12 +411,34 @@ static merak_status sync_peers(merak_tmp_t *h, const PeerSync &ps, cudaStream_t 
 // from its owner's slot ("gathered" mode).  NVLink bytes per rank: 2(T-1)/T of a slot instead of
 // (T-1) for one-shot.  Returns the chunk (rows per owner) for the epilogue kernel.
 static bool two_shot_on(merak_tmp_t *h, bool comm) { return comm && h->T > 1 && !h->nccl && h->two_shot; }
+// Push layout of a row-parallel slot (h->push, sequence parallel or two-shot, every owner's rows a whole number of
+// 32-row boxes): the m rows of sub-batch region r0 in OWNER q's slot hold, at rows [p*m/T, (p+1)*m/T), source
+// rank p's partial of q's rows; the reduce-scatter phase then sums T local row blocks in rank order (the same
+// arithmetic as pulling them from the peers' slots, so results are bit-identical).
+static bool push_on(merak_tmp_t *h, bool comm, int m) {
+  return h->push && comm && (h->sp || two_shot_on(h, comm)) && m % h->T == 0 && (m / h->T) % 32 == 0;
+}
+// Output of a row-parallel GEMM into slot `slot`, sub-batch rows from r0: own slot, or pushed to the owners.
+static void slot_out(merak_tmp_t *h, GemmArgs &g, bool comm, int slot, size_t r0, int m) {
+  g.out = slot_ptr(h, h->r, slot) + r0 * h->h;
+  g.ldo = h->h;
+  if (push_on(h, comm, m)) {
+    g.scatter = reinterpret_cast<const char *>(h->push_maps) + (size_t)slot * h->T * 128;
+    g.scatter_rows = m / h->T;
+    g.scatter_row0 = (int)r0 + h->r * g.scatter_rows;
+  }
+}
+// Partial q of the own rows [r0 + r*m/T, ...) (sequence parallel) / owner rows (two-shot phase 1) of slot `slot`
+static const bf16 *own_partial(merak_tmp_t *h, bool pushed, int slot, size_t r0, int q, int rows_per) {
+  if (pushed) return slot_ptr(h, h->r, slot) + (r0 + (size_t)q * rows_per) * h->h;
+  return slot_ptr(h, q, slot) + (r0 + (size_t)h->r * rows_per) * h->h;
+}
 // With h->fused_wait the second handshake kernel disappears: the phase-1 kernel's last CTA publishes the epoch
 // and the phase-2 epilogue kernel waits for the peers' epochs in kernel (*wait_ps, PeerSync::wait).  Safe from
 // the deadlock of DESIGN.md §7: the waiting kernel depends only on the peers' phase-1 kernels, which precede
 // their own phase-2 kernels on their communication streams and never wait themselves.
 static merak_status two_shot_rs(merak_tmp_t *h, int slot, size_t r0, int m, const bf16 *resid, const bf16 *bias,
-                                int *chunk, PeerSync *wait_ps) {
+                                int *chunk, PeerSync *wait_ps, bool pushed = false) {
   const int c = (m + h->T - 1) / h->T;
   PeerSync pub = make_sync(h, true);
   pub.publish = h->fused_wait;
@@ -445,7 +472,10 @@ static merak_status two_shot_rs(merak_tmp_t *h, int slot, size_t r0, int m, cons
   }
   ArRsArgs a;
   memset(&a, 0, sizeof(a));
-  for (int q = 0; q < h->T; ++q) a.partial[q] = slot_ptr(h, q, slot) + r0 * h->h;
+  // pull: partial q = rank q's slot (rows row0.. read over NVLink); pushed: the T local row blocks (push_on)
+  for (int q = 0; q < h->T; ++q)
+    a.partial[q] = pushed ? slot_ptr(h, h->r, slot) + ((ptrdiff_t)r0 + (ptrdiff_t)(q - h->r) * c) * h->h
+                          : slot_ptr(h, q, slot) + r0 * h->h;
   a.T = h->T; a.h = h->h;
   a.row0 = h->r * c < m ? h->r * c : m;
   a.row1 = (h->r + 1) * c < m ? (h->r + 1) * c : m;
@@ -546,7 +576,7 @@ static merak_status ar2_issue(merak_tmp_t *h, int j, ArFwdArgs a, bool comm) {
   if (comm && h->nccl) TRY(nccl_allreduce(h, slot_ptr(h, h->r, 1) + r0 * h->h, (size_t)a.m * h->h));
   PeerSync ps = make_sync(h, comm);
   TRY(sync_peers(h, ps));
-  if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 1, r0, a.m, a.resid, a.bias, &a.chunk, &ps));
+  if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 1, r0, a.m, a.resid, a.bias, &a.chunk, &ps, push_on(h, comm, a.m)));
   {
     Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
     a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
@@ -629,7 +659,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     }
     if (h->ev_ar_valid[0][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[0][j], 0));
     g = gargs(ctx, w->w_o, m, hh, hr, L.ld_ctx, hr, false, false, EPI_STORE_BF16);
-    g.out = slot_ptr(h, h->r, 0) + r0 * hh; g.ldo = hh;
+    slot_out(h, g, comm, 0, r0, m);
     TRY(run_gemm(h, g, cst));
     CK(h, cudaEventRecord(h->ev_p[j], cst));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
@@ -645,7 +675,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.eps = h->eps; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
-      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 0, r0, m, xj, (const bf16 *)w->b_o, &a.chunk, &ps));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 0, r0, m, xj, (const bf16 *)w->b_o, &a.chunk, &ps, push_on(h, comm, m)));
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
       a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
       CK(h, ar_fwd(a, ps, h->ms));
@@ -669,7 +699,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     }
     if (h->ev_ar_valid[1][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[1][j], 0));
     g = gargs(gg, w->w_2, m, hh, fr, L.ld_g, fr, false, false, EPI_STORE_BF16);
-    g.out = slot_ptr(h, h->r, 1) + r0 * hh; g.ldo = hh;
+    slot_out(h, g, comm, 1, r0, m);
     TRY(run_gemm(h, g, cst));
     CK(h, cudaEventRecord(h->ev_p[j], cst));
     ArFwdArgs a;
@@ -734,7 +764,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     CK(h, cudaEventRecord(h->ev_dz[j], cst));
     if (h->ev_ar_valid[2][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[2][j], 0));
     g = gargs(dz, w->w_1, m, hh, fr, fr, hh, false, true, EPI_STORE_BF16);
-    g.out = slot_ptr(h, h->r, 2) + r0 * hh; g.ldo = hh;
+    slot_out(h, g, comm, 2, r0, m);
     TRY(run_gemm(h, g, cst));
     CK(h, cudaEventRecord(h->ev_p[j], cst));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
@@ -751,7 +781,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.G = h->G; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
-      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 2, r0, m, nullptr, nullptr, &a.chunk, &ps));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 2, r0, m, nullptr, nullptr, &a.chunk, &ps, push_on(h, comm, m)));
       {
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         a.pdl = h->pdl && !h->prof && ps.enabled;
@@ -800,7 +830,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     CK(h, cudaEventRecord(h->ev_dq[j], cst));
     if (h->ev_ar_valid[3][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[3][j], 0));
     g = gargs(dqkv, w->w_qkv, m, hh, 3 * hr, 3 * hr, hh, false, true, EPI_STORE_BF16);
-    g.out = slot_ptr(h, h->r, 3) + r0 * hh; g.ldo = hh;
+    slot_out(h, g, comm, 3, r0, m);
     TRY(run_gemm(h, g, cst));
     CK(h, cudaEventRecord(h->ev_p[j], cst));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
@@ -816,7 +846,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.G = h->G; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
-      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 3, r0, m, nullptr, nullptr, &a.chunk, &ps));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 3, r0, m, nullptr, nullptr, &a.chunk, &ps, push_on(h, comm, m)));
       {
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         a.pdl = h->pdl && !h->prof && ps.enabled;
@@ -920,7 +950,7 @@ static merak_status layer_fwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, con
     }
     if (h->ev_ar_valid[0][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[0][j], 0));
     g = gargs(ctx, w->w_o, m, hh, hr, L.ld_ctx, hr, false, false, EPI_STORE_BF16);
-    g.out = slot_ptr(h, r, 0) + r0 * hh; g.ldo = hh;
+    slot_out(h, g, true, 0, r0, m);
     TRY(run_gemm(h, g, cst));
     CK(h, cudaEventRecord(h->ev_p[j], cst));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
@@ -929,7 +959,7 @@ static merak_status layer_fwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, con
       TRY(sp_handshake(h, &ps));
       ArFwdArgs a;
       memset(&a, 0, sizeof(a));
-      for (int q = 0; q < h->T; ++q) a.partial[q] = slot_ptr(h, q, 0) + own * hh;
+      for (int q = 0; q < h->T; ++q) a.partial[q] = own_partial(h, push_on(h, true, m), 0, r0, q, mr);
       a.T = h->T; a.m = mr; a.h = hh; a.resid = xj; a.bias = (const bf16 *)w->b_o;
       a.out = (bf16 *)S(L.x1) + l0 * hh;
       a.do_ln = true; a.gamma = (const bf16 *)w->ln2_g; a.beta = (const bf16 *)w->ln2_b;
@@ -963,7 +993,7 @@ static merak_status layer_fwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, con
     TRY(run_gemm(h, g, cst));
     if (h->ev_ar_valid[1][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[1][j], 0));
     g = gargs(gg, w->w_2, m, hh, fr, L.ld_g, fr, false, false, EPI_STORE_BF16);
-    g.out = slot_ptr(h, r, 1) + r0 * hh; g.ldo = hh;
+    slot_out(h, g, true, 1, r0, m);
     TRY(run_gemm(h, g, cst));
     CK(h, cudaEventRecord(h->ev_p[j], cst));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
@@ -972,7 +1002,7 @@ static merak_status layer_fwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, con
       TRY(sp_handshake(h, &ps));
       ArFwdArgs a;
       memset(&a, 0, sizeof(a));
-      for (int q = 0; q < h->T; ++q) a.partial[q] = slot_ptr(h, q, 1) + own * hh;
+      for (int q = 0; q < h->T; ++q) a.partial[q] = own_partial(h, push_on(h, true, m), 1, r0, q, mr);
       a.T = h->T; a.m = mr; a.h = hh; a.resid = (const bf16 *)S(L.x1) + l0 * hh; a.bias = (const bf16 *)w->b_2;
       a.out = y + l0 * hh; a.do_ln = false; a.ctas = h->cfg.comm_ctas;
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
@@ -1018,7 +1048,7 @@ static merak_status layer_bwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, con
     CK(h, cudaEventRecord(h->ev_dz[j], cst));
     if (h->ev_ar_valid[2][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[2][j], 0));
     g = gargs(dz, w->w_1, m, hh, fr, fr, hh, false, true, EPI_STORE_BF16);
-    g.out = slot_ptr(h, r, 2) + r0 * hh; g.ldo = hh;
+    slot_out(h, g, true, 2, r0, m);
     TRY(run_gemm(h, g, cst));
     CK(h, cudaEventRecord(h->ev_p[j], cst));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
@@ -1027,7 +1057,7 @@ static merak_status layer_bwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, con
       TRY(sp_handshake(h, &ps));
       ArBwdArgs a;
       memset(&a, 0, sizeof(a));
-      for (int q = 0; q < h->T; ++q) a.partial[q] = slot_ptr(h, q, 2) + own * hh;
+      for (int q = 0; q < h->T; ++q) a.partial[q] = own_partial(h, push_on(h, true, m), 2, r0, q, mr);
       a.T = h->T; a.m = mr; a.h = hh; a.x_ln = (const bf16 *)S(L.x1) + l0 * hh;
       a.mean = (const float *)S(L.mean2) + l0; a.rstd = (const float *)S(L.rstd2) + l0;
       a.gamma = (const bf16 *)w->ln2_g; a.dres = dy + l0 * hh; a.dx = ag_own;  // dx1 rows for the all-gather
@@ -1091,7 +1121,7 @@ static merak_status layer_bwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, con
     CK(h, cudaEventRecord(h->ev_dq[j], cst));
     if (h->ev_ar_valid[3][j]) CK(h, cudaStreamWaitEvent(cst, h->ev_ar[3][j], 0));
     g = gargs(dqkv, w->w_qkv, m, hh, 3 * hr, 3 * hr, hh, false, true, EPI_STORE_BF16);
-    g.out = slot_ptr(h, r, 3) + r0 * hh; g.ldo = hh;
+    slot_out(h, g, true, 3, r0, m);
     TRY(run_gemm(h, g, cst));
     CK(h, cudaEventRecord(h->ev_p[j], cst));
     CK(h, cudaStreamWaitEvent(h->ms, h->ev_p[j], 0));
@@ -1100,7 +1130,7 @@ static merak_status layer_bwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, con
       TRY(sp_handshake(h, &ps));
       ArBwdArgs a;
       memset(&a, 0, sizeof(a));
-      for (int q = 0; q < h->T; ++q) a.partial[q] = slot_ptr(h, q, 3) + own * hh;
+      for (int q = 0; q < h->T; ++q) a.partial[q] = own_partial(h, push_on(h, true, m), 3, r0, q, mr);
       a.T = h->T; a.m = mr; a.h = hh; a.x_ln = x + l0 * hh;
       a.mean = (const float *)S(L.mean1) + l0; a.rstd = (const float *)S(L.rstd1) + l0;
       a.gamma = (const bf16 *)w->ln1_g; a.dres = h->dx1 + own * hh; a.dx = dx + l0 * hh;
@@ -1385,6 +1415,7 @@ static void release(merak_tmp_t *h) {
   if (h->nccl) g_nccl.CommDestroy(h->nccl);
   if (h->use_nvls) nvls_release(&h->nvls);
   if (h->pv) cudaFree(h->pv);
+  if (h->push_maps) cudaFree(h->push_maps);
   if (h->ws) cudaFree(h->ws);
   if (h->ws32) cudaFree(h->ws32);
   if (h->err_host) cudaFreeHost(h->err_host);
@@ -1527,6 +1558,7 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
   if (const char *t = getenv("MERAK_AR_TWO_SHOT")) h->two_shot = h->T > 1 && !h->f32 && atoi(t) == 1;
   if (const char *t = getenv("MERAK_AR_FUSED_WAIT")) h->fused_wait = atoi(t) != 0;
   if (const char *t = getenv("MERAK_FUSE_LN1")) h->fuse_ln1 = atoi(t) != 0;
+  if (const char *t = getenv("MERAK_AR_PUSH")) h->push_req = atoi(t) != 0;
   if (h->f32) h->fuse_ln1 = false;
   // in-process groups share ONE GPU: a waiting epilogue kernel of one rank can fill the SMs that another rank's
   // phase-1 kernel (the one it waits for) needs, so they keep the 1-warp handshake kernel
@@ -1652,6 +1684,21 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
   return MERAK_OK;
 }
 
+// Peer store maps of the fused GEMM -> reduce-scatter push (h->push): for each row-parallel slot s and owner q, the
+// TMA store map of q's slot s as a bf16 [M, h] tensor; built once the peers' slots are mapped (PEER / INPROC).
+static merak_status setup_push(merak_tmp_t *h) {
+  if (!h->push_req || h->T == 1 || h->local || h->f32 || h->nccl || h->use_nvls) return MERAK_OK;
+  std::vector<uint8_t> maps((size_t)4 * h->T * 128);
+  for (int sl = 0; sl < 4; ++sl)
+    for (int q = 0; q < h->T; ++q)
+      CK(h, gemm_store_map(maps.data() + ((size_t)sl * h->T + q) * 128, slot_ptr(h, q, sl), h->M, h->h, h->h));
+  CK(h, cudaSetDevice(h->dev));
+  CK(h, cudaMalloc(&h->push_maps, maps.size()));
+  CK(h, cudaMemcpy(h->push_maps, maps.data(), maps.size(), cudaMemcpyHostToDevice));
+  h->push = true;
+  return MERAK_OK;
+}
+
 merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, void *ag_ctx, merak_tmp_t **out) {
   if (!out) return fail(nullptr, MERAK_EINVAL, "out is NULL");
   *out = nullptr;
@@ -1732,6 +1779,10 @@ merak_status merak_tmp_init(const merak_tmp_config *cfg, merak_allgather_fn ag, 
       return bail(MERAK_EPEER);
     }
   }
+  {
+    const merak_status ps = setup_push(h);
+    if (ps != MERAK_OK) return bail(ps);
+  }
 #undef CKI
   *out = h;
   return MERAK_OK;
@@ -1762,6 +1813,18 @@ merak_status merak_tmp_init_group(const merak_tmp_config *cfg, merak_tmp_t **out
   // every rank maps every peer's peer-visible buffer directly: same process, same device, same context
   for (int q = 0; q < T; ++q)
     for (int p = 0; p < T; ++p) out[q]->peer_pv[p] = out[p]->pv;
+  for (int q = 0; q < T; ++q) {
+    const merak_status st = setup_push(out[q]);
+    if (st != MERAK_OK) {
+      const std::string e = out[q]->err;
+      for (int p = 0; p < T; ++p) {
+        release(out[p]);
+        out[p] = nullptr;
+      }
+      g_init_err = e;
+      return st;
+    }
+  }
   InprocGroup *g = new InprocGroup();
   g->T = g->alive = T;
   for (int q = 0; q < T; ++q) {
@@ -2002,6 +2065,8 @@ merak_status merak_tmp_debug_host(const merak_tmp_t *h, int32_t *out) {
   out[5] = (int32_t)h->epoch;
   out[6] = (int32_t)h->launches;
   for (int i = 0; i < 5; ++i) out[7 + i] = (int32_t)h->tr_n[i];
+  out[12] = h->push ? 1 : 0;
+  out[13] = h->two_shot ? 1 : 0;
   return MERAK_OK;
 }
 

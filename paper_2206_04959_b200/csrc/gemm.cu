@@ -58,6 +58,10 @@ struct EpiParams {
   int *tile_ctr;  // dynamic tile scheduler counter (zero between launches), nullptr = static schedule
   int group_m;    // m-tiles per raster band (tile_coords): 1 = n fastest over all of N, tiles_m = m fastest
   int hint_a, hint_b, hint_c;  // L2 eviction priority of the A / B TMA loads and the fp32 C accesses (l2_policy)
+  // Scatter store (EPI_STORE_BF16 only, GemmArgs::scatter): output row i goes to owner q = i / scatter_rows,
+  // row scatter_row0 + i - q * scatter_rows of the tensor map scatter[q] (a peer's slot, in global memory)
+  const CUtensorMap *scatter;
+  int scatter_row0, scatter_rows;
 };
 
 template <int EPI>
@@ -494,7 +498,16 @@ __global__ void __launch_bounds__(256, 1)
           uint32_t w[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) w[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
-          stage_store(&tmO, w, gn0, grow0);
+          if (EPI == EPI_STORE_BF16 && p.scatter) {
+            // the warp's 32-row box lies inside one owner's rows (scatter_rows % 32 == 0): push it into that
+            // rank's slot over NVLink; boxes past M (last m-tile) are not stored
+            if (grow0 < p.M) {
+              const int q = grow0 / p.scatter_rows;
+              stage_store(p.scatter + q, w, gn0, p.scatter_row0 + grow0 - q * p.scatter_rows);
+            }
+          } else {
+            stage_store(&tmO, w, gn0, grow0);
+          }
           if constexpr (EPI == EPI_BIAS_GELU) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) w[i] = pack_bf16(gelu_f(v[2 * i]), gelu_f(v[2 * i + 1]));
@@ -557,6 +570,11 @@ static bool make_map(CUtensorMap *m, const void *ptr, int rows, int cols, int ld
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+cudaError_t gemm_store_map(void *map, const void *ptr, int rows, int cols, int ld) {
+  return make_map(reinterpret_cast<CUtensorMap *>(map), ptr, rows, cols, ld, 32) ? cudaSuccess
+                                                                               : cudaErrorInvalidValue;
 }
 
 struct Maps {
@@ -746,6 +764,10 @@ cudaError_t gemm(const GemmArgs &a, cudaStream_t st) {
     }
   }
   p.n_main = a.db32 ? a.N - 1 : a.N;
+  p.scatter = reinterpret_cast<const CUtensorMap *>(a.scatter); p.scatter_row0 = a.scatter_row0; p.scatter_rows = a.scatter_rows;
+  if (a.scatter && (a.epi != EPI_STORE_BF16 || a.scatter_rows <= 0 || a.scatter_rows % 32 != 0 ||
+                    a.M % a.scatter_rows != 0))
+    return cudaErrorInvalidValue;
   if (cg == 2 && a.epi >= 5 && !a.a_mn && !a.b_mn) {  // microbenchmark-only variants
     if (a.epi == 5) return launch<2, 256, false, false, 5>(a, mp, p, st);            // no stores
     if (a.epi == 6) return launch<2, 256, false, false, EPI_STORE_BF16, 192>(a, mp, p, st);  // 6 stages

@@ -75,8 +75,17 @@ struct GemmArgs {
                      // all-reduce kernels when T > 1)
   int *tile_ctr;     // dynamic tile scheduler: a device int that is 0 between launches and used by one
                      // stream at a time (the kernel resets it); nullptr = static schedule
+  // Scatter store (fused GEMM -> reduce-scatter push, EPI_STORE_BF16 only): instead of out, row i of C is
+  // stored through the TMA map scatter[q], q = i / scatter_rows (the owner rank of the row), at map row
+  // scatter_row0 + i - q * scatter_rows.  scatter points to T maps in device memory (gemm_store_map);
+  // scatter_rows % 32 == 0 and M % scatter_rows == 0, else cudaErrorInvalidValue.
+  const void *scatter;
+  int scatter_row0, scatter_rows;
 };
 cudaError_t gemm(const GemmArgs &a, cudaStream_t st);
+// Encode (host) the 128-byte TMA store map of a bf16 [rows, cols] tensor (row stride ld) that the GEMM's
+// scatter store uses: boxes of 64 cols x 32 rows, 128-B swizzle (the same encoding as its own output map).
+cudaError_t gemm_store_map(void *map, const void *ptr, int rows, int cols, int ld);
 int gemm_num_sms();
 
 // ---------------------------------------------------------------- attention (attention_tc.cu, attention_bwd_tc.cu)
