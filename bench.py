@@ -583,11 +583,12 @@ def push_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step):
     from paper_2206_04959_b200 import FLAG_NO_COMM, MerakError
     nx = max(3, args.steps // 2)
     keep = {k: os.environ.get(k) for k in ("MERAK_AR_PUSH", "MERAK_AR_TWO_SHOT")}
-    os.environ["MERAK_AR_PUSH"] = "1"
     os.environ["MERAK_AR_TWO_SHOT"] = "1"
     out = {}
     try:
-        for name, sp in (("two_shot", False), ("seq_parallel", True)):
+        # mode 1: reduce-scatter push; mode 2: + the reduced rows pushed into every rank's all-gather slot
+        for name, sp, mode in (("two_shot", False, "1"), ("two_shot_ag", False, "2"), ("seq_parallel", True, "1")):
+            os.environ["MERAK_AR_PUSH"] = mode
             try:
                 st = Stack(cfg, L, T, rank, dev, group, n_sub, comm_ctas=args.comm_ctas, seq_parallel=sp)
             except MerakError as e:
@@ -733,6 +734,17 @@ def side_workloads(args, T, rank, dev, group, timed, main_stack):
         out[name] = {"tflops_per_gpu": fl / (ms * 1e-3) / 1e12, "ms_per_step": ms, "ms_per_layer": ms / args.layers,
                      "tmp_degree": tt, "n_sub": c.n_sub, "layers": args.layers,
                      "mode": "per-rank compute only (MERAK_COMM_LOCAL)" if comm else f"full layer at T={tt}"}
+        if comm:  # where the shard's time goes: per-class kernel ms per layer, all compute on one stream
+            st = Stack(c, args.layers, tt, 0, dev, None, c.n_sub, comm=comm, streams1=True)
+            st.step()
+            np_ = 3
+            ms1, _, prof = timed(st, np_, prof=True)
+            st.close()
+            out[name]["serialized_ms_per_layer"] = ms1 / args.layers
+            out[name]["class_ms_per_layer"] = {k: v["ms"] / np_ / args.layers for k, v in prof.items()}
+            g = prof.get("gemm")
+            if g and g["ms"] > 0:
+                out[name]["gemm_tflops_serialized"] = g["flops"] / (g["ms"] * 1e-3) / 1e12
     return out
 
 

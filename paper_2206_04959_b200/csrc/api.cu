@@ -133,6 +133,9 @@ struct merak_tmp {
   // fc2, fc1 dgrad, QKV dgrad) store each 32-row output box straight into the slot of the rank that owns the
   // rows (TMA store through a peer tensor map), so the reduce-scatter phase reads only local HBM.
   bool push_req = false, push = false;
+  // MERAK_AR_PUSH=2 adds the all-gather push of the replicated two-shot all-reduce: phase 1 stores the reduced owner
+  // rows into every rank's all-gather slot (AG_SLOT) over NVLink, so the phase-2 epilogue reads only local HBM
+  bool push_ag = false;
   void *push_maps = nullptr;  // device: [4 row-parallel slots][T owners] CUtensorMap (128 B each)
   bool pdl = false;       // programmatic dependent launch along the all-reduce kernel chain (env MERAK_AR_PDL)
   int gemm_smem_kb = 192;  // GEMM TMA ring: 160 KB at T > 1 leaves smem for co-resident all-reduce kernels
@@ -366,10 +369,15 @@ static merak_status nccl_allreduce(merak_tmp_t *h, void *rows, size_t count, boo
 }
 
 // Partials the all-reduce epilogue kernel sums for slot `slot`, rows starting at r0.
-static int ar_partials(merak_tmp_t *h, bool comm, int slot, size_t r0, const bf16 **out) {
+static bool push_ag_on(merak_tmp_t *h, bool comm, int m);
+static int ar_partials(merak_tmp_t *h, bool comm, int slot, size_t r0, const bf16 **out, int m) {
   if (!comm || h->T == 1 || h->nccl) {
     out[0] = slot_ptr(h, h->r, slot) + r0 * h->h;
     return 1;
+  }
+  if (push_ag_on(h, comm, m)) {  // every reduced row was pushed into this rank's all-gather slot
+    for (int q = 0; q < h->T; ++q) out[q] = slot_ptr(h, h->r, AG_SLOT) + r0 * h->h;
+    return h->T;
   }
   // NVLS: after the in-switch reduction every row is in this rank's own slot ("gathered" mode reads locally)
   for (int q = 0; q < h->T; ++q) out[q] = slot_ptr(h, h->use_nvls ? h->r : q, slot) + r0 * h->h;
@@ -418,6 +426,11 @@ static bool two_shot_on(merak_tmp_t *h, bool comm) { return comm && h->T > 1 && 
 static bool push_on(merak_tmp_t *h, bool comm, int m) {
   return h->push && comm && (h->sp || two_shot_on(h, comm)) && m % h->T == 0 && (m / h->T) % 32 == 0;
 }
+// All-gather push (h->push_ag): the replicated two-shot all-reduce's phase 1 writes the reduced owner rows into every
+// rank's AG_SLOT region of the sub-batch and the phase-2 epilogue reads every row from its own AG_SLOT.  AG_SLOT is
+// shared by the 4 all-reduces and both sub-batches: a rank's phase 1 writes a peer's region only after a handshake
+// that the peer entered after its previous phase 2 finished reading (all on the in-order communication stream).
+static bool push_ag_on(merak_tmp_t *h, bool comm, int m) { return h->push_ag && !h->sp && push_on(h, comm, m); }
 // Output of a row-parallel GEMM into slot `slot`, sub-batch rows from r0: own slot, or pushed to the owners.
 static void slot_out(merak_tmp_t *h, GemmArgs &g, bool comm, int slot, size_t r0, int m) {
   g.out = slot_ptr(h, h->r, slot) + r0 * h->h;
@@ -481,6 +494,11 @@ static merak_status two_shot_rs(merak_tmp_t *h, int slot, size_t r0, int m, cons
   a.row1 = (h->r + 1) * c < m ? (h->r + 1) * c : m;
   a.resid = resid; a.bias = bias;
   a.out = slot_ptr(h, h->r, slot) + r0 * h->h;
+  if (pushed && push_ag_on(h, true, m)) {  // reduced rows straight into every rank's all-gather slot
+    a.n_peer = h->T;
+    a.rank = h->r;
+    for (int q = 0; q < h->T; ++q) a.out_peer[q] = slot_ptr(h, q, AG_SLOT) + r0 * h->h;
+  }
   a.ctas = h->cfg.comm_ctas;
   a.pdl = h->pdl && !h->prof;  // (profiling events between launches would break the PDL pairing)
   a.ps = pub;
@@ -667,7 +685,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       ArFwdArgs a;
       memset(&a, 0, sizeof(a));
       if (comm && h->nccl) TRY(nccl_allreduce(h, slot_ptr(h, h->r, 0) + r0 * hh, (size_t)m * hh));
-      a.T = ar_partials(h, comm, 0, r0, a.partial);
+      a.T = ar_partials(h, comm, 0, r0, a.partial, m);
       a.m = m; a.h = hh; a.resid = xj; a.bias = (const bf16 *)w->b_o; a.out = (bf16 *)S(L.x1) + r0 * hh;
       a.do_ln = true; a.gamma = (const bf16 *)w->ln2_g; a.beta = (const bf16 *)w->ln2_b;
       a.ln_out = (bf16 *)S(L.u2) + r0 * L.ld_u2; a.ld_ln = L.ld_u2;
@@ -704,7 +722,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
     CK(h, cudaEventRecord(h->ev_p[j], cst));
     ArFwdArgs a;
     memset(&a, 0, sizeof(a));
-    a.T = ar_partials(h, comm, 1, r0, a.partial);
+    a.T = ar_partials(h, comm, 1, r0, a.partial, m);
     a.m = m; a.h = hh; a.resid = (const bf16 *)S(L.x1) + r0 * hh; a.bias = (const bf16 *)w->b_2;
     a.out = y + r0 * hh; a.do_ln = false; a.ctas = h->cfg.comm_ctas;
     if (defer_ar2) {  // issued by the next call (flush_ar2), possibly with the next layer's LN1
@@ -772,7 +790,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       ArBwdArgs a;
       memset(&a, 0, sizeof(a));
       if (comm && h->nccl) TRY(nccl_allreduce(h, slot_ptr(h, h->r, 2) + r0 * hh, (size_t)m * hh));
-      a.T = ar_partials(h, comm, 2, r0, a.partial);
+      a.T = ar_partials(h, comm, 2, r0, a.partial, m);
       a.m = m; a.h = hh; a.x_ln = (const bf16 *)S(L.x1) + r0 * hh;
       a.mean = (const float *)S(L.mean2) + r0; a.rstd = (const float *)S(L.rstd2) + r0;
       a.gamma = (const bf16 *)w->ln2_g; a.dres = dyj; a.dx = h->dx1 + r0 * hh;
@@ -838,7 +856,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       ArBwdArgs a;
       memset(&a, 0, sizeof(a));
       if (comm && h->nccl) TRY(nccl_allreduce(h, slot_ptr(h, h->r, 3) + r0 * hh, (size_t)m * hh));
-      a.T = ar_partials(h, comm, 3, r0, a.partial);
+      a.T = ar_partials(h, comm, 3, r0, a.partial, m);
       a.m = m; a.h = hh; a.x_ln = x + r0 * hh;
       a.mean = (const float *)S(L.mean1) + r0; a.rstd = (const float *)S(L.rstd1) + r0;
       a.gamma = (const bf16 *)w->ln1_g; a.dres = dx1; a.dx = dx + r0 * hh;
@@ -1558,7 +1576,10 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
   if (const char *t = getenv("MERAK_AR_TWO_SHOT")) h->two_shot = h->T > 1 && !h->f32 && atoi(t) == 1;
   if (const char *t = getenv("MERAK_AR_FUSED_WAIT")) h->fused_wait = atoi(t) != 0;
   if (const char *t = getenv("MERAK_FUSE_LN1")) h->fuse_ln1 = atoi(t) != 0;
-  if (const char *t = getenv("MERAK_AR_PUSH")) h->push_req = atoi(t) != 0;
+  if (const char *t = getenv("MERAK_AR_PUSH")) {
+    h->push_req = atoi(t) != 0;
+    h->push_ag = atoi(t) == 2;
+  }
   if (h->f32) h->fuse_ln1 = false;
   // in-process groups share ONE GPU: a waiting epilogue kernel of one rank can fill the SMs that another rank's
   // phase-1 kernel (the one it waits for) needs, so they keep the 1-warp handshake kernel
@@ -1622,7 +1643,8 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
   // block holds the handshake flags only
   const bool nvls = cfg->comm == MERAK_COMM_NVLS && h->T > 1;
   h->sp = cfg->seq_parallel && h->T > 1;
-  const int nslot_pv = h->sp ? NSLOT : NSLOT - 1;  // the all-gather slot exists only in the sp layout
+  // the all-gather slot exists in the sp layout and for the all-gather push of the two-shot all-reduce
+  const int nslot_pv = (h->sp || (h->push_ag && h->T > 1)) ? NSLOT : NSLOT - 1;
   h->flags_off = nvls ? 0 : nslot_pv * h->slot_bytes;
   h->pv_bytes = h->flags_off + align256(2 * MAX_AR_CTAS * MAX_T * sizeof(uint32_t));
   if (h->sp) {  // LN-gradient partial exchange: [MAXN sub-batches][dγ2, dβ2, dγ1, dβ1][h] fp32
@@ -1687,7 +1709,10 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
 // Peer store maps of the fused GEMM -> reduce-scatter push (h->push): for each row-parallel slot s and owner q, the
 // TMA store map of q's slot s as a bf16 [M, h] tensor; built once the peers' slots are mapped (PEER / INPROC).
 static merak_status setup_push(merak_tmp_t *h) {
-  if (!h->push_req || h->T == 1 || h->local || h->f32 || h->nccl || h->use_nvls) return MERAK_OK;
+  if (!h->push_req || h->T == 1 || h->local || h->f32 || h->nccl || h->use_nvls) {
+    h->push_ag = false;
+    return MERAK_OK;
+  }
   std::vector<uint8_t> maps((size_t)4 * h->T * 128);
   for (int sl = 0; sl < 4; ++sl)
     for (int q = 0; q < h->T; ++q)
@@ -2133,19 +2158,19 @@ merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t ro
       if (which == 0) {
         ArFwdArgs a;
         memset(&a, 0, sizeof(a));
-        a.T = ar_partials(h, true, 1, 0, a.partial);
+        a.T = ar_partials(h, true, 1, 0, a.partial, rows);
         a.m = rows; a.h = (int)hh; a.resid = resid; a.bias = gam; a.out = out; a.ctas = h->cfg.comm_ctas;
-        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, resid, gam, &a.chunk, &ps));
+        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, resid, gam, &a.chunk, &ps, push_on(h, true, rows)));
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
       CK(h, ar_fwd(a, ps, h->ms));
       } else {
         ArBwdArgs a;
         memset(&a, 0, sizeof(a));
-        a.T = ar_partials(h, true, 1, 0, a.partial);
+        a.T = ar_partials(h, true, 1, 0, a.partial, rows);
         a.m = rows; a.h = (int)hh; a.x_ln = resid; a.mean = mean; a.rstd = rstd; a.gamma = gam; a.dres = resid;
         a.dx = out; a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
-        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, nullptr, nullptr, &a.chunk, &ps));
+        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, nullptr, nullptr, &a.chunk, &ps, push_on(h, true, rows)));
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         a.pdl = h->pdl && !h->prof && ps.enabled;
         CK(h, ar_bwd(a, ps, h->ms));

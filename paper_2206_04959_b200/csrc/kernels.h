@@ -220,6 +220,10 @@ struct ArRsArgs {
   const __nv_bfloat16 *resid;  // nullptr: plain sum (backward); else forward AR epilogue terms
   const __nv_bfloat16 *bias;
   __nv_bfloat16 *out;
+  // all-gather push: n_peer > 0 stores every reduced row into out_peer[q] (rank q's all-gather slot, same row
+  // offsets as out) for all q, starting with q = rank + 1 (spreads the NVLink writes), instead of into out
+  __nv_bfloat16 *out_peer[MAX_T];
+  int n_peer, rank;
   int ctas;
   bool pdl;
 };

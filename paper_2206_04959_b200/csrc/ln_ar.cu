@@ -300,7 +300,14 @@ __global__ void __launch_bounds__(256) ar_rs_kernel(ArRsArgs a) {
           add8(a.bias + c * 8, v[i]);
           add8(a.resid + ro + c * 8, v[i]);
         }
-        store8(a.out + ro + c * 8, v[i]);
+        if (a.n_peer > 0) {
+          for (int k = 1; k <= a.n_peer; ++k) {
+            const int q = (a.rank + k) % a.n_peer;
+            store8(a.out_peer[q] + ro + c * 8, v[i]);
+          }
+        } else {
+          store8(a.out + ro + c * 8, v[i]);
+        }
       }
     }
   }

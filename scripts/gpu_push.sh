@@ -17,4 +17,5 @@ run() {  # name, env...
 }
 run main MERAK_BENCH_NONE=1
 BENCH_ARGS=--no-extras run push_main MERAK_AR_PUSH=1 MERAK_AR_TWO_SHOT=1
+BENCH_ARGS=--no-extras run pushag_main MERAK_AR_PUSH=2 MERAK_AR_TWO_SHOT=1
 BENCH_ARGS=--no-extras run pull_main2 MERAK_BENCH_NONE=1

@@ -75,16 +75,17 @@ def main():
                 failures.append((name, f"{k}: one-shot vs two-shot all-reduce not bit-identical"))
         # fused GEMM -> reduce-scatter push (MERAK_AR_PUSH=1, two-shot): row-parallel GEMM epilogues store their
         # boxes into the owners' slots over NVLink (peer TMA maps); same sums, so bit-identical
-        os.environ["MERAK_AR_PUSH"] = "1"
-        os.environ["MERAK_AR_TWO_SHOT"] = "1"
-        try:
-            outq = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group)
-        finally:
-            del os.environ["MERAK_AR_PUSH"]
-            del os.environ["MERAK_AR_TWO_SHOT"]
-        for k in out:
-            if not torch.equal(out[k], outq[k]):
-                failures.append((name, f"{k}: pushed reduce-scatter not bit-identical"))
+        for mode in ("1", "2"):  # 2: the reduced rows are pushed into every rank's all-gather slot as well
+            os.environ["MERAK_AR_PUSH"] = mode
+            os.environ["MERAK_AR_TWO_SHOT"] = "1"
+            try:
+                outq = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group)
+            finally:
+                del os.environ["MERAK_AR_PUSH"]
+                del os.environ["MERAK_AR_TWO_SHOT"]
+            for k in out:
+                if not torch.equal(out[k], outq[k]):
+                    failures.append((name, f"{k}: pushed reduce-scatter (mode {mode}) not bit-identical"))
         # programmatic dependent launch along the all-reduce chain (opt-in) must not change a bit
         os.environ["MERAK_AR_PDL"] = "1"
         try:

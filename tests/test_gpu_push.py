@@ -31,7 +31,7 @@ def _gpu():
 
 def _run(monkeypatch, push, cfg, plist, x, dy, T, seq_parallel, two_shot=None, n_sub=2):
     from test_gpu_seqpar import run_sp_group
-    monkeypatch.setenv("MERAK_AR_PUSH", "1" if push else "0")
+    monkeypatch.setenv("MERAK_AR_PUSH", push if isinstance(push, str) else ("1" if push else "0"))
     if two_shot is not None:
         monkeypatch.setenv("MERAK_AR_TWO_SHOT", "1" if two_shot else "0")
     return run_sp_group(cfg, plist, x, dy, T, n_sub=n_sub, seq_parallel=seq_parallel)
@@ -57,16 +57,21 @@ def test_push_seqpar_chain_bit_identical(T, monkeypatch):
     _assert_identical(push, pull, T)
 
 
+@pytest.mark.parametrize("mode", ["1", "2"], ids=["rs", "rs+ag"])
 @pytest.mark.parametrize("T", [2, 4, 8])
-def test_push_two_shot_chain_bit_identical(T, monkeypatch):
-    """Replicated layout, two-shot all-reduce: phase 1 reads the pushed local blocks instead of the peers' slots."""
+def test_push_two_shot_chain_bit_identical(T, mode, monkeypatch):
+    """Replicated layout, two-shot all-reduce: phase 1 reads the pushed local blocks instead of the peers' slots
+    (mode 1); mode 2 also pushes the reduced rows into every rank's all-gather slot, so phase 2 reads locally."""
     cfg = CFG.with_(tmp_degree=T)
     K = 3
     plist = [make_params(cfg, layer=k) for k in range(K)]
     x, dy = make_activations(cfg)
     pull = _run(monkeypatch, False, cfg, plist, x, dy, T, False, two_shot=True)
-    push = _run(monkeypatch, True, cfg, plist, x, dy, T, False, two_shot=True)
+    push = _run(monkeypatch, mode, cfg, plist, x, dy, T, False, two_shot=True)
     _assert_identical(push, pull, T)
+    if T == 4:  # one-shot reference (default pull) too
+        one = _run(monkeypatch, False, cfg, plist, x, dy, T, False, two_shot=False)
+        _assert_identical(push, one, T)
 
 
 @pytest.mark.parametrize("T", [2, 4])
@@ -94,7 +99,7 @@ def test_push_ineligible_falls_back(monkeypatch):
     cfg = CFG.with_(tmp_degree=T, seq_len=64)  # m = 128, m / T = 16
     params, x, dy = make_all(cfg, seed=4500)
     pull = _run(monkeypatch, False, cfg, [params], x, dy, T, False, two_shot=True)
-    push = _run(monkeypatch, True, cfg, [params], x, dy, T, False, two_shot=True)
+    push = _run(monkeypatch, "2", cfg, [params], x, dy, T, False, two_shot=True)
     _assert_identical(push, pull, T)
 
 
