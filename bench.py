@@ -342,13 +342,18 @@ def main():
             extras["no_comm_ms_per_step"] = ms_nc
             stage("no-comm done")
             rows = cfg.tokens // n_sub
-            two = (T >= 4) if os.environ.get("MERAK_AR_TWO_SHOT") is None else os.environ["MERAK_AR_TWO_SHOT"] == "1"
+            dh = stack.layer.debug_host()
+            two, push = dh["two_shot"], dh["push"] and dh["two_shot"] and (rows // T) % 32 == 0
             t_f = stack.layer.bench_allreduce(0, rows, 20)
             t_b = stack.layer.bench_allreduce(1, rows, 20)
             t_h = stack.layer.bench_allreduce(0, rows // 2, 20)
             msg = rows * cfg.hidden * 2
-            nvl = (2 * (T - 1) / T if two else (T - 1)) * msg  # bytes each GPU pulls from its peers per AR
-            extras["allreduce"] = {"algorithm": "two-shot" if two else "one-shot", "rows": rows, "msg_bytes": msg,
+            # bytes each GPU moves over NVLink per AR in the timed kernels (pull: loads from the peers; push: the
+            # reduce-scatter half travels inside the GEMM epilogue, the timed part stores the all-gather half)
+            nvl = ((T - 1) / T if push else 2 * (T - 1) / T if two else (T - 1)) * msg
+            alg = "two-shot, reduce-scatter pushed by the GEMM epilogue (not timed here)" if push else \
+                "two-shot" if two else "one-shot"
+            extras["allreduce"] = {"algorithm": alg, "rows": rows, "msg_bytes": msg,
                                    "nvlink_bytes_in_per_gpu": nvl, "fwd_ar_us": t_f * 1e3, "bwd_ar_us": t_b * 1e3,
                                    "achieved_GBps": nvl / (t_f * 1e-3) / 1e9, "peak_GBps": 900.0,
                                    "frac": nvl / (t_f * 1e-3) / 900e9,

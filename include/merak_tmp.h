@@ -114,6 +114,15 @@ enum { MERAK_BF16 = 0, MERAK_FP32_CHECK = 1 };      /* merak_tmp_config.precisio
  * (pidfd_getfd: the ranks must run as the same user).  EUNSUPPORTED when a device lacks multicast support
  * or in the fp32 check mode.  Same call sequence and results (up to the switch's rounding) as PEER. */
 enum { MERAK_COMM_PEER = 0, MERAK_COMM_NCCL = 1, MERAK_COMM_LOCAL = 2, MERAK_COMM_INPROC = 3, MERAK_COMM_NVLS = 4 };
+/* All-reduce algorithm of MERAK_COMM_PEER / INPROC (P:558's 2+2 AllReduces per layer, in-kernel): one-shot at
+ * T = 2 (every rank sums all T partials), two-shot at T >= 4 (owner rows reduced, then gathered; env
+ * MERAK_AR_TWO_SHOT=0/1 at init overrides).  Fused GEMM -> reduce-scatter push (env
+ * MERAK_AR_PUSH at init, default 2 at T >= 4, else 0): 1 = the row-parallel GEMMs (proj, fc2, fc1 dgrad, QKV
+ * dgrad) store each 32-row output box into the slot of the rank owning those rows (TMA stores over NVLink
+ * through peer tensor maps), so the reduce-scatter reads local memory only; 2 = in addition the two-shot's
+ * reduced rows are pushed into every rank's all-gather slot and the fused epilogue reads locally.  Applies to
+ * calls whose owner row blocks B*s/(n T) are whole 32-row boxes, with the two-shot all-reduce or the
+ * sequence-parallel layout; other calls use the pull layout.  Results are bit-identical in every mode. */
 
 /* flags for layer_fwd / layer_bwd */
 enum {
@@ -282,9 +291,8 @@ merak_status merak_tmp_debug_state(const merak_tmp_t *h, int32_t *out);
 /* Host-memory-only part of the diagnostics (no CUDA call, so it cannot block behind a launch):
  * out[0..4] = watchdog error word, out[5] = handshake epoch, out[6] = launches enqueued so far,
  * out[7..11] = traced launches enqueued per stream (cs, cs1, cw, cr, ms; MERAK_DEBUG_TRACE=1), out[12] = 1 when
- * the fused GEMM -> reduce-scatter push is set up (env MERAK_AR_PUSH=1 at init, PEER / INPROC, T > 1, bf16; it
- * applies to calls whose owner row blocks B*s/(n T) are whole 32-row boxes, in the sequence-parallel layout or
- * with the two-shot all-reduce), out[13] = 1 when the two-shot all-reduce is selected.  out has 14 entries. */
+ * the fused GEMM -> reduce-scatter push is set up (MERAK_AR_PUSH above; PEER / INPROC, T > 1, bf16), out[13] = 1
+ * when the two-shot all-reduce is selected.  out has 14 entries. */
 merak_status merak_tmp_debug_host(const merak_tmp_t *h, int32_t *out);
 
 #ifdef __cplusplus

@@ -16,29 +16,64 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2206_04959_b200 import TmpLayer  # noqa: E402
 
 
-def nvlink_counters(dev_index):
-    """Summed NVLink data TX / RX counters of one GPU (KiB throughput fields, else byte counters); None if absent."""
+def _nvml_fields(dev_index):
+    """Summed NVLink TX / RX bytes over the links from NVML field values; tries the byte counters first, then the
+    KiB data-throughput fields.  Returns ({"tx": bytes, "rx": bytes, "source": name}, diagnostics)."""
     try:
         import pynvml as nv
     except ImportError:
-        return None
+        return None, "no pynvml"
     nv.nvmlInit()
     hdl = nv.nvmlDeviceGetHandleByIndex(dev_index)
-    out = {}
-    for name, fid, scale in (("tx", nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, 1024),
-                             ("rx", nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 1024)):
-        tot, ok = 0, False
-        for link in range(18):
-            try:
-                v = nv.nvmlDeviceGetFieldValues(hdl, [(fid, link)])[0]
-            except Exception:  # noqa: BLE001
-                continue
-            if v.nvmlReturn != 0:
-                continue
-            ok = True
-            tot += int(v.value.ullVal) * scale
-        out[name] = tot if ok else None
-    return out
+    diag = {}
+    for src, ftx, frx, scale in (("COUNT_BYTES", nv.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES,
+                                  nv.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, 1),
+                                 ("THROUGHPUT_DATA_KiB", nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX,
+                                  nv.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 1024)):
+        out, ok = {}, True
+        for name, fid in (("tx", ftx), ("rx", frx)):
+            tot, n = 0, 0
+            for link in range(18):
+                try:
+                    v = nv.nvmlDeviceGetFieldValues(hdl, [(fid, link)])[0]
+                except Exception as e:  # noqa: BLE001
+                    diag[f"{src}/{name}/{link}"] = repr(e)[:80]
+                    continue
+                if v.nvmlReturn != 0:
+                    diag[f"{src}/{name}/{link}"] = int(v.nvmlReturn)
+                    continue
+                tot += int(v.value.ullVal) * scale
+                n += 1
+            ok = ok and n > 0
+            out[name] = tot
+        if ok:
+            out["source"] = "NVML " + src
+            return out, None
+    return None, dict(list(diag.items())[:6])
+
+
+def _smi(dev_index):
+    """`nvidia-smi nvlink -gt d -i N`: per-link 'Data Tx / Rx' counters in KiB, summed."""
+    import re
+    import subprocess
+    try:
+        txt = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(dev_index)], capture_output=True,
+                             text=True, timeout=30).stdout
+    except Exception as e:  # noqa: BLE001
+        return None, repr(e)[:80]
+    tx = sum(int(v) for v in re.findall(r"Tx:\s*(\d+)\s*KiB", txt))
+    rx = sum(int(v) for v in re.findall(r"Rx:\s*(\d+)\s*KiB", txt))
+    if not re.search(r"Tx:\s*\d+", txt):
+        return None, txt[:200]
+    return {"tx": tx * 1024, "rx": rx * 1024, "source": "nvidia-smi nvlink -gt d"}, None
+
+
+def nvlink_counters(dev_index):
+    c, d1 = _nvml_fields(dev_index)
+    if c:
+        return c, None
+    c, d2 = _smi(dev_index)
+    return c, {"nvml": d1, "smi": d2}
 
 
 def main():
@@ -51,9 +86,11 @@ def main():
     iters = int(os.environ.get("ITERS", 50))
     layer = TmpLayer(h, h // 96, 2048, 4, tmp_degree=world, tmp_rank=rank, n_sub=2, group=dist.group.WORLD)
     two = layer.debug_host()["two_shot"]
-    push = layer.debug_host()["push"]
+    push = layer.debug_host()["push"] and two and (rows // world) % 32 == 0
     msg = rows * h * 2
-    algo = (2 * (world - 1) / world if two else (world - 1)) * msg
+    # bench_allreduce zeroes the slot and runs the all-reduce alone: with the push, the reduce-scatter half would
+    # travel inside the GEMM, so only the all-gather half moves here
+    algo = ((world - 1) / world if push else 2 * (world - 1) / world if two else (world - 1)) * msg
     phys = os.environ.get("CUDA_VISIBLE_DEVICES")
     nvml_index = int(phys.split(",")[local]) if phys else local
     res = {}
@@ -61,16 +98,18 @@ def main():
         layer.bench_allreduce(which, rows, 5)
         torch.cuda.synchronize()
         dist.barrier()
-        c0 = nvlink_counters(nvml_index)
+        c0, diag = nvlink_counters(nvml_index)
         ms = layer.bench_allreduce(which, rows, iters)
         torch.cuda.synchronize()
-        c1 = nvlink_counters(nvml_index)
+        c1, _ = nvlink_counters(nvml_index)
         r = {"us": ms * 1e3}
         if c0 and c1:
+            r["source"] = c0["source"]
             for k in ("tx", "rx"):
-                if c0[k] is not None and c1[k] is not None:
-                    # merak_tmp_bench_allreduce runs 3 untimed warm-up all-reduces before the timed `iters`
-                    r[f"{k}_bytes_per_ar"] = (c1[k] - c0[k]) / (iters + 3)
+                # merak_tmp_bench_allreduce runs 3 untimed warm-up all-reduces before the timed `iters`
+                r[f"{k}_bytes_per_ar"] = (c1[k] - c0[k]) / (iters + 3)
+        else:
+            r["counters_unavailable"] = diag
         gathered = [None] * world
         dist.all_gather_object(gathered, r)
         res[name] = gathered
