@@ -384,14 +384,18 @@ def main():
         extras["side_workloads"] = side_workloads(args, T, rank, dev, group, timed, stack)
         stage("side workloads done")
         if world > 1:
-            extras["nvls"] = nvls_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step)
-            stage("nvls pass done")
-            extras["seq_parallel"] = seqpar_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step)
-            stage("seq-parallel pass done")
-            extras["push"] = push_pass(args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step)
-            stage("push pass done")
-            extras["pipeline"] = pipeline_pass(args, rank, world, dev, barrier, max_over_ranks)
-            stage("pipeline pass done")
+            def guarded(name, fn, *a):
+                # side passes are deterministic across ranks: a failure on one is a failure on all, so it is
+                # recorded in the line instead of losing the measured headline
+                try:
+                    extras[name] = fn(*a)
+                except Exception as e:  # noqa: BLE001
+                    extras[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+                stage(f"{name} pass done")
+            guarded("nvls", nvls_pass, args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step)
+            guarded("seq_parallel", seqpar_pass, args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step)
+            guarded("push", push_pass, args, cfg, L, T, rank, dev, group, n_sub, timed, ms_step)
+            guarded("pipeline", pipeline_pass, args, rank, world, dev, barrier, max_over_ranks)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,

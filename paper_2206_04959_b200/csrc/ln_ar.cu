@@ -188,24 +188,42 @@ __global__ void __launch_bounds__(256, 2) ar_fwd_kernel(ArFwdArgs a, PeerSync ps
   const int nsub = blockDim.x / tpr, sub = threadIdx.x / tpr, t = threadIdx.x % tpr;
   const int h = a.h, nc = h >> 3;
   const bool gathered = a.chunk > 0;
+  // Row prefetch (registers permitting): the next row's loads are issued before this row's arithmetic,
+  // reductions and stores, so every sub-block keeps two rows of HBM reads in flight (the kernel is HBM-bound
+  // and runs 16 warps per SM).
+  constexpr bool PF = NT * CPT <= 6 && CPT <= 3;
   int par = 0;
-  for (int row = blockIdx.x * nsub + sub; row < a.m; row += gridDim.x * nsub) {
+  uint4 bb[CPT];  // bias: the same columns for every row
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const int c = t + k * tpr;
+    bb[k] = (!gathered && c < nc) ? ldg16(a.bias + c * 8) : make_uint4(0, 0, 0, 0);
+  }
+  auto load_row = [&](int row, uint4 (&raw)[CPT][NT], uint4 (&rr)[CPT]) {
     const size_t ro = (size_t)row * h;
     const __nv_bfloat16 *src[NT];
     row_sources<NT>(a.partial, a.chunk, row, src);
-    uint4 raw[CPT][NT], rr[CPT], bb[CPT];
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {  // every load of the row is in flight before any arithmetic
       const int c = t + k * tpr;
-      const bool ok = c < nc;
+      const bool ok = c < nc && row < a.m;
 #pragma unroll
       for (int r = 0; r < NT; ++r) raw[k][r] = ok ? ldg16(src[r] + ro + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
-      if (!gathered) {
-        rr[k] = ok ? ldg16(a.resid + ro + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
-        bb[k] = ok ? ldg16(a.bias + c * 8) : make_uint4(0, 0, 0, 0);
-      }
+      rr[k] = (ok && !gathered) ? ldg16(a.resid + ro + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
     }
-    float q[CPT][8];
+  };
+  const int stride = gridDim.x * nsub;
+  uint4 raw[CPT][NT], rr[CPT];
+  if constexpr (PF) load_row(blockIdx.x * nsub + sub, raw, rr);
+  for (int row = blockIdx.x * nsub + sub; row < a.m; row += stride) {
+    const size_t ro = (size_t)row * h;
+    uint4 nraw[CPT][NT], nrr[CPT];
+    if constexpr (PF) {
+      load_row(row + stride, nraw, nrr);  // (zero-filled past the last row)
+    } else {
+      load_row(row, raw, rr);
+    }
+    uint4 xq[CPT];  // the stored bf16 x1 row (LN2 reads it, R12)
     float sum[1] = {0.f};
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
@@ -230,47 +248,62 @@ __global__ void __launch_bounds__(256, 2) ar_fwd_kernel(ArFwdArgs a, PeerSync ps
       uint4 pk;
       pk.x = pack_bf16(v[0], v[1]); pk.y = pack_bf16(v[2], v[3]);
       pk.z = pack_bf16(v[4], v[5]); pk.w = pack_bf16(v[6], v[7]);
+      xq[k] = pk;
       const int c = t + k * tpr;
       if (c < nc) {
         *reinterpret_cast<uint4 *>(a.out + ro + c * 8) = pk;
-        unpack8(pk, q[k]);  // LN2 reads the stored bf16 x1 (R12)
+        float q[8];
+        unpack8(pk, q);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) sum[0] += q[k][e];
+        for (int e = 0; e < 8; ++e) sum[0] += q[e];
       }
     }
-    if (!a.do_ln) continue;
-    sub_reduce<1>(sum, tpr, sub, t, red, par);
-    const float mean = sum[0] / h;
-    float var[1] = {0.f};
+    if (a.do_ln) {
+      sub_reduce<1>(sum, tpr, sub, t, red, par);
+      const float mean = sum[0] / h;
+      float var[1] = {0.f};
 #pragma unroll
-    for (int k = 0; k < CPT; ++k)
-      if (t + k * tpr < nc)
+      for (int k = 0; k < CPT; ++k)
+        if (t + k * tpr < nc) {
+          float q[8];
+          unpack8(xq[k], q);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) var[0] += (q[k][e] - mean) * (q[k][e] - mean);
-    sub_reduce<1>(var, tpr, sub, t, red, par);
-    const float rstd = rsqrtf(var[0] / h + a.eps);
+          for (int e = 0; e < 8; ++e) var[0] += (q[e] - mean) * (q[e] - mean);
+        }
+      sub_reduce<1>(var, tpr, sub, t, red, par);
+      const float rstd = rsqrtf(var[0] / h + a.eps);
 #pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-      const int c = t + k * tpr;
-      if (c >= nc) continue;
-      float gm[8], bt[8], o[8];
-      load8(a.gamma + c * 8, gm);
-      load8(a.beta + c * 8, bt);
+      for (int k = 0; k < CPT; ++k) {
+        const int c = t + k * tpr;
+        if (c >= nc) continue;
+        float gm[8], bt[8], o[8], q[8];
+        unpack8(xq[k], q);
+        load8(a.gamma + c * 8, gm);
+        load8(a.beta + c * 8, bt);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] = (q[k][e] - mean) * rstd * gm[e] + bt[e];
-      store8(a.ln_out + (size_t)row * a.ld_ln + c * 8, o);
+        for (int e = 0; e < 8; ++e) o[e] = (q[e] - mean) * rstd * gm[e] + bt[e];
+        store8(a.ln_out + (size_t)row * a.ld_ln + c * 8, o);
+      }
+      if (t < a.pad.n) {  // LN1 fused into a chained AR#2: the next layer's ones-column pads (as ln_fwd_kernel)
+        uint4 one;
+        one.x = pack_bf16(1.f, 0.f);
+        one.y = one.z = one.w = 0u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k == t) *reinterpret_cast<uint4 *>(a.pad.ptr[k] + (size_t)row * a.pad.ld[k] + a.pad.col[k]) = one;
+      }
+      if (t == 0) {
+        a.mean[row] = mean;
+        a.rstd[row] = rstd;
+      }
     }
-    if (t < a.pad.n) {  // LN1 fused into a chained AR#2: the next layer's ones-column pads (as ln_fwd_kernel)
-      uint4 one;
-      one.x = pack_bf16(1.f, 0.f);
-      one.y = one.z = one.w = 0u;
+    if constexpr (PF) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (k == t) *reinterpret_cast<uint4 *>(a.pad.ptr[k] + (size_t)row * a.pad.ld[k] + a.pad.col[k]) = one;
-    }
-    if (t == 0) {
-      a.mean[row] = mean;
-      a.rstd[row] = rstd;
+      for (int k = 0; k < CPT; ++k) {
+#pragma unroll
+        for (int r = 0; r < NT; ++r) raw[k][r] = nraw[k][r];
+        rr[k] = nrr[k];
+      }
     }
   }
 }
@@ -430,7 +463,7 @@ __global__ void __launch_bounds__(256, 2) ar_bwd_kernel(ArBwdArgs a, PeerSync ps
 
 // ------------------------------------------------------------------------------ LayerNorm forward
 template <int CPT>
-__global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16 *x, const __nv_bfloat16 *gamma,
+__global__ void __launch_bounds__(256, 4) ln_fwd_kernel(const __nv_bfloat16 *x, const __nv_bfloat16 *gamma,
                                                      const __nv_bfloat16 *beta, __nv_bfloat16 *u, int ld_u,
                                                      float *mean_out, float *rstd_out, int m, int h, float eps,
                                                      OnesPad pad, int tpr) {
@@ -438,41 +471,52 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16 *x, con
   const int nsub = blockDim.x / tpr, sub = threadIdx.x / tpr, t = threadIdx.x % tpr;
   const int nc = h >> 3;
   int par = 0;
-  for (int row = blockIdx.x * nsub + sub; row < m; row += gridDim.x * nsub) {
+  // row prefetch as in ar_fwd_kernel: the next row's loads are in flight during this row's work
+  const int stride = gridDim.x * nsub;
+  auto load_row = [&](int row, uint4 (&raw)[CPT]) {
     const size_t ro = (size_t)row * h;
-    uint4 raw[CPT];
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
       const int c = t + k * tpr;
-      raw[k] = c < nc ? ldg16(x + ro + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
+      raw[k] = (c < nc && row < m) ? ldg16(x + ro + (size_t)c * 8) : make_uint4(0, 0, 0, 0);
     }
-    float q[CPT][8];
+  };
+  uint4 raw[CPT];
+  load_row(blockIdx.x * nsub + sub, raw);
+  for (int row = blockIdx.x * nsub + sub; row < m; row += stride) {
+    uint4 nraw[CPT];
+    load_row(row + stride, nraw);
     float sum[1] = {0.f};
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
-      unpack8(raw[k], q[k]);
+      float q[8];
+      unpack8(raw[k], q);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) sum[0] += q[k][e];  // zero-filled beyond the row
+      for (int e = 0; e < 8; ++e) sum[0] += q[e];  // zero-filled beyond the row
     }
     sub_reduce<1>(sum, tpr, sub, t, red, par);
     const float mean = sum[0] / h;
     float var[1] = {0.f};
 #pragma unroll
     for (int k = 0; k < CPT; ++k)
-      if (t + k * tpr < nc)
+      if (t + k * tpr < nc) {
+        float q[8];
+        unpack8(raw[k], q);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) var[0] += (q[k][e] - mean) * (q[k][e] - mean);
+        for (int e = 0; e < 8; ++e) var[0] += (q[e] - mean) * (q[e] - mean);
+      }
     sub_reduce<1>(var, tpr, sub, t, red, par);
     const float rstd = rsqrtf(var[0] / h + eps);
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
       const int c = t + k * tpr;
       if (c >= nc) continue;
-      float gm[8], bt[8], o[8];
+      float gm[8], bt[8], o[8], q[8];
+      unpack8(raw[k], q);
       load8(gamma + c * 8, gm);
       load8(beta + c * 8, bt);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) o[e] = (q[k][e] - mean) * rstd * gm[e] + bt[e];
+      for (int e = 0; e < 8; ++e) o[e] = (q[e] - mean) * rstd * gm[e] + bt[e];
       store8(u + (size_t)row * ld_u + c * 8, o);
     }
     if (t < pad.n) {  // the ones-column pads of u, ctx, u2, g
@@ -487,6 +531,8 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16 *x, con
       mean_out[row] = mean;
       rstd_out[row] = rstd;
     }
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) raw[k] = nraw[k];
   }
 }
 
