@@ -122,7 +122,9 @@ enum { MERAK_COMM_PEER = 0, MERAK_COMM_NCCL = 1, MERAK_COMM_LOCAL = 2, MERAK_COM
  * through peer tensor maps), so the reduce-scatter reads local memory only; 2 = in addition the two-shot's
  * reduced rows are pushed into every rank's all-gather slot and the fused epilogue reads locally.  Applies to
  * calls whose owner row blocks B*s/(n T) are whole 32-row boxes, with the two-shot all-reduce or the
- * sequence-parallel layout; other calls use the pull layout.  Results are bit-identical in every mode. */
+ * sequence-parallel layout; other calls use the pull layout.  A GEMM pushes only when its compute covers its
+ * NVLink transfer, K T / (T-1) >= 1400 (env MERAK_AR_PUSH_MINK; e.g. proj at T = 8 stays on pull).  Results are
+ * bit-identical in every mode. */
 
 /* flags for layer_fwd / layer_bwd */
 enum {

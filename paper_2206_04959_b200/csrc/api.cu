@@ -136,6 +136,11 @@ struct merak_tmp {
   // MERAK_AR_PUSH=2 adds the all-gather push of the replicated two-shot all-reduce: phase 1 stores the reduced owner
   // rows into every rank's all-gather slot (AG_SLOT) over NVLink, so the phase-2 epilogue reads only local HBM
   bool push_ag = false;
+  // a row-parallel GEMM pushes only if its compute time covers its NVLink transfer: 2 m N K FLOPs against
+  // (T-1)/T m N 2 bytes, i.e. K T / (T-1) >= push_min_k FLOP/byte (~0.8 x 1689 TFLOP/s / 900 GB/s); below it
+  // (proj at T = 8: K = h/8) the GEMM would wait on the link, and the pull all-reduce kernel moves the bytes
+  // while other kernels hold the tensor cores.  Env MERAK_AR_PUSH_MINK at init.
+  int push_min_k = 1400;
   void *push_maps = nullptr;  // device: [4 row-parallel slots][T owners] CUtensorMap (128 B each)
   bool pdl = false;       // programmatic dependent launch along the all-reduce kernel chain (env MERAK_AR_PDL)
   int gemm_smem_kb = 192;  // GEMM TMA ring: 160 KB at T > 1 leaves smem for co-resident all-reduce kernels
@@ -371,6 +376,7 @@ static merak_status nccl_allreduce(merak_tmp_t *h, void *rows, size_t count, boo
 // Partials the all-reduce epilogue kernel sums for slot `slot`, rows starting at r0.
 static bool push_ag_on(merak_tmp_t *h, bool comm, int m);
 static int ar_partials(merak_tmp_t *h, bool comm, int slot, size_t r0, const bf16 **out, int m) {
+  (void)slot;
   if (!comm || h->T == 1 || h->nccl) {
     out[0] = slot_ptr(h, h->r, slot) + r0 * h->h;
     return 1;
@@ -423,19 +429,28 @@ static bool two_shot_on(merak_tmp_t *h, bool comm) { return comm && h->T > 1 && 
 // 32-row boxes): the m rows of sub-batch region r0 in OWNER q's slot hold, at rows [p*m/T, (p+1)*m/T), source
 // rank p's partial of q's rows; the reduce-scatter phase then sums T local row blocks in rank order (the same
 // arithmetic as pulling them from the peers' slots, so results are bit-identical).
-static bool push_on(merak_tmp_t *h, bool comm, int m) {
-  return h->push && comm && (h->sp || two_shot_on(h, comm)) && m % h->T == 0 && (m / h->T) % 32 == 0;
+static bool push_rows_ok(merak_tmp_t *h, bool comm, int m) {
+  return comm && h->T > 1 && m % h->T == 0 && (m / h->T) % 32 == 0;
+}
+// K of the row-parallel GEMM writing slot `slot`: proj (h_r), fc2 (f_r), fc1 dgrad (f_r), QKV dgrad (3 h_r)
+static int slot_k(const merak_tmp_t *h, int slot) { return slot == 0 ? h->hr : slot == 3 ? 3 * h->hr : h->fr; }
+static bool push_on(merak_tmp_t *h, bool comm, int m, int slot) {
+  return h->push && (h->sp || two_shot_on(h, comm)) && push_rows_ok(h, comm, m) &&
+         (long)slot_k(h, slot) * h->T >= (long)h->push_min_k * (h->T - 1);
 }
 // All-gather push (h->push_ag): the replicated two-shot all-reduce's phase 1 writes the reduced owner rows into every
 // rank's AG_SLOT region of the sub-batch and the phase-2 epilogue reads every row from its own AG_SLOT.  AG_SLOT is
 // shared by the 4 all-reduces and both sub-batches: a rank's phase 1 writes a peer's region only after a handshake
 // that the peer entered after its previous phase 2 finished reading (all on the in-order communication stream).
-static bool push_ag_on(merak_tmp_t *h, bool comm, int m) { return h->push_ag && !h->sp && push_on(h, comm, m); }
+// Independent of whether the slot's GEMM pushed (phase 1 reads either layout).
+static bool push_ag_on(merak_tmp_t *h, bool comm, int m) {
+  return h->push && h->push_ag && !h->sp && two_shot_on(h, comm) && push_rows_ok(h, comm, m);
+}
 // Output of a row-parallel GEMM into slot `slot`, sub-batch rows from r0: own slot, or pushed to the owners.
 static void slot_out(merak_tmp_t *h, GemmArgs &g, bool comm, int slot, size_t r0, int m) {
   g.out = slot_ptr(h, h->r, slot) + r0 * h->h;
   g.ldo = h->h;
-  if (push_on(h, comm, m)) {
+  if (push_on(h, comm, m, slot)) {
     g.scatter = reinterpret_cast<const char *>(h->push_maps) + (size_t)slot * h->T * 128;
     g.scatter_rows = m / h->T;
     g.scatter_row0 = (int)r0 + h->r * g.scatter_rows;
@@ -494,7 +509,7 @@ static merak_status two_shot_rs(merak_tmp_t *h, int slot, size_t r0, int m, cons
   a.row1 = (h->r + 1) * c < m ? (h->r + 1) * c : m;
   a.resid = resid; a.bias = bias;
   a.out = slot_ptr(h, h->r, slot) + r0 * h->h;
-  if (pushed && push_ag_on(h, true, m)) {  // reduced rows straight into every rank's all-gather slot
+  if (push_ag_on(h, true, m)) {  // reduced rows straight into every rank's all-gather slot
     a.n_peer = h->T;
     a.rank = h->r;
     for (int q = 0; q < h->T; ++q) a.out_peer[q] = slot_ptr(h, q, AG_SLOT) + r0 * h->h;
@@ -594,7 +609,7 @@ static merak_status ar2_issue(merak_tmp_t *h, int j, ArFwdArgs a, bool comm) {
   if (comm && h->nccl) TRY(nccl_allreduce(h, slot_ptr(h, h->r, 1) + r0 * h->h, (size_t)a.m * h->h));
   PeerSync ps = make_sync(h, comm);
   TRY(sync_peers(h, ps));
-  if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 1, r0, a.m, a.resid, a.bias, &a.chunk, &ps, push_on(h, comm, a.m)));
+  if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 1, r0, a.m, a.resid, a.bias, &a.chunk, &ps, push_on(h, comm, a.m, 1)));
   {
     Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
     a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
@@ -693,7 +708,7 @@ static merak_status layer_fwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.eps = h->eps; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
-      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 0, r0, m, xj, (const bf16 *)w->b_o, &a.chunk, &ps, push_on(h, comm, m)));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 0, r0, m, xj, (const bf16 *)w->b_o, &a.chunk, &ps, push_on(h, comm, m, 0)));
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
       a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
       CK(h, ar_fwd(a, ps, h->ms));
@@ -799,7 +814,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.G = h->G; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
-      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 2, r0, m, nullptr, nullptr, &a.chunk, &ps, push_on(h, comm, m)));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 2, r0, m, nullptr, nullptr, &a.chunk, &ps, push_on(h, comm, m, 2)));
       {
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         a.pdl = h->pdl && !h->prof && ps.enabled;
@@ -864,7 +879,7 @@ static merak_status layer_bwd(merak_tmp_t *h, const merak_tmp_weights *w, const 
       a.G = h->G; a.ctas = h->cfg.comm_ctas;
       PeerSync ps = make_sync(h, comm);
       TRY(sync_peers(h, ps));
-      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 3, r0, m, nullptr, nullptr, &a.chunk, &ps, push_on(h, comm, m)));
+      if (two_shot_on(h, comm)) TRY(two_shot_rs(h, 3, r0, m, nullptr, nullptr, &a.chunk, &ps, push_on(h, comm, m, 3)));
       {
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         a.pdl = h->pdl && !h->prof && ps.enabled;
@@ -977,7 +992,7 @@ static merak_status layer_fwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, con
       TRY(sp_handshake(h, &ps));
       ArFwdArgs a;
       memset(&a, 0, sizeof(a));
-      for (int q = 0; q < h->T; ++q) a.partial[q] = own_partial(h, push_on(h, true, m), 0, r0, q, mr);
+      for (int q = 0; q < h->T; ++q) a.partial[q] = own_partial(h, push_on(h, true, m, 0), 0, r0, q, mr);
       a.T = h->T; a.m = mr; a.h = hh; a.resid = xj; a.bias = (const bf16 *)w->b_o;
       a.out = (bf16 *)S(L.x1) + l0 * hh;
       a.do_ln = true; a.gamma = (const bf16 *)w->ln2_g; a.beta = (const bf16 *)w->ln2_b;
@@ -1020,7 +1035,7 @@ static merak_status layer_fwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, con
       TRY(sp_handshake(h, &ps));
       ArFwdArgs a;
       memset(&a, 0, sizeof(a));
-      for (int q = 0; q < h->T; ++q) a.partial[q] = own_partial(h, push_on(h, true, m), 1, r0, q, mr);
+      for (int q = 0; q < h->T; ++q) a.partial[q] = own_partial(h, push_on(h, true, m, 1), 1, r0, q, mr);
       a.T = h->T; a.m = mr; a.h = hh; a.resid = (const bf16 *)S(L.x1) + l0 * hh; a.bias = (const bf16 *)w->b_2;
       a.out = y + l0 * hh; a.do_ln = false; a.ctas = h->cfg.comm_ctas;
       Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
@@ -1075,7 +1090,7 @@ static merak_status layer_bwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, con
       TRY(sp_handshake(h, &ps));
       ArBwdArgs a;
       memset(&a, 0, sizeof(a));
-      for (int q = 0; q < h->T; ++q) a.partial[q] = own_partial(h, push_on(h, true, m), 2, r0, q, mr);
+      for (int q = 0; q < h->T; ++q) a.partial[q] = own_partial(h, push_on(h, true, m, 2), 2, r0, q, mr);
       a.T = h->T; a.m = mr; a.h = hh; a.x_ln = (const bf16 *)S(L.x1) + l0 * hh;
       a.mean = (const float *)S(L.mean2) + l0; a.rstd = (const float *)S(L.rstd2) + l0;
       a.gamma = (const bf16 *)w->ln2_g; a.dres = dy + l0 * hh; a.dx = ag_own;  // dx1 rows for the all-gather
@@ -1148,7 +1163,7 @@ static merak_status layer_bwd_sp(merak_tmp_t *h, const merak_tmp_weights *w, con
       TRY(sp_handshake(h, &ps));
       ArBwdArgs a;
       memset(&a, 0, sizeof(a));
-      for (int q = 0; q < h->T; ++q) a.partial[q] = own_partial(h, push_on(h, true, m), 3, r0, q, mr);
+      for (int q = 0; q < h->T; ++q) a.partial[q] = own_partial(h, push_on(h, true, m, 3), 3, r0, q, mr);
       a.T = h->T; a.m = mr; a.h = hh; a.x_ln = x + l0 * hh;
       a.mean = (const float *)S(L.mean1) + l0; a.rstd = (const float *)S(L.rstd1) + l0;
       a.gamma = (const bf16 *)w->ln1_g; a.dres = h->dx1 + own * hh; a.dx = dx + l0 * hh;
@@ -1583,6 +1598,7 @@ static merak_status create_local(const merak_tmp_config *cfg, merak_tmp_t **out)
     h->push_req = atoi(t) != 0;
     h->push_ag = atoi(t) == 2;
   }
+  if (const char *t = getenv("MERAK_AR_PUSH_MINK")) h->push_min_k = atoi(t);
   if (h->f32) h->fuse_ln1 = false;
   // in-process groups share ONE GPU: a waiting epilogue kernel of one rank can fill the SMs that another rank's
   // phase-1 kernel (the one it waits for) needs, so they keep the 1-warp handshake kernel
@@ -2163,7 +2179,7 @@ merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t ro
         memset(&a, 0, sizeof(a));
         a.T = ar_partials(h, true, 1, 0, a.partial, rows);
         a.m = rows; a.h = (int)hh; a.resid = resid; a.bias = gam; a.out = out; a.ctas = h->cfg.comm_ctas;
-        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, resid, gam, &a.chunk, &ps, push_on(h, true, rows)));
+        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, resid, gam, &a.chunk, &ps, push_on(h, true, rows, 1)));
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         a.pdl = h->pdl && !h->prof && ps.enabled;  // after the handshake kernel
       CK(h, ar_fwd(a, ps, h->ms));
@@ -2173,7 +2189,7 @@ merak_status merak_tmp_bench_allreduce(merak_tmp_t *h, int32_t which, int32_t ro
         a.T = ar_partials(h, true, 1, 0, a.partial, rows);
         a.m = rows; a.h = (int)hh; a.x_ln = resid; a.mean = mean; a.rstd = rstd; a.gamma = gam; a.dres = resid;
         a.dx = out; a.part_dg = h->part_lng; a.part_db = h->part_lnb; a.G = h->G; a.ctas = h->cfg.comm_ctas;
-        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, nullptr, nullptr, &a.chunk, &ps, push_on(h, true, rows)));
+        if (two_shot_on(h, true)) TRY(two_shot_rs(h, 1, 0, rows, nullptr, nullptr, &a.chunk, &ps, push_on(h, true, rows, 1)));
         Launch Lk(h, MERAK_K_ALLREDUCE, h->ms, 0.0);
         a.pdl = h->pdl && !h->prof && ps.enabled;
         CK(h, ar_bwd(a, ps, h->ms));

@@ -78,11 +78,13 @@ def main():
         for mode in ("1", "2"):  # 2: the reduced rows are pushed into every rank's all-gather slot as well
             os.environ["MERAK_AR_PUSH"] = mode
             os.environ["MERAK_AR_TWO_SHOT"] = "1"
+            os.environ["MERAK_AR_PUSH_MINK"] = "0"  # every row-parallel GEMM pushes at these shapes
             try:
                 outq = run_gpu_layer(cfg, params, x, dy, T=T, rank=rank, group=group)
             finally:
                 del os.environ["MERAK_AR_PUSH"]
                 del os.environ["MERAK_AR_TWO_SHOT"]
+                del os.environ["MERAK_AR_PUSH_MINK"]
             for k in out:
                 if not torch.equal(out[k], outq[k]):
                     failures.append((name, f"{k}: pushed reduce-scatter (mode {mode}) not bit-identical"))

@@ -32,6 +32,8 @@ def _gpu():
 def _run(monkeypatch, push, cfg, plist, x, dy, T, seq_parallel, two_shot=None, n_sub=2):
     from test_gpu_seqpar import run_sp_group
     monkeypatch.setenv("MERAK_AR_PUSH", push if isinstance(push, str) else ("1" if push else "0"))
+    # every row-parallel GEMM pushes at these small shapes (the default K threshold keeps short-K GEMMs on pull)
+    monkeypatch.setenv("MERAK_AR_PUSH_MINK", "0")
     if two_shot is not None:
         monkeypatch.setenv("MERAK_AR_TWO_SHOT", "1" if two_shot else "0")
     return run_sp_group(cfg, plist, x, dy, T, n_sub=n_sub, seq_parallel=seq_parallel)
