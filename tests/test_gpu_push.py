@@ -118,3 +118,25 @@ def test_push_is_set_up(T, monkeypatch):
         finally:
             for r in ranks:
                 r.close()
+
+
+def test_push_mixed_slots_T8(monkeypatch):
+    """Realistic T = 8 mix: with the K threshold at 200 the proj GEMM (K T/(T-1) = 96 * 8/7 = 110) keeps the pull
+    reduce-scatter while fc2 / fc1 dgrad (439) and QKV dgrad (329) push; the all-gather push covers every slot.
+    Bit-identical to the pull layout and within the oracle tolerance."""
+    from gpu_layer_util import compare_to_oracle, oracle_rank_slices
+    from oracle import layer_fwd_bwd
+    T = 8
+    cfg = CFG.with_(hidden=768, heads=8, seq_len=128, microbatch=4, n_sub=2, tmp_degree=T)
+    params, x, dy = make_all(cfg, seed=4600)
+    pull = _run(monkeypatch, False, cfg, [params], x, dy, T, False, two_shot=True)
+    monkeypatch.setenv("MERAK_AR_PUSH", "2")
+    monkeypatch.setenv("MERAK_AR_PUSH_MINK", "200")
+    from test_gpu_seqpar import run_sp_group
+    mixed = run_sp_group(cfg, [params], x, dy, T, n_sub=2, seq_parallel=False)
+    _assert_identical(mixed, pull, T)
+    y, dx, g = layer_fwd_bwd(params, x, dy, cfg.heads)
+    for r in range(T):
+        o = {"y": mixed[r]["y"], "dx": mixed[r]["dx"], **mixed[r]["grads"][0]}
+        errs, bad = compare_to_oracle(o, y, dx, oracle_rank_slices(g, cfg, T, r), cfg)
+        assert not bad, (r, bad)
