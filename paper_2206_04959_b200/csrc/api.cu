@@ -137,7 +137,7 @@ struct merak_tmp {
   // rows into every rank's all-gather slot (AG_SLOT) over NVLink, so the phase-2 epilogue reads only local HBM
   bool push_ag = false;
   // a row-parallel GEMM pushes only if its compute time covers its NVLink transfer: 2 m N K FLOPs against
-  // (T-1)/T m N 2 bytes, i.e. K T / (T-1) >= push_min_k FLOP/byte (~0.8 x 1689 TFLOP/s / 900 GB/s); below it
+  // (T-1)/T m N 2 bytes, i.e. K T / (T-1) >= push_min_k FLOP/byte (~0.75 x 1689 TFLOP/s / 900 GB/s); below it
   // (proj at T = 8: K = h/8) the GEMM would wait on the link, and the pull all-reduce kernel moves the bytes
   // while other kernels hold the tensor cores.  Env MERAK_AR_PUSH_MINK at init.
   int push_min_k = 1400;
@@ -376,7 +376,6 @@ static merak_status nccl_allreduce(merak_tmp_t *h, void *rows, size_t count, boo
 // Partials the all-reduce epilogue kernel sums for slot `slot`, rows starting at r0.
 static bool push_ag_on(merak_tmp_t *h, bool comm, int m);
 static int ar_partials(merak_tmp_t *h, bool comm, int slot, size_t r0, const bf16 **out, int m) {
-  (void)slot;
   if (!comm || h->T == 1 || h->nccl) {
     out[0] = slot_ptr(h, h->r, slot) + r0 * h->h;
     return 1;
